@@ -1,0 +1,531 @@
+// capi.cu — the extern "C" surface of include/wn.h: argument checks, error reporting, launch accounting,
+// and the host orchestration of the operators and of Alg. 3.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "wn_comm.cuh"
+#include "wn_internal.cuh"
+#include "wn_ops.cuh"
+
+namespace wn {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+wn_status set_error(wn_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+wn_status cuda_status(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-free errors
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? WN_ERR_OOM : WN_ERR_CUDA;
+}
+
+void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+// ---- profiling: CUDA events on the launching stream ----
+struct ProfRec {
+  int cls;
+  int nlaunch;
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+
+ProfScope::ProfScope(int c, cudaStream_t st, int nlaunch) : cls(c), s(st) {
+  count_launches(nlaunch);
+  if (!g_prof_on) return;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, s);
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof.push_back({c, nlaunch, a, b});
+}
+ProfScope::~ProfScope() {
+  if (b) cudaEventRecord(b, s);
+}
+
+// ---- algorithmic-work counting (node tests, representative terms, leaf-point terms per class) ----
+static bool g_count_on = false;
+static int64_t* g_work = nullptr;
+
+int64_t* work_counters(int cls) {
+  if (!g_count_on || !g_work || cls < 0 || cls > 2) return nullptr;
+  return g_work + 3 * cls;
+}
+
+static wn_status check_device() {
+  int dev = 0, n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return set_error(WN_ERR_CUDA, "no CUDA device available (libwn has no CPU path)");
+  if (cudaGetDevice(&dev) != cudaSuccess) return set_error(WN_ERR_CUDA, "cudaGetDevice failed");
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return set_error(WN_ERR_CUDA, "libwn is built for sm_100a (B200); device is not compute 10.x");
+  return WN_OK;
+}
+
+#define WN_TRY(x)                 \
+  do {                            \
+    wn_status st_ = (x);          \
+    if (st_ != WN_OK) return st_; \
+  } while (0)
+
+static wn_status ensure_scratch(wn_tree_s* t, cudaStream_t s) {
+  IterScratch& it = t->it;
+  if (it.mu) return WN_OK;
+  const int64_t n = t->n;
+  it.n = n;
+  it.nblk = trav_blocks(n);
+  WN_CUDA(cudaMallocAsync((void**)&it.mu, n * sizeof(float4), s));
+  WN_CUDA(cudaMallocAsync((void**)&it.mup, n * sizeof(float4), s));
+  WN_CUDA(cudaMallocAsync((void**)&it.r, n * sizeof(float4), s));
+  WN_CUDA(cudaMallocAsync((void**)&it.s, n * sizeof(float), s));
+  WN_CUDA(cudaMallocAsync((void**)&it.tmp, n * sizeof(float4), s));
+  WN_CUDA(cudaMallocAsync((void**)&it.part, 3 * (size_t)it.nblk * sizeof(double), s));
+  WN_CUDA(cudaMallocAsync((void**)&it.alpha, sizeof(double), s));
+  return WN_OK;
+}
+
+static int stack_depth(const wn_tree_s* t) { return 8 * (t->depth_used + 2); }
+
+static TravArgs base_args(const wn_tree_s* t, float w2) {
+  TravArgs a;
+  a.pts = t->pts;
+  a.nrange_pb = t->pb;
+  a.nrange_pe = t->pe;
+  a.queries = t->pts;
+  a.q_begin = 0;
+  a.q_end = t->n;
+  a.w2 = w2;
+  a.stack_depth = stack_depth(t);
+  return a;
+}
+
+static bool bad_width(float w) { return !(w > 0.f) || std::isnan(w); }
+static bool bad_theta(float c) { return !(c > 0.f) || std::isnan(c); }
+
+// ---- Alg. 3 loop over a query range [q0, q1) of the sorted points (multi-GPU: this rank's shard) ----
+static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm, cudaStream_t s) {
+  IterScratch& it = t->it;
+  const int total = p.total_iters > 0 ? p.total_iters : p.iters;
+  const bool transpose = p.adjoint_mode == WN_ADJ_TRANSPOSE;
+  const int64_t stride = it.nblk;
+  int64_t q0 = 0, q1 = t->n;
+  if (comm) WN_TRY(comm_shard(comm, t->n, &q0, &q1));
+  for (int i = 0; i < p.iters; ++i) {
+    const int k = p.first_iter + i;
+    const float w = width_at(k, total, (double)p.w_min, (double)p.w_max);
+    const float w2 = w * w;
+    // (1) s = ½ − A_w μ  (+ Σ s² partials)
+    MomentArgs m1;
+    m1.kind = ATTR_VEC;
+    m1.vec = it.mu;
+    m1.theta = p.theta;
+    m1.out = transpose ? t->set[1] : t->set[0];
+    WN_TRY(build_moments(t, m1, s));
+    TravArgs a1 = base_args(t, w2);
+    a1.op = OP_A;
+    a1.epi = EPI_S;
+    a1.nodes = m1.out;
+    a1.vec = it.mu;
+    a1.q_begin = q0;
+    a1.q_end = q1;
+    a1.out_f = it.s;
+    a1.partial = it.part;
+    WN_TRY(traverse(a1, s));
+    if (comm) WN_TRY(comm_allgather_f(comm, it.s, 1, t->n, s));
+    // (2) r = A_wᵀ s  (+ Σ|r|² partials)
+    if (transpose) {
+      WN_TRY(adjoint_transpose(t, t->set[1], it.s, w2, it.r, it.part + stride, s));
+    } else {
+      MomentArgs m2;
+      m2.kind = ATTR_SCALAR;
+      m2.scal = it.s;
+      m2.theta = p.theta;
+      m2.out = t->set[0];
+      WN_TRY(build_moments(t, m2, s));
+      TravArgs a2 = base_args(t, w2);
+      a2.op = OP_AT;
+      a2.epi = EPI_R;
+      a2.nodes = t->set[0];
+      a2.scal = it.s;
+      a2.q_begin = q0;
+      a2.q_end = q1;
+      a2.out_v4 = it.r;
+      a2.partial = it.part + stride;
+      WN_TRY(traverse(a2, s));
+      if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.r, 4, t->n, s));
+    }
+    // (3) Σ (A_w r)²  — gather: r's own representatives; transpose: μ's frozen geometry
+    MomentArgs m3;
+    m3.kind = ATTR_VEC;
+    m3.vec = it.r;
+    m3.theta = p.theta;
+    m3.out = t->set[0];
+    WN_TRY(build_moments(t, m3, s));
+    TravArgs a3 = base_args(t, w2);
+    a3.op = OP_A;
+    a3.epi = EPI_SQ;
+    a3.nodes = transpose ? t->set[1] : t->set[0];
+    a3.attrA = transpose ? t->set[0].A : nullptr;
+    a3.vec = it.r;
+    a3.q_begin = q0;
+    a3.q_end = q1;
+    a3.partial = it.part + 2 * stride;
+    WN_TRY(traverse(a3, s));
+    if (comm) WN_TRY(comm_allgather_partials(comm, it.part, stride, t->n, s));
+    // α = Σr² / Σ(Ar)²  (Alg. 2), fixed-order reduction of the partials
+    if (it.stats_cap < p.iters) {
+      if (it.dstats) cudaFreeAsync(it.dstats, s);
+      WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)p.iters, s));
+      it.stats_cap = p.iters;
+    }
+    alpha_step(it.part, (int)stride, stride, (double)w, it.alpha, it.dstats + 5 * i, s);
+    // (4) μ' = μ + α r (fused into the moment build), μ̂ = G_w(μ'), μ = μ̂ |μ'|/|μ̂|
+    MomentArgs m4;
+    m4.kind = ATTR_VEC;
+    m4.vec = it.mu;
+    m4.axpy_r = it.r;
+    m4.alpha = it.alpha;
+    m4.axpy_out = it.mup;
+    m4.theta = p.theta;
+    m4.out = t->set[0];
+    WN_TRY(build_moments(t, m4, s));
+    TravArgs a4 = base_args(t, w2);
+    a4.op = OP_G;
+    a4.epi = EPI_RESCALE;
+    a4.nodes = t->set[0];
+    a4.vec = it.mup;
+    a4.mup = it.mup;
+    a4.q_begin = q0;
+    a4.q_end = q1;
+    a4.out_v4 = it.mu;
+    WN_TRY(traverse(a4, s));
+    if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, s));
+  }
+  return WN_OK;
+}
+
+}  // namespace wn
+
+using namespace wn;
+
+extern "C" {
+
+const char* wn_last_error(void) { return g_last_error.c_str(); }
+const char* wn_version(void) { return "libwn 0.1 (sm_100a, " __DATE__ ")"; }
+uint64_t wn_launch_count(void) { return g_launches.load(); }
+
+wn_status wn_prof_enable(int32_t enable) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& r : g_prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  g_prof_on = enable != 0;
+  return WN_OK;
+}
+
+wn_status wn_prof_read(double ms[WN_PROF_NCLASS], int64_t launches[WN_PROF_NCLASS]) {
+  for (int c = 0; c < WN_PROF_NCLASS; ++c) {
+    ms[c] = 0.0;
+    launches[c] = 0;
+  }
+  WN_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& r : g_prof) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) ms[r.cls] += t;
+    launches[r.cls] += r.nlaunch;
+  }
+  return WN_OK;
+}
+
+wn_status wn_work_count_enable(int32_t enable) {
+  if (enable && !g_work) WN_CUDA(cudaMalloc((void**)&g_work, 9 * sizeof(int64_t)));
+  if (enable) WN_CUDA(cudaMemset(g_work, 0, 9 * sizeof(int64_t)));
+  g_count_on = enable != 0;
+  return WN_OK;
+}
+
+wn_status wn_work_count_read(int64_t counts[9]) {
+  for (int k = 0; k < 9; ++k) counts[k] = 0;
+  if (!g_work) return WN_OK;
+  WN_CUDA(cudaDeviceSynchronize());
+  WN_CUDA(cudaMemcpy(counts, g_work, 9 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return WN_OK;
+}
+
+wn_status wn_build_tree(const float* pts, int64_t n, int32_t max_depth, void* stream, wn_tree* out) {
+  if (!out) return set_error(WN_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 1) return set_error(WN_ERR_EMPTY, "empty point set (n < 1)");
+  if (!pts) return set_error(WN_ERR_ARG, "pts is NULL");
+  if (max_depth < 1 || max_depth > kMaxDepth) return set_error(WN_ERR_ARG, "max_depth must be in [1, 21]");
+  if (n > (int64_t)1 << 27) return set_error(WN_ERR_ARG, "n > 2^27 points is not supported");
+  WN_TRY(check_device());
+  wn_tree_s* t = new (std::nothrow) wn_tree_s();
+  if (!t) return set_error(WN_ERR_OOM, "host allocation failed");
+  cudaGetDevice(&t->device);
+  wn_status st = build_tree(pts, n, max_depth, (cudaStream_t)stream, t);
+  if (st != WN_OK) {
+    cudaStreamSynchronize((cudaStream_t)stream);
+    free_tree(t);
+    delete t;
+    return st;
+  }
+  *out = t;
+  return WN_OK;
+}
+
+wn_status wn_tree_destroy(wn_tree t) {
+  if (!t) return WN_OK;
+  cudaDeviceSynchronize();
+  free_tree(t);
+  delete t;
+  return WN_OK;
+}
+
+wn_status wn_tree_info(wn_tree t, int64_t* num_points, int64_t* num_nodes, int32_t* depth_used, double xform[4]) {
+  if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
+  if (num_points) *num_points = t->n;
+  if (num_nodes) *num_nodes = t->nn;
+  if (depth_used) *depth_used = t->depth_used;
+  if (xform)
+    for (int a = 0; a < 4; ++a) xform[a] = t->xf[a];
+  return WN_OK;
+}
+
+wn_status wn_tree_export(wn_tree t, uint64_t* keys, int32_t* perm, float* xn, int32_t* depth, int32_t* pb,
+                         int32_t* pe, int32_t* child_begin, int32_t* child_count, void* stream) {
+  if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t N = t->n, NN = t->nn;
+  if (keys) WN_CUDA(cudaMemcpyAsync(keys, t->keys, N * 8, cudaMemcpyDeviceToDevice, s));
+  if (perm) WN_CUDA(cudaMemcpyAsync(perm, t->perm, N * 4, cudaMemcpyDeviceToDevice, s));
+  if (xn) WN_CUDA(cudaMemcpy2DAsync(xn, 12, t->pts, 16, 12, N, cudaMemcpyDeviceToDevice, s));
+  if (depth) WN_CUDA(cudaMemcpyAsync(depth, t->depth, NN * 4, cudaMemcpyDeviceToDevice, s));
+  if (pb) WN_CUDA(cudaMemcpyAsync(pb, t->pb, NN * 4, cudaMemcpyDeviceToDevice, s));
+  if (pe) WN_CUDA(cudaMemcpyAsync(pe, t->pe, NN * 4, cudaMemcpyDeviceToDevice, s));
+  if (child_begin) WN_CUDA(cudaMemcpyAsync(child_begin, t->cb, NN * 4, cudaMemcpyDeviceToDevice, s));
+  if (child_count) WN_CUDA(cudaMemcpyAsync(child_count, t->cc, NN * 4, cudaMemcpyDeviceToDevice, s));
+  return WN_OK;
+}
+
+wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, float* rep, float* attr, double* W,
+                     void* stream) {
+  if (!t || !nu) return set_error(WN_ERR_ARG, "tree or nu is NULL");
+  if (dim != 1 && dim != 3) return set_error(WN_ERR_ARG, "dim must be 1 or 3");
+  cudaStream_t s = (cudaStream_t)stream;
+  WN_TRY(ensure_scratch(t, s));
+  IterScratch& it = t->it;
+  MomentArgs m;
+  m.theta = 2.0f;
+  m.out = t->set[0];
+  if (dim == 3) {
+    gather_vec_a(t->n, t->perm, nu, a, it.mu, it.s, it.mup, s);
+    m.kind = ATTR_VEC;
+    m.vec = it.mu;
+  } else {
+    gather_scal(t->n, t->perm, nu, it.s, s);
+    if (a) gather_scal(t->n, t->perm, a, (float*)it.tmp, s);
+    m.kind = ATTR_SCALAR;
+    m.scal = it.s;
+  }
+  if (a) m.a_sorted = dim == 3 ? it.s : (const float*)it.tmp;
+  WN_TRY(build_moments(t, m, s));
+  const size_t NN = t->nn;
+  if (rep) WN_CUDA(cudaMemcpy2DAsync(rep, 12, t->set[0].R, 16, 12, NN, cudaMemcpyDeviceToDevice, s));
+  if (attr) WN_CUDA(cudaMemcpy2DAsync(attr, 4 * dim, t->set[0].A, 16, 4 * dim, NN, cudaMemcpyDeviceToDevice, s));
+  if (W) WN_CUDA(cudaMemcpy2DAsync(W, 8, t->sums, 64, 8, NN, cudaMemcpyDeviceToDevice, s));
+  return WN_OK;
+}
+
+static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a, const float* q, int64_t m,
+                             float width, float theta, float* out, void* stream) {
+  if (!t || !mu || !out) return set_error(WN_ERR_ARG, "tree, mu or output is NULL");
+  if (bad_width(width)) return set_error(WN_ERR_ARG, "width must be > 0");
+  if (bad_theta(theta)) return set_error(WN_ERR_ARG, "theta must be > 0");
+  if (q && m < 0) return set_error(WN_ERR_ARG, "m < 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  WN_TRY(ensure_scratch(t, s));
+  IterScratch& it = t->it;
+  // ν = a·μ: moments use μ and a separately (exact fp64 products); leaf terms use fl(a·μ)
+  gather_vec_a(t->n, t->perm, mu, a, it.mu, (float*)it.tmp, it.mup, s);
+  MomentArgs mm;
+  mm.kind = ATTR_VEC;
+  mm.vec = it.mu;
+  mm.a_sorted = a ? (const float*)it.tmp : nullptr;
+  mm.theta = theta;
+  mm.out = t->set[0];
+  WN_TRY(build_moments(t, mm, s));
+  TravArgs ta = base_args(t, width * width);
+  ta.op = op;
+  ta.epi = EPI_PLAIN;
+  ta.nodes = t->set[0];
+  ta.vec = a ? it.mup : it.mu;
+  const double sc = t->xf[3];
+  // frame factors (include/wn.h): F_in = s²·Σ_n(ν), ∇F_in = −s³·G_n(ν)
+  ta.scale_out = op == OP_A ? (float)(sc * sc) : (float)(-sc * sc * sc);
+  if (q) {
+    if (m == 0) return WN_OK;
+    if (t->qcap < m) {
+      if (t->qbuf) cudaFreeAsync(t->qbuf, s);
+      WN_CUDA(cudaMallocAsync((void**)&t->qbuf, m * sizeof(float4), s));
+      t->qcap = m;
+    }
+    normalize_queries(m, q, t->xf, t->qbuf, s);
+    ta.queries = t->qbuf;
+    ta.q_end = m;
+    ta.out_map = nullptr;
+  } else {
+    ta.out_map = t->perm;
+  }
+  if (op == OP_A) ta.out_f = out;
+  else ta.out_v3 = out;
+  return traverse(ta, s);
+}
+
+wn_status wn_eval(wn_tree t, const float* mu, const float* a, const float* q, int64_t m, float width, float theta,
+                  float* F, void* stream) {
+  return eval_common(t, OP_A, mu, a, q, m, width, theta, F, stream);
+}
+
+wn_status wn_eval_grad(wn_tree t, const float* mu, const float* a, const float* q, int64_t m, float width,
+                       float theta, float* gradF, void* stream) {
+  return eval_common(t, OP_G, mu, a, q, m, width, theta, gradF, stream);
+}
+
+wn_status wn_eval_adjoint(wn_tree t, const float* sv, float width, float theta, int32_t mode, const float* mu_geom,
+                          float* out, void* stream) {
+  if (!t || !sv || !out) return set_error(WN_ERR_ARG, "tree, s or output is NULL");
+  if (bad_width(width)) return set_error(WN_ERR_ARG, "width must be > 0");
+  if (bad_theta(theta)) return set_error(WN_ERR_ARG, "theta must be > 0");
+  if (mode != WN_ADJ_GATHER && mode != WN_ADJ_TRANSPOSE) return set_error(WN_ERR_ARG, "bad adjoint mode");
+  if (mode == WN_ADJ_TRANSPOSE && !mu_geom) return set_error(WN_ERR_ARG, "transpose mode needs mu_geom");
+  cudaStream_t s = (cudaStream_t)stream;
+  WN_TRY(ensure_scratch(t, s));
+  IterScratch& it = t->it;
+  const double sc2 = t->xf[3] * t->xf[3];   // Aᵀ_in = s²·Aᵀ_n
+  gather_scal(t->n, t->perm, sv, it.s, s);
+  const float w2 = width * width;
+  if (mode == WN_ADJ_GATHER) {
+    MomentArgs m;
+    m.kind = ATTR_SCALAR;
+    m.scal = it.s;
+    m.theta = theta;
+    m.out = t->set[0];
+    WN_TRY(build_moments(t, m, s));
+    TravArgs ta = base_args(t, w2);
+    ta.op = OP_AT;
+    ta.epi = EPI_PLAIN;
+    ta.nodes = t->set[0];
+    ta.scal = it.s;
+    ta.out_map = t->perm;
+    ta.out_v3 = out;
+    ta.scale_out = (float)sc2;
+    return traverse(ta, s);
+  }
+  gather_vec(t->n, t->perm, mu_geom, 1.0, it.mu, s);
+  MomentArgs m;
+  m.kind = ATTR_VEC;
+  m.vec = it.mu;
+  m.theta = theta;
+  m.out = t->set[1];
+  WN_TRY(build_moments(t, m, s));
+  WN_TRY(adjoint_transpose(t, t->set[1], it.s, w2, it.r, nullptr, s));
+  scatter_vec(t->n, t->perm, it.r, sc2, out, s);
+  return WN_OK;
+}
+
+static wn_status check_params(const wnnc_params* p) {
+  if (!p) return set_error(WN_ERR_ARG, "params is NULL");
+  if (bad_width(p->w_min) || bad_width(p->w_max)) return set_error(WN_ERR_ARG, "widths must be > 0");
+  if (p->w_min > p->w_max) return set_error(WN_ERR_ARG, "w_min > w_max");
+  if (bad_theta(p->theta)) return set_error(WN_ERR_ARG, "theta must be > 0");
+  if (p->iters < 1) return set_error(WN_ERR_ARG, "iters < 1");
+  const int total = p->total_iters > 0 ? p->total_iters : p->iters;
+  if (p->first_iter < 1 || p->first_iter + p->iters - 1 > total) return set_error(WN_ERR_ARG, "bad first_iter");
+  if (p->adjoint_mode != WN_ADJ_GATHER && p->adjoint_mode != WN_ADJ_TRANSPOSE)
+    return set_error(WN_ERR_ARG, "bad adjoint_mode");
+  return WN_OK;
+}
+
+wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm, wnnc_iter_stats* stats,
+                       void* stream) {
+  if (!t || !mu) return set_error(WN_ERR_ARG, "tree or mu is NULL");
+  WN_TRY(check_params(p));
+  if (comm && p->adjoint_mode == WN_ADJ_TRANSPOSE)
+    return set_error(WN_ERR_ARG, "transpose-mode adjoint is single-GPU only in this build");
+  cudaStream_t s = (cudaStream_t)stream;
+  WN_TRY(ensure_scratch(t, s));
+  const double sc2 = t->xf[3] * t->xf[3];
+  gather_vec(t->n, t->perm, mu, sc2, t->it.mu, s);        // μ_norm = scale²·μ
+  WN_TRY(run_iterations(t, *p, comm, s));
+  scatter_vec(t->n, t->perm, t->it.mu, 1.0 / sc2, mu, s);  // back to the input frame
+  if (stats) {
+    std::vector<double> h(5 * (size_t)p->iters);
+    WN_CUDA(cudaMemcpyAsync(h.data(), t->it.dstats, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < p->iters; ++i)
+      stats[i] = {h[5 * i], h[5 * i + 1], h[5 * i + 2], h[5 * i + 3], h[5 * i + 4]};
+  }
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
+wn_status wnnc_solve_host(const float* pts_host, int64_t n, int32_t max_depth, const wnnc_params* p,
+                          float* normals_host, float* mu_host, wnnc_iter_stats* stats, void* stream) {
+  if (!pts_host || !normals_host) return set_error(WN_ERR_ARG, "host buffer is NULL");
+  if (n < 1) return set_error(WN_ERR_EMPTY, "empty point set (n < 1)");
+  WN_TRY(check_params(p));
+  WN_TRY(check_device());
+  cudaStream_t s = (cudaStream_t)stream;
+  float *dp = nullptr, *dmu = nullptr, *dn = nullptr;
+  const size_t bytes = (size_t)n * 3 * sizeof(float);
+  WN_CUDA(cudaMallocAsync((void**)&dp, bytes, s));
+  WN_CUDA(cudaMallocAsync((void**)&dmu, bytes, s));
+  WN_CUDA(cudaMallocAsync((void**)&dn, bytes, s));
+  WN_CUDA(cudaMemcpyAsync(dp, pts_host, bytes, cudaMemcpyHostToDevice, s));
+  WN_CUDA(cudaMemsetAsync(dmu, 0, bytes, s));
+  wn_tree t = nullptr;
+  wn_status st = wn_build_tree(dp, n, max_depth, stream, &t);
+  if (st == WN_OK) st = wnnc_iterate(t, dmu, p, nullptr, stats, stream);
+  if (st == WN_OK) {
+    unit_normals(n, dmu, dn, s);
+    cudaMemcpyAsync(normals_host, dn, bytes, cudaMemcpyDeviceToHost, s);
+    if (mu_host) cudaMemcpyAsync(mu_host, dmu, bytes, cudaMemcpyDeviceToHost, s);
+  }
+  cudaFreeAsync(dp, s);
+  cudaFreeAsync(dmu, s);
+  cudaFreeAsync(dn, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (t) wn_tree_destroy(t);
+  if (st != WN_OK) return st;
+  if (e != cudaSuccess) return cuda_status(e, "wnnc_solve_host");
+  return WN_OK;
+}
+
+wn_status wn_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin, int64_t* end) {
+  if (world < 1 || rank < 0 || rank >= world || n < 0 || !begin || !end)
+    return set_error(WN_ERR_ARG, "bad shard arguments");
+  const int64_t blocks = (n + WN_SHARD_ALIGN - 1) / WN_SHARD_ALIGN;
+  const int64_t b0 = blocks * rank / world, b1 = blocks * (rank + 1) / world;
+  *begin = std::min<int64_t>(n, b0 * WN_SHARD_ALIGN);
+  *end = std::min<int64_t>(n, b1 * WN_SHARD_ALIGN);
+  return WN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// transpose.cu — exact-transpose adjoint of the treecode (BASELINE north star:
+// "the adjoint kernel, which scatters into node moments and is then pushed down the tree").
+//
+// Treecode A at frozen geometry g(μ) (reps and per-query decisions of A(μ), Alg. 4)
+// is linear in the attribute ν:  (T_g ν)_i = Σ_{far B} ∇Φ_w(x_i − x_B)·Σ_{j∈B} ν_j + Σ_{near j} ∇Φ_w(x_i − x_j)·ν_j.
+// Its exact transpose is  (T_gᵀ s)_j = U_j + Σ_{B ∋ j} V_B  with
+//     V_B = Σ_{i: B far for i} s_i ∇Φ_w(x_i − x_B),   U_j = Σ_{i: j near for i} s_i ∇Φ_w(x_i − x_j).
+// Kernel 1 runs the same warp-cooperative traversal as A (same fp32 decisions); for every node the
+// warp sums its lanes' contributions with shuffles and lane 0 issues one fp64 atomic per component.
+// Kernel 2 pushes down: r_j = U_j + Σ over the ancestors of j's leaf, and emits Σ|r|² block partials.
+#include <cuda_runtime.h>
+
+#include "wn_internal.cuh"
+
+namespace wn {
+namespace {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+__device__ __forceinline__ float dist2(float dx, float dy, float dz) {
+  return __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+}
+
+__device__ __forceinline__ void warp_add3(float x, float y, float z, double* dst, int lane) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    x += __shfl_xor_sync(FULL, x, o);
+    y += __shfl_xor_sync(FULL, y, o);
+    z += __shfl_xor_sync(FULL, z, o);
+  }
+  if (lane == 0) {
+    atomicAdd(dst + 0, (double)x);
+    atomicAdd(dst + 1, (double)y);
+    atomicAdd(dst + 2, (double)z);
+  }
+}
+
+__global__ void __launch_bounds__(kTravBlock) scatter_kernel(
+    const float4* __restrict__ NR, const float4* __restrict__ NA, const float4* __restrict__ pts,
+    const int32_t* __restrict__ npb, const int32_t* __restrict__ npe, const float* __restrict__ s_sorted,
+    int64_t n, float w2, int stack_depth, double* __restrict__ VB, double* __restrict__ U) {
+  extern __shared__ int2 stk_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int2* stk = stk_all + warp * stack_depth;
+  const int64_t q = (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
+  const bool valid = q < n;
+  const float4 xq = valid ? pts[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float sq = valid ? s_sorted[q] * kInv4Pi : 0.f;
+  const uint32_t active = __ballot_sync(FULL, valid);
+  if (!active) return;
+  int sp = 0;
+  if (lane == 0) stk[0] = make_int2(0, (int)active);
+  sp = 1;
+  __syncwarp();
+  while (sp > 0) {
+    --sp;
+    const int2 e = stk[sp];
+    __syncwarp();
+    const int cb = e.x >> 4, ncc = (e.x & 7) + 1;
+    const bool mine = ((uint32_t)e.y >> lane) & 1u;
+    for (int k = 0; k < ncc; ++k) {
+      const int node = cb + k;
+      const float4 R = __ldg(NR + node);
+      const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
+      const float d2 = dist2(dx, dy, dz);
+      const bool far = d2 > R.w;
+      // s_i ∇Φ(x_i − x_B) = s_i d / (4π r³), d = x_B − x_i
+      float cx = 0.f, cy = 0.f, cz = 0.f;
+      const bool live = mine && far && !(d2 < w2);
+      if (live) {
+        const float inv = rsqrtf(d2);
+        const float c = sq * inv * inv * inv;
+        cx = c * dx; cy = c * dy; cz = c * dz;
+      }
+      if (__any_sync(FULL, live)) warp_add3(cx, cy, cz, VB + 3 * (int64_t)node, lane);
+      const uint32_t open = __ballot_sync(FULL, mine && !far);
+      if (open) {
+        const int topo = __float_as_int(__ldg(NA + node).w);
+        if (!(topo & 8)) {
+          if (lane == 0) stk[sp] = make_int2(topo, (int)open);
+          ++sp;
+        } else {
+          const bool lm = (open >> lane) & 1u;
+          const int j1 = npe[node];
+          for (int j = npb[node]; j < j1; ++j) {
+            const float4 P = __ldg(pts + j);
+            const float ex = __fsub_rn(P.x, xq.x), ey = __fsub_rn(P.y, xq.y), ez = __fsub_rn(P.z, xq.z);
+            const float e2 = dist2(ex, ey, ez);
+            float ux = 0.f, uy = 0.f, uz = 0.f;
+            const bool lv = lm && !(e2 < w2);
+            if (lv) {
+              const float inv = rsqrtf(e2);
+              const float c = sq * inv * inv * inv;
+              ux = c * ex; uy = c * ey; uz = c * ez;
+            }
+            if (__any_sync(FULL, lv)) warp_add3(ux, uy, uz, U + 3 * (int64_t)j, lane);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void pushdown_kernel(int64_t n, const int32_t* __restrict__ leaf_of, const int32_t* __restrict__ parent,
+                                const double* __restrict__ VB, const double* __restrict__ U, float scale,
+                                float4* __restrict__ r, double* __restrict__ partial) {
+  __shared__ double red[kTravBlock / 32];
+  const int64_t j = (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
+  double part = 0.0;
+  if (j < n) {
+    double x = U[3 * j], y = U[3 * j + 1], z = U[3 * j + 2];
+    for (int b = leaf_of[j]; b >= 0; b = parent[b]) {
+      x += VB[3 * (int64_t)b];
+      y += VB[3 * (int64_t)b + 1];
+      z += VB[3 * (int64_t)b + 2];
+    }
+    const float fx = (float)x * scale, fy = (float)y * scale, fz = (float)z * scale;
+    r[j] = make_float4(fx, fy, fz, 0.f);
+    part = (double)fx * fx + (double)fy * fy + (double)fz * fz;
+  }
+  if (partial) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int k = 0; k < kTravBlock / 32; ++k) b += red[k];
+      partial[blockIdx.x] = b;
+    }
+  }
+}
+
+}  // namespace
+
+wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sorted, float w2, float4* r_out,
+                            double* partial, cudaStream_t st) {
+  if (!t->tvb) {
+    WN_CUDA(cudaMallocAsync((void**)&t->tvb, 3 * sizeof(double) * (size_t)t->nn, st));
+    WN_CUDA(cudaMallocAsync((void**)&t->tu, 3 * sizeof(double) * (size_t)t->n, st));
+  }
+  WN_CUDA(cudaMemsetAsync(t->tvb, 0, 3 * sizeof(double) * (size_t)t->nn, st));
+  WN_CUDA(cudaMemsetAsync(t->tu, 0, 3 * sizeof(double) * (size_t)t->n, st));
+  const int stack_depth = 8 * (t->depth_used + 2);
+  const unsigned grid = (unsigned)trav_blocks(t->n);
+  {
+    ProfScope ps(WN_PROF_TRAV_AT, st, 2);
+    scatter_kernel<<<grid, kTravBlock, (size_t)(kTravBlock / 32) * stack_depth * sizeof(int2), st>>>(
+        geo.R, geo.A, t->pts, t->pb, t->pe, s_sorted, t->n, w2, stack_depth, t->tvb, t->tu);
+    pushdown_kernel<<<grid, kTravBlock, 0, st>>>(t->n, t->leaf_of, t->parent, t->tvb, t->tu, 1.0f, r_out, partial);
+  }
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
+}  // namespace wn

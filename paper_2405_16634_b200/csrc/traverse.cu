@@ -1,0 +1,235 @@
+// traverse.cu — warp-cooperative treecode traversal.
+//
+// Algorithm 4 apply_A, per query x_i and node B:
+//     if |x_i − x_B| > c·width(B):  representative term            ("modified by w")
+//     elif B is not a leaf:         recurse into the children
+//     else:                         direct sum over the points of B  ("modified by w")
+// "Other operators Aᵀ and G are accelerated in the same way" (L406).  Terms (d = x_src − x_i):
+//     A  : ∇Φ(x_i − x_src)·ν      =  (d·ν) / (4π r³)                 (Eq wnf-discretization)
+//     Aᵀ : s ∇Φ(x_src − x_i)      = −s d / (4π r³)                   (Alg. 2; ν = s, L371)
+//     G  : −HΦ(x_i − x_src) ν     = (ν − 3 (d·ν) d / r²) / (4π r³)   (L264-L272)
+// and every term is 0 when r < w (§4.4).
+//
+// B200 design:
+//   * one warp = 32 consecutive Morton-sorted queries; a per-warp shared-memory stack of
+//     (child group, lane mask) entries; every lane takes ITS OWN opening decision (exact per-query
+//     semantics of Alg. 4 — no "open if any lane opens"), the ballot of lanes that open becomes the
+//     mask of the pushed child group;
+//   * node records are broadcast loads (all lanes read the same 2×16 B), L1/L2 resident;
+//   * one-point nodes carry thr = −1 so they always take the representative branch, which equals the
+//     leaf branch exactly (rep = the point, ν_B = ν_j): no leaf loop, no divergence for them;
+//   * the decision and the cutoff are fp32 with the operation sequence d = a − b,
+//     d² = fma(dx,dx, fma(dy,dy, dz·dz)) (DESIGN.md R-prec); A accumulates per child group in fp32
+//     and across groups in fp64 (s = ½ − Aμ cancels near convergence);
+//   * epilogues fuse the solver's elementwise work (s = ½ − Aμ, Σ partials, rescale).
+#include <cuda_runtime.h>
+
+#include "wn_internal.cuh"
+
+namespace wn {
+namespace {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+__device__ __forceinline__ float dist2(float dx, float dy, float dz) {
+  return __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+}
+
+template <int OP>
+struct Acc {
+  float x = 0.f, y = 0.f, z = 0.f;
+  double d = 0.0;
+  __device__ __forceinline__ void term(float dx, float dy, float dz, float d2, const float4& V) {
+    const float inv = rsqrtf(d2);
+    if (OP == OP_A) {
+      const float inv3 = inv * inv * inv;
+      x = fmaf(fmaf(dx, V.x, fmaf(dy, V.y, dz * V.z)), inv3, x);
+    } else if (OP == OP_AT) {
+      const float c = -V.x * (inv * inv * inv);
+      x = fmaf(c, dx, x);
+      y = fmaf(c, dy, y);
+      z = fmaf(c, dz, z);
+    } else {
+      const float inv2 = inv * inv;
+      const float inv3 = inv2 * inv;
+      const float t = 3.0f * fmaf(dx, V.x, fmaf(dy, V.y, dz * V.z)) * inv2;
+      x = fmaf(inv3, fmaf(-t, dx, V.x), x);
+      y = fmaf(inv3, fmaf(-t, dy, V.y), y);
+      z = fmaf(inv3, fmaf(-t, dz, V.z), z);
+    }
+  }
+  __device__ __forceinline__ void flush() {
+    if (OP == OP_A) {
+      d += (double)x;
+      x = 0.f;
+    }
+  }
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+template <int OP, int EPI, bool COUNT>
+__global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
+  extern __shared__ int2 stk_all[];
+  __shared__ double red[kTravBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int2* stk = stk_all + warp * a.stack_depth;
+  const int64_t q = a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
+  const bool valid = q < a.q_end;
+  const float4 xq = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t active = __ballot_sync(FULL, valid);
+  const float4* __restrict__ NR = a.nodes.R;
+  const float4* __restrict__ NA = a.attrA ? a.attrA : a.nodes.A;
+  const float w2 = a.w2;
+  Acc<OP> acc;
+  int ntest = 0, nfar = 0, nnear = 0;
+  if (active) {
+    int sp = 0;
+    if (lane == 0) stk[0] = make_int2(0, (int)active);  // the root as a group of one: (0 << 4) | 0
+    sp = 1;
+    __syncwarp();
+    while (sp > 0) {
+      --sp;
+      const int2 e = stk[sp];
+      __syncwarp();
+      const int cb = e.x >> 4, ncc = (e.x & 7) + 1;
+      const bool mine = ((uint32_t)e.y >> lane) & 1u;
+      for (int k = 0; k < ncc; ++k) {
+        const int node = cb + k;
+        const float4 R = __ldg(NR + node);
+        const float4 V = __ldg(NA + node);
+        const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
+        const float d2 = dist2(dx, dy, dz);
+        const bool far = d2 > R.w;
+        if (mine && far) {
+          if (!(d2 < w2)) acc.term(dx, dy, dz, d2, V);
+        }
+        if (COUNT && mine) {
+          ++ntest;
+          nfar += far && !(d2 < w2);
+        }
+        const uint32_t open = __ballot_sync(FULL, mine && !far);
+        if (open) {
+          const int topo = __float_as_int(V.w);
+          if (!(topo & 8)) {
+            if (lane == 0) stk[sp] = make_int2(topo, (int)open);
+            ++sp;
+          } else {  // multi-point leaf (depth D): direct sum for the lanes that opened it
+            const bool lm = (open >> lane) & 1u;
+            const int j1 = a.nrange_pe[node];
+            for (int j = a.nrange_pb[node]; j < j1; ++j) {
+              const float4 P = __ldg(a.pts + j);
+              float4 Vj;
+              if (OP == OP_AT) Vj = make_float4(__ldg(a.scal + j), 0.f, 0.f, 0.f);
+              else Vj = __ldg(a.vec + j);
+              const float ex = __fsub_rn(P.x, xq.x), ey = __fsub_rn(P.y, xq.y), ez = __fsub_rn(P.z, xq.z);
+              const float e2 = dist2(ex, ey, ez);
+              if (lm && !(e2 < w2)) acc.term(ex, ey, ez, e2, Vj);
+              if (COUNT && lm) nnear += !(e2 < w2);
+            }
+          }
+        }
+      }
+      acc.flush();
+      __syncwarp();
+    }
+  }
+  // ---------------- epilogue ----------------
+  double part = 0.0;
+  if (valid) {
+    const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
+    if (OP == OP_A) {
+      const double val = acc.d * 0.0795774715459476679;  // Σ / (4π)
+      if (EPI == EPI_PLAIN) a.out_f[oq] = (float)(val * (double)a.scale_out);
+      if (EPI == EPI_S) {
+        const double sv = 0.5 - val;
+        a.out_f[q] = (float)sv;
+        part = sv * sv;
+      }
+      if (EPI == EPI_SQ) part = val * val;
+    } else {
+      const float vx = acc.x * kInv4Pi, vy = acc.y * kInv4Pi, vz = acc.z * kInv4Pi;
+      if (EPI == EPI_PLAIN) {
+        a.out_v3[3 * oq + 0] = vx * a.scale_out;
+        a.out_v3[3 * oq + 1] = vy * a.scale_out;
+        a.out_v3[3 * oq + 2] = vz * a.scale_out;
+      }
+      if (EPI == EPI_R) {
+        a.out_v4[q] = make_float4(vx, vy, vz, 0.f);
+        part = (double)vx * vx + (double)vy * vy + (double)vz * vz;
+      }
+      if (EPI == EPI_RESCALE) {
+        const float4 m = a.mup[q];
+        const double hm = sqrt((double)vx * vx + (double)vy * vy + (double)vz * vz);
+        const double mm = sqrt((double)m.x * m.x + (double)m.y * m.y + (double)m.z * m.z);
+        float4 o = m;
+        if (hm > 0.0) {
+          const double f = mm / hm;
+          o = make_float4((float)(vx * f), (float)(vy * f), (float)(vz * f), 0.f);
+        }
+        a.out_v4[q] = o;
+      }
+    }
+  }
+  if (COUNT) {  // algorithmic work of this launch: node tests, representative terms, leaf-point terms
+    unsigned long long c0 = ntest, c1 = nfar, c2 = nnear;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      c0 += __shfl_xor_sync(FULL, c0, o);
+      c1 += __shfl_xor_sync(FULL, c1, o);
+      c2 += __shfl_xor_sync(FULL, c2, o);
+    }
+    if (lane == 0) {
+      atomicAdd((unsigned long long*)a.work + 0, c0);
+      atomicAdd((unsigned long long*)a.work + 1, c1);
+      atomicAdd((unsigned long long*)a.work + 2, c2);
+    }
+  }
+  if (EPI == EPI_S || EPI == EPI_SQ || EPI == EPI_R) {
+    part = warp_sum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int k = 0; k < kTravBlock / 32; ++k) b += red[k];
+      a.partial[(a.q_begin / kTravBlock) + blockIdx.x] = b;
+    }
+  }
+}
+
+template <int OP, int EPI>
+void launch(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
+  if (a.work) trav_kernel<OP, EPI, true><<<grid, kTravBlock, smem, s>>>(a);
+  else trav_kernel<OP, EPI, false><<<grid, kTravBlock, smem, s>>>(a);
+}
+
+}  // namespace
+
+wn_status traverse(const TravArgs& a, cudaStream_t s) {
+  const int64_t nq = a.q_end - a.q_begin;
+  if (nq <= 0) return WN_OK;
+  const unsigned grid = (unsigned)trav_blocks(nq);
+  const size_t smem = (size_t)(kTravBlock / 32) * a.stack_depth * sizeof(int2);
+  const int cls = a.op == OP_A ? WN_PROF_TRAV_A : a.op == OP_AT ? WN_PROF_TRAV_AT : WN_PROF_TRAV_G;
+  ProfScope ps(cls, s);
+  TravArgs b = a;
+  b.work = work_counters(cls);
+  switch (a.op * 8 + a.epi) {
+    case OP_A * 8 + EPI_PLAIN: launch<OP_A, EPI_PLAIN>(b, s, grid, smem); break;
+    case OP_A * 8 + EPI_S: launch<OP_A, EPI_S>(b, s, grid, smem); break;
+    case OP_A * 8 + EPI_SQ: launch<OP_A, EPI_SQ>(b, s, grid, smem); break;
+    case OP_AT * 8 + EPI_PLAIN: launch<OP_AT, EPI_PLAIN>(b, s, grid, smem); break;
+    case OP_AT * 8 + EPI_R: launch<OP_AT, EPI_R>(b, s, grid, smem); break;
+    case OP_G * 8 + EPI_PLAIN: launch<OP_G, EPI_PLAIN>(b, s, grid, smem); break;
+    case OP_G * 8 + EPI_RESCALE: launch<OP_G, EPI_RESCALE>(b, s, grid, smem); break;
+    default: return set_error(WN_ERR_ARG, "internal: unsupported traversal variant");
+  }
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
+}  // namespace wn

@@ -1,0 +1,497 @@
+// tree_build.cu — octree construction on the device.
+//
+// PAPER.md:L370 (§4.5): "we first build an octree T to spatially partition the input point set.
+// The partitioning stops if the node contains only one point or if the user-specified maximum depth
+// D is reached."  PAPER.md:L419 (§5.1.1): points are "normalized to fit into the cube [−1,1]^3 with
+// a margin of 1/11".  Readings: root cell = [−1,1]^3, bbox-centred uniform scale with the
+// longest half-extent at 10/11, children in ascending octant digit 4·x + 2·y + z, a coordinate on a
+// split plane goes to the upper octant.
+//
+// B200 design: instead of the recursive partition the paper implies, the tree is emitted from sorted
+// Morton keys.  For sorted keys k_0 ≤ … ≤ k_{N−1} let lcp(k) be the number of leading octal digits
+// shared by keys k−1 and k (lcp(0) = lcp(N) = −1).  A node at level ℓ is a run of points sharing ℓ
+// digits whose parent run holds ≥ 2 points; point k starts exactly the nodes of levels
+//     lo_k = lcp(k) + 1  …  hi_k = min(D, max(lcp(k) + 1, lcp(k+1) + 1))
+// and node (ℓ, k) is internal iff ℓ < hi_k (its first child is (ℓ+1, k)).  BFS order = (level, k).
+// Kernels: bbox → normalize + keys → stable LSD radix sort (8-bit digits, match_any ranking) →
+// gather → per-tile level counts → one flat scan → emission → parent / child-count → per-level pe.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "wn_internal.cuh"
+
+namespace wn {
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 8;                    // per thread → 2048 keys per tile
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kEmitThreads = 256;                // points per emission tile
+
+struct BBox {
+  float lo[3], hi[3];
+  int nonfinite;
+  int pad;
+  double xf[4];
+};
+
+__global__ void bbox_partial(const float* __restrict__ p, int64_t n, float* __restrict__ part, int* bad) {
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  int nf = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float v = p[3 * i + a];
+      if (!isfinite(v)) nf = 1;
+      lo[a] = fminf(lo[a], v);
+      hi[a] = fmaxf(hi[a], v);
+    }
+  }
+  __shared__ float slo[3][32], shi[3][32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o; o >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+    if (lane == 0) { slo[a][w] = lo[a]; shi[a][w] = hi[a]; }
+  }
+  if (__any_sync(0xffffffffu, nf) && lane == 0) atomicOr(bad, 1);
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    int a = threadIdx.x;
+    float l = INFINITY, h = -INFINITY;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { l = fminf(l, slo[a][k]); h = fmaxf(h, shi[a][k]); }
+    part[6 * blockIdx.x + a] = l;
+    part[6 * blockIdx.x + 3 + a] = h;
+  }
+}
+
+// xf = (c, scale): c = (lo + hi)/2, half = max_a (hi − lo)/2, scale = (10/11)/half  (fp64)
+__global__ void bbox_final(const float* __restrict__ part, int nb, const int* bad, BBox* out) {
+  if (threadIdx.x != 0) return;
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int b = 0; b < nb; ++b)
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = fminf(lo[a], part[6 * b + a]);
+      hi[a] = fmaxf(hi[a], part[6 * b + 3 + a]);
+    }
+  double half = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    out->lo[a] = lo[a];
+    out->hi[a] = hi[a];
+    out->xf[a] = ((double)lo[a] + (double)hi[a]) * 0.5;
+    double h = ((double)hi[a] - (double)lo[a]) * 0.5;
+    if (h > half) half = h;
+  }
+  out->xf[3] = half > 0.0 ? (10.0 / 11.0) / half : 0.0;
+  out->nonfinite = *bad;
+}
+
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {  // 21 bits → every third bit
+  uint64_t x = v & 0x1fffffu;
+  x = (x | (x << 32)) & 0x1f00000000ffffull;
+  x = (x | (x << 16)) & 0x1f0000ff0000ffull;
+  x = (x | (x << 8)) & 0x100f00f00f00f00full;
+  x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+  x = (x | (x << 2)) & 0x1249249249249249ull;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t quantize(float xn, int D) {
+  double v = floor(((double)xn + 1.0) * ldexp(1.0, D - 1));
+  double qmax = (double)((1u << D) - 1u);
+  v = fmin(fmax(v, 0.0), qmax);
+  return (uint32_t)v;
+}
+
+__global__ void normalize_keys(const float* __restrict__ p, int64_t n, const BBox* bb, int D,
+                               float4* __restrict__ xn, uint64_t* __restrict__ keys, int32_t* __restrict__ idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double c0 = bb->xf[0], c1 = bb->xf[1], c2 = bb->xf[2], sc = bb->xf[3];
+  float x = (float)(__dsub_rn((double)p[3 * i + 0], c0) * sc);
+  float y = (float)(__dsub_rn((double)p[3 * i + 1], c1) * sc);
+  float z = (float)(__dsub_rn((double)p[3 * i + 2], c2) * sc);
+  xn[i] = make_float4(x, y, z, 0.f);
+  uint32_t qx = quantize(x, D), qy = quantize(y, D), qz = quantize(z, D);
+  keys[i] = (spread3(qx) << 2) | (spread3(qy) << 1) | spread3(qz);
+  idx[i] = (int32_t)i;
+}
+
+// ---- stable LSD radix sort of (key, idx) ------------------------------------------------------
+__global__ void radix_hist(const uint64_t* __restrict__ keys, int64_t n, int shift, int ntiles,
+                           uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * kSortTile;
+  for (int k = 0; k < kSortItems; ++k) {
+    int64_t i = base + k * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void radix_scatter(const uint64_t* __restrict__ kin, const int32_t* __restrict__ vin,
+                              uint64_t* __restrict__ kout, int32_t* __restrict__ vout, int64_t n, int shift,
+                              int ntiles, const uint32_t* __restrict__ offs) {
+  constexpr int W = kSortThreads / 32;
+  __shared__ uint32_t wcnt[W][256];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int d = threadIdx.x; d < W * 256; d += kSortThreads) (&wcnt[0][0])[d] = 0;
+  __syncthreads();
+  // each warp owns a contiguous chunk of kSortItems*32 keys of the tile → tile order preserved
+  int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)w * (kSortItems * 32);
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int r = 0; r < kSortItems; ++r) {
+    int64_t i = base + r * 32 + lane;
+    uint32_t d = i < n ? (uint32_t)((kin[i] >> shift) & 255u) : 256u;
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (d < 256u && lane == __ffs(peers) - 1) wcnt[w][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    int d = threadIdx.x;  // 256 threads ↔ 256 digits
+    uint32_t run = offs[(int64_t)d * ntiles + blockIdx.x];
+    for (int k = 0; k < W; ++k) {
+      uint32_t c = wcnt[k][d];
+      wcnt[k][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < kSortItems; ++r) {
+    int64_t i = base + r * 32 + lane;
+    uint64_t key = i < n ? kin[i] : 0;
+    uint32_t d = i < n ? (uint32_t)((key >> shift) & 255u) : 256u;
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    uint32_t pos = 0;
+    if (d < 256u) pos = wcnt[w][d] + __popc(peers & lt);
+    __syncwarp();
+    if (d < 256u) {
+      kout[pos] = key;
+      vout[pos] = vin[i];
+      if (lane == __ffs(peers) - 1) wcnt[w][d] += __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+// exclusive scan of m uint32 with one block of 1024 threads; total → *total
+__global__ void scan_excl_1block(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t m,
+                                 uint32_t* total) {
+  __shared__ uint32_t sh[1024];
+  int64_t chunk = (m + 1023) / 1024;
+  int64_t b = threadIdx.x * chunk, e = min(b + chunk, m);
+  uint32_t sum = 0;
+  for (int64_t i = b; i < e; ++i) sum += in[i];
+  sh[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    uint32_t v = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = sh[threadIdx.x] - sum;
+  for (int64_t i = b; i < e; ++i) {
+    uint32_t v = in[i];
+    out[i] = run;
+    run += v;
+  }
+  if (threadIdx.x == 1023 && total) *total = sh[1023];
+}
+
+__global__ void gather_sorted(const float4* __restrict__ xn, const int32_t* __restrict__ idx, int64_t n,
+                              float4* __restrict__ pts, int32_t* __restrict__ perm) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int32_t j = idx[k];
+  pts[k] = xn[j];
+  perm[k] = j;
+}
+
+__device__ __forceinline__ int common_digits(uint64_t a, uint64_t b, int D) {
+  if (a == b) return D;
+  return (__clzll((long long)(a ^ b)) - (64 - 3 * D)) / 3;
+}
+
+// levels started by point k: [lo, hi] (lo > hi ⇒ none)
+__device__ __forceinline__ void level_range(const uint64_t* keys, int64_t n, int D, int64_t k, int& lo, int& hi) {
+  int l0 = k == 0 ? -1 : common_digits(keys[k - 1], keys[k], D);
+  int l1 = k + 1 >= n ? -1 : common_digits(keys[k], keys[k + 1], D);
+  lo = l0 + 1;
+  hi = min(D, max(l0 + 1, l1 + 1));
+}
+
+__global__ void level_counts(const uint64_t* __restrict__ keys, int64_t n, int D, int ntiles,
+                             uint32_t* __restrict__ cnt) {
+  __shared__ uint32_t c[kMaxDepth + 1];
+  if (threadIdx.x <= D) c[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t k = blockIdx.x * (int64_t)kEmitThreads + threadIdx.x;
+  int lo = 1, hi = 0;
+  if (k < n) level_range(keys, n, D, k, lo, hi);
+  int lane = threadIdx.x & 31;
+  for (int l = 0; l <= D; ++l) {
+    uint32_t b = __ballot_sync(0xffffffffu, lo <= l && l <= hi);
+    if (lane == 0 && b) atomicAdd(&c[l], __popc(b));
+  }
+  __syncthreads();
+  if (threadIdx.x <= D) cnt[(int64_t)threadIdx.x * ntiles + blockIdx.x] = c[threadIdx.x];
+}
+
+__global__ void emit_nodes(const uint64_t* __restrict__ keys, int64_t n, int D, int ntiles,
+                           const uint32_t* __restrict__ offs, int32_t* __restrict__ depth, int32_t* __restrict__ pb,
+                           int32_t* __restrict__ cb, int32_t* __restrict__ cc, int32_t* __restrict__ parent) {
+  constexpr int W = kEmitThreads / 32;
+  __shared__ uint32_t wtot[W][kMaxDepth + 1];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t k = blockIdx.x * (int64_t)kEmitThreads + threadIdx.x;
+  int lo = 1, hi = 0;
+  if (k < n) level_range(keys, n, D, k, lo, hi);
+  for (int l = 0; l <= D; ++l) {
+    uint32_t b = __ballot_sync(0xffffffffu, lo <= l && l <= hi);
+    if (lane == 0) wtot[w][l] = __popc(b);
+  }
+  __syncthreads();
+  if (threadIdx.x <= D) {  // exclusive scan over warps, per level
+    uint32_t run = 0;
+    for (int q = 0; q < W; ++q) {
+      uint32_t v = wtot[q][threadIdx.x];
+      wtot[q][threadIdx.x] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+  int32_t prev = -1;
+  for (int l = 0; l <= D; ++l) {
+    bool f = lo <= l && l <= hi;
+    uint32_t b = __ballot_sync(0xffffffffu, f);
+    if (!f) continue;
+    int32_t idx = (int32_t)(offs[(int64_t)l * ntiles + blockIdx.x] + wtot[w][l] + __popc(b & lt));
+    depth[idx] = l;
+    pb[idx] = (int32_t)k;
+    if (l < hi) {          // internal: first child is (l+1, k), count filled by child_counts
+      cc[idx] = 0;
+    } else {               // leaf
+      cb[idx] = -1;
+      cc[idx] = 0;
+    }
+    if (l > lo) {
+      parent[idx] = prev;
+      cb[prev] = idx;
+    } else {
+      parent[idx] = l == 0 ? -1 : -2;   // −2: parent starts at an earlier point → binary search
+    }
+    prev = idx;
+  }
+}
+
+__global__ void find_parents(int64_t nn, const int32_t* __restrict__ depth, const int32_t* __restrict__ pb,
+                             const int64_t* __restrict__ loff, int32_t* __restrict__ parent) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn || parent[i] != -2) return;
+  int l = depth[i];
+  int32_t key = pb[i];
+  int64_t a = loff[l - 1], b = loff[l] - 1;   // largest j in [a, b] with pb[j] ≤ key
+  while (a < b) {
+    int64_t m = (a + b + 1) >> 1;
+    if (pb[m] <= key) a = m; else b = m - 1;
+  }
+  parent[i] = (int32_t)a;
+}
+
+__global__ void child_counts(int64_t nn, const int32_t* __restrict__ depth, const int32_t* __restrict__ parent,
+                             const int64_t* __restrict__ loff, const int32_t* __restrict__ cb,
+                             int32_t* __restrict__ cc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < 1 || i >= nn) return;
+  int32_t p = parent[i];
+  bool last = (i + 1 == loff[depth[i] + 1]) || parent[i + 1] != p;
+  if (last) cc[p] = (int32_t)(i - cb[p] + 1);
+}
+
+__global__ void level_pe(int64_t i0, int64_t i1, int64_t n, const int32_t* __restrict__ parent,
+                         const int32_t* __restrict__ pb, int32_t* __restrict__ pe) {
+  int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= i1) return;
+  int32_t p = parent[i];
+  if (p < 0) { pe[i] = (int32_t)n; return; }
+  bool last = (i + 1 == i1) || parent[i + 1] != p;
+  pe[i] = last ? pe[p] : pb[i + 1];
+}
+
+template <typename T>
+wn_status dalloc(T** p, size_t count, cudaStream_t s) {
+  cudaError_t e = cudaMallocAsync((void**)p, std::max<size_t>(count, 1) * sizeof(T), s);
+  if (e == cudaErrorMemoryAllocation) return set_error(WN_ERR_OOM, "device allocation failed");
+  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync");
+  return WN_OK;
+}
+
+}  // namespace
+
+#define WN_TRY(x)                       \
+  do {                                  \
+    wn_status st_ = (x);                \
+    if (st_ != WN_OK) return st_;       \
+  } while (0)
+
+wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree_s* t) {
+  t->n = n;
+  t->D = D;
+  // --- bbox + transform (a1) ---
+  int nb = (int)std::min<int64_t>((n + 255) / 256, 1184);
+  float* part = nullptr;
+  int* bad = nullptr;
+  BBox* bb = nullptr;
+  WN_TRY(dalloc(&part, 6 * (size_t)nb, s));
+  WN_TRY(dalloc(&bad, 1, s));
+  WN_TRY(dalloc(&bb, 1, s));
+  WN_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  {
+    ProfScope ps(WN_PROF_TREE, s, 2);
+    bbox_partial<<<nb, 256, 0, s>>>(pts, n, part, bad);
+    bbox_final<<<1, 32, 0, s>>>(part, nb, bad, bb);
+  }
+  BBox hb;
+  WN_CUDA(cudaMemcpyAsync(&hb, bb, sizeof(BBox), cudaMemcpyDeviceToHost, s));
+  WN_CUDA(cudaStreamSynchronize(s));
+  if (hb.nonfinite) {
+    cudaFreeAsync(part, s); cudaFreeAsync(bad, s); cudaFreeAsync(bb, s);
+    return set_error(WN_ERR_NONFINITE, "non-finite point coordinate");
+  }
+  if (!(hb.xf[3] > 0.0)) {
+    cudaFreeAsync(part, s); cudaFreeAsync(bad, s); cudaFreeAsync(bb, s);
+    return set_error(WN_ERR_DEGENERATE, "all points coincide (zero extent)");
+  }
+  for (int a = 0; a < 4; ++a) t->xf[a] = hb.xf[a];
+
+  // --- normalize, keys, sort (a1) ---
+  float4* xn = nullptr;
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  int32_t *v0 = nullptr, *v1 = nullptr;
+  WN_TRY(dalloc(&xn, n, s));
+  WN_TRY(dalloc(&k0, n, s));
+  WN_TRY(dalloc(&k1, n, s));
+  WN_TRY(dalloc(&v0, n, s));
+  WN_TRY(dalloc(&v1, n, s));
+  int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+  uint32_t* hist = nullptr;
+  WN_TRY(dalloc(&hist, (size_t)256 * ntiles, s));
+  int passes = (3 * D + 7) / 8;
+  {
+    ProfScope ps(WN_PROF_TREE, s, 1 + 3 * passes + 1);
+    normalize_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pts, n, bb, D, xn, k0, v0);
+    for (int p = 0; p < passes; ++p) {
+      radix_hist<<<ntiles, kSortThreads, 0, s>>>(k0, n, 8 * p, ntiles, hist);
+      scan_excl_1block<<<1, 1024, 0, s>>>(hist, hist, (int64_t)256 * ntiles, nullptr);
+      radix_scatter<<<ntiles, kSortThreads, 0, s>>>(k0, v0, k1, v1, n, 8 * p, ntiles, hist);
+      std::swap(k0, k1);
+      std::swap(v0, v1);
+    }
+    WN_TRY(dalloc(&t->pts, n, s));
+    WN_TRY(dalloc(&t->perm, n, s));
+    gather_sorted<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(xn, v0, n, t->pts, t->perm);
+  }
+  t->keys = k0;
+  cudaFreeAsync(k1, s);
+  cudaFreeAsync(v0, s);
+  cudaFreeAsync(v1, s);
+  cudaFreeAsync(xn, s);
+  cudaFreeAsync(hist, s);
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(bad, s);
+  cudaFreeAsync(bb, s);
+
+  // --- node counts per level (a2) ---
+  int etiles = (int)((n + kEmitThreads - 1) / kEmitThreads);
+  int64_t m = (int64_t)(D + 1) * etiles;
+  uint32_t *cnt = nullptr, *offs = nullptr;
+  WN_TRY(dalloc(&cnt, m + 1, s));
+  WN_TRY(dalloc(&offs, m + 1, s));
+  {
+    ProfScope ps(WN_PROF_TREE, s, 2);
+    level_counts<<<etiles, kEmitThreads, 0, s>>>(t->keys, n, D, etiles, cnt);
+    scan_excl_1block<<<1, 1024, 0, s>>>(cnt, offs, m, offs + m);
+  }
+  std::vector<uint32_t> hoffs(m + 1);
+  WN_CUDA(cudaMemcpyAsync(hoffs.data(), offs, (m + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  WN_CUDA(cudaStreamSynchronize(s));
+  t->nn = hoffs[m];
+  t->level_off.assign(D + 2, t->nn);
+  int used = 0;
+  for (int l = 0; l <= D; ++l) {
+    t->level_off[l] = hoffs[(int64_t)l * etiles];
+    if (t->level_off[l] < t->nn) used = l;
+  }
+  t->depth_used = used;
+  t->level_off.resize(used + 2);
+  t->level_off[used + 1] = t->nn;
+  int64_t nn = t->nn;
+
+  // --- emission ---
+  WN_TRY(dalloc(&t->depth, nn, s));
+  WN_TRY(dalloc(&t->pb, nn, s));
+  WN_TRY(dalloc(&t->pe, nn, s));
+  WN_TRY(dalloc(&t->cb, nn, s));
+  WN_TRY(dalloc(&t->cc, nn, s));
+  WN_TRY(dalloc(&t->parent, nn, s));
+  WN_TRY(dalloc(&t->arrive, nn, s));
+  WN_TRY(dalloc(&t->centroid, nn, s));
+  WN_TRY(dalloc(&t->leaf_of, n, s));
+  WN_TRY(dalloc(&t->sums, 8 * (size_t)nn, s));
+  for (int k = 0; k < 2; ++k) {
+    WN_TRY(dalloc(&t->set[k].R, nn, s));
+    WN_TRY(dalloc(&t->set[k].A, nn, s));
+  }
+  int64_t* loff = nullptr;
+  WN_TRY(dalloc(&loff, t->level_off.size(), s));
+  WN_CUDA(cudaMemcpyAsync(loff, t->level_off.data(), t->level_off.size() * sizeof(int64_t),
+                          cudaMemcpyHostToDevice, s));
+  WN_CUDA(cudaMemsetAsync(t->arrive, 0, nn * sizeof(int32_t), s));
+  {
+    unsigned g = (unsigned)((nn + 255) / 256);
+    ProfScope ps(WN_PROF_TREE, s, 3 + used + 1);
+    emit_nodes<<<etiles, kEmitThreads, 0, s>>>(t->keys, n, D, etiles, offs, t->depth, t->pb, t->cb, t->cc,
+                                                t->parent);
+    find_parents<<<g, 256, 0, s>>>(nn, t->depth, t->pb, loff, t->parent);
+    child_counts<<<g, 256, 0, s>>>(nn, t->depth, t->parent, loff, t->cb, t->cc);
+    for (int l = 0; l <= used; ++l) {
+      int64_t i0 = t->level_off[l], i1 = t->level_off[l + 1];
+      level_pe<<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, s>>>(i0, i1, n, t->parent, t->pb, t->pe);
+    }
+  }
+  cudaFreeAsync(loff, s);
+  cudaFreeAsync(cnt, s);
+  cudaFreeAsync(offs, s);
+  WN_CUDA(cudaGetLastError());
+
+  // --- fixed node data: unweighted centroids (unit weights) ---
+  MomentArgs ma;
+  ma.kind = ATTR_UNIT;
+  ma.out = t->set[1];
+  ma.centroid_out = t->centroid;
+  ma.leaf_of_out = t->leaf_of;
+  WN_TRY(build_moments(t, ma, s));
+  return WN_OK;
+}
+
+void free_tree(wn_tree_s* t) {
+  void* ptrs[] = {t->pts, t->perm, t->keys, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
+                  t->arrive, t->centroid, t->sums, t->set[0].R, t->set[0].A, t->set[1].R, t->set[1].A,
+                  t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
+                  t->qbuf, t->tvb, t->tu};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
+
+}  // namespace wn

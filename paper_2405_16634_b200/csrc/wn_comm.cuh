@@ -1,0 +1,15 @@
+// wn_comm.cuh — query-sharded multi-GPU plumbing; NCCL is loaded at run time.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/wn.h"
+
+namespace wn {
+wn_status comm_shard(wn_comm c, int64_t n, int64_t* q0, int64_t* q1);
+// Every rank owns rows [q0, q1) of a sorted-order array of n rows × comps floats; make it whole on all ranks.
+wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, cudaStream_t s);
+// The three per-block partial arrays (stride entries each, blocks of WN_SHARD_ALIGN queries).
+wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64_t n, cudaStream_t s);
+}  // namespace wn

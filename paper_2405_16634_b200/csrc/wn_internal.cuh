@@ -1,0 +1,161 @@
+// wn_internal.cuh — shared declarations of the libwn CUDA sources (sm_100a).
+// Not part of the ABI; see include/wn.h for the public contract.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/wn.h"
+
+namespace wn {
+
+constexpr int kMaxDepth = 21;
+constexpr float kInv4Pi = 0.0795774715459476679f;  // 1/(4π)
+
+// Kinds of attribute a moment build aggregates.
+enum AttrKind { ATTR_VEC = 0, ATTR_SCALAR = 1, ATTR_UNIT = 2 };
+
+// One moment build's output: what the traversal reads per node (BFS order).
+//   R = (x_B, y_B, z_B, thr)   thr = (c·edge)² in fp32, or −1 for a one-point node (always "far":
+//                               rep = the point, ν_B = ν_j, so far and leaf terms coincide)
+//   A = (ν_B.x, ν_B.y, ν_B.z, topo) for vector ν, (s_B, 0, 0, topo) for scalar ν
+//   topo (int bits) = internal: (child_begin << 4) | (child_count − 1);  leaf: 8
+struct NodeSet {
+  float4* R = nullptr;
+  float4* A = nullptr;
+};
+
+struct IterScratch {
+  int64_t n = 0;
+  float4* mu = nullptr;      // μ, normalized frame, sorted order
+  float4* mup = nullptr;     // μ' = μ + α r
+  float4* r = nullptr;       // r = Aᵀ s
+  float* s = nullptr;        // s = ½ − A μ
+  double* part = nullptr;    // per-block partials: [3][nblk] (Σs², Σ|r|², Σq²)
+  double* dstats = nullptr;  // per-iteration (E, α, rr, qq, w) — device
+  int64_t stats_cap = 0;
+  double* alpha = nullptr;   // current α (device)
+  float* tmp = nullptr;      // generic N×4 scratch
+  int nblk = 0;
+};
+
+}  // namespace wn
+
+struct wn_tree_s {
+  int64_t n = 0, nn = 0, nleaves = 0;
+  int D = 15, depth_used = 0;
+  double xf[4] = {0, 0, 0, 1};
+  int device = 0;
+  float4* pts = nullptr;        // N normalized points, Morton order (w unused)
+  int32_t* perm = nullptr;      // sorted position → caller index
+  uint64_t* keys = nullptr;     // sorted keys
+  int32_t* depth = nullptr;     // per node (BFS)
+  int32_t* pb = nullptr;
+  int32_t* pe = nullptr;
+  int32_t* cb = nullptr;        // first child (BFS), −1 for leaves
+  int32_t* cc = nullptr;        // child count
+  int32_t* parent = nullptr;    // −1 for the root
+  int32_t* leaf_of = nullptr;   // sorted point → its leaf node
+  int32_t* arrive = nullptr;    // bottom-up arrival counters (kept at 0 between builds)
+  float4* centroid = nullptr;   // unweighted centroid per node (Σ|ν| = 0 fallback)
+  double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
+  wn::NodeSet set[2];           // [0] = current attribute, [1] = frozen geometry (transpose mode)
+  std::vector<int64_t> level_off;  // host: BFS offset of each level, size depth_used + 2
+  wn::IterScratch it;
+  float4* qbuf = nullptr;       // normalized arbitrary queries
+  int64_t qcap = 0;
+  // transpose-mode accumulators
+  double* tvb = nullptr;        // node accumulators V_B (Nn×3, fp64)
+  double* tu = nullptr;         // point accumulators U_j (N×3, fp64)
+};
+
+namespace wn {
+
+// ---- error plumbing (capi.cu) ----
+wn_status set_error(wn_status st, const std::string& msg);
+wn_status cuda_status(cudaError_t e, const char* what);
+#define WN_CUDA(call)                                                      \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess) return ::wn::cuda_status(e_, #call);            \
+  } while (0)
+
+// ---- launch accounting / profiling (capi.cu) ----
+struct ProfScope {
+  ProfScope(int cls, cudaStream_t s, int nlaunch = 1);
+  ~ProfScope();
+  int cls;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+void count_launches(int n);
+int64_t* work_counters(int cls);  // device counters of a traversal class, or null when counting is off
+
+// ---- tree build (tree_build.cu) ----
+wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree_s* t);
+void free_tree(wn_tree_s* t);
+
+// ---- moments (moments.cu) ----
+// Build node records for attribute `kind` into `out`.  vec: float4 ν (sorted order), scal: float s.
+// a (optional, caller order) multiplies ν per point in fp64 before aggregation.
+// If axpy_r != nullptr: ν = vec + α·axpy_r (α read on device from *alpha) and ν is written to axpy_out.
+struct MomentArgs {
+  int kind = ATTR_VEC;
+  const float4* vec = nullptr;
+  const float* scal = nullptr;
+  const float* a_sorted = nullptr;  // per sorted point multiplier, or null
+  const float4* axpy_r = nullptr;
+  const double* alpha = nullptr;
+  float4* axpy_out = nullptr;
+  float theta = 2.0f;
+  NodeSet out;
+  float4* centroid_out = nullptr;   // ATTR_UNIT: writes the centroid table
+  int32_t* leaf_of_out = nullptr;   // ATTR_UNIT: writes the leaf node of every sorted point
+};
+wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s);
+
+// ---- traversal (traverse.cu) ----
+enum TravOp { OP_A = 0, OP_AT = 1, OP_G = 2 };
+enum Epi {
+  EPI_PLAIN = 0,     // out_f (A) or out_v (AT/G) = scale_out · Σ/(4π), G negated when `negate`
+  EPI_S = 1,         // s = ½ − Σ/(4π); partial Σ s²
+  EPI_SQ = 2,        // partial Σ (Σ/(4π))² only
+  EPI_R = 3,         // r = Σ/(4π); partial Σ|r|²
+  EPI_RESCALE = 4    // μ_out = μ̂ |μ'| / |μ̂| (μ̂ = Σ/(4π)); keep μ' if |μ̂| = 0
+};
+struct TravArgs {
+  int op = OP_A;
+  int epi = EPI_PLAIN;
+  NodeSet nodes;                 // decisions + representative positions + (by default) attributes
+  const float4* attrA = nullptr; // optional override of the far-term attributes (frozen geometry)
+  const float4* pts = nullptr;   // sorted sources
+  const float4* vec = nullptr;   // leaf-point vector attributes (sorted)
+  const float* scal = nullptr;   // leaf-point scalar attributes (sorted)
+  const int32_t* nrange_pb = nullptr;
+  const int32_t* nrange_pe = nullptr;
+  const float4* queries = nullptr;  // query points (normalized)
+  int64_t q_begin = 0, q_end = 0;   // query index range
+  const int32_t* out_map = nullptr; // output index = out_map[q] (perm) or q
+  float* out_f = nullptr;
+  float4* out_v4 = nullptr;         // float4 output (internal vectors)
+  float* out_v3 = nullptr;          // N×3 output (caller layout)
+  float scale_out = 1.0f;
+  const float4* mup = nullptr;      // EPI_RESCALE: μ'
+  double* partial = nullptr;        // per-block partials (indexed by global block of 256 queries)
+  float w2 = 0.0f;
+  int stack_depth = 128;
+  int64_t* work = nullptr;          // set by traverse(): counting variant accumulates (tests, far, leaf pts)
+};
+wn_status traverse(const TravArgs& a, cudaStream_t s);
+
+// ---- transpose-mode adjoint (transpose.cu) ----
+wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sorted, float w2,
+                            float4* r_out, double* partial, cudaStream_t st);
+
+// ---- small utility kernels (iterate.cu) ----
+constexpr int kTravBlock = 256;  // queries per block (8 warps)
+inline int trav_blocks(int64_t nq) { return (int)((nq + kTravBlock - 1) / kTravBlock); }
+
+}  // namespace wn

@@ -1,0 +1,290 @@
+"""GPU ↔ oracle parity through the C ABI (needs a B200).
+
+Protocol: structure and Morton order bit-exact; representatives ≤ 1e-6 relative;
+operators per query |gpu − oracle| ≤ 1e-4·max(|oracle_i|, 1e-3·rms(oracle)) — a query may exceed it only
+if the oracle flags an opening/cutoff decision within its tie band, and at most 1e-3 of the queries;
+40 iterations: orientation agreement with the oracle ≥ 99.9 %.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2405_16634_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+T5 = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table5.json")))
+W1, W2 = float(np.float32(0.002)), float(np.float32(0.016))
+
+
+@pytest.fixture(scope="module")
+def wn():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2405_16634_b200.wn as wn
+
+    return wn
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def _check_queries(gpu, ref, counters, tol=1e-4, name=""):
+    gpu = np.asarray(gpu, np.float64).reshape(len(ref), -1)
+    ref = np.asarray(ref, np.float64).reshape(len(ref), -1)
+    mag = np.linalg.norm(ref, axis=1)
+    err = np.linalg.norm(gpu - ref, axis=1)
+    rms = np.sqrt(np.mean(mag ** 2))
+    bad = err > tol * np.maximum(mag, 1e-3 * rms)
+    nb = int(bad.sum())
+    if nb:
+        ties = counters[bad, 3] if counters is not None else np.zeros(nb)
+        assert np.all(ties > 0), f"{name}: {nb} queries off without a tie, worst {np.max(err[bad] / np.maximum(mag[bad], 1e-3 * rms)):.3e}"
+        assert nb <= max(1, 1e-3 * len(ref)), f"{name}: {nb} tie queries off"
+    return nb
+
+
+CLOUDS = {
+    "sphere2k": lambda: synth.config("C1")["points"],
+    "torus50k": lambda: synth.config("C2")["points"],
+    "clustered": lambda: (np.random.default_rng(5).uniform(-1, 1, (60, 3))[np.random.default_rng(6).integers(0, 60, 3001)]
+                          + 1e-6 * np.random.default_rng(7).standard_normal((3001, 3))).astype(np.float32),
+    "dups": lambda: np.repeat(synth.sphere(700, seed=8)[0], 3, axis=0),
+    "tiny7": lambda: synth.sphere(7, seed=9)[0],
+}
+
+
+@pytest.mark.parametrize("name", list(CLOUDS))
+@pytest.mark.parametrize("D", [15, 5])
+def test_tree_bit_exact(wn, name, D):
+    p = CLOUDS[name]()
+    t = wn.wn_build_tree(_cuda(p), D)
+    e = {k: v.cpu().numpy() for k, v in wn.wn_tree_export(t).items()}
+    xn, xf = oracle.normalize(p)
+    np.testing.assert_array_equal(np.array(t.xform), xf)
+    ot = oracle.Tree(xn, D)
+    o = ot.export()
+    keys = oracle.keys(xn, D)
+    np.testing.assert_array_equal(e["perm"], o["perm"])
+    np.testing.assert_array_equal(e["keys"].view(np.uint64), keys[o["perm"]])
+    np.testing.assert_array_equal(e["xn"], xn[o["perm"]])
+    for k in ("depth", "pb", "pe", "child_begin", "child_count"):
+        np.testing.assert_array_equal(e[k], o[k], err_msg=k)
+    assert t.num_nodes == ot.num_nodes and t.depth_used == ot.max_depth
+
+
+def test_tree_errors(wn):
+    with pytest.raises(wn.WnError, match="EMPTY"):
+        wn.wn_build_tree(torch.zeros(0, 3, device="cuda"))
+    bad = torch.zeros(10, 3, device="cuda")
+    bad[3, 1] = float("nan")
+    with pytest.raises(wn.WnError, match="NONFINITE"):
+        wn.wn_build_tree(bad)
+    with pytest.raises(wn.WnError, match="DEGENERATE"):
+        wn.wn_build_tree(torch.ones(10, 3, device="cuda"))
+    with pytest.raises(wn.WnError, match="ARG"):
+        wn.wn_build_tree(torch.rand(10, 3, device="cuda"), 0)
+    t = wn.wn_build_tree(torch.rand(100, 3, device="cuda"))
+    mu = torch.rand(100, 3, device="cuda")
+    with pytest.raises(wn.WnError, match="ARG"):
+        wn.wn_eval(t, mu, 0.0)
+    with pytest.raises(wn.WnError, match="ARG"):
+        wn.wn_eval(t, mu, 0.01, theta=-1.0)
+    with pytest.raises(wn.WnError, match="ARG"):
+        wn.wn_eval_adjoint(t, torch.rand(100, device="cuda"), 0.01, mode=wn.WN_ADJ_TRANSPOSE)
+    with pytest.raises(wn.WnError, match="ARG"):
+        wn.wnnc_iterate(t, mu, w_min=0.02, w_max=0.01)
+
+
+@pytest.mark.parametrize("name", ["sphere2k", "torus50k", "dups"])
+def test_moments(wn, name):
+    p = CLOUDS[name]()
+    n = len(p)
+    rng = np.random.default_rng(11)
+    nu = rng.standard_normal((n, 3)).astype(np.float32)
+    nu[: n // 10] = 0
+    s = rng.standard_normal(n).astype(np.float32)
+    a = rng.uniform(0.5, 2, n).astype(np.float32)
+    t = wn.wn_build_tree(_cuda(p))
+    xn, _ = oracle.normalize(p)
+    ot = oracle.Tree(xn)
+    o = ot.export()
+    edge = 2.0 ** (1 - o["depth"].astype(np.float64))
+    for nu_in, a_in in ((nu, None), (nu, a), (s, None), (s, a)):
+        rep, attr, W = [x.cpu().numpy() for x in wn.wn_moments(t, _cuda(nu_in), None if a_in is None else _cuda(a_in))]
+        nu64 = nu_in.astype(np.float64) * (1 if a_in is None else a_in.astype(np.float64)[:, None] if nu_in.ndim == 2 else a_in.astype(np.float64))
+        orep, oattr, oW = ot.moments(nu64)
+        assert np.all(np.abs(rep - orep).max(1) <= 1e-6 * edge + 6e-8 * np.abs(orep).max(1)), "rep"
+        sc = np.abs(oattr).reshape(len(oattr), -1).max(1)
+        scale = np.maximum(sc, 1e-6 * np.abs(oattr).max())
+        assert np.all(np.abs(attr.reshape(len(oattr), -1) - oattr.reshape(len(oattr), -1)).max(1) <= 1e-6 * scale + 1e-30)
+        np.testing.assert_allclose(W, oW, rtol=1e-12, atol=1e-300)
+
+
+OPS = [("F", 0.016), ("gradF", 0.002), ("AT", 0.009)]
+
+
+@pytest.mark.parametrize("name", ["sphere2k", "torus50k", "clustered"])
+@pytest.mark.parametrize("op,w", OPS)
+@pytest.mark.parametrize("theta", [2.0, 1.0])
+def test_operators_at_sources(wn, name, op, w, theta):
+    p = CLOUDS[name]()
+    n = len(p)
+    rng = np.random.default_rng(12)
+    mu = rng.standard_normal((n, 3)).astype(np.float32) * np.float32(4 * np.pi / n)
+    a = rng.uniform(0.5, 2, n).astype(np.float32)
+    s = (0.5 - rng.uniform(0, 1, n)).astype(np.float32)
+    w = float(np.float32(w))
+    t = wn.wn_build_tree(_cuda(p))
+    cl = oracle.Cloud(p)
+    if op == "F":
+        g = wn.wn_eval(t, _cuda(mu), w, theta, a=_cuda(a)).cpu().numpy()
+        ref, cnt = cl.F(mu, w, theta, a=a, counters=True)
+    elif op == "gradF":
+        g = wn.wn_eval_grad(t, _cuda(mu), w, theta).cpu().numpy()
+        ref, cnt = cl.gradF(mu, w, theta, counters=True)
+    else:
+        g = wn.wn_eval_adjoint(t, _cuda(s), w, theta).cpu().numpy()
+        ref, cnt = cl.AT(s, w, theta, counters=True)
+    _check_queries(g, ref, cnt, name=f"{name}/{op}")
+
+
+def test_operators_exact_sum(wn):
+    # θ = +inf: Alg. 4 never takes a representative → the dense O(N²) definition
+    p = CLOUDS["sphere2k"]()
+    rng = np.random.default_rng(13)
+    mu = rng.standard_normal((2000, 3)).astype(np.float32)
+    s = rng.standard_normal(2000).astype(np.float32)
+    t = wn.wn_build_tree(_cuda(p))
+    cl = oracle.Cloud(p)
+    w = float(np.float32(0.004))
+    _check_queries(wn.wn_eval(t, _cuda(mu), w, float("inf")).cpu().numpy(), cl.F(mu, w, dense=True), None)
+    _check_queries(wn.wn_eval_grad(t, _cuda(mu), w, float("inf")).cpu().numpy(), cl.gradF(mu, w, dense=True), None)
+    _check_queries(wn.wn_eval_adjoint(t, _cuda(s), w, float("inf")).cpu().numpy(), cl.AT(s, w, dense=True), None)
+
+
+def test_field_at_arbitrary_queries(wn):
+    # F and ∇F off the surface (Theorem 1 indicator) vs the oracle treecode
+    p, n_ = synth.fibonacci_sphere(20000)
+    mu = (n_ * (4 * np.pi / 20000)).astype(np.float32)
+    g = np.linspace(-1.6, 1.6, 23, dtype=np.float32)
+    q = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3).astype(np.float32)
+    t = wn.wn_build_tree(_cuda(p))
+    cl = oracle.Cloud(p)
+    w = float(np.float32(0.002))
+    F = wn.wn_eval(t, _cuda(mu), w, 2.0, q=_cuda(q)).cpu().numpy()
+    Fo, cnt = cl.F(mu, w, 2.0, queries=q, counters=True)
+    _check_queries(F, Fo, cnt, name="F(q)")
+    r = np.linalg.norm(q, axis=1)
+    assert np.all(np.abs(F[r < 0.9] - 1) < 2e-3) and np.all(np.abs(F[r > 1.1]) < 2e-3)
+    G = wn.wn_eval_grad(t, _cuda(mu), w, 2.0, q=_cuda(q)).cpu().numpy()
+    Go, cnt = cl.gradF(mu, w, 2.0, queries=q, counters=True)
+    _check_queries(G, Go, cnt, name="gradF(q)")
+
+
+def test_transpose_adjoint(wn):
+    p, nr = synth.sphere(3000, seed=15)
+    rng = np.random.default_rng(14)
+    mu = (nr * 0.004 * (1 + 0.2 * rng.standard_normal((3000, 1)))).astype(np.float32)
+    s = rng.standard_normal(3000).astype(np.float32)
+    t = wn.wn_build_tree(_cuda(p))
+    cl = oracle.Cloud(p)
+    w = float(np.float32(0.005))
+    g = wn.wn_eval_adjoint(t, _cuda(s), w, 2.0, mode=wn.WN_ADJ_TRANSPOSE, mu_geom=_cuda(mu)).cpu().numpy()
+    ref = cl.AT_transpose(s, mu, w)
+    _check_queries(g, ref, None, name="AT transpose")
+
+
+def test_full_size_sampled(wn):
+    # BASELINE headline size (C3, N = 500k) — the launch configuration bench.py times; oracle on samples
+    cfg = synth.config("C3")
+    p = cfg["points"]
+    n = len(p)
+    rng = np.random.default_rng(16)
+    mu = (synth.random_signs(cfg["normals"], 1005) * (4 * np.pi / n)).astype(np.float32)
+    s = (0.5 - rng.uniform(0, 1, n)).astype(np.float32)
+    t = wn.wn_build_tree(_cuda(p))
+    cl = oracle.Cloud(p)
+    idx = rng.choice(n, 3000, replace=False)
+    w = float(np.float32(0.002))
+    F = wn.wn_eval(t, _cuda(mu), w).cpu().numpy()
+    Fo, c = cl.F(mu, w, qidx=idx, counters=True)
+    _check_queries(F[idx], Fo, c, name="F 500k")
+    G = wn.wn_eval_grad(t, _cuda(mu), w).cpu().numpy()
+    Go, c = cl.gradF(mu, w, qidx=idx, counters=True)
+    _check_queries(G[idx], Go, c, name="gradF 500k")
+    R = wn.wn_eval_adjoint(t, _cuda(s), w).cpu().numpy()
+    Ro, c = cl.AT(s, w, qidx=idx, counters=True)
+    _check_queries(R[idx], Ro, c, name="AT 500k")
+
+
+def test_one_iteration_matches_oracle(wn):
+    # one Alg. 3 iteration from μ = 0 (w = w2): per point ≤ 1e-3 relative (s = ½ − Aμ cancels)
+    p = CLOUDS["torus50k"]()
+    t = wn.wn_build_tree(_cuda(p))
+    mu = torch.zeros(len(p), 3, device="cuda")
+    st = wn.wnnc_iterate(t, mu, stats=True, iters=1, total_iters=40)
+    cl = oracle.Cloud(p)
+    mo, so = cl.solve(iters=1, total_iters=40, w1=W1, w2=W2)
+    m = mu.cpu().numpy()
+    err = np.linalg.norm(m - mo, axis=1) / np.linalg.norm(mo, axis=1)
+    assert np.mean(err < 1e-3) >= 0.999, np.percentile(err, [50, 99, 100])
+    assert st[0]["E"] == pytest.approx(so[0, 0], rel=1e-6)
+    assert st[0]["alpha"] == pytest.approx(so[0, 1], rel=1e-3)
+    assert st[0]["width"] == so[0, 4]
+
+
+@pytest.mark.parametrize("cfg,mode", [("C1", "gather"), ("C2", "gather"), ("C1", "transpose")])
+def test_forty_iterations_orientation(wn, cfg, mode):
+    c = synth.config(cfg)
+    p, nr = c["points"], c["normals"]
+    t = wn.wn_build_tree(_cuda(p))
+    mu = torch.zeros(len(p), 3, device="cuda")
+    wn.wnnc_iterate(t, mu, iters=40, adjoint_mode=wn.WN_ADJ_TRANSPOSE if mode == "transpose" else wn.WN_ADJ_GATHER)
+    m = mu.cpu().numpy()
+    cl = oracle.Cloud(p)
+    mo, _ = cl.solve(iters=40, w1=W1, w2=W2, mode=mode)
+    agree = np.mean(np.sum(m * mo, axis=1) > 0)
+    assert agree >= 0.999, agree
+    if cfg == "C1":
+        assert oracle.p_co(m, nr) >= 0.999
+
+
+def test_table5_on_gpu(wn):
+    # PAPER.md:L945-L961 Table 5 (solved |μ| mean / total on the level-7 icosphere), ±0.2 %
+    p, nr, _ = synth.icosphere(7)
+    t = wn.wn_build_tree(_cuda(p))
+    mu = torch.zeros(len(p), 3, device="cuda")
+    wn.wnnc_iterate(t, mu, iters=40)
+    a = np.linalg.norm(mu.cpu().numpy(), axis=1)
+    g = T5["solved_area_abs_mu"]
+    assert abs(a.mean() / g["mean"] - 1) < 2e-3
+    assert abs(a.sum() / g["total"] - 1) < 2e-3
+    assert oracle.p_co(mu.cpu().numpy(), nr) == 1.0
+
+
+def test_solve_host_matches_device_path(wn):
+    p = CLOUDS["sphere2k"]()
+    pts = torch.from_numpy(p).pin_memory()
+    nrm, mu_h = wn.wnnc_solve_host(pts, return_mu=True, iters=40)
+    t = wn.wn_build_tree(_cuda(p))
+    mu = torch.zeros(len(p), 3, device="cuda")
+    wn.wnnc_iterate(t, mu, iters=40)
+    np.testing.assert_array_equal(mu_h.numpy(), mu.cpu().numpy())
+    np.testing.assert_allclose(np.linalg.norm(nrm.numpy(), axis=1), 1, rtol=1e-6)
+
+
+def test_deterministic(wn):
+    p = CLOUDS["torus50k"]()
+    outs = []
+    for _ in range(2):
+        t = wn.wn_build_tree(_cuda(p))
+        mu = torch.zeros(len(p), 3, device="cuda")
+        wn.wnnc_iterate(t, mu, iters=3, total_iters=40)
+        outs.append(mu.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
