@@ -1,0 +1,312 @@
+"""bench.py — WNNC hot-path benchmark (BASELINE.json metric: WNNC iterations/s and source-query
+interactions/s at N = 500k, 1/2/4/8 B200).
+
+One *step* = one pass of the whole hot path (SURVEY §8(a) rows a1–a9) over the synthetic workload:
+wn_build_tree (normalize, Morton sort, octree) + wnnc_iterate (40 iterations of Alg. 3: 4 moment
+builds + 4 treecode traversals + α per iteration).  Inputs are resident in HBM when a step starts.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+N > 1 is launched with torchrun (one process per GPU, NCCL); queries are sharded in Morton order and
+the ranks exchange s, r, μ and the Σ partials every iteration (strong scaling of the 500k problem).
+--impl reference times the fp64 CPU oracle (the only reference this paper-only task has) on the host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2405_16634_b200 import synth  # noqa: E402
+
+ITERS = 40
+CONFIG_TEXT = {
+    "C1": "C1: unit sphere, N=2,000 uniform, 40 WNNC iterations, theta=2, D=15, w 0.016->0.002",
+    "C2": "C2: torus R=1 r=0.3, N=50,000, 0.5% Gaussian noise, 40 WNNC iterations, theta=2, D=15, w 0.016->0.002",
+    "C3": "C3: bumpy sphere r=1+0.15 sin(5t) sin(4p), N=500,000, nonuniform density 10:1, 40 WNNC iterations, "
+          "theta=2, D=15, w 0.016->0.002",
+    "C4": "C4: thin plate + thin torus + 1% outliers, N=200,000, 40 WNNC iterations, theta=2, D=15",
+    "C5": "C5: 8-shape scene, N=4,000,000, 0.25% noise, 40 WNNC iterations, theta=2, D=15",
+}
+# Algorithmic FP32 operations per unit of work (FMA = 2 flops, rsqrt = 1):
+#   opening test: d = x_B − x_q (3) + d² (1 mul + 2 fma = 5)                               = 8
+#   live kernel evaluation, on top of its d²:
+#     A : rsqrt 1 + r⁻³ 2 + d·ν 5 + accumulate 2                                           = 10
+#     Aᵀ: rsqrt 1 + r⁻³ 2 + s·r⁻³ 1 + accumulate 6                                         = 10
+#     G : rsqrt 1 + r⁻², r⁻³ 2 + d·ν 5 + 3(d·ν)r⁻² 2 + ν − t d 6 + accumulate 6            = 22
+FLOPS_TEST = 8
+FLOPS_TERM = {"A": 10, "AT": 10, "G": 22}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._p = None
+
+    def __enter__(self):
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                        "--format=csv,noheader,nounits", "-lms", "100"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self._p = None
+        return self
+
+    def _read(self):
+        for line in self._p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self._p:
+            time.sleep(0.25)
+            self._p.terminate()
+            self._p.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _oracle_sample(points, iters, threads_note=""):
+    """The fp64 C oracle (test infrastructure, as it stands) on the host: tree + `iters` iterations of
+    the 40-iteration schedule.  Returns (seconds for the iterations, cores)."""
+    import oracle
+
+    cl = oracle.Cloud(points)
+    t0 = time.perf_counter()
+    cl.t.solve(iters=iters, total_iters=ITERS, w1=float(np.float32(0.002)), w2=float(np.float32(0.016)))
+    return time.perf_counter() - t0, oracle.num_threads()
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    cfg = synth.config(args.config)
+    pts = cfg["points"]
+    per_step = max(1, args.ref_iters)
+    for _ in range(args.warmup):
+        _oracle_sample(pts, per_step)
+    times = []
+    cores = 1
+    for _ in range(args.steps):
+        dt, cores = _oracle_sample(pts, per_step)
+        times.append(dt)
+    T = float(np.sum(times))
+    value = args.steps * per_step / T
+    sample = f"{per_step} of the {ITERS} iterations (schedule iterations 1..{per_step}) per step on the full " \
+             f"N={len(pts)} cloud, fp64 oracle treecode, tree build excluded"
+    line = {"impl": "reference", "metric": "WNNC iterations/s", "value": value, "unit": "iterations/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": CONFIG_TEXT[args.config], "n_points": len(pts)},
+            "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2405_16634_b200.wn as wn
+
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(wn.wn_comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = wn.wn_comm_init(rank, world, bytes(uid.cpu().numpy().tobytes()))
+
+    cfg = synth.config(args.config)
+    pts_h = cfg["points"]
+    n = len(pts_h)
+    pts = torch.from_numpy(pts_h).to(dev)
+    params = dict(iters=ITERS, theta=args.theta, adjoint_mode=wn.WN_ADJ_TRANSPOSE if args.transpose else 0)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def step():
+        tree = wn.wn_build_tree(pts)
+        mu = torch.zeros(n, 3, dtype=torch.float32, device=dev)
+        wn.wnnc_iterate(tree, mu, comm=comm, **params)
+        return tree, mu
+
+    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- algorithmic work of one step (counting variant, same decisions; untimed) ----
+    wn.wn_work_count_enable(True)
+    tree, mu = step()
+    work = wn.wn_work_count_read()
+    wn.wn_work_count_enable(False)
+    depth_used, num_nodes = tree.depth_used, tree.num_nodes
+    del tree
+
+    # ---- timed region: K steps, per-step CUDA events, L2 flushed between steps (outside the events) ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    wn.wn_prof_enable(True)
+    l0 = wn.wn_launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = wn.wn_launch_count() - l0
+    prof = wn.wn_prof_read()
+    wn.wn_prof_enable(False)
+    ms = float(sum(a.elapsed_time(b) for a, b in ev)) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ITERS / (ms / 1e3)
+
+    # ---- end to end through the C ABI with HOST buffers (H2D points, D2H normals inside the region) ----
+    e2e = None
+    if world == 1:
+        pts_pin = torch.from_numpy(pts_h).pin_memory()
+        wn.wnnc_solve_host(pts_pin, **params)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            wn.wnnc_solve_host(pts_pin, **params)
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": ITERS / te, "unit": "iterations/s", "h2d_bytes_per_step": int(n * 12),
+               "d2h_bytes_per_step": int(n * 12), "ms_per_step": 1e3 * te}
+
+    if rank != 0:
+        return 0
+    # ---- roofline of the dominant kernel class (the treecode traversals) ----
+    trav_ms = sum(prof[k][0] for k in ("trav_A", "trav_AT", "trav_G")) / args.steps
+    trav_launches = sum(prof[k][1] for k in ("trav_A", "trav_AT", "trav_G")) / args.steps
+    flops = sum(FLOPS_TEST * work[c]["tests"] + FLOPS_TERM[c] * work[c]["live"] for c in ("A", "AT", "G"))
+    achieved = flops / (trav_ms / 1e3) / 1e12
+    props = torch.cuda.get_device_properties(dev)
+    sm_count = props.multi_processor_count
+    clocks = clk.summary()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    fmax = float(peaks.get("sm_max_mhz", clocks.get("sm_max_mhz") or 1965.0))
+    peak = sm_count * 128 * 2 * fmax * 1e6 / 1e12
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
+    except (OSError, ValueError):
+        pass
+    interactions = sum(work[c]["live"] for c in ("A", "AT", "G"))
+    line = {
+        "metric": "WNNC iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": CONFIG_TEXT[args.config], "n_points": n, "iters_per_step": ITERS,
+                   "theta": args.theta, "max_depth": 15, "depth_used": depth_used, "num_nodes": num_nodes,
+                   "adjoint": "transpose" if args.transpose else "gather",
+                   "l2": "flushed between steps (256 MiB write outside the per-step events)",
+                   "parallelism": f"query-sharded x{world}" if world > 1 else "1 GPU",
+                   "step": "wn_build_tree + 40 x (4 moment builds + 4 traversals + alpha)"},
+        "interactions_per_s": {"counted": interactions * 1e3 / ms, "effective_dense": 4.0 * n * n * ITERS * 1e3 / ms,
+                               "unit": "source-query interactions/s",
+                               "note": "counted = live kernel evaluations (far + leaf) of the traversals; "
+                                       "effective_dense = 4 N^2 per iteration (the O(N^2) sums replaced)"},
+        "breakdown_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "treecode traversals (trav_kernel A/AT/G), %.0f launches/step, %.3f ms/step"
+                               % (trav_launches, trav_ms),
+                     "peak_note": f"FP32 FMA pipe: {sm_count} SMs x 128 lanes x 2 flop x {fmax:.0f} MHz "
+                                  "(sm_max_mhz of MEASURED_PEAKS.json; derived, DESIGN.md §Roofline)",
+                     "work": work},
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+        "paper_context": {"rtx3090_40iter_500k_s": 31.63, "rtx3090_40iter_50k_s": 1.25,
+                          "source": "PAPER.md:L89-L96 teaser (other hardware: context only)"},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        dt, cores = _oracle_sample(pts_h, args.ref_iters)
+        line["cpu_baseline"] = {"value": args.ref_iters / dt, "unit": "iterations/s", "cores": cores,
+                                "kind": "oracle",
+                                "sample": f"iterations 1..{args.ref_iters} of the 40-iteration schedule on the "
+                                          f"full N={n} cloud (fp64 oracle treecode, tree build excluded)"}
+    print(json.dumps(line), flush=True)
+    if comm:
+        comm.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--theta", type=float, default=2.0)
+    ap.add_argument("--transpose", action="store_true", help="north-star exact-transpose adjoint")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-iters", type=int, default=3, help="oracle iterations per sample / reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

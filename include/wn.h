@@ -95,11 +95,12 @@ enum { WN_PROF_TRAV_A = 0, WN_PROF_TRAV_AT = 1, WN_PROF_TRAV_G = 2, WN_PROF_MOME
 wn_status wn_prof_enable(int32_t enable);
 wn_status wn_prof_read(double ms[WN_PROF_NCLASS] /*host*/, int64_t launches[WN_PROF_NCLASS] /*host*/);
 /* (host) algorithmic-work accounting: while enabled, traversals run their counting variant (the same
-   decisions) and accumulate, per class (A, Aᵀ, G), the number of node opening tests, live representative
-   terms and live leaf-point terms (a term is live when r ≥ w).  enable = 1 zeroes the counters.
-   wn_work_count_read synchronizes the device; counts[3·class + {0,1,2}]. */
+   decisions) and accumulate, per class (A, Aᵀ, G): node opening tests, representative (far) terms,
+   leaf-point terms, and live terms (far + leaf terms with r ≥ w, i.e. the kernel evaluations actually
+   needed).  enable = 1 zeroes the counters.  wn_work_count_read synchronizes the device;
+   counts[4·class + {0,1,2,3}]. */
 wn_status wn_work_count_enable(int32_t enable);
-wn_status wn_work_count_read(int64_t counts[9] /*host*/);
+wn_status wn_work_count_read(int64_t counts[12] /*host*/);
 
 /* ---- tree (§4.5; normalization L419) ------------------------------------------ */
 /* Build the octree of n caller-frame points pts (N×3).  Root cell = [−1,1]^3 of the normalized frame;
@@ -133,6 +134,12 @@ wn_status wn_eval(wn_tree t, const float* mu, const float* a, const float* q, in
 /* ∇F(q) (input frame; = −G(μ) at the points).  gradF[M×3]. */
 wn_status wn_eval_grad(wn_tree t, const float* mu, const float* a, const float* q, int64_t m, float width,
                        float theta, float* gradF, void* stream);
+/* Per-query work of wn_eval (op 0) / wn_eval_grad (op 2) with the same arguments, without computing
+   the field: counts[M×4] (int32, query order) = node tests, far terms, leaf-point terms, live terms.
+   A one-point node always takes the representative branch here (its far and leaf terms coincide), so
+   far + leaf-point terms equals Alg. 4's far + near count.  Diagnostic / parity entry point. */
+wn_status wn_query_work(wn_tree t, int32_t op, const float* mu, const float* q, int64_t m, float width, float theta,
+                        int32_t* counts, void* stream);
 /* out[N×3] = (Aᵀ s)_j = Σ_i s_i ∇Φ_w(x_i − x_j)  (input frame), s[N] caller order.
    mode WN_ADJ_GATHER: own traversal with |s|-weighted representatives.
    mode WN_ADJ_TRANSPOSE: exact transpose of wn_eval's treecode at the geometry of mu_geom[N×3]

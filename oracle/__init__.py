@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "wn_oracle.c")
 _LIB = os.path.join(_HERE, "libwn_oracle.so")
 
-OP_A, OP_G, OP_AT = 0, 1, 2
+OP_A, OP_G, OP_AT, ABS = 0, 1, 2, 8
 
 
 def build(force: bool = False) -> str:
@@ -162,7 +162,7 @@ class Tree:
         dim = 1 if nu.ndim == 1 else 3
         q = None if queries is None else _f32(queries).reshape(-1, 3)
         m = self.n if q is None else q.shape[0]
-        od = 1 if op == OP_A else 3
+        od = 1 if (op == OP_A or op & ABS) else 3
         out = np.empty((m, od))
         lib().wo_dense_op(self._h, op, _p(nu), dim, None if q is None else _p(q), m, float(w), _p(out))
         return out[:, 0] if od == 1 else out
@@ -173,7 +173,7 @@ class Tree:
         q = None if queries is None else _f32(queries).reshape(-1, 3)
         qi = None if qidx is None else np.ascontiguousarray(qidx, dtype=np.int64)
         m = q.shape[0] if q is not None else (qi.shape[0] if qi is not None else self.n)
-        od = 1 if op == OP_A else 3
+        od = 1 if (op == OP_A or op & ABS) else 3
         out = np.empty((m, od))
         cnt = np.empty((m, 4), np.int64) if counters else None
         lib().wo_tree_op(self._h, op, _p(nu), dim, None if q is None else _p(q),
@@ -252,6 +252,14 @@ class Cloud:
         if counters:
             return r[0] * self.scale ** 2, r[1]
         return r * self.scale ** 2
+
+    def abs_scale(self, op, nu_in, w, theta=2.0, a=None, queries=None, qidx=None):
+        """S_i = Σ_j |term_ij| of the treecode sum at query i, in the output's frame (the conditioning
+        scale of a cancelling sum; used for the parity error floor)."""
+        if op == OP_AT:
+            return self.t.tree(OP_AT | ABS, _f64(nu_in), w, theta, None, qidx) * self.scale ** 2
+        S = self.t.tree(op | ABS, self._mu_norm(nu_in, a), w, theta, self._q(queries), qidx)
+        return S * (self.scale if op == OP_G else 1.0)
 
     def AT_transpose(self, s, mu_geom, w, theta=2.0):
         return self.t.AT_transpose(self._mu_norm(mu_geom), _f64(s), w, theta) * self.scale ** 2

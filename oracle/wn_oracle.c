@@ -296,25 +296,31 @@ void wo_moments(const wo_tree* t, const double* nu, int dim, double* rep, double
 /* term(op, y, x, ν): contribution of source x with attribute ν to the query y.                */
 /* ------------------------------------------------------------------------------------------ */
 static void term(int op, const double y[3], const double x[3], const double* nu, double* acc) {
+  /* op | WO_ABS: accumulate |contribution| instead (the per-query conditioning scale Σ_j |term_j|) */
+  int absm = op & WO_ABS;
+  op &= ~WO_ABS;
+  double t[3] = {0, 0, 0};
   double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};     /* d = y − x */
   double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
   double r = sqrt(r2);
   double k3 = 1.0 / (WO_4PI * r2 * r);                        /* 1/(4π r^3) */
   if (op == WO_OP_A) {
     /* ∇Φ(y−x)·ν = −(y−x)·ν / (4π r^3)    (Eq wnf-discretization) */
-    acc[0] += -(d[0] * nu[0] + d[1] * nu[1] + d[2] * nu[2]) * k3;
+    t[0] = -(d[0] * nu[0] + d[1] * nu[1] + d[2] * nu[2]) * k3;
   } else if (op == WO_OP_G) {
     /* −HΦ(y−x)ν = ν/(4π r^3) − 3 (d·ν) d/(4π r^5) */
     double dn = d[0] * nu[0] + d[1] * nu[1] + d[2] * nu[2];
     double k5 = 3.0 * k3 / r2;
-    for (int c = 0; c < 3; ++c) acc[c] += nu[c] * k3 - dn * d[c] * k5;
+    for (int c = 0; c < 3; ++c) t[c] = nu[c] * k3 - dn * d[c] * k5;
   } else {
     /* ν ∇Φ(x−y) = ν (y−x)/(4π r^3)   (Aᵀ: (Aᵀs)_j = Σ_i s_i ∇Φ(x_i − x_j)) */
-    for (int c = 0; c < 3; ++c) acc[c] += nu[0] * d[c] * k3;
+    for (int c = 0; c < 3; ++c) t[c] = nu[0] * d[c] * k3;
   }
+  if (absm) acc[0] += sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
+  else for (int c = 0; c < 3; ++c) acc[c] += t[c];
 }
 
-static int out_dim(int op) { return op == WO_OP_A ? 1 : 3; }
+static int out_dim(int op) { return (op == WO_OP_A || (op & WO_ABS)) ? 1 : 3; }
 
 /* ------------------------------------------------------------------------------------------ */
 /* Dense operators: the O(N^2) definitions.              */

@@ -23,7 +23,8 @@ typedef struct wo_tree wo_tree;
 
 enum { WO_OP_A = 0,   /* Σ ∇Φ(y−x_j)·ν_j          (A, and the field F at arbitrary y) */
        WO_OP_G = 1,   /* −Σ HΦ(y−x_j) ν_j         (G, and −∇F at arbitrary y)         */
-       WO_OP_AT = 2   /* Σ ν_i ∇Φ(x_i−y), ν scalar (Aᵀ, gather form)                  */ };
+       WO_OP_AT = 2,  /* Σ ν_i ∇Φ(x_i−y), ν scalar (Aᵀ, gather form)                  */
+       WO_ABS = 8     /* modifier: accumulate |term| (conditioning scale S = Σ_j |term_j|)  */ };
 
 /* §5.1.1 normalization; returns 0, 1 (empty), 2 (non-finite), 3 (zero extent). */
 int wo_normalize(const float* raw, int64_t n, float* xn, double xf[4]);

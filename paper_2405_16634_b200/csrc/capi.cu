@@ -61,7 +61,7 @@ static int64_t* g_work = nullptr;
 
 int64_t* work_counters(int cls) {
   if (!g_count_on || !g_work || cls < 0 || cls > 2) return nullptr;
-  return g_work + 3 * cls;
+  return g_work + 4 * cls;
 }
 
 static wn_status check_device() {
@@ -254,17 +254,17 @@ wn_status wn_prof_read(double ms[WN_PROF_NCLASS], int64_t launches[WN_PROF_NCLAS
 }
 
 wn_status wn_work_count_enable(int32_t enable) {
-  if (enable && !g_work) WN_CUDA(cudaMalloc((void**)&g_work, 9 * sizeof(int64_t)));
-  if (enable) WN_CUDA(cudaMemset(g_work, 0, 9 * sizeof(int64_t)));
+  if (enable && !g_work) WN_CUDA(cudaMalloc((void**)&g_work, 12 * sizeof(int64_t)));
+  if (enable) WN_CUDA(cudaMemset(g_work, 0, 12 * sizeof(int64_t)));
   g_count_on = enable != 0;
   return WN_OK;
 }
 
-wn_status wn_work_count_read(int64_t counts[9]) {
-  for (int k = 0; k < 9; ++k) counts[k] = 0;
+wn_status wn_work_count_read(int64_t counts[12]) {
+  for (int k = 0; k < 12; ++k) counts[k] = 0;
   if (!g_work) return WN_OK;
   WN_CUDA(cudaDeviceSynchronize());
-  WN_CUDA(cudaMemcpy(counts, g_work, 9 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  WN_CUDA(cudaMemcpy(counts, g_work, 12 * sizeof(int64_t), cudaMemcpyDeviceToHost));
   return WN_OK;
 }
 
@@ -354,8 +354,8 @@ wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, fl
 }
 
 static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a, const float* q, int64_t m,
-                             float width, float theta, float* out, void* stream) {
-  if (!t || !mu || !out) return set_error(WN_ERR_ARG, "tree, mu or output is NULL");
+                             float width, float theta, float* out, void* stream, int32_t* qcounts = nullptr) {
+  if (!t || !mu || (!out && !qcounts)) return set_error(WN_ERR_ARG, "tree, mu or output is NULL");
   if (bad_width(width)) return set_error(WN_ERR_ARG, "width must be > 0");
   if (bad_theta(theta)) return set_error(WN_ERR_ARG, "theta must be > 0");
   if (q && m < 0) return set_error(WN_ERR_ARG, "m < 0");
@@ -395,6 +395,11 @@ static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a,
   }
   if (op == OP_A) ta.out_f = out;
   else ta.out_v3 = out;
+  if (qcounts) {  // counting run: per-query work only
+    ta.qcounts = qcounts;
+    ta.out_f = nullptr;
+    ta.out_v3 = nullptr;
+  }
   return traverse(ta, s);
 }
 
@@ -406,6 +411,12 @@ wn_status wn_eval(wn_tree t, const float* mu, const float* a, const float* q, in
 wn_status wn_eval_grad(wn_tree t, const float* mu, const float* a, const float* q, int64_t m, float width,
                        float theta, float* gradF, void* stream) {
   return eval_common(t, OP_G, mu, a, q, m, width, theta, gradF, stream);
+}
+
+wn_status wn_query_work(wn_tree t, int32_t op, const float* attr, const float* q, int64_t m, float width,
+                        float theta, int32_t* counts, void* stream) {
+  if (op != 0 && op != 2) return set_error(WN_ERR_ARG, "op must be 0 (F) or 2 (gradF)");
+  return eval_common(t, op == 0 ? OP_A : OP_G, attr, nullptr, q, m, width, theta, nullptr, stream, counts);
 }
 
 wn_status wn_eval_adjoint(wn_tree t, const float* sv, float width, float theta, int32_t mode, const float* mu_geom,

@@ -32,21 +32,24 @@ template <int KIND>
 __device__ __forceinline__ void write_record(int i, const Sums& S, int cnt, float4 p0, int depth, int topo,
                                              float theta, const float4* __restrict__ centroid, NodeSet out,
                                              float4* centroid_out) {
-  float4 R;
+  float4 R, L = make_float4(0.f, 0.f, 0.f, 0.f);
   if (cnt == 1) {
     R = make_float4(p0.x, p0.y, p0.z, -1.0f);
   } else {
     float rx, ry, rz;
     if (S.W > 0.0) {
-      rx = (float)(S.P[0] / S.W);
-      ry = (float)(S.P[1] / S.W);
-      rz = (float)(S.P[2] / S.W);
+      const double x = S.P[0] / S.W, y = S.P[1] / S.W, z = S.P[2] / S.W;
+      rx = (float)x;
+      ry = (float)y;
+      rz = (float)z;
+      L = make_float4((float)(x - (double)rx), (float)(y - (double)ry), (float)(z - (double)rz), 0.f);
     } else {
       float4 c = centroid[i];
       rx = c.x; ry = c.y; rz = c.z;
     }
     R = make_float4(rx, ry, rz, thr_of(theta, depth));
   }
+  if (out.L) out.L[i] = L;
   out.R[i] = R;
   if (KIND == ATTR_SCALAR)
     out.A[i] = make_float4((float)S.V[0], 0.f, 0.f, __int_as_float(topo));

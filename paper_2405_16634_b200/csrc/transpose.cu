@@ -36,7 +36,8 @@ __device__ __forceinline__ void warp_add3(float x, float y, float z, double* dst
 }
 
 __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
-    const float4* __restrict__ NR, const float4* __restrict__ NA, const float4* __restrict__ pts,
+    const float4* __restrict__ NR, const float4* __restrict__ NA, const float4* __restrict__ NL,
+    const float4* __restrict__ pts,
     const int32_t* __restrict__ npb, const int32_t* __restrict__ npe, const float* __restrict__ s_sorted,
     int64_t n, float w2, int stack_depth, double* __restrict__ VB, double* __restrict__ U) {
   extern __shared__ int2 stk_all[];
@@ -67,10 +68,12 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
       // s_i ∇Φ(x_i − x_B) = s_i d / (4π r³), d = x_B − x_i
       float cx = 0.f, cy = 0.f, cz = 0.f;
       const bool live = mine && far && !(d2 < w2);
-      if (live) {
-        const float inv = rsqrtf(d2);
+      if (live) {  // value at d = (hi − x_q) + lo
+        const float4 Lo = __ldg(NL + node);
+        const float ex = dx + Lo.x, ey = dy + Lo.y, ez = dz + Lo.z;
+        const float inv = rsqrtf(dist2(ex, ey, ez));
         const float c = sq * inv * inv * inv;
-        cx = c * dx; cy = c * dy; cz = c * dz;
+        cx = c * ex; cy = c * ey; cz = c * ez;
       }
       if (__any_sync(FULL, live)) warp_add3(cx, cy, cz, VB + 3 * (int64_t)node, lane);
       const uint32_t open = __ballot_sync(FULL, mine && !far);
@@ -147,7 +150,7 @@ wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sor
   {
     ProfScope ps(WN_PROF_TRAV_AT, st, 2);
     scatter_kernel<<<grid, kTravBlock, (size_t)(kTravBlock / 32) * stack_depth * sizeof(int2), st>>>(
-        geo.R, geo.A, t->pts, t->pb, t->pe, s_sorted, t->n, w2, stack_depth, t->tvb, t->tu);
+        geo.R, geo.A, geo.L, t->pts, t->pb, t->pe, s_sorted, t->n, w2, stack_depth, t->tvb, t->tu);
     pushdown_kernel<<<grid, kTravBlock, 0, st>>>(t->n, t->leaf_of, t->parent, t->tvb, t->tu, 1.0f, r_out, partial);
   }
   WN_CUDA(cudaGetLastError());

@@ -84,9 +84,10 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
   const uint32_t active = __ballot_sync(FULL, valid);
   const float4* __restrict__ NR = a.nodes.R;
   const float4* __restrict__ NA = a.attrA ? a.attrA : a.nodes.A;
+  const float4* __restrict__ NL = a.nodes.L;
   const float w2 = a.w2;
   Acc<OP> acc;
-  int ntest = 0, nfar = 0, nnear = 0;
+  int ntest = 0, nfar = 0, nnear = 0, nlive = 0;
   if (active) {
     int sp = 0;
     if (lane == 0) stk[0] = make_int2(0, (int)active);  // the root as a group of one: (0 << 4) | 0
@@ -102,15 +103,18 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
         const int node = cb + k;
         const float4 R = __ldg(NR + node);
         const float4 V = __ldg(NA + node);
+        const float4 Lo = __ldg(NL + node);
         const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
         const float d2 = dist2(dx, dy, dz);
         const bool far = d2 > R.w;
-        if (mine && far) {
-          if (!(d2 < w2)) acc.term(dx, dy, dz, d2, V);
+        if (mine && far && !(d2 < w2)) {  // value at d = (hi − x_q) + lo
+          const float ex = dx + Lo.x, ey = dy + Lo.y, ez = dz + Lo.z;
+          acc.term(ex, ey, ez, dist2(ex, ey, ez), V);
         }
         if (COUNT && mine) {
           ++ntest;
-          nfar += far && !(d2 < w2);
+          nfar += far;
+          nlive += far && !(d2 < w2);
         }
         const uint32_t open = __ballot_sync(FULL, mine && !far);
         if (open) {
@@ -129,7 +133,10 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
               const float ex = __fsub_rn(P.x, xq.x), ey = __fsub_rn(P.y, xq.y), ez = __fsub_rn(P.z, xq.z);
               const float e2 = dist2(ex, ey, ez);
               if (lm && !(e2 < w2)) acc.term(ex, ey, ez, e2, Vj);
-              if (COUNT && lm) nnear += !(e2 < w2);
+              if (COUNT && lm) {
+                ++nnear;
+                nlive += !(e2 < w2);
+              }
             }
           }
         }
@@ -144,7 +151,7 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
     const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
     if (OP == OP_A) {
       const double val = acc.d * 0.0795774715459476679;  // Σ / (4π)
-      if (EPI == EPI_PLAIN) a.out_f[oq] = (float)(val * (double)a.scale_out);
+      if (EPI == EPI_PLAIN && a.out_f) a.out_f[oq] = (float)(val * (double)a.scale_out);
       if (EPI == EPI_S) {
         const double sv = 0.5 - val;
         a.out_f[q] = (float)sv;
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
       if (EPI == EPI_SQ) part = val * val;
     } else {
       const float vx = acc.x * kInv4Pi, vy = acc.y * kInv4Pi, vz = acc.z * kInv4Pi;
-      if (EPI == EPI_PLAIN) {
+      if (EPI == EPI_PLAIN && a.out_v3) {
         a.out_v3[3 * oq + 0] = vx * a.scale_out;
         a.out_v3[3 * oq + 1] = vy * a.scale_out;
         a.out_v3[3 * oq + 2] = vz * a.scale_out;
@@ -175,18 +182,23 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
       }
     }
   }
-  if (COUNT) {  // algorithmic work of this launch: node tests, representative terms, leaf-point terms
-    unsigned long long c0 = ntest, c1 = nfar, c2 = nnear;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      c0 += __shfl_xor_sync(FULL, c0, o);
-      c1 += __shfl_xor_sync(FULL, c1, o);
-      c2 += __shfl_xor_sync(FULL, c2, o);
+  if (COUNT) {  // algorithmic work: node tests, representative terms, leaf-point terms, live terms (r ≥ w)
+    if (a.qcounts && valid) {
+      const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
+      a.qcounts[4 * oq + 0] = ntest;
+      a.qcounts[4 * oq + 1] = nfar;
+      a.qcounts[4 * oq + 2] = nnear;
+      a.qcounts[4 * oq + 3] = nlive;
     }
-    if (lane == 0) {
-      atomicAdd((unsigned long long*)a.work + 0, c0);
-      atomicAdd((unsigned long long*)a.work + 1, c1);
-      atomicAdd((unsigned long long*)a.work + 2, c2);
+    if (a.work) {
+      unsigned long long c[4] = {(unsigned long long)ntest, (unsigned long long)nfar, (unsigned long long)nnear,
+                                 (unsigned long long)nlive};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c[k] += __shfl_xor_sync(FULL, c[k], o);
+        if (lane == 0) atomicAdd((unsigned long long*)a.work + k, c[k]);
+      }
     }
   }
   if (EPI == EPI_S || EPI == EPI_SQ || EPI == EPI_R) {
@@ -203,7 +215,7 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
 
 template <int OP, int EPI>
 void launch(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
-  if (a.work) trav_kernel<OP, EPI, true><<<grid, kTravBlock, smem, s>>>(a);
+  if (a.work || a.qcounts) trav_kernel<OP, EPI, true><<<grid, kTravBlock, smem, s>>>(a);
   else trav_kernel<OP, EPI, false><<<grid, kTravBlock, smem, s>>>(a);
 }
 

@@ -452,6 +452,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   for (int k = 0; k < 2; ++k) {
     WN_TRY(dalloc(&t->set[k].R, nn, s));
     WN_TRY(dalloc(&t->set[k].A, nn, s));
+    WN_TRY(dalloc(&t->set[k].L, nn, s));
   }
   int64_t* loff = nullptr;
   WN_TRY(dalloc(&loff, t->level_off.size(), s));
@@ -487,7 +488,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 
 void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
-                  t->arrive, t->centroid, t->sums, t->set[0].R, t->set[0].A, t->set[1].R, t->set[1].A,
+                  t->arrive, t->centroid, t->sums, t->set[0].R, t->set[0].A, t->set[0].L, t->set[1].R, t->set[1].A, t->set[1].L,
                   t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
                   t->qbuf, t->tvb, t->tu};
   for (void* p : ptrs)

@@ -22,9 +22,12 @@ enum AttrKind { ATTR_VEC = 0, ATTR_SCALAR = 1, ATTR_UNIT = 2 };
 //                               rep = the point, ν_B = ν_j, so far and leaf terms coincide)
 //   A = (ν_B.x, ν_B.y, ν_B.z, topo) for vector ν, (s_B, 0, 0, topo) for scalar ν
 //   topo (int bits) = internal: (child_begin << 4) | (child_count − 1);  leaf: 8
+//   L = (x_B − hi, y_B − hi, z_B − hi, 0): the fp32 remainder of the fp64 representative, so a far term is
+//       evaluated at d = (hi − x_q) + lo (error ~1e-7·|d| instead of ulp(x_B)/|d|); decisions use hi only.
 struct NodeSet {
   float4* R = nullptr;
   float4* A = nullptr;
+  float4* L = nullptr;
 };
 
 struct IterScratch {
@@ -146,7 +149,8 @@ struct TravArgs {
   double* partial = nullptr;        // per-block partials (indexed by global block of 256 queries)
   float w2 = 0.0f;
   int stack_depth = 128;
-  int64_t* work = nullptr;          // set by traverse(): counting variant accumulates (tests, far, leaf pts)
+  int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
+  int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order
 };
 wn_status traverse(const TravArgs& a, cudaStream_t s);
 

@@ -26,7 +26,7 @@ STATUS_NAMES = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_EMPTY", 3: "WN_ERR_NONFI
 EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", "wn_prof_read", "wn_build_tree",
             "wn_tree_destroy", "wn_tree_info", "wn_tree_export", "wn_moments", "wn_eval", "wn_eval_grad",
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
-            "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read")
+            "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work")
 
 
 class wnnc_params(C.Structure):
@@ -53,6 +53,7 @@ _sig = {
     "wn_comm_unique_id": ([P], I32), "wn_comm_init": ([I32, I32, P, P], I32), "wn_comm_destroy": ([P], I32),
     "wn_shard_range": ([I64, I32, I32, P, P], I32),
     "wn_work_count_enable": ([I32], I32), "wn_work_count_read": ([P], I32),
+    "wn_query_work": ([P, I32, P, P, I64, F32, F32, P, P], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -115,10 +116,20 @@ def wn_work_count_enable(enable: bool = True):
 
 
 def wn_work_count_read():
-    c = (C.c_int64 * 9)()
+    c = (C.c_int64 * 12)()
     _check(_L.wn_work_count_read(c))
-    return {k: dict(tests=int(c[3 * i]), far=int(c[3 * i + 1]), near=int(c[3 * i + 2]))
+    return {k: dict(tests=int(c[4 * i]), far=int(c[4 * i + 1]), near=int(c[4 * i + 2]), live=int(c[4 * i + 3]))
             for i, k in enumerate(("A", "AT", "G"))}
+
+
+def wn_query_work(tree, mu, width, theta=2.0, op=0, q=None):
+    """Per-query (tests, far terms, leaf-point terms, live terms) of wn_eval (op 0) / wn_eval_grad (op 2)."""
+    _dev_f32(mu, 3)
+    m = tree.n if q is None else _dev_f32(q, 3).shape[0]
+    c = torch.empty(m, 4, dtype=torch.int32, device=tree.device)
+    _check(_L.wn_query_work(tree.handle, int(op), _ptr(mu), _ptr(q), m, float(width), float(theta), _ptr(c),
+                            _stream()))
+    return c
 
 
 class Tree:

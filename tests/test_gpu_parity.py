@@ -34,19 +34,35 @@ def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
 
 
-def _check_queries(gpu, ref, counters, tol=1e-4, name=""):
+def _check_queries(gpu, ref, counters, S=None, tol=1e-4, name=""):
+    """|gpu − ref| ≤ max(tol·|ref_i|, 2e-6·S_i) per query, S_i = Σ_j |term_ij| (the oracle's conditioning
+    scale: fp32 evaluation error grows with Σ|terms|, not with the cancelled sum).  Without S the floor is
+    tol·1e-3·rms(ref).  A query may exceed it only if the oracle flags a tie (≤ 1e-3 of the queries)."""
     gpu = np.asarray(gpu, np.float64).reshape(len(ref), -1)
     ref = np.asarray(ref, np.float64).reshape(len(ref), -1)
     mag = np.linalg.norm(ref, axis=1)
     err = np.linalg.norm(gpu - ref, axis=1)
-    rms = np.sqrt(np.mean(mag ** 2))
-    bad = err > tol * np.maximum(mag, 1e-3 * rms)
+    floor = 2e-6 * np.asarray(S) if S is not None else tol * 1e-3 * np.sqrt(np.mean(mag ** 2))
+    lim = np.maximum(tol * mag, floor)
+    bad = err > lim
     nb = int(bad.sum())
     if nb:
         ties = counters[bad, 3] if counters is not None else np.zeros(nb)
-        assert np.all(ties > 0), f"{name}: {nb} queries off without a tie, worst {np.max(err[bad] / np.maximum(mag[bad], 1e-3 * rms)):.3e}"
+        assert np.all(ties > 0), f"{name}: {nb} queries off without a tie, worst {np.max(err[bad] / lim[bad]):.3e}"
         assert nb <= max(1, 1e-3 * len(ref)), f"{name}: {nb} tie queries off"
     return nb
+
+
+def _check_decisions(gpu_counts, ora_counts, name=""):
+    """Same opening decisions per query: equal node tests and equal far + leaf terms (a one-point node
+    is a far term on the GPU and may be a leaf term in the oracle — the same term)."""
+    g = np.asarray(gpu_counts, np.int64)
+    o = np.asarray(ora_counts, np.int64)
+    diff = (g[:, 0] != o[:, 0]) | (g[:, 1] + g[:, 2] != o[:, 1] + o[:, 2])
+    nd = int(diff.sum())
+    if nd:
+        assert np.all(o[diff, 3] > 0), f"{name}: {nd} queries decide differently without a tie"
+        assert nd <= max(1, 1e-3 * len(o)), f"{name}: {nd} tie queries decide differently"
 
 
 CLOUDS = {
@@ -145,13 +161,19 @@ def test_operators_at_sources(wn, name, op, w, theta):
     if op == "F":
         g = wn.wn_eval(t, _cuda(mu), w, theta, a=_cuda(a)).cpu().numpy()
         ref, cnt = cl.F(mu, w, theta, a=a, counters=True)
+        S = cl.abs_scale(oracle.OP_A, mu, w, theta, a=a)
+        _check_decisions(wn.wn_query_work(t, _cuda(mu * a[:, None]), w, theta, op=0).cpu().numpy(), cnt,
+                         name=f"{name}/{op}")
     elif op == "gradF":
         g = wn.wn_eval_grad(t, _cuda(mu), w, theta).cpu().numpy()
         ref, cnt = cl.gradF(mu, w, theta, counters=True)
+        S = cl.abs_scale(oracle.OP_G, mu, w, theta)
+        _check_decisions(wn.wn_query_work(t, _cuda(mu), w, theta, op=2).cpu().numpy(), cnt, name=f"{name}/{op}")
     else:
         g = wn.wn_eval_adjoint(t, _cuda(s), w, theta).cpu().numpy()
         ref, cnt = cl.AT(s, w, theta, counters=True)
-    _check_queries(g, ref, cnt, name=f"{name}/{op}")
+        S = cl.abs_scale(oracle.OP_AT, s, w, theta)
+    _check_queries(g, ref, cnt, S, name=f"{name}/{op}")
 
 
 def test_operators_exact_sum(wn):
@@ -163,9 +185,13 @@ def test_operators_exact_sum(wn):
     t = wn.wn_build_tree(_cuda(p))
     cl = oracle.Cloud(p)
     w = float(np.float32(0.004))
-    _check_queries(wn.wn_eval(t, _cuda(mu), w, float("inf")).cpu().numpy(), cl.F(mu, w, dense=True), None)
-    _check_queries(wn.wn_eval_grad(t, _cuda(mu), w, float("inf")).cpu().numpy(), cl.gradF(mu, w, dense=True), None)
-    _check_queries(wn.wn_eval_adjoint(t, _cuda(s), w, float("inf")).cpu().numpy(), cl.AT(s, w, dense=True), None)
+    inf = float("inf")
+    _check_queries(wn.wn_eval(t, _cuda(mu), w, inf).cpu().numpy(), cl.F(mu, w, dense=True), None,
+                   cl.abs_scale(oracle.OP_A, mu, w, inf))
+    _check_queries(wn.wn_eval_grad(t, _cuda(mu), w, inf).cpu().numpy(), cl.gradF(mu, w, dense=True), None,
+                   cl.abs_scale(oracle.OP_G, mu, w, inf))
+    _check_queries(wn.wn_eval_adjoint(t, _cuda(s), w, inf).cpu().numpy(), cl.AT(s, w, dense=True), None,
+                   cl.abs_scale(oracle.OP_AT, s, w, inf))
 
 
 def test_field_at_arbitrary_queries(wn):
@@ -179,12 +205,14 @@ def test_field_at_arbitrary_queries(wn):
     w = float(np.float32(0.002))
     F = wn.wn_eval(t, _cuda(mu), w, 2.0, q=_cuda(q)).cpu().numpy()
     Fo, cnt = cl.F(mu, w, 2.0, queries=q, counters=True)
-    _check_queries(F, Fo, cnt, name="F(q)")
+    _check_queries(F, Fo, cnt, cl.abs_scale(oracle.OP_A, mu, w, queries=q), name="F(q)")
+    _check_decisions(wn.wn_query_work(t, _cuda(mu), w, 2.0, op=0, q=_cuda(q)).cpu().numpy(), cnt, name="F(q)")
     r = np.linalg.norm(q, axis=1)
-    assert np.all(np.abs(F[r < 0.9] - 1) < 2e-3) and np.all(np.abs(F[r > 1.1]) < 2e-3)
+    # indicator up to the c = 2 treecode's own error (≈2 %; the oracle pins the exact value)
+    assert np.all(np.abs(F[r < 0.9] - 1) < 0.05) and np.all(np.abs(F[r > 1.1]) < 0.05)
     G = wn.wn_eval_grad(t, _cuda(mu), w, 2.0, q=_cuda(q)).cpu().numpy()
     Go, cnt = cl.gradF(mu, w, 2.0, queries=q, counters=True)
-    _check_queries(G, Go, cnt, name="gradF(q)")
+    _check_queries(G, Go, cnt, cl.abs_scale(oracle.OP_G, mu, w, queries=q), name="gradF(q)")
 
 
 def test_transpose_adjoint(wn):
@@ -214,13 +242,14 @@ def test_full_size_sampled(wn):
     w = float(np.float32(0.002))
     F = wn.wn_eval(t, _cuda(mu), w).cpu().numpy()
     Fo, c = cl.F(mu, w, qidx=idx, counters=True)
-    _check_queries(F[idx], Fo, c, name="F 500k")
+    _check_queries(F[idx], Fo, c, cl.abs_scale(oracle.OP_A, mu, w, qidx=idx), name="F 500k")
+    _check_decisions(wn.wn_query_work(t, _cuda(mu), w, op=0).cpu().numpy()[idx], c, name="F 500k")
     G = wn.wn_eval_grad(t, _cuda(mu), w).cpu().numpy()
     Go, c = cl.gradF(mu, w, qidx=idx, counters=True)
-    _check_queries(G[idx], Go, c, name="gradF 500k")
+    _check_queries(G[idx], Go, c, cl.abs_scale(oracle.OP_G, mu, w, qidx=idx), name="gradF 500k")
     R = wn.wn_eval_adjoint(t, _cuda(s), w).cpu().numpy()
     Ro, c = cl.AT(s, w, qidx=idx, counters=True)
-    _check_queries(R[idx], Ro, c, name="AT 500k")
+    _check_queries(R[idx], Ro, c, cl.abs_scale(oracle.OP_AT, s, w, qidx=idx), name="AT 500k")
 
 
 def test_one_iteration_matches_oracle(wn):
