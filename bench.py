@@ -162,7 +162,8 @@ def run_ours(args):
     pts_h = cfg["points"]
     n = len(pts_h)
     pts = torch.from_numpy(pts_h).to(dev)
-    params = dict(iters=ITERS, theta=args.theta, adjoint_mode=wn.WN_ADJ_TRANSPOSE if args.transpose else 0)
+    params = dict(iters=ITERS, theta=args.theta, adjoint_mode=wn.WN_ADJ_TRANSPOSE if args.transpose else 0,
+                  flags=0 if args.no_graph else wn.WN_FLAG_GRAPH)
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
@@ -170,27 +171,34 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
 
-    def step():
+    def step(**over):
         tree = wn.wn_build_tree(pts)
         mu = torch.zeros(n, 3, dtype=torch.float32, device=dev)
-        wn.wnnc_iterate(tree, mu, comm=comm, **params)
+        wn.wnnc_iterate(tree, mu, comm=comm, **{**params, **over})
         return tree, mu
 
-    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+    for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
     # ---- algorithmic work of one step (counting variant, same decisions; untimed) ----
     wn.wn_work_count_enable(True)
-    tree, mu = step()
+    tree, mu = step(flags=0)
     work = wn.wn_work_count_read()
     wn.wn_work_count_enable(False)
     depth_used, num_nodes = tree.depth_used, tree.num_nodes
     del tree
 
+    # ---- per-kernel-class device time (CUDA events around every launch group; untimed pass, no graph) ----
+    wn.wn_prof_enable(True)
+    for _ in range(args.prof_steps):
+        flush.zero_()
+        step(flags=0)
+    prof = wn.wn_prof_read()
+    wn.wn_prof_enable(False)
+
     # ---- timed region: K steps, per-step CUDA events, L2 flushed between steps (outside the events) ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    wn.wn_prof_enable(True)
     l0 = wn.wn_launch_count()
     barrier()
     torch.cuda.synchronize()
@@ -203,9 +211,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     barrier()
     launches = wn.wn_launch_count() - l0
-    prof = wn.wn_prof_read()
-    wn.wn_prof_enable(False)
-    ms = float(sum(a.elapsed_time(b) for a, b in ev)) / args.steps
+    ms =float(sum(a.elapsed_time(b) for a, b in ev)) / args.steps
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -229,8 +235,8 @@ def run_ours(args):
     if rank != 0:
         return 0
     # ---- roofline of the dominant kernel class (the treecode traversals) ----
-    trav_ms = sum(prof[k][0] for k in ("trav_A", "trav_AT", "trav_G")) / args.steps
-    trav_launches = sum(prof[k][1] for k in ("trav_A", "trav_AT", "trav_G")) / args.steps
+    trav_ms = sum(prof[k][0] for k in ("trav_A", "trav_AT", "trav_G")) / args.prof_steps
+    trav_launches = sum(prof[k][1] for k in ("trav_A", "trav_AT", "trav_G")) / args.prof_steps
     flops = sum(FLOPS_TEST * work[c]["tests"] + FLOPS_TERM[c] * work[c]["live"] for c in ("A", "AT", "G"))
     achieved = flops / (trav_ms / 1e3) / 1e12
     props = torch.cuda.get_device_properties(dev)
@@ -264,7 +270,7 @@ def run_ours(args):
                                "unit": "source-query interactions/s",
                                "note": "counted = live kernel evaluations (far + leaf) of the traversals; "
                                        "effective_dense = 4 N^2 per iteration (the O(N^2) sums replaced)"},
-        "breakdown_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+        "breakdown_ms_per_step": {k: v[0] / args.prof_steps for k, v in prof.items()},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "treecode traversals (trav_kernel A/AT/G), %.0f launches/step, %.3f ms/step"
@@ -302,6 +308,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-iters", type=int, default=3, help="oracle iterations per sample / reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prof-steps", type=int, default=2, help="untimed steps with per-kernel CUDA events")
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels one by one (no CUDA graph)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

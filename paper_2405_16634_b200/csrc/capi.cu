@@ -30,7 +30,11 @@ wn_status cuda_status(cudaError_t e, const char* what) {
   return e == cudaErrorMemoryAllocation ? WN_ERR_OOM : WN_ERR_CUDA;
 }
 
-void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+static thread_local bool g_capturing = false;  // inside a CUDA-graph capture of the iteration loop
+
+void count_launches(int n) {
+  if (!g_capturing) g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed);
+}
 
 // ---- profiling: CUDA events on the launching stream ----
 struct ProfRec {
@@ -43,6 +47,7 @@ static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
 
 ProfScope::ProfScope(int c, cudaStream_t st, int nlaunch) : cls(c), s(st) {
+  if (g_capturing) return;  // recorded into a graph: counted per graph launch instead
   count_launches(nlaunch);
   if (!g_prof_on) return;
   cudaEventCreate(&a);
@@ -72,6 +77,16 @@ static wn_status check_device() {
   int major = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   if (major != 10) return set_error(WN_ERR_CUDA, "libwn is built for sm_100a (B200); device is not compute 10.x");
+  // keep freed stream-ordered allocations cached in the device pool (tree builds reuse them)
+  static bool pool_done[64] = {false};
+  if (dev < 64 && !pool_done[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_done[dev] = true;
+  }
   return WN_OK;
 }
 
@@ -178,7 +193,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a3.op = OP_A;
     a3.epi = EPI_SQ;
     a3.nodes = transpose ? t->set[1] : t->set[0];
-    a3.attrA = transpose ? t->set[0].A : nullptr;
+    a3.attr = transpose ? t->set[0].rec : nullptr;
     a3.vec = it.r;
     a3.q_begin = q0;
     a3.q_end = q1;
@@ -186,11 +201,6 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     WN_TRY(traverse(a3, s));
     if (comm) WN_TRY(comm_allgather_partials(comm, it.part, stride, t->n, s));
     // α = Σr² / Σ(Ar)²  (Alg. 2), fixed-order reduction of the partials
-    if (it.stats_cap < p.iters) {
-      if (it.dstats) cudaFreeAsync(it.dstats, s);
-      WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)p.iters, s));
-      it.stats_cap = p.iters;
-    }
     alpha_step(it.part, (int)stride, stride, (double)w, it.alpha, it.dstats + 5 * i, s);
     // (4) μ' = μ + α r (fused into the moment build), μ̂ = G_w(μ'), μ = μ̂ |μ'|/|μ̂|
     MomentArgs m4;
@@ -292,7 +302,6 @@ wn_status wn_build_tree(const float* pts, int64_t n, int32_t max_depth, void* st
 
 wn_status wn_tree_destroy(wn_tree t) {
   if (!t) return WN_OK;
-  cudaDeviceSynchronize();
   free_tree(t);
   delete t;
   return WN_OK;
@@ -347,8 +356,10 @@ wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, fl
   if (a) m.a_sorted = dim == 3 ? it.s : (const float*)it.tmp;
   WN_TRY(build_moments(t, m, s));
   const size_t NN = t->nn;
-  if (rep) WN_CUDA(cudaMemcpy2DAsync(rep, 12, t->set[0].R, 16, 12, NN, cudaMemcpyDeviceToDevice, s));
-  if (attr) WN_CUDA(cudaMemcpy2DAsync(attr, 4 * dim, t->set[0].A, 16, 4 * dim, NN, cudaMemcpyDeviceToDevice, s));
+  const size_t pitch = kRec * sizeof(float4);
+  if (rep) WN_CUDA(cudaMemcpy2DAsync(rep, 12, t->set[0].rec, pitch, 12, NN, cudaMemcpyDeviceToDevice, s));
+  if (attr)
+    WN_CUDA(cudaMemcpy2DAsync(attr, 4 * dim, t->set[0].rec + 1, pitch, 4 * dim, NN, cudaMemcpyDeviceToDevice, s));
   if (W) WN_CUDA(cudaMemcpy2DAsync(W, 8, t->sums, 64, 8, NN, cudaMemcpyDeviceToDevice, s));
   return WN_OK;
 }
@@ -482,9 +493,55 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
     return set_error(WN_ERR_ARG, "transpose-mode adjoint is single-GPU only in this build");
   cudaStream_t s = (cudaStream_t)stream;
   WN_TRY(ensure_scratch(t, s));
+  IterScratch& it = t->it;
+  if (it.stats_cap < p->iters) {
+    if (it.dstats) cudaFreeAsync(it.dstats, s);
+    WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)p->iters, s));
+    it.stats_cap = p->iters;
+  }
   const double sc2 = t->xf[3] * t->xf[3];
   gather_vec(t->n, t->perm, mu, sc2, t->it.mu, s);        // μ_norm = scale²·μ
-  WN_TRY(run_iterations(t, *p, comm, s));
+  if (p->flags & WN_FLAG_GRAPH) {
+    // the whole iteration loop as one CUDA graph: captured on a private stream, cached per parameters
+    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm));
+    memcpy(key.data(), p, sizeof(wnnc_params));
+    memcpy(key.data() + sizeof(wnnc_params), &comm, sizeof(comm));
+    if (!t->graph_exec || key != t->graph_key) {
+      if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
+      t->graph_exec = nullptr;
+      if (!t->cap_stream) WN_CUDA(cudaStreamCreateWithFlags(&t->cap_stream, cudaStreamNonBlocking));
+      WN_CUDA(cudaStreamBeginCapture(t->cap_stream, cudaStreamCaptureModeThreadLocal));
+      g_capturing = true;
+      wn_status st = run_iterations(t, *p, comm, t->cap_stream);
+      g_capturing = false;
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(t->cap_stream, &graph);
+      if (st != WN_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (e != cudaSuccess) return cuda_status(e, "cudaStreamEndCapture");
+      size_t nnodes = 0;
+      cudaGraphGetNodes(graph, nullptr, &nnodes);
+      std::vector<cudaGraphNode_t> nodes(nnodes);
+      cudaGraphGetNodes(graph, nodes.data(), &nnodes);
+      t->graph_launches = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaGraphNodeGetType(nd, &ty);
+        t->graph_launches += ty == cudaGraphNodeTypeKernel;
+      }
+      e = cudaGraphInstantiate(&t->graph_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return cuda_status(e, "cudaGraphInstantiate");
+      t->graph_key = key;
+    }
+    ProfScope ps(WN_PROF_OTHER, s, 0);
+    count_launches((int)t->graph_launches);
+    WN_CUDA(cudaGraphLaunch(t->graph_exec, s));
+  } else {
+    WN_TRY(run_iterations(t, *p, comm, s));
+  }
   scatter_vec(t->n, t->perm, t->it.mu, 1.0 / sc2, mu, s);  // back to the input frame
   if (stats) {
     std::vector<double> h(5 * (size_t)p->iters);

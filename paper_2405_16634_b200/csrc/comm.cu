@@ -85,7 +85,7 @@ wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, cudaStre
   }
   ncclResult_t r2 = N.GroupEnd();
   if (r == ncclSuccess) r = r2;
-  count_launches(1);
+
   return nccl_status(r, "ncclBroadcast (all-gather)");
 }
 
@@ -104,7 +104,7 @@ wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64
     }
   ncclResult_t r2 = N.GroupEnd();
   if (r == ncclSuccess) r = r2;
-  count_launches(1);
+
   return nccl_status(r, "ncclBroadcast (partials)");
 }
 

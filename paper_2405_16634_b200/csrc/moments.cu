@@ -5,12 +5,12 @@
 // Readings: Σ|ν| = 0 ⇒ the node's unweighted centroid; a one-point node's rep is the
 // point itself; |ν| is the Euclidean norm (vector) or |s| (scalar).
 //
-// B200 design: ONE launch per build.  A thread per leaf sums its points in fp64, writes the node's
-// fp64 sums and its fp32 traversal record, then walks up: at each parent it bumps an arrival counter
-// and the last-arriving child sums the parent's children IN CHILD ORDER (so the result is
-// deterministic and independent of scheduling), writes the parent and continues.  Counters are
-// reset by the finisher, so the tree carries zeroed counters between builds.  Traffic is O(N + Nn)
-// (≈ 16 B/point read + 64 B/node fp64 sums + 32 B/node record); no per-level launches.
+// B200 design: fp64 node sums (W, P, V) built bottom-up, level-synchronously: one launch sums every
+// leaf over its points (thread per node), then one launch per level (deepest first) sums the children
+// of that level's internal nodes IN CHILD ORDER.  Kernel boundaries order the levels, so there are no
+// fences or atomics and the result is deterministic.  Each node writes its 64-byte traversal record
+// (rep hi + lo, threshold, ν_B, topology code).  Traffic O(N + Nn): ≈ 32 B/point + 64 B sums +
+// 64 B record per node.
 #include <cuda_runtime.h>
 
 #include "wn_internal.cuh"
@@ -29,9 +29,8 @@ __device__ __forceinline__ float thr_of(float theta, int depth) {
 }
 
 template <int KIND>
-__device__ __forceinline__ void write_record(int i, const Sums& S, int cnt, float4 p0, int depth, int topo,
-                                             float theta, const float4* __restrict__ centroid, NodeSet out,
-                                             float4* centroid_out) {
+__device__ __forceinline__ void write_record(int64_t i, const Sums& S, int cnt, float4 p0, int depth, int topo,
+                                             float theta, const float4* __restrict__ centroid, const MomentArgs& m) {
   float4 R, L = make_float4(0.f, 0.f, 0.f, 0.f);
   if (cnt == 1) {
     R = make_float4(p0.x, p0.y, p0.z, -1.0f);
@@ -44,29 +43,37 @@ __device__ __forceinline__ void write_record(int i, const Sums& S, int cnt, floa
       rz = (float)z;
       L = make_float4((float)(x - (double)rx), (float)(y - (double)ry), (float)(z - (double)rz), 0.f);
     } else {
-      float4 c = centroid[i];
+      const float4 c = centroid[i];
       rx = c.x; ry = c.y; rz = c.z;
     }
     R = make_float4(rx, ry, rz, thr_of(theta, depth));
   }
-  if (out.L) out.L[i] = L;
-  out.R[i] = R;
+  float4* rec = m.out.rec + kRec * i;
+  rec[0] = R;
   if (KIND == ATTR_SCALAR)
-    out.A[i] = make_float4((float)S.V[0], 0.f, 0.f, __int_as_float(topo));
+    rec[1] = make_float4((float)S.V[0], 0.f, 0.f, __int_as_float(topo));
   else
-    out.A[i] = make_float4((float)S.V[0], (float)S.V[1], (float)S.V[2], __int_as_float(topo));
-  if (KIND == ATTR_UNIT) centroid_out[i] = make_float4(R.x, R.y, R.z, 0.f);
+    rec[1] = make_float4((float)S.V[0], (float)S.V[1], (float)S.V[2], __int_as_float(topo));
+  rec[2] = L;
+  if (KIND == ATTR_UNIT) m.centroid_out[i] = make_float4(R.x, R.y, R.z, 0.f);
+}
+
+__device__ __forceinline__ void store_sums(double* __restrict__ sums, int64_t i, const Sums& S) {
+  double2* o = reinterpret_cast<double2*>(sums + 8 * i);
+  o[0] = make_double2(S.W, S.P[0]);
+  o[1] = make_double2(S.P[1], S.P[2]);
+  o[2] = make_double2(S.V[0], S.V[1]);
+  o[3] = make_double2(S.V[2], 0.0);
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(256) moments_up(
-    int64_t nn, const float4* __restrict__ pts, const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
-    const int32_t* __restrict__ cb, const int32_t* __restrict__ cc, const int32_t* __restrict__ depth,
-    const int32_t* __restrict__ parent, int32_t* __restrict__ arrive, double* __restrict__ sums,
-    MomentArgs m, const float4* __restrict__ centroid) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) moments_leaves(int64_t nn, const float4* __restrict__ pts,
+                                                      const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
+                                                      const int32_t* __restrict__ cc,
+                                                      const int32_t* __restrict__ depth, double* __restrict__ sums,
+                                                      MomentArgs m, const float4* __restrict__ centroid) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nn || cc[i] != 0) return;
-  // ---- leaf: direct sums over its points ----
   Sums S = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   const int j0 = pb[i], j1 = pe[i];
   float alpha = 0.f;
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(256) moments_up(
     double a, v0 = 0, v1 = 0, v2 = 0;
     if (KIND == ATTR_VEC) {
       float4 v = m.vec[j];
-      if (m.axpy_r) {
+      if (m.axpy_r) {  // μ' = μ + α r (Alg. 2 line 3), fused: written once, read by the G traversal
         const float4 r = m.axpy_r[j];
         v = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
         m.axpy_out[j] = v;
@@ -103,61 +110,59 @@ __global__ void __launch_bounds__(256) moments_up(
     S.V[1] += v1;
     S.V[2] += v2;
   }
-  double* o = sums + 8 * i;
-  o[0] = S.W; o[1] = S.P[0]; o[2] = S.P[1]; o[3] = S.P[2]; o[4] = S.V[0]; o[5] = S.V[1]; o[6] = S.V[2];
-  write_record<KIND>((int)i, S, j1 - j0, pts[j0], depth[i], 8, m.theta, centroid, m.out, m.centroid_out);
+  store_sums(sums, i, S);
+  write_record<KIND>(i, S, j1 - j0, pts[j0], depth[i], 0, m.theta, centroid, m);
   if (KIND == ATTR_UNIT)
     for (int j = j0; j < j1; ++j) m.leaf_of_out[j] = (int32_t)i;
-  // ---- walk up: the last child to arrive finishes the parent ----
-  int node = (int)i;
-  while (true) {
-    const int p = parent[node];
-    if (p < 0) break;
-    __threadfence();
-    const int prev = atomicAdd(&arrive[p], 1);
-    const int nc = cc[p];
-    if (prev != nc - 1) break;
-    arrive[p] = 0;
-    __threadfence();
-    const int c0 = cb[p];
-    Sums T = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-    for (int c = c0; c < c0 + nc; ++c) {
-      const double* s = sums + 8 * (int64_t)c;
-      T.W += __ldcg(s + 0);
-      T.P[0] += __ldcg(s + 1);
-      T.P[1] += __ldcg(s + 2);
-      T.P[2] += __ldcg(s + 3);
-      T.V[0] += __ldcg(s + 4);
-      T.V[1] += __ldcg(s + 5);
-      T.V[2] += __ldcg(s + 6);
-    }
-    double* q = sums + 8 * (int64_t)p;
-    q[0] = T.W; q[1] = T.P[0]; q[2] = T.P[1]; q[3] = T.P[2]; q[4] = T.V[0]; q[5] = T.V[1]; q[6] = T.V[2];
-    const int topo = (c0 << 4) | (nc - 1);
-    write_record<KIND>(p, T, pe[p] - pb[p], make_float4(0, 0, 0, 0), depth[p], topo, m.theta, centroid, m.out,
-                       m.centroid_out);
-    node = p;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) moments_level(int64_t i0, int64_t i1, const int32_t* __restrict__ pb,
+                                                     const int32_t* __restrict__ pe, const int32_t* __restrict__ cb,
+                                                     const int32_t* __restrict__ cc, const int32_t* __restrict__ topo,
+                                                     int depth, double* __restrict__ sums, MomentArgs m,
+                                                     const float4* __restrict__ centroid) {
+  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= i1) return;
+  const int nc = cc[i];
+  if (nc == 0) return;  // leaf: done by moments_leaves
+  const int c0 = cb[i];
+  Sums T = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+  for (int c = c0; c < c0 + nc; ++c) {  // fixed child order ⇒ deterministic sums
+    const double2* s = reinterpret_cast<const double2*>(sums + 8 * (int64_t)c);
+    const double2 a = s[0], b = s[1], d = s[2], e = s[3];
+    T.W += a.x;
+    T.P[0] += a.y;
+    T.P[1] += b.x;
+    T.P[2] += b.y;
+    T.V[0] += d.x;
+    T.V[1] += d.y;
+    T.V[2] += e.x;
+  }
+  store_sums(sums, i, T);
+  write_record<KIND>(i, T, pe[i] - pb[i], make_float4(0, 0, 0, 0), depth, topo[i], m.theta, centroid, m);
+}
+
+template <int KIND>
+void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
+  const int64_t nn = t->nn;
+  moments_leaves<KIND><<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(nn, t->pts, t->pb, t->pe, t->cc, t->depth,
+                                                                      t->sums, m, t->centroid);
+  for (int l = t->depth_used - 1; l >= 0; --l) {
+    const int64_t i0 = t->level_off[l], i1 = t->level_off[l + 1];
+    moments_level<KIND><<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, s>>>(i0, i1, t->pb, t->pe, t->cb, t->cc,
+                                                                           t->topo, l, t->sums, m, t->centroid);
   }
 }
 
 }  // namespace
 
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
-  unsigned g = (unsigned)((t->nn + 255) / 256);
-  ProfScope ps(WN_PROF_MOMENTS, s);
+  ProfScope ps(WN_PROF_MOMENTS, s, 1 + t->depth_used);
   switch (m.kind) {
-    case ATTR_VEC:
-      moments_up<ATTR_VEC><<<g, 256, 0, s>>>(t->nn, t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->parent,
-                                              t->arrive, t->sums, m, t->centroid);
-      break;
-    case ATTR_SCALAR:
-      moments_up<ATTR_SCALAR><<<g, 256, 0, s>>>(t->nn, t->pts, t->pb, t->pe, t->cb, t->cc, t->depth,
-                                                 t->parent, t->arrive, t->sums, m, t->centroid);
-      break;
-    default:
-      moments_up<ATTR_UNIT><<<g, 256, 0, s>>>(t->nn, t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->parent,
-                                               t->arrive, t->sums, m, t->centroid);
-      break;
+    case ATTR_VEC: launch_all<ATTR_VEC>(t, m, s); break;
+    case ATTR_SCALAR: launch_all<ATTR_SCALAR>(t, m, s); break;
+    default: launch_all<ATTR_UNIT>(t, m, s); break;
   }
   WN_CUDA(cudaGetLastError());
   return WN_OK;

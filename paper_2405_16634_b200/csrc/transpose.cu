@@ -36,8 +36,7 @@ __device__ __forceinline__ void warp_add3(float x, float y, float z, double* dst
 }
 
 __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
-    const float4* __restrict__ NR, const float4* __restrict__ NA, const float4* __restrict__ NL,
-    const float4* __restrict__ pts,
+    const float4* __restrict__ G, const float4* __restrict__ pts,
     const int32_t* __restrict__ npb, const int32_t* __restrict__ npe, const float* __restrict__ s_sorted,
     int64_t n, float w2, int stack_depth, double* __restrict__ VB, double* __restrict__ U) {
   extern __shared__ int2 stk_all[];
@@ -61,7 +60,7 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
     const bool mine = ((uint32_t)e.y >> lane) & 1u;
     for (int k = 0; k < ncc; ++k) {
       const int node = cb + k;
-      const float4 R = __ldg(NR + node);
+      const float4 R = __ldg(G + kRec * (int64_t)node);
       const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
       const float d2 = dist2(dx, dy, dz);
       const bool far = d2 > R.w;
@@ -69,7 +68,7 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
       float cx = 0.f, cy = 0.f, cz = 0.f;
       const bool live = mine && far && !(d2 < w2);
       if (live) {  // value at d = (hi − x_q) + lo
-        const float4 Lo = __ldg(NL + node);
+        const float4 Lo = __ldg(G + kRec * (int64_t)node + 2);
         const float ex = dx + Lo.x, ey = dy + Lo.y, ez = dz + Lo.z;
         const float inv = rsqrtf(dist2(ex, ey, ez));
         const float c = sq * inv * inv * inv;
@@ -78,8 +77,8 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
       if (__any_sync(FULL, live)) warp_add3(cx, cy, cz, VB + 3 * (int64_t)node, lane);
       const uint32_t open = __ballot_sync(FULL, mine && !far);
       if (open) {
-        const int topo = __float_as_int(__ldg(NA + node).w);
-        if (!(topo & 8)) {
+        const int topo = __float_as_int(__ldg(G + kRec * (int64_t)node + 1).w);
+        if (topo != 0) {
           if (lane == 0) stk[sp] = make_int2(topo, (int)open);
           ++sp;
         } else {
@@ -150,7 +149,7 @@ wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sor
   {
     ProfScope ps(WN_PROF_TRAV_AT, st, 2);
     scatter_kernel<<<grid, kTravBlock, (size_t)(kTravBlock / 32) * stack_depth * sizeof(int2), st>>>(
-        geo.R, geo.A, geo.L, t->pts, t->pb, t->pe, s_sorted, t->n, w2, stack_depth, t->tvb, t->tu);
+        geo.rec, t->pts, t->pb, t->pe, s_sorted, t->n, w2, stack_depth, t->tvb, t->tu);
     pushdown_kernel<<<grid, kTravBlock, 0, st>>>(t->n, t->leaf_of, t->parent, t->tvb, t->tu, 1.0f, r_out, partial);
   }
   WN_CUDA(cudaGetLastError());

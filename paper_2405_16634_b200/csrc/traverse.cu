@@ -13,14 +13,16 @@
 // B200 design:
 //   * one warp = 32 consecutive Morton-sorted queries; a per-warp shared-memory stack of
 //     (child group, lane mask) entries; every lane takes ITS OWN opening decision (exact per-query
-//     semantics of Alg. 4 — no "open if any lane opens"), the ballot of lanes that open becomes the
-//     mask of the pushed child group;
-//   * node records are broadcast loads (all lanes read the same 2×16 B), L1/L2 resident;
-//   * one-point nodes carry thr = −1 so they always take the representative branch, which equals the
-//     leaf branch exactly (rep = the point, ν_B = ν_j): no leaf loop, no divergence for them;
-//   * the decision and the cutoff are fp32 with the operation sequence d = a − b,
-//     d² = fma(dx,dx, fma(dy,dy, dz·dz)) (DESIGN.md R-prec); A accumulates per child group in fp32
-//     and across groups in fp64 (s = ½ − Aμ cancels near convergence);
+//     semantics of Alg. 4 — no "open if any lane opens"); the ballot of the lanes that open a node
+//     becomes the mask of the pushed child group;
+//   * node records are 64-byte AoS (R | V | L | pad): three broadcast LDG.128 from one L1 line;
+//   * one-point nodes carry thr = −1, so they always take the representative branch (which equals
+//     the leaf branch: rep = the point, ν_B = ν_j); a group whose children are all one-point leaves
+//     (flag in the topology code) runs a test-free, ballot-free loop;
+//   * the kernel term is branch-free (predicated by `live`), rsqrt is one MUFU op (ftz; r ≥ w > 0);
+//   * decisions and cutoff are fp32 on d = hi − x_q, d² = fma(dx,dx, fma(dy,dy, dz·dz))
+//     (DESIGN.md R-prec); the term value uses d = (hi − x_q) + lo; A accumulates per child group in
+//     fp32 and across groups in fp64 (s = ½ − Aμ cancels near convergence);
 //   * epilogues fuse the solver's elementwise work (s = ½ − Aμ, Σ partials, rescale).
 #include <cuda_runtime.h>
 
@@ -35,27 +37,34 @@ __device__ __forceinline__ float dist2(float dx, float dy, float dz) {
   return __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
 }
 
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 template <int OP>
 struct Acc {
   float x = 0.f, y = 0.f, z = 0.f;
   double d = 0.0;
-  __device__ __forceinline__ void term(float dx, float dy, float dz, float d2, const float4& V) {
-    const float inv = rsqrtf(d2);
+  // source at offset e = x_src − x_q (|e|² = e2), attribute V; contributes only if `live`
+  __device__ __forceinline__ void term(bool live, float ex, float ey, float ez, float e2, const float4& V) {
+    const float inv = rsqrt_ftz(live ? e2 : 1.0f);
     if (OP == OP_A) {
-      const float inv3 = inv * inv * inv;
-      x = fmaf(fmaf(dx, V.x, fmaf(dy, V.y, dz * V.z)), inv3, x);
+      const float inv3 = live ? inv * inv * inv : 0.0f;
+      x = fmaf(fmaf(ex, V.x, fmaf(ey, V.y, ez * V.z)), inv3, x);
     } else if (OP == OP_AT) {
-      const float c = -V.x * (inv * inv * inv);
-      x = fmaf(c, dx, x);
-      y = fmaf(c, dy, y);
-      z = fmaf(c, dz, z);
+      const float c = live ? -V.x * (inv * inv * inv) : 0.0f;
+      x = fmaf(c, ex, x);
+      y = fmaf(c, ey, y);
+      z = fmaf(c, ez, z);
     } else {
       const float inv2 = inv * inv;
-      const float inv3 = inv2 * inv;
-      const float t = 3.0f * fmaf(dx, V.x, fmaf(dy, V.y, dz * V.z)) * inv2;
-      x = fmaf(inv3, fmaf(-t, dx, V.x), x);
-      y = fmaf(inv3, fmaf(-t, dy, V.y), y);
-      z = fmaf(inv3, fmaf(-t, dz, V.z), z);
+      const float inv3 = live ? inv2 * inv : 0.0f;
+      const float t = 3.0f * fmaf(ex, V.x, fmaf(ey, V.y, ez * V.z)) * inv2;
+      x = fmaf(inv3, fmaf(-t, ex, V.x), x);
+      y = fmaf(inv3, fmaf(-t, ey, V.y), y);
+      z = fmaf(inv3, fmaf(-t, ez, V.z), z);
     }
   }
   __device__ __forceinline__ void flush() {
@@ -72,7 +81,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-template <int OP, int EPI, bool COUNT>
+// node record address: one 32-bit byte offset from the base (records are 64 B, Nn < 2^26)
+__device__ __forceinline__ const float4* rec_at(const float4* base, int node) {
+  return reinterpret_cast<const float4*>(reinterpret_cast<const char*>(base) + ((uint32_t)node << 6));
+}
+
+template <int OP, int EPI, bool COUNT, bool FROZEN>
 __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
   extern __shared__ int2 stk_all[];
   __shared__ double red[kTravBlock / 32];
@@ -82,60 +96,80 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
   const bool valid = q < a.q_end;
   const float4 xq = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
   const uint32_t active = __ballot_sync(FULL, valid);
-  const float4* __restrict__ NR = a.nodes.R;
-  const float4* __restrict__ NA = a.attrA ? a.attrA : a.nodes.A;
-  const float4* __restrict__ NL = a.nodes.L;
+  const float4* __restrict__ G = a.nodes.rec;             // geometry: R (+0), L (+2)
+  const float4* __restrict__ Vr = FROZEN ? a.attr : G;    // attributes: V (+1)
   const float w2 = a.w2;
   Acc<OP> acc;
   int ntest = 0, nfar = 0, nnear = 0, nlive = 0;
   if (active) {
     int sp = 0;
-    if (lane == 0) stk[0] = make_int2(0, (int)active);  // the root as a group of one: (0 << 4) | 0
+    if (lane == 0) stk[0] = make_int2(0, (int)active);  // the root as a group of one
     sp = 1;
     __syncwarp();
     while (sp > 0) {
       --sp;
       const int2 e = stk[sp];
       __syncwarp();
-      const int cb = e.x >> 4, ncc = (e.x & 7) + 1;
+      const int code = e.x;
+      const int cb = code >> 4, ncc = (code & 7) + 1;
       const bool mine = ((uint32_t)e.y >> lane) & 1u;
-      for (int k = 0; k < ncc; ++k) {
-        const int node = cb + k;
-        const float4 R = __ldg(NR + node);
-        const float4 V = __ldg(NA + node);
-        const float4 Lo = __ldg(NL + node);
-        const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
-        const float d2 = dist2(dx, dy, dz);
-        const bool far = d2 > R.w;
-        if (mine && far && !(d2 < w2)) {  // value at d = (hi − x_q) + lo
-          const float ex = dx + Lo.x, ey = dy + Lo.y, ez = dz + Lo.z;
-          acc.term(ex, ey, ez, dist2(ex, ey, ez), V);
+      if (code & kTopoAllSingle) {
+        // every child is a one-point leaf: the representative branch, no opening test (thr = −1)
+        for (int k = 0; k < ncc; ++k) {
+          const int node = cb + k;
+          const float4* rp = rec_at(G, node);
+          const float4 R = __ldg(rp);
+          const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
+          const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
+          const float d2 = dist2(dx, dy, dz);
+          const bool live = mine && !(d2 < w2);
+          acc.term(live, dx, dy, dz, d2, V);
+          if (COUNT && mine) {
+            ++ntest;
+            ++nfar;
+            nlive += live;
+          }
         }
-        if (COUNT && mine) {
-          ++ntest;
-          nfar += far;
-          nlive += far && !(d2 < w2);
-        }
-        const uint32_t open = __ballot_sync(FULL, mine && !far);
-        if (open) {
-          const int topo = __float_as_int(V.w);
-          if (!(topo & 8)) {
-            if (lane == 0) stk[sp] = make_int2(topo, (int)open);
-            ++sp;
-          } else {  // multi-point leaf (depth D): direct sum for the lanes that opened it
-            const bool lm = (open >> lane) & 1u;
-            const int j1 = a.nrange_pe[node];
-            for (int j = a.nrange_pb[node]; j < j1; ++j) {
-              const float4 P = __ldg(a.pts + j);
-              float4 Vj;
-              if (OP == OP_AT) Vj = make_float4(__ldg(a.scal + j), 0.f, 0.f, 0.f);
-              else Vj = __ldg(a.vec + j);
-              const float ex = __fsub_rn(P.x, xq.x), ey = __fsub_rn(P.y, xq.y), ez = __fsub_rn(P.z, xq.z);
-              const float e2 = dist2(ex, ey, ez);
-              if (lm && !(e2 < w2)) acc.term(ex, ey, ez, e2, Vj);
-              if (COUNT && lm) {
-                ++nnear;
-                nlive += !(e2 < w2);
+      } else {
+        for (int k = 0; k < ncc; ++k) {
+          const int node = cb + k;
+          const float4* rp = rec_at(G, node);
+          const float4 R = __ldg(rp);
+          const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
+          const float4 L = __ldg(rp + 2);
+          const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
+          const float d2 = dist2(dx, dy, dz);
+          const bool far = d2 > R.w;
+          const bool live = mine && far && !(d2 < w2);
+          const float ex = dx + L.x, ey = dy + L.y, ez = dz + L.z;  // value at d = (hi − x_q) + lo
+          acc.term(live, ex, ey, ez, dist2(ex, ey, ez), V);
+          if (COUNT && mine) {
+            ++ntest;
+            nfar += far;
+            nlive += live;
+          }
+          const uint32_t open = __ballot_sync(FULL, mine && !far);
+          if (open) {
+            const int topo = __float_as_int(V.w);
+            if (topo != 0) {
+              if (lane == 0) stk[sp] = make_int2(topo, (int)open);
+              ++sp;
+            } else {  // multi-point leaf (depth D): direct sum for the lanes that opened it
+              const bool lm = (open >> lane) & 1u;
+              const int j1 = a.nrange_pe[node];
+              for (int j = a.nrange_pb[node]; j < j1; ++j) {
+                const float4 P = __ldg(a.pts + j);
+                float4 Vj;
+                if (OP == OP_AT) Vj = make_float4(__ldg(a.scal + j), 0.f, 0.f, 0.f);
+                else Vj = __ldg(a.vec + j);
+                const float px = __fsub_rn(P.x, xq.x), py = __fsub_rn(P.y, xq.y), pz = __fsub_rn(P.z, xq.z);
+                const float p2 = dist2(px, py, pz);
+                const bool lv = lm && !(p2 < w2);
+                acc.term(lv, px, py, pz, p2, Vj);
+                if (COUNT && lm) {
+                  ++nnear;
+                  nlive += lv;
+                }
               }
             }
           }
@@ -169,7 +203,7 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
         a.out_v4[q] = make_float4(vx, vy, vz, 0.f);
         part = (double)vx * vx + (double)vy * vy + (double)vz * vz;
       }
-      if (EPI == EPI_RESCALE) {
+      if (EPI == EPI_RESCALE) {  // μ_i = μ̂_i |μ'_i| / |μ̂_i|, μ'_i kept if |μ̂_i| = 0 (Alg. 3)
         const float4 m = a.mup[q];
         const double hm = sqrt((double)vx * vx + (double)vy * vy + (double)vz * vz);
         const double mm = sqrt((double)m.x * m.x + (double)m.y * m.y + (double)m.z * m.z);
@@ -215,8 +249,14 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
 
 template <int OP, int EPI>
 void launch(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
-  if (a.work || a.qcounts) trav_kernel<OP, EPI, true><<<grid, kTravBlock, smem, s>>>(a);
-  else trav_kernel<OP, EPI, false><<<grid, kTravBlock, smem, s>>>(a);
+  const bool cnt = a.work || a.qcounts;
+  if (OP == OP_A && EPI == EPI_SQ && a.attr) {  // frozen geometry (transpose-mode A(r))
+    if (cnt) trav_kernel<OP, EPI, true, true><<<grid, kTravBlock, smem, s>>>(a);
+    else trav_kernel<OP, EPI, false, true><<<grid, kTravBlock, smem, s>>>(a);
+    return;
+  }
+  if (cnt) trav_kernel<OP, EPI, true, false><<<grid, kTravBlock, smem, s>>>(a);
+  else trav_kernel<OP, EPI, false, false><<<grid, kTravBlock, smem, s>>>(a);
 }
 
 }  // namespace

@@ -319,6 +319,19 @@ __global__ void child_counts(int64_t nn, const int32_t* __restrict__ depth, cons
   if (last) cc[p] = (int32_t)(i - cb[p] + 1);
 }
 
+// traversal code per node: leaf 0; internal (child_begin << 4) | all-children-one-point-leaves << 3 | (count − 1)
+__global__ void topo_codes(int64_t nn, const int32_t* __restrict__ cb, const int32_t* __restrict__ cc,
+                           const int32_t* __restrict__ pb, const int32_t* __restrict__ pe, int32_t* __restrict__ topo) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  const int nc = cc[i];
+  if (nc == 0) { topo[i] = 0; return; }
+  const int c0 = cb[i];
+  int single = 1;
+  for (int c = c0; c < c0 + nc; ++c) single &= (cc[c] == 0) && (pe[c] - pb[c] == 1);
+  topo[i] = (c0 << 4) | (single ? kTopoAllSingle : 0) | (nc - 1);
+}
+
 __global__ void level_pe(int64_t i0, int64_t i1, int64_t n, const int32_t* __restrict__ parent,
                          const int32_t* __restrict__ pb, int32_t* __restrict__ pe) {
   int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -445,23 +458,21 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   WN_TRY(dalloc(&t->cb, nn, s));
   WN_TRY(dalloc(&t->cc, nn, s));
   WN_TRY(dalloc(&t->parent, nn, s));
-  WN_TRY(dalloc(&t->arrive, nn, s));
+  WN_TRY(dalloc(&t->topo, nn, s));
   WN_TRY(dalloc(&t->centroid, nn, s));
   WN_TRY(dalloc(&t->leaf_of, n, s));
   WN_TRY(dalloc(&t->sums, 8 * (size_t)nn, s));
   for (int k = 0; k < 2; ++k) {
-    WN_TRY(dalloc(&t->set[k].R, nn, s));
-    WN_TRY(dalloc(&t->set[k].A, nn, s));
-    WN_TRY(dalloc(&t->set[k].L, nn, s));
+    WN_TRY(dalloc(&t->set[k].rec, (size_t)kRec * nn, s));
+    WN_CUDA(cudaMemsetAsync(t->set[k].rec, 0, sizeof(float4) * kRec * nn, s));
   }
   int64_t* loff = nullptr;
   WN_TRY(dalloc(&loff, t->level_off.size(), s));
   WN_CUDA(cudaMemcpyAsync(loff, t->level_off.data(), t->level_off.size() * sizeof(int64_t),
                           cudaMemcpyHostToDevice, s));
-  WN_CUDA(cudaMemsetAsync(t->arrive, 0, nn * sizeof(int32_t), s));
   {
     unsigned g = (unsigned)((nn + 255) / 256);
-    ProfScope ps(WN_PROF_TREE, s, 3 + used + 1);
+    ProfScope ps(WN_PROF_TREE, s, 4 + used + 1);
     emit_nodes<<<etiles, kEmitThreads, 0, s>>>(t->keys, n, D, etiles, offs, t->depth, t->pb, t->cb, t->cc,
                                                 t->parent);
     find_parents<<<g, 256, 0, s>>>(nn, t->depth, t->pb, loff, t->parent);
@@ -470,6 +481,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
       int64_t i0 = t->level_off[l], i1 = t->level_off[l + 1];
       level_pe<<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, s>>>(i0, i1, n, t->parent, t->pb, t->pe);
     }
+    topo_codes<<<g, 256, 0, s>>>(nn, t->cb, t->cc, t->pb, t->pe, t->topo);
   }
   cudaFreeAsync(loff, s);
   cudaFreeAsync(cnt, s);
@@ -488,11 +500,14 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 
 void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
-                  t->arrive, t->centroid, t->sums, t->set[0].R, t->set[0].A, t->set[0].L, t->set[1].R, t->set[1].A, t->set[1].L,
+                  t->topo, t->centroid, t->sums, t->set[0].rec, t->set[1].rec,
                   t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
                   t->qbuf, t->tvb, t->tu};
+  // stream-ordered frees on the legacy stream: no device-wide synchronization, memory returns to the pool
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
+  if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
+  if (t->cap_stream) cudaStreamDestroy(t->cap_stream);
 }
 
 }  // namespace wn

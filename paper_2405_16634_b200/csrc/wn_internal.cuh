@@ -17,17 +17,18 @@ constexpr float kInv4Pi = 0.0795774715459476679f;  // 1/(4π)
 // Kinds of attribute a moment build aggregates.
 enum AttrKind { ATTR_VEC = 0, ATTR_SCALAR = 1, ATTR_UNIT = 2 };
 
-// One moment build's output: what the traversal reads per node (BFS order).
+// One moment build's output: a 64-byte record per node (BFS order), rec[4·i + {0,1,2,3}]:
 //   R = (x_B, y_B, z_B, thr)   thr = (c·edge)² in fp32, or −1 for a one-point node (always "far":
 //                               rep = the point, ν_B = ν_j, so far and leaf terms coincide)
-//   A = (ν_B.x, ν_B.y, ν_B.z, topo) for vector ν, (s_B, 0, 0, topo) for scalar ν
-//   topo (int bits) = internal: (child_begin << 4) | (child_count − 1);  leaf: 8
+//   V = (ν_B.x, ν_B.y, ν_B.z, topo) for vector ν, (s_B, 0, 0, topo) for scalar ν
 //   L = (x_B − hi, y_B − hi, z_B − hi, 0): the fp32 remainder of the fp64 representative, so a far term is
 //       evaluated at d = (hi − x_q) + lo (error ~1e-7·|d| instead of ulp(x_B)/|d|); decisions use hi only.
+//   X = unused (pads the record to one aligned 64-byte half line)
+// topo (int bits): leaf = 0; internal = (child_begin << 4) | (all children one-point leaves) << 3 | (count − 1)
+constexpr int kRec = 4;  // float4 per record
+constexpr int kTopoAllSingle = 8;
 struct NodeSet {
-  float4* R = nullptr;
-  float4* A = nullptr;
-  float4* L = nullptr;
+  float4* rec = nullptr;
 };
 
 struct IterScratch {
@@ -61,7 +62,7 @@ struct wn_tree_s {
   int32_t* cc = nullptr;        // child count
   int32_t* parent = nullptr;    // −1 for the root
   int32_t* leaf_of = nullptr;   // sorted point → its leaf node
-  int32_t* arrive = nullptr;    // bottom-up arrival counters (kept at 0 between builds)
+  int32_t* topo = nullptr;      // per node traversal code (see NodeSet)
   float4* centroid = nullptr;   // unweighted centroid per node (Σ|ν| = 0 fallback)
   double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
   wn::NodeSet set[2];           // [0] = current attribute, [1] = frozen geometry (transpose mode)
@@ -72,6 +73,11 @@ struct wn_tree_s {
   // transpose-mode accumulators
   double* tvb = nullptr;        // node accumulators V_B (Nn×3, fp64)
   double* tu = nullptr;         // point accumulators U_j (N×3, fp64)
+  // CUDA graph of the iteration loop (WN_FLAG_GRAPH), cached per parameter set
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_launches = 0;  // kernel nodes in the graph
+  std::vector<uint8_t> graph_key;
 };
 
 namespace wn {
@@ -132,7 +138,7 @@ struct TravArgs {
   int op = OP_A;
   int epi = EPI_PLAIN;
   NodeSet nodes;                 // decisions + representative positions + (by default) attributes
-  const float4* attrA = nullptr; // optional override of the far-term attributes (frozen geometry)
+  const float4* attr = nullptr;  // optional override of the records supplying V (frozen geometry)
   const float4* pts = nullptr;   // sorted sources
   const float4* vec = nullptr;   // leaf-point vector attributes (sorted)
   const float* scal = nullptr;   // leaf-point scalar attributes (sorted)

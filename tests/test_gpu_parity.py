@@ -317,3 +317,20 @@ def test_deterministic(wn):
         wn.wnnc_iterate(t, mu, iters=3, total_iters=40)
         outs.append(mu.cpu().numpy())
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_graph_mode_identical(wn):
+    # WN_FLAG_GRAPH captures the iteration loop in a CUDA graph: same kernels, same results
+    p = CLOUDS["torus50k"]()
+    outs = []
+    for flags in (0, wn.WN_FLAG_GRAPH, wn.WN_FLAG_GRAPH):
+        t = wn.wn_build_tree(_cuda(p))
+        mu = torch.zeros(len(p), 3, device="cuda")
+        wn.wnnc_iterate(t, mu, iters=3, total_iters=40, flags=flags)
+        if flags:  # replay of the cached graph on the same tree
+            mu2 = torch.zeros(len(p), 3, device="cuda")
+            wn.wnnc_iterate(t, mu2, iters=3, total_iters=40, flags=flags)
+            np.testing.assert_array_equal(mu.cpu().numpy(), mu2.cpu().numpy())
+        outs.append(mu.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
