@@ -124,6 +124,7 @@ static TravArgs base_args(const wn_tree_s* t, float w2) {
   a.q_end = t->n;
   a.w2 = w2;
   a.stack_depth = stack_depth(t);
+  a.root_single = t->n == 1;
   return a;
 }
 

@@ -30,7 +30,8 @@ __device__ __forceinline__ float thr_of(float theta, int depth) {
 
 template <int KIND>
 __device__ __forceinline__ void write_record(int64_t i, const Sums& S, int cnt, float4 p0, int depth, int topo,
-                                             float theta, const float4* __restrict__ centroid, const MomentArgs& m) {
+                                             int smask, float theta, const float4* __restrict__ centroid,
+                                             const MomentArgs& m) {
   float4 R, L = make_float4(0.f, 0.f, 0.f, 0.f);
   if (cnt == 1) {
     R = make_float4(p0.x, p0.y, p0.z, -1.0f);
@@ -54,6 +55,7 @@ __device__ __forceinline__ void write_record(int64_t i, const Sums& S, int cnt, 
     rec[1] = make_float4((float)S.V[0], 0.f, 0.f, __int_as_float(topo));
   else
     rec[1] = make_float4((float)S.V[0], (float)S.V[1], (float)S.V[2], __int_as_float(topo));
+  L.w = __int_as_float(smask);  // which children are one-point leaves (traversal fast path)
   rec[2] = L;
   if (KIND == ATTR_UNIT) m.centroid_out[i] = make_float4(R.x, R.y, R.z, 0.f);
 }
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(256) moments_leaves(int64_t nn, const float4* 
     S.V[2] += v2;
   }
   store_sums(sums, i, S);
-  write_record<KIND>(i, S, j1 - j0, pts[j0], depth[i], 0, m.theta, centroid, m);
+  write_record<KIND>(i, S, j1 - j0, pts[j0], depth[i], 0, 0, m.theta, centroid, m);
   if (KIND == ATTR_UNIT)
     for (int j = j0; j < j1; ++j) m.leaf_of_out[j] = (int32_t)i;
 }
@@ -120,7 +122,7 @@ template <int KIND>
 __global__ void __launch_bounds__(256) moments_level(int64_t i0, int64_t i1, const int32_t* __restrict__ pb,
                                                      const int32_t* __restrict__ pe, const int32_t* __restrict__ cb,
                                                      const int32_t* __restrict__ cc, const int32_t* __restrict__ topo,
-                                                     int depth, double* __restrict__ sums, MomentArgs m,
+                                                     const int32_t* __restrict__ smask, int depth, double* __restrict__ sums, MomentArgs m,
                                                      const float4* __restrict__ centroid) {
   const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= i1) return;
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(256) moments_level(int64_t i0, int64_t i1, con
     T.V[2] += e.x;
   }
   store_sums(sums, i, T);
-  write_record<KIND>(i, T, pe[i] - pb[i], make_float4(0, 0, 0, 0), depth, topo[i], m.theta, centroid, m);
+  write_record<KIND>(i, T, pe[i] - pb[i], make_float4(0, 0, 0, 0), depth, topo[i], smask[i], m.theta, centroid, m);
 }
 
 template <int KIND>
@@ -151,7 +153,8 @@ void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
   for (int l = t->depth_used - 1; l >= 0; --l) {
     const int64_t i0 = t->level_off[l], i1 = t->level_off[l + 1];
     moments_level<KIND><<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, s>>>(i0, i1, t->pb, t->pe, t->cb, t->cc,
-                                                                           t->topo, l, t->sums, m, t->centroid);
+                                                                           t->topo, t->smask, l, t->sums, m,
+                                                                           t->centroid);
   }
 }
 

@@ -321,15 +321,21 @@ __global__ void child_counts(int64_t nn, const int32_t* __restrict__ depth, cons
 
 // traversal code per node: leaf 0; internal (child_begin << 4) | all-children-one-point-leaves << 3 | (count − 1)
 __global__ void topo_codes(int64_t nn, const int32_t* __restrict__ cb, const int32_t* __restrict__ cc,
-                           const int32_t* __restrict__ pb, const int32_t* __restrict__ pe, int32_t* __restrict__ topo) {
+                           const int32_t* __restrict__ pb, const int32_t* __restrict__ pe, int32_t* __restrict__ topo,
+                           int32_t* __restrict__ smask) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nn) return;
   const int nc = cc[i];
-  if (nc == 0) { topo[i] = 0; return; }
+  if (nc == 0) {
+    topo[i] = 0;
+    smask[i] = 0;
+    return;
+  }
   const int c0 = cb[i];
-  int single = 1;
-  for (int c = c0; c < c0 + nc; ++c) single &= (cc[c] == 0) && (pe[c] - pb[c] == 1);
-  topo[i] = (c0 << 4) | (single ? kTopoAllSingle : 0) | (nc - 1);
+  int single = 0;  // bit k: child k is a one-point leaf
+  for (int c = c0; c < c0 + nc; ++c) single |= ((cc[c] == 0) && (pe[c] - pb[c] == 1)) << (c - c0);
+  topo[i] = (c0 << 4) | (nc - 1);
+  smask[i] = single;
 }
 
 __global__ void level_pe(int64_t i0, int64_t i1, int64_t n, const int32_t* __restrict__ parent,
@@ -459,6 +465,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   WN_TRY(dalloc(&t->cc, nn, s));
   WN_TRY(dalloc(&t->parent, nn, s));
   WN_TRY(dalloc(&t->topo, nn, s));
+  WN_TRY(dalloc(&t->smask, nn, s));
   WN_TRY(dalloc(&t->centroid, nn, s));
   WN_TRY(dalloc(&t->leaf_of, n, s));
   WN_TRY(dalloc(&t->sums, 8 * (size_t)nn, s));
@@ -481,7 +488,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
       int64_t i0 = t->level_off[l], i1 = t->level_off[l + 1];
       level_pe<<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, s>>>(i0, i1, n, t->parent, t->pb, t->pe);
     }
-    topo_codes<<<g, 256, 0, s>>>(nn, t->cb, t->cc, t->pb, t->pe, t->topo);
+    topo_codes<<<g, 256, 0, s>>>(nn, t->cb, t->cc, t->pb, t->pe, t->topo, t->smask);
   }
   cudaFreeAsync(loff, s);
   cudaFreeAsync(cnt, s);
@@ -500,7 +507,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 
 void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
-                  t->topo, t->centroid, t->sums, t->set[0].rec, t->set[1].rec,
+                  t->topo, t->smask, t->centroid, t->sums, t->set[0].rec, t->set[1].rec,
                   t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
                   t->qbuf, t->tvb, t->tu};
   // stream-ordered frees on the legacy stream: no device-wide synchronization, memory returns to the pool

@@ -24,9 +24,8 @@ enum AttrKind { ATTR_VEC = 0, ATTR_SCALAR = 1, ATTR_UNIT = 2 };
 //   L = (x_B − hi, y_B − hi, z_B − hi, 0): the fp32 remainder of the fp64 representative, so a far term is
 //       evaluated at d = (hi − x_q) + lo (error ~1e-7·|d| instead of ulp(x_B)/|d|); decisions use hi only.
 //   X = unused (pads the record to one aligned 64-byte half line)
-// topo (int bits): leaf = 0; internal = (child_begin << 4) | (all children one-point leaves) << 3 | (count − 1)
+// topo (int bits): leaf = 0; internal = (child_begin << 4) | (count − 1); L.w = one-point-leaf child mask
 constexpr int kRec = 4;  // float4 per record
-constexpr int kTopoAllSingle = 8;
 struct NodeSet {
   float4* rec = nullptr;
 };
@@ -63,6 +62,7 @@ struct wn_tree_s {
   int32_t* parent = nullptr;    // −1 for the root
   int32_t* leaf_of = nullptr;   // sorted point → its leaf node
   int32_t* topo = nullptr;      // per node traversal code (see NodeSet)
+  int32_t* smask = nullptr;     // per node: bit k set iff child k is a one-point leaf
   float4* centroid = nullptr;   // unweighted centroid per node (Σ|ν| = 0 fallback)
   double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
   wn::NodeSet set[2];           // [0] = current attribute, [1] = frozen geometry (transpose mode)
@@ -155,6 +155,7 @@ struct TravArgs {
   double* partial = nullptr;        // per-block partials (indexed by global block of 256 queries)
   float w2 = 0.0f;
   int stack_depth = 128;
+  int root_single = 0;              // 1 iff the root is a one-point leaf (n = 1)
   int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
   int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order
 };
