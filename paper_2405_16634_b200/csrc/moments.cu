@@ -5,21 +5,35 @@
 // Readings: Σ|ν| = 0 ⇒ the node's unweighted centroid; a one-point node's rep is the
 // point itself; |ν| is the Euclidean norm (vector) or |s| (scalar).
 //
-// B200 design: fp64 node sums (W, P, V) built bottom-up, level-synchronously: one launch sums every
-// leaf over its points (thread per node), then one launch per level (deepest first) sums the children
-// of that level's internal nodes IN CHILD ORDER.  Kernel boundaries order the levels, so there are no
-// fences or atomics and the result is deterministic.  Each node writes its 64-byte traversal record
-// (rep hi + lo, threshold, ν_B, topology code).  Traffic O(N + Nn): ≈ 32 B/point + 64 B sums +
-// 64 B record per node.
+// B200 design: fp64 node sums (W, P, V) are built bottom-up: a leaf sums its points, an internal node
+// sums its children IN CHILD ORDER (deterministic).  Two launches per build, no fences, no atomics:
+//   1. subtree kernel — the nodes of level `mom_cut` are split into contiguous ranges, one per block;
+//      at every deeper level a block's descendants form one contiguous BFS range (precomputed), so a
+//      block walks its levels deepest-first with __syncthreads() between them;
+//   2. top kernel — one block walks the (few) levels above the cut the same way.
+// Each node writes its 64-byte traversal record (rep hi + lo, threshold, ν_B, topology code).
+// Traffic O(N + Nn): ≈ 32 B/point + 64 B fp64 sums + 64 B record per node.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "wn_internal.cuh"
 
 namespace wn {
 namespace {
 
+constexpr int kMomThreads = 256;
+constexpr int kTopThreads = 1024;
+
 struct Sums {
   double W, P[3], V[3];
+};
+
+struct TreeView {
+  const float4* pts;
+  const int32_t *pb, *pe, *cb, *cc, *depth, *topo, *smask;
+  double* sums;
+  const float4* centroid;
 };
 
 __device__ __forceinline__ float thr_of(float theta, int depth) {
@@ -55,117 +69,161 @@ __device__ __forceinline__ void write_record(int64_t i, const Sums& S, int cnt, 
     rec[1] = make_float4((float)S.V[0], 0.f, 0.f, __int_as_float(topo));
   else
     rec[1] = make_float4((float)S.V[0], (float)S.V[1], (float)S.V[2], __int_as_float(topo));
-  L.w = __int_as_float(smask);  // which children are one-point leaves (traversal fast path)
+  L.w = __int_as_float(smask);  // which children are one-point leaves
   rec[2] = L;
   if (KIND == ATTR_UNIT) m.centroid_out[i] = make_float4(R.x, R.y, R.z, 0.f);
 }
 
-__device__ __forceinline__ void store_sums(double* __restrict__ sums, int64_t i, const Sums& S) {
-  double2* o = reinterpret_cast<double2*>(sums + 8 * i);
+// one node: a leaf sums its points, an internal node its children's fp64 sums (child order)
+template <int KIND>
+__device__ __forceinline__ void process_node(int64_t i, int depth, const TreeView& tv, const MomentArgs& m,
+                                             float alpha) {
+  Sums S = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+  const int nc = tv.cc[i];
+  const int j0 = tv.pb[i], j1 = tv.pe[i];
+  if (nc == 0) {
+    for (int j = j0; j < j1; ++j) {
+      const float4 x = tv.pts[j];
+      double a, v0 = 0, v1 = 0, v2 = 0;
+      if (KIND == ATTR_VEC) {
+        float4 v = m.vec[j];
+        if (m.axpy_r) {  // μ' = μ + α r (Alg. 2 line 3), fused: written once, read by the G traversal
+          const float4 r = m.axpy_r[j];
+          v = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
+          m.axpy_out[j] = v;
+        }
+        v0 = v.x; v1 = v.y; v2 = v.z;
+        if (m.a_sorted) {
+          const double f = m.a_sorted[j];
+          v0 *= f; v1 *= f; v2 *= f;
+        }
+        a = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+      } else if (KIND == ATTR_SCALAR) {
+        v0 = m.scal[j];
+        if (m.a_sorted) v0 *= (double)m.a_sorted[j];
+        a = fabs(v0);
+      } else {
+        a = 1.0;
+        v0 = 1.0;
+        m.leaf_of_out[j] = (int32_t)i;
+      }
+      S.W += a;
+      S.P[0] += a * (double)x.x;
+      S.P[1] += a * (double)x.y;
+      S.P[2] += a * (double)x.z;
+      S.V[0] += v0;
+      S.V[1] += v1;
+      S.V[2] += v2;
+    }
+  } else {
+    const int c0 = tv.cb[i];
+    for (int c = c0; c < c0 + nc; ++c) {
+      const double2* s = reinterpret_cast<const double2*>(tv.sums + 8 * (int64_t)c);
+      const double2 a = s[0], b = s[1], d = s[2], e = s[3];
+      S.W += a.x;
+      S.P[0] += a.y;
+      S.P[1] += b.x;
+      S.P[2] += b.y;
+      S.V[0] += d.x;
+      S.V[1] += d.y;
+      S.V[2] += e.x;
+    }
+  }
+  double2* o = reinterpret_cast<double2*>(tv.sums + 8 * i);
   o[0] = make_double2(S.W, S.P[0]);
   o[1] = make_double2(S.P[1], S.P[2]);
   o[2] = make_double2(S.V[0], S.V[1]);
   o[3] = make_double2(S.V[2], 0.0);
+  const float4 p0 = (j1 - j0 == 1) ? tv.pts[j0] : make_float4(0.f, 0.f, 0.f, 0.f);
+  write_record<KIND>(i, S, j1 - j0, p0, depth, tv.topo[i], tv.smask[i], m.theta, tv.centroid, m);
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(256) moments_leaves(int64_t nn, const float4* __restrict__ pts,
-                                                      const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
-                                                      const int32_t* __restrict__ cc,
-                                                      const int32_t* __restrict__ depth, double* __restrict__ sums,
-                                                      MomentArgs m, const float4* __restrict__ centroid) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nn || cc[i] != 0) return;
-  Sums S = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-  const int j0 = pb[i], j1 = pe[i];
-  float alpha = 0.f;
-  if (KIND == ATTR_VEC && m.axpy_r) alpha = (float)(*m.alpha);
-  for (int j = j0; j < j1; ++j) {
-    const float4 x = pts[j];
-    double a, v0 = 0, v1 = 0, v2 = 0;
-    if (KIND == ATTR_VEC) {
-      float4 v = m.vec[j];
-      if (m.axpy_r) {  // μ' = μ + α r (Alg. 2 line 3), fused: written once, read by the G traversal
-        const float4 r = m.axpy_r[j];
-        v = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
-        m.axpy_out[j] = v;
-      }
-      v0 = v.x; v1 = v.y; v2 = v.z;
-      if (m.a_sorted) {
-        const double f = m.a_sorted[j];
-        v0 *= f; v1 *= f; v2 *= f;
-      }
-      a = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
-    } else if (KIND == ATTR_SCALAR) {
-      v0 = m.scal[j];
-      if (m.a_sorted) v0 *= (double)m.a_sorted[j];
-      a = fabs(v0);
-    } else {
-      a = 1.0;
-      v0 = 1.0;
-    }
-    S.W += a;
-    S.P[0] += a * (double)x.x;
-    S.P[1] += a * (double)x.y;
-    S.P[2] += a * (double)x.z;
-    S.V[0] += v0;
-    S.V[1] += v1;
-    S.V[2] += v2;
+__global__ void __launch_bounds__(kMomThreads) moments_subtrees(TreeView tv, MomentArgs m, const int2* __restrict__ rng,
+                                                                int cut, int deepest) {
+  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
+  const int2* r = rng + (int64_t)blockIdx.x * (kMaxDepth + 1);
+  for (int l = deepest; l >= cut; --l) {
+    const int2 R = r[l];
+    for (int64_t i = R.x + threadIdx.x; i < R.y; i += kMomThreads) process_node<KIND>(i, l, tv, m, alpha);
+    __syncthreads();  // this block's level l is complete before its level l − 1 reads it
   }
-  store_sums(sums, i, S);
-  write_record<KIND>(i, S, j1 - j0, pts[j0], depth[i], 0, 0, m.theta, centroid, m);
-  if (KIND == ATTR_UNIT)
-    for (int j = j0; j < j1; ++j) m.leaf_of_out[j] = (int32_t)i;
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(256) moments_level(int64_t i0, int64_t i1, const int32_t* __restrict__ pb,
-                                                     const int32_t* __restrict__ pe, const int32_t* __restrict__ cb,
-                                                     const int32_t* __restrict__ cc, const int32_t* __restrict__ topo,
-                                                     const int32_t* __restrict__ smask, int depth, double* __restrict__ sums, MomentArgs m,
-                                                     const float4* __restrict__ centroid) {
-  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= i1) return;
-  const int nc = cc[i];
-  if (nc == 0) return;  // leaf: done by moments_leaves
-  const int c0 = cb[i];
-  Sums T = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-  for (int c = c0; c < c0 + nc; ++c) {  // fixed child order ⇒ deterministic sums
-    const double2* s = reinterpret_cast<const double2*>(sums + 8 * (int64_t)c);
-    const double2 a = s[0], b = s[1], d = s[2], e = s[3];
-    T.W += a.x;
-    T.P[0] += a.y;
-    T.P[1] += b.x;
-    T.P[2] += b.y;
-    T.V[0] += d.x;
-    T.V[1] += d.y;
-    T.V[2] += e.x;
+__global__ void __launch_bounds__(kTopThreads) moments_top(TreeView tv, MomentArgs m, const int64_t* __restrict__ loff,
+                                                           int cut) {
+  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
+  for (int l = cut - 1; l >= 0; --l) {
+    for (int64_t i = loff[l] + threadIdx.x; i < loff[l + 1]; i += kTopThreads) process_node<KIND>(i, l, tv, m, alpha);
+    __syncthreads();
   }
-  store_sums(sums, i, T);
-  write_record<KIND>(i, T, pe[i] - pb[i], make_float4(0, 0, 0, 0), depth, topo[i], smask[i], m.theta, centroid, m);
+}
+
+// per block and level: the BFS range of the nodes whose first point lies in the block's point range
+__global__ void plan_ranges(int nblk, int cut, int deepest, int64_t c0, int64_t ncut, const int32_t* __restrict__ pb,
+                            const int32_t* __restrict__ pe, const int64_t* __restrict__ loff, int2* __restrict__ rng) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nblk) return;
+  const int64_t n0 = c0 + ncut * b / nblk, n1 = c0 + ncut * (b + 1) / nblk;
+  for (int l = 0; l <= kMaxDepth; ++l) rng[(int64_t)b * (kMaxDepth + 1) + l] = make_int2(0, 0);
+  if (n1 <= n0) return;
+  const int32_t P0 = pb[n0], P1 = pe[n1 - 1];
+  for (int l = cut; l <= deepest; ++l) {
+    int64_t lo = loff[l], hi = loff[l + 1];
+    // first node with pb ≥ P0, first node with pb ≥ P1 (pb ascending within a level)
+    int64_t a = lo, z = hi;
+    while (a < z) { const int64_t mid = (a + z) >> 1; if (pb[mid] < P0) a = mid + 1; else z = mid; }
+    int64_t a2 = a, z2 = hi;
+    while (a2 < z2) { const int64_t mid = (a2 + z2) >> 1; if (pb[mid] < P1) a2 = mid + 1; else z2 = mid; }
+    rng[(int64_t)b * (kMaxDepth + 1) + l] = make_int2((int)a, (int)a2);
+  }
 }
 
 template <int KIND>
-void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
-  const int64_t nn = t->nn;
-  moments_leaves<KIND><<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(nn, t->pts, t->pb, t->pe, t->cc, t->depth,
-                                                                      t->sums, m, t->centroid);
-  for (int l = t->depth_used - 1; l >= 0; --l) {
-    const int64_t i0 = t->level_off[l], i1 = t->level_off[l + 1];
-    moments_level<KIND><<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, s>>>(i0, i1, t->pb, t->pe, t->cb, t->cc,
-                                                                           t->topo, t->smask, l, t->sums, m,
-                                                                           t->centroid);
-  }
+void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s, const int64_t* loff_dev) {
+  TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->topo, t->smask, t->sums, t->centroid};
+  if (t->mom_blocks > 0)
+    moments_subtrees<KIND><<<t->mom_blocks, kMomThreads, 0, s>>>(tv, m, t->mom_rng, t->mom_cut, t->depth_used);
+  if (t->mom_cut > 0) moments_top<KIND><<<1, kTopThreads, 0, s>>>(tv, m, loff_dev, t->mom_cut);
 }
 
 }  // namespace
 
+wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
+  // cut at the first level with enough nodes to spread over the GPU; small trees: one top block only
+  const int deepest = t->depth_used;
+  int cut = -1;
+  for (int l = 0; l <= deepest; ++l)
+    if (t->level_off[l + 1] - t->level_off[l] >= 4096) {
+      cut = l;
+      break;
+    }
+  WN_CUDA(cudaMallocAsync((void**)&t->mom_loff, t->level_off.size() * sizeof(int64_t), s));
+  WN_CUDA(cudaMemcpyAsync(t->mom_loff, t->level_off.data(), t->level_off.size() * sizeof(int64_t),
+                          cudaMemcpyHostToDevice, s));
+  if (cut < 0) {
+    t->mom_cut = deepest + 1;
+    t->mom_blocks = 0;
+    return WN_OK;
+  }
+  const int64_t c0 = t->level_off[cut], ncut = t->level_off[cut + 1] - c0;
+  t->mom_cut = cut;
+  t->mom_blocks = (int)std::min<int64_t>(ncut / 8, 148 * 8);
+  WN_CUDA(cudaMallocAsync((void**)&t->mom_rng, sizeof(int2) * (size_t)t->mom_blocks * (kMaxDepth + 1), s));
+  plan_ranges<<<(t->mom_blocks + 127) / 128, 128, 0, s>>>(t->mom_blocks, cut, deepest, c0, ncut, t->pb, t->pe,
+                                                          t->mom_loff, t->mom_rng);
+  count_launches(1);
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
-  ProfScope ps(WN_PROF_MOMENTS, s, 1 + t->depth_used);
+  ProfScope ps(WN_PROF_MOMENTS, s, (t->mom_blocks > 0) + (t->mom_cut > 0));
   switch (m.kind) {
-    case ATTR_VEC: launch_all<ATTR_VEC>(t, m, s); break;
-    case ATTR_SCALAR: launch_all<ATTR_SCALAR>(t, m, s); break;
-    default: launch_all<ATTR_UNIT>(t, m, s); break;
+    case ATTR_VEC: launch_all<ATTR_VEC>(t, m, s, t->mom_loff); break;
+    case ATTR_SCALAR: launch_all<ATTR_SCALAR>(t, m, s, t->mom_loff); break;
+    default: launch_all<ATTR_UNIT>(t, m, s, t->mom_loff); break;
   }
   WN_CUDA(cudaGetLastError());
   return WN_OK;

@@ -17,8 +17,7 @@
 //     becomes the mask of the pushed child group;
 //   * node records are 64-byte AoS (R | V | L | pad): three broadcast LDG.128 from one L1 line;
 //   * one-point nodes carry thr = −1, so they always take the representative branch (which equals
-//     the leaf branch: rep = the point, ν_B = ν_j); the stack entry carries a mask of a group's
-//     one-point-leaf children, which run a test-free, ballot-free loop;
+//     the leaf branch: rep = the point, ν_B = ν_j) and are never opened;
 //   * the kernel term is branch-free (predicated by `live`), rsqrt is one MUFU op (ftz; r ≥ w > 0);
 //   * decisions and cutoff are fp32 on d = hi − x_q, d² = fma(dx,dx, fma(dy,dy, dz·dz))
 //     (DESIGN.md R-prec); the term value uses d = (hi − x_q) + lo; A accumulates per child group in
@@ -88,10 +87,10 @@ __device__ __forceinline__ const float4* rec_at(const float4* base, int node) {
 
 template <int OP, int EPI, bool COUNT, bool FROZEN>
 __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
-  extern __shared__ int4 stk_all[];
+  extern __shared__ int2 stk_all[];
   __shared__ double red[kTravBlock / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int4* stk = stk_all + warp * a.stack_depth;
+  int2* stk = stk_all + warp * a.stack_depth;
   const int64_t q = a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
   const bool valid = q < a.q_end;
   const float4 xq = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -103,72 +102,56 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
   int ntest = 0, nfar = 0, nnear = 0, nlive = 0;
   if (active) {
     int sp = 0;
-    // stack entry: (child group code, lane mask, one-point-leaf child mask); the root is a group of one
-    if (lane == 0) stk[0] = make_int4(0, (int)active, a.root_single, 0);
+    if (lane == 0) stk[0] = make_int2(0, (int)active);  // the root as a group of one
     sp = 1;
     __syncwarp();
     while (sp > 0) {
       --sp;
-      const int4 e = stk[sp];
+      const int2 e = stk[sp];
       __syncwarp();
-      const int cb = e.x >> 4, ncc = (e.x & 7) + 1;
+      const int code = e.x;
+      const int cb = code >> 4, ncc = (code & 7) + 1;
       const bool mine = ((uint32_t)e.y >> lane) & 1u;
-      const uint32_t single = (uint32_t)e.z;
-      // (1) one-point-leaf children: always the representative (= the point) branch, no test, no descent
-      for (uint32_t b = single; b; b &= b - 1) {
-        const int node = cb + __ffs(b) - 1;
-        const float4* rp = rec_at(G, node);
-        const float4 R = __ldg(rp);
-        const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
-        const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
-        const float d2 = dist2(dx, dy, dz);
-        const bool live = mine && !(d2 < w2);
-        acc.term(live, dx, dy, dz, d2, V);
-        if (COUNT && mine) {
-          ++ntest;
-          ++nfar;
-          nlive += live;
-        }
-      }
-      // (2) the other children: Alg. 4 per lane
-      for (uint32_t b = ~single & ((1u << ncc) - 1u); b; b &= b - 1) {
-        const int node = cb + __ffs(b) - 1;
-        const float4* rp = rec_at(G, node);
-        const float4 R = __ldg(rp);
-        const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
-        const float4 L = __ldg(rp + 2);
-        const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
-        const float d2 = dist2(dx, dy, dz);
-        const bool far = d2 > R.w;
-        const bool live = mine && far && !(d2 < w2);
-        const float ex = dx + L.x, ey = dy + L.y, ez = dz + L.z;  // value at d = (hi − x_q) + lo
-        acc.term(live, ex, ey, ez, dist2(ex, ey, ez), V);
-        if (COUNT && mine) {
-          ++ntest;
-          nfar += far;
-          nlive += live;
-        }
-        const uint32_t open = __ballot_sync(FULL, mine && !far);
-        if (open) {
-          const int topo = __float_as_int(V.w);
-          if (topo != 0) {
-            if (lane == 0) stk[sp] = make_int4(topo, (int)open, __float_as_int(L.w), 0);
-            ++sp;
-          } else {  // multi-point leaf (depth D): direct sum for the lanes that opened it
-            const bool lm = (open >> lane) & 1u;
-            const int j1 = a.nrange_pe[node];
-            for (int j = a.nrange_pb[node]; j < j1; ++j) {
-              const float4 P = __ldg(a.pts + j);
-              float4 Vj;
-              if (OP == OP_AT) Vj = make_float4(__ldg(a.scal + j), 0.f, 0.f, 0.f);
-              else Vj = __ldg(a.vec + j);
-              const float px = __fsub_rn(P.x, xq.x), py = __fsub_rn(P.y, xq.y), pz = __fsub_rn(P.z, xq.z);
-              const float p2 = dist2(px, py, pz);
-              const bool lv = lm && !(p2 < w2);
-              acc.term(lv, px, py, pz, p2, Vj);
-              if (COUNT && lm) {
-                ++nnear;
-                nlive += lv;
+      {
+        for (int k = 0; k < ncc; ++k) {
+          const int node = cb + k;
+          const float4* rp = rec_at(G, node);
+          const float4 R = __ldg(rp);
+          const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
+          const float4 L = __ldg(rp + 2);
+          const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
+          const float d2 = dist2(dx, dy, dz);
+          const bool far = d2 > R.w;
+          const bool live = mine && far && !(d2 < w2);
+          const float ex = dx + L.x, ey = dy + L.y, ez = dz + L.z;  // value at d = (hi − x_q) + lo
+          acc.term(live, ex, ey, ez, dist2(ex, ey, ez), V);
+          if (COUNT && mine) {
+            ++ntest;
+            nfar += far;
+            nlive += live;
+          }
+          const uint32_t open = __ballot_sync(FULL, mine && !far);
+          if (open) {
+            const int topo = __float_as_int(V.w);
+            if (topo != 0) {
+              if (lane == 0) stk[sp] = make_int2(topo, (int)open);
+              ++sp;
+            } else {  // multi-point leaf (depth D): direct sum for the lanes that opened it
+              const bool lm = (open >> lane) & 1u;
+              const int j1 = a.nrange_pe[node];
+              for (int j = a.nrange_pb[node]; j < j1; ++j) {
+                const float4 P = __ldg(a.pts + j);
+                float4 Vj;
+                if (OP == OP_AT) Vj = make_float4(__ldg(a.scal + j), 0.f, 0.f, 0.f);
+                else Vj = __ldg(a.vec + j);
+                const float px = __fsub_rn(P.x, xq.x), py = __fsub_rn(P.y, xq.y), pz = __fsub_rn(P.z, xq.z);
+                const float p2 = dist2(px, py, pz);
+                const bool lv = lm && !(p2 < w2);
+                acc.term(lv, px, py, pz, p2, Vj);
+                if (COUNT && lm) {
+                  ++nnear;
+                  nlive += lv;
+                }
               }
             }
           }
@@ -264,7 +247,7 @@ wn_status traverse(const TravArgs& a, cudaStream_t s) {
   const int64_t nq = a.q_end - a.q_begin;
   if (nq <= 0) return WN_OK;
   const unsigned grid = (unsigned)trav_blocks(nq);
-  const size_t smem = (size_t)(kTravBlock / 32) * a.stack_depth * sizeof(int4);
+  const size_t smem = (size_t)(kTravBlock / 32) * a.stack_depth * sizeof(int2);
   const int cls = a.op == OP_A ? WN_PROF_TRAV_A : a.op == OP_AT ? WN_PROF_TRAV_AT : WN_PROF_TRAV_G;
   ProfScope ps(cls, s);
   TravArgs b = a;

@@ -65,6 +65,10 @@ struct wn_tree_s {
   int32_t* smask = nullptr;     // per node: bit k set iff child k is a one-point leaf
   float4* centroid = nullptr;   // unweighted centroid per node (Σ|ν| = 0 fallback)
   double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
+  int mom_cut = 0;              // moment builds: levels ≥ mom_cut run as per-block subtrees
+  int mom_blocks = 0;           //   number of subtree blocks
+  int2* mom_rng = nullptr;      //   [block][level] node range (BFS) of each block's subtrees
+  int64_t* mom_loff = nullptr;  //   level offsets on the device
   wn::NodeSet set[2];           // [0] = current attribute, [1] = frozen geometry (transpose mode)
   std::vector<int64_t> level_off;  // host: BFS offset of each level, size depth_used + 2
   wn::IterScratch it;
@@ -124,6 +128,7 @@ struct MomentArgs {
   int32_t* leaf_of_out = nullptr;   // ATTR_UNIT: writes the leaf node of every sorted point
 };
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s);
+wn_status plan_moments(wn_tree_s* t, cudaStream_t s);  // once per tree, after the topology
 
 // ---- traversal (traverse.cu) ----
 enum TravOp { OP_A = 0, OP_AT = 1, OP_G = 2 };
