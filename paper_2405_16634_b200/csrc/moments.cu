@@ -5,9 +5,9 @@
 // Readings: Σ|ν| = 0 ⇒ the node's unweighted centroid; a one-point node's rep is the
 // point itself; |ν| is the Euclidean norm (vector) or |s| (scalar).
 //
-// B200 design: fp64 node sums (W, P, V) are built bottom-up by teams of 8 lanes per node: a leaf sums its
-// points, an internal node its children (one per lane), then a fixed pairwise team reduction
-// (deterministic; all loads of a node in flight at once).  Two launches per build, no fences/atomics:
+// B200 design: fp64 node sums (W, P, V) are built bottom-up: a leaf sums its points, an internal node
+// sums its children IN CHILD ORDER (deterministic; child sums are loaded 4 at a time so their
+// latencies overlap).  Two launches per build, no fences, no atomics:
 //   1. subtree kernel — the nodes of level `mom_cut` are split into contiguous ranges, one per block;
 //      at every deeper level a block's descendants form one contiguous BFS range (precomputed), so a
 //      block walks its levels deepest-first with __syncthreads() between them;
@@ -24,6 +24,7 @@ namespace wn {
 namespace {
 
 constexpr int kMomThreads = 256;
+constexpr int kTopThreads = 512;
 
 struct Sums {
   double W, P[3], V[3];
@@ -74,24 +75,16 @@ __device__ __forceinline__ void write_record(int64_t i, const Sums& S, int cnt, 
   if (KIND == ATTR_UNIT) m.centroid_out[i] = make_float4(R.x, R.y, R.z, 0.f);
 }
 
-__device__ __forceinline__ double team_sum(double v, uint32_t mask) {
-  // pairwise tree over the 8 lanes of a team: every lane ends with the same bits (fixed order)
-  v += __shfl_xor_sync(mask, v, 1);
-  v += __shfl_xor_sync(mask, v, 2);
-  v += __shfl_xor_sync(mask, v, 4);
-  return v;
-}
-
-// one node, processed by a team of 8 lanes (tl = lane in team): a leaf sums its points (lane-strided),
-// an internal node its children's fp64 sums (one child per lane); then a fixed-order team reduction
+// one node per thread: a leaf sums its points, an internal node its children's fp64 sums in child order;
+// the children's sums are loaded 4 at a time so their L2 latencies overlap
 template <int KIND>
 __device__ __forceinline__ void process_node(int64_t i, int depth, const TreeView& tv, const MomentArgs& m,
-                                             float alpha, int tl, uint32_t mask) {
+                                             float alpha) {
   Sums S = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   const int nc = tv.cc[i];
   const int j0 = tv.pb[i], j1 = tv.pe[i];
   if (nc == 0) {
-    for (int j = j0 + tl; j < j1; j += 8) {
+    for (int j = j0; j < j1; ++j) {
       const float4 x = tv.pts[j];
       double a, v0 = 0, v1 = 0, v2 = 0;
       if (KIND == ATTR_VEC) {
@@ -124,17 +117,28 @@ __device__ __forceinline__ void process_node(int64_t i, int depth, const TreeVie
       S.V[1] += v1;
       S.V[2] += v2;
     }
-  } else if (tl < nc) {
-    const double2* c = reinterpret_cast<const double2*>(tv.sums + 8 * (int64_t)(tv.cb[i] + tl));
-    const double2 a = c[0], b = c[1], d = c[2], e = c[3];
-    S.W = a.x; S.P[0] = a.y; S.P[1] = b.x; S.P[2] = b.y; S.V[0] = d.x; S.V[1] = d.y; S.V[2] = e.x;
+  } else {
+    const double2* c = reinterpret_cast<const double2*>(tv.sums + 8 * (int64_t)tv.cb[i]);
+    for (int k0 = 0; k0 < nc; k0 += 4) {
+      double2 q[4][4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k0 + k < nc)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) q[k][u] = c[4 * (k0 + k) + u];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k0 + k < nc) {
+          S.W += q[k][0].x;
+          S.P[0] += q[k][0].y;
+          S.P[1] += q[k][1].x;
+          S.P[2] += q[k][1].y;
+          S.V[0] += q[k][2].x;
+          S.V[1] += q[k][2].y;
+          S.V[2] += q[k][3].x;
+        }
+    }
   }
-  S.W = team_sum(S.W, mask);
-  for (int k = 0; k < 3; ++k) {
-    S.P[k] = team_sum(S.P[k], mask);
-    S.V[k] = team_sum(S.V[k], mask);
-  }
-  if (tl != 0) return;
   double2* o = reinterpret_cast<double2*>(tv.sums + 8 * i);
   o[0] = make_double2(S.W, S.P[0]);
   o[1] = make_double2(S.P[1], S.P[2]);
@@ -149,24 +153,20 @@ __global__ void __launch_bounds__(kMomThreads) moments_subtrees(TreeView tv, Mom
                                                                 int cut, int deepest) {
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
   const int2* r = rng + (int64_t)blockIdx.x * (kMaxDepth + 1);
-  const int team = threadIdx.x >> 3, tl = threadIdx.x & 7;
-  const uint32_t mask = 0xffu << (threadIdx.x & 24);
   for (int l = deepest; l >= cut; --l) {
     const int2 R = r[l];
-    for (int64_t i = R.x + team; i < R.y; i += kMomThreads / 8) process_node<KIND>(i, l, tv, m, alpha, tl, mask);
+    for (int64_t i = R.x + threadIdx.x; i < R.y; i += kMomThreads) process_node<KIND>(i, l, tv, m, alpha);
     __syncthreads();  // this block's level l is complete before its level l − 1 reads it
   }
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kMomThreads) moments_top(TreeView tv, MomentArgs m, const int64_t* __restrict__ loff,
+__global__ void __launch_bounds__(kTopThreads) moments_top(TreeView tv, MomentArgs m, const int64_t* __restrict__ loff,
                                                            int cut) {
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-  const int team = threadIdx.x >> 3, tl = threadIdx.x & 7;
-  const uint32_t mask = 0xffu << (threadIdx.x & 24);
   for (int l = cut - 1; l >= 0; --l) {
     const int64_t i0 = loff[l], i1 = loff[l + 1];
-    for (int64_t i = i0 + team; i < i1; i += kMomThreads / 8) process_node<KIND>(i, l, tv, m, alpha, tl, mask);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += kTopThreads) process_node<KIND>(i, l, tv, m, alpha);
     __syncthreads();
   }
 }
@@ -196,7 +196,7 @@ void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s, const int64_t
   TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->topo, t->smask, t->sums, t->centroid};
   if (t->mom_blocks > 0)
     moments_subtrees<KIND><<<t->mom_blocks, kMomThreads, 0, s>>>(tv, m, t->mom_rng, t->mom_cut, t->depth_used);
-  if (t->mom_cut > 0) moments_top<KIND><<<1, kMomThreads, 0, s>>>(tv, m, loff_dev, t->mom_cut);
+  if (t->mom_cut > 0) moments_top<KIND><<<1, kTopThreads, 0, s>>>(tv, m, loff_dev, t->mom_cut);
 }
 
 }  // namespace
