@@ -220,7 +220,11 @@ wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
   }
   const int64_t c0 = t->level_off[cut], ncut = t->level_off[cut + 1] - c0;
   t->mom_cut = cut;
-  t->mom_blocks = (int)std::min<int64_t>(ncut / 8, 148 * 8);
+  // one wave: every subtree block must be resident at once (the kernel is latency bound per level)
+  int sms = 148, per_sm = 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, moments_subtrees<ATTR_VEC>, kMomThreads, 0);
+  t->mom_blocks = (int)std::min<int64_t>(ncut / 8, (int64_t)sms * std::max(per_sm, 1));
   WN_CUDA(cudaMallocAsync((void**)&t->mom_rng, sizeof(int2) * (size_t)t->mom_blocks * (kMaxDepth + 1), s));
   plan_ranges<<<(t->mom_blocks + 127) / 128, 128, 0, s>>>(t->mom_blocks, cut, deepest, c0, ncut, t->pb, t->pe,
                                                           t->mom_loff, t->mom_rng);
