@@ -7,11 +7,10 @@
 //
 // B200 design: fp64 node sums (W, P, V) are built bottom-up: a leaf sums its points, an internal node
 // sums its children IN CHILD ORDER (deterministic; child sums are loaded 4 at a time so their
-// latencies overlap).  Two launches per build, no fences, no atomics:
-//   1. subtree kernel — the nodes of level `mom_cut` are split into contiguous ranges, one per block;
-//      at every deeper level a block's descendants form one contiguous BFS range (precomputed), so a
-//      block walks its levels deepest-first with __syncthreads() between them;
-//   2. top kernel — one block walks the (few) levels above the cut the same way.
+// latencies overlap).  No fences, no atomics; kernel boundaries order the levels:
+//   1. one launch for every leaf at or below the cut level (the first level with ≥ 1024 nodes);
+//   2. one launch per level, deepest first, for the internal nodes at or below the cut;
+//   3. one single-block launch for the few levels above the cut (__syncthreads() between levels).
 // Each node writes its 64-byte traversal record (rep hi + lo, threshold, ν_B, topology code).
 // Traffic O(N + Nn): ≈ 32 B/point + 64 B fp64 sums + 64 B record per node.
 #include <cuda_runtime.h>
@@ -149,18 +148,6 @@ __device__ __forceinline__ void process_node(int64_t i, int depth, const TreeVie
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kMomThreads) moments_subtrees(TreeView tv, MomentArgs m, const int2* __restrict__ rng,
-                                                                int cut, int deepest) {
-  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-  const int2* r = rng + (int64_t)blockIdx.x * (kMaxDepth + 1);
-  for (int l = deepest; l >= cut; --l) {
-    const int2 R = r[l];
-    for (int64_t i = R.x + threadIdx.x; i < R.y; i += kMomThreads) process_node<KIND>(i, l, tv, m, alpha);
-    __syncthreads();  // this block's level l is complete before its level l − 1 reads it
-  }
-}
-
-template <int KIND>
 __global__ void __launch_bounds__(kTopThreads) moments_top(TreeView tv, MomentArgs m, const int64_t* __restrict__ loff,
                                                            int cut) {
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
@@ -171,70 +158,57 @@ __global__ void __launch_bounds__(kTopThreads) moments_top(TreeView tv, MomentAr
   }
 }
 
-// per block and level: the BFS range of the nodes whose first point lies in the block's point range
-__global__ void plan_ranges(int nblk, int cut, int deepest, int64_t c0, int64_t ncut, const int32_t* __restrict__ pb,
-                            const int32_t* __restrict__ pe, const int64_t* __restrict__ loff, int2* __restrict__ rng) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nblk) return;
-  const int64_t n0 = c0 + ncut * b / nblk, n1 = c0 + ncut * (b + 1) / nblk;
-  for (int l = 0; l <= kMaxDepth; ++l) rng[(int64_t)b * (kMaxDepth + 1) + l] = make_int2(0, 0);
-  if (n1 <= n0) return;
-  const int32_t P0 = pb[n0], P1 = pe[n1 - 1];
-  for (int l = cut; l <= deepest; ++l) {
-    int64_t lo = loff[l], hi = loff[l + 1];
-    // first node with pb ≥ P0, first node with pb ≥ P1 (pb ascending within a level)
-    int64_t a = lo, z = hi;
-    while (a < z) { const int64_t mid = (a + z) >> 1; if (pb[mid] < P0) a = mid + 1; else z = mid; }
-    int64_t a2 = a, z2 = hi;
-    while (a2 < z2) { const int64_t mid = (a2 + z2) >> 1; if (pb[mid] < P1) a2 = mid + 1; else z2 = mid; }
-    rng[(int64_t)b * (kMaxDepth + 1) + l] = make_int2((int)a, (int)a2);
-  }
+// leaves (MODE 0: every leaf in [i0, i1), any level) or internal nodes of one level (MODE 1)
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(kMomThreads) moments_range(TreeView tv, MomentArgs m, int64_t i0, int64_t i1,
+                                                             int level) {
+  const int64_t i = i0 + blockIdx.x * (int64_t)kMomThreads + threadIdx.x;
+  if (i >= i1) return;
+  const bool leaf = tv.cc[i] == 0;
+  if (leaf != (MODE == 0)) return;
+  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
+  process_node<KIND>(i, MODE == 0 ? tv.depth[i] : level, tv, m, alpha);
 }
 
 template <int KIND>
 void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s, const int64_t* loff_dev) {
   TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->topo, t->smask, t->sums, t->centroid};
-  if (t->mom_blocks > 0)
-    moments_subtrees<KIND><<<t->mom_blocks, kMomThreads, 0, s>>>(tv, m, t->mom_rng, t->mom_cut, t->depth_used);
-  if (t->mom_cut > 0) moments_top<KIND><<<1, kTopThreads, 0, s>>>(tv, m, loff_dev, t->mom_cut);
+  const int cut = t->mom_cut;
+  if (cut <= t->depth_used) {
+    // levels ≥ cut: all their leaves in one launch, then one launch per level for the internal nodes
+    const int64_t i0 = t->level_off[cut], nn = t->nn;
+    moments_range<KIND, 0><<<(unsigned)((nn - i0 + kMomThreads - 1) / kMomThreads), kMomThreads, 0, s>>>(
+        tv, m, i0, nn, 0);
+    for (int l = t->depth_used - 1; l >= cut; --l) {
+      const int64_t a = t->level_off[l], b = t->level_off[l + 1];
+      moments_range<KIND, 1><<<(unsigned)((b - a + kMomThreads - 1) / kMomThreads), kMomThreads, 0, s>>>(
+          tv, m, a, b, l);
+    }
+  }
+  // the few levels above the cut: one block, __syncthreads() between levels
+  if (cut > 0) moments_top<KIND><<<1, kTopThreads, 0, s>>>(tv, m, loff_dev, cut);
 }
 
 }  // namespace
 
 wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
-  // cut at the first level with enough nodes to spread over the GPU; small trees: one top block only
+  // cut at the first level with ≥ 1024 nodes: the levels above it run in one block
   const int deepest = t->depth_used;
-  int cut = -1;
+  int cut = deepest + 1;
   for (int l = 0; l <= deepest; ++l)
-    if (t->level_off[l + 1] - t->level_off[l] >= 4096) {
+    if (t->level_off[l + 1] - t->level_off[l] >= 1024) {
       cut = l;
       break;
     }
+  t->mom_cut = cut;
   WN_CUDA(cudaMallocAsync((void**)&t->mom_loff, t->level_off.size() * sizeof(int64_t), s));
   WN_CUDA(cudaMemcpyAsync(t->mom_loff, t->level_off.data(), t->level_off.size() * sizeof(int64_t),
                           cudaMemcpyHostToDevice, s));
-  if (cut < 0) {
-    t->mom_cut = deepest + 1;
-    t->mom_blocks = 0;
-    return WN_OK;
-  }
-  const int64_t c0 = t->level_off[cut], ncut = t->level_off[cut + 1] - c0;
-  t->mom_cut = cut;
-  // one wave: every subtree block must be resident at once (the kernel is latency bound per level)
-  int sms = 148, per_sm = 1;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, moments_subtrees<ATTR_VEC>, kMomThreads, 0);
-  t->mom_blocks = (int)std::min<int64_t>(ncut / 8, (int64_t)sms * std::max(per_sm, 1));
-  WN_CUDA(cudaMallocAsync((void**)&t->mom_rng, sizeof(int2) * (size_t)t->mom_blocks * (kMaxDepth + 1), s));
-  plan_ranges<<<(t->mom_blocks + 127) / 128, 128, 0, s>>>(t->mom_blocks, cut, deepest, c0, ncut, t->pb, t->pe,
-                                                          t->mom_loff, t->mom_rng);
-  count_launches(1);
-  WN_CUDA(cudaGetLastError());
   return WN_OK;
 }
 
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
-  ProfScope ps(WN_PROF_MOMENTS, s, (t->mom_blocks > 0) + (t->mom_cut > 0));
+  ProfScope ps(WN_PROF_MOMENTS, s, (t->mom_cut <= t->depth_used ? 1 + t->depth_used - t->mom_cut : 0) + (t->mom_cut > 0));
   switch (m.kind) {
     case ATTR_VEC: launch_all<ATTR_VEC>(t, m, s, t->mom_loff); break;
     case ATTR_SCALAR: launch_all<ATTR_SCALAR>(t, m, s, t->mom_loff); break;

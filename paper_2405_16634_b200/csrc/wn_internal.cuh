@@ -65,9 +65,7 @@ struct wn_tree_s {
   int32_t* smask = nullptr;     // per node: bit k set iff child k is a one-point leaf
   float4* centroid = nullptr;   // unweighted centroid per node (Σ|ν| = 0 fallback)
   double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
-  int mom_cut = 0;              // moment builds: levels ≥ mom_cut run as per-block subtrees
-  int mom_blocks = 0;           //   number of subtree blocks
-  int2* mom_rng = nullptr;      //   [block][level] node range (BFS) of each block's subtrees
+  int mom_cut = 0;              // moment builds: levels < mom_cut run in one block
   int64_t* mom_loff = nullptr;  //   level offsets on the device
   wn::NodeSet set[2];           // [0] = current attribute, [1] = frozen geometry (transpose mode)
   std::vector<int64_t> level_off;  // host: BFS offset of each level, size depth_used + 2
