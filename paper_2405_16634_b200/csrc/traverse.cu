@@ -112,60 +112,46 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
       const int code = e.x;
       const int cb = code >> 4, ncc = (code & 7) + 1;
       const bool mine = ((uint32_t)e.y >> lane) & 1u;
-      // children two at a time: six loads in flight, one branch per pair (records are padded by one)
-      for (int k = 0; k < ncc; k += 2) {
-        const int n0 = cb + k;
-        const bool two = k + 1 < ncc;
-        const float4* rp = rec_at(G, n0);
-        const float4 R0 = __ldg(rp), L0 = __ldg(rp + 2);
-        const float4 R1 = __ldg(rp + kRec), L1 = __ldg(rp + kRec + 2);
-        const float4* vp = FROZEN ? rec_at(Vr, n0) : rp;
-        const float4 V0 = __ldg(vp + 1), V1 = __ldg(vp + kRec + 1);
-        const bool mine1 = mine && two;
-        const float dx0 = __fsub_rn(R0.x, xq.x), dy0 = __fsub_rn(R0.y, xq.y), dz0 = __fsub_rn(R0.z, xq.z);
-        const float dx1 = __fsub_rn(R1.x, xq.x), dy1 = __fsub_rn(R1.y, xq.y), dz1 = __fsub_rn(R1.z, xq.z);
-        const float d20 = dist2(dx0, dy0, dz0), d21 = dist2(dx1, dy1, dz1);
-        const bool far0 = d20 > R0.w, far1 = d21 > R1.w;
-        const bool live0 = mine && far0 && !(d20 < w2), live1 = mine1 && far1 && !(d21 < w2);
-        const float ex0 = dx0 + L0.x, ey0 = dy0 + L0.y, ez0 = dz0 + L0.z;  // value at d = (hi − x_q) + lo
-        const float ex1 = dx1 + L1.x, ey1 = dy1 + L1.y, ez1 = dz1 + L1.z;
-        acc.term(live0, ex0, ey0, ez0, dist2(ex0, ey0, ez0), V0);
-        acc.term(live1, ex1, ey1, ez1, dist2(ex1, ey1, ez1), V1);
-        if (COUNT) {
-          ntest += mine + mine1;
-          nfar += (mine && far0) + (mine1 && far1);
-          nlive += live0 + live1;
-        }
-        const uint32_t open0 = __ballot_sync(FULL, mine && !far0);
-        const uint32_t open1 = __ballot_sync(FULL, mine1 && !far1);
-        if (open0 | open1) {
-          // an opened child: push its children as a group (lane mask = the lanes that opened it),
-          // or run the direct leaf sum of a multi-point leaf (depth D) for those lanes
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t open = h ? open1 : open0;
-            if (!open) continue;
-            const int node = n0 + h;
-            const int topo = __float_as_int(h ? V1.w : V0.w);
+      {
+        for (int k = 0; k < ncc; ++k) {
+          const int node = cb + k;
+          const float4* rp = rec_at(G, node);
+          const float4 R = __ldg(rp);
+          const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
+          const float4 L = __ldg(rp + 2);
+          const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
+          const float d2 = dist2(dx, dy, dz);
+          const bool far = d2 > R.w;
+          const bool live = mine && far && !(d2 < w2);
+          const float ex = dx + L.x, ey = dy + L.y, ez = dz + L.z;  // value at d = (hi − x_q) + lo
+          acc.term(live, ex, ey, ez, dist2(ex, ey, ez), V);
+          if (COUNT && mine) {
+            ++ntest;
+            nfar += far;
+            nlive += live;
+          }
+          const uint32_t open = __ballot_sync(FULL, mine && !far);
+          if (open) {
+            const int topo = __float_as_int(V.w);
             if (topo != 0) {
               if (lane == 0) stk[sp] = make_int2(topo, (int)open);
               ++sp;
-              continue;
-            }
-            const bool lm = (open >> lane) & 1u;
-            const int j1 = a.nrange_pe[node];
-            for (int j = a.nrange_pb[node]; j < j1; ++j) {
-              const float4 P = __ldg(a.pts + j);
-              float4 Vj;
-              if (OP == OP_AT) Vj = make_float4(__ldg(a.scal + j), 0.f, 0.f, 0.f);
-              else Vj = __ldg(a.vec + j);
-              const float px = __fsub_rn(P.x, xq.x), py = __fsub_rn(P.y, xq.y), pz = __fsub_rn(P.z, xq.z);
-              const float p2 = dist2(px, py, pz);
-              const bool lv = lm && !(p2 < w2);
-              acc.term(lv, px, py, pz, p2, Vj);
-              if (COUNT && lm) {
-                ++nnear;
-                nlive += lv;
+            } else {  // multi-point leaf (depth D): direct sum for the lanes that opened it
+              const bool lm = (open >> lane) & 1u;
+              const int j1 = a.nrange_pe[node];
+              for (int j = a.nrange_pb[node]; j < j1; ++j) {
+                const float4 P = __ldg(a.pts + j);
+                float4 Vj;
+                if (OP == OP_AT) Vj = make_float4(__ldg(a.scal + j), 0.f, 0.f, 0.f);
+                else Vj = __ldg(a.vec + j);
+                const float px = __fsub_rn(P.x, xq.x), py = __fsub_rn(P.y, xq.y), pz = __fsub_rn(P.z, xq.z);
+                const float p2 = dist2(px, py, pz);
+                const bool lv = lm && !(p2 < w2);
+                acc.term(lv, px, py, pz, p2, Vj);
+                if (COUNT && lm) {
+                  ++nnear;
+                  nlive += lv;
+                }
               }
             }
           }
