@@ -251,8 +251,8 @@ def run_ours(args):
     peak = sm_count * 128 * 2 * fmax * 1e6 / 1e12
     traffic = None
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
-    except (OSError, ValueError):
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[args.config]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
         pass
     interactions = sum(work[c]["live"] for c in ("A", "AT", "G"))
     line = {
