@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
           if (open) {
             const int topo = __float_as_int(V.w);
             if (topo != 0) {
-              if (lane == 0) stk[sp] = make_int2(topo, (int)open);
+              stk[sp] = make_int2(topo, (int)open);  // every lane writes the same word: no divergence
               ++sp;
             } else {  // multi-point leaf (depth D): direct sum for the lanes that opened it
               const bool lm = (open >> lane) & 1u;
