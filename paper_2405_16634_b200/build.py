@@ -36,16 +36,17 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, obj: str = OBJ, defines=()) -> str:
+    """Compile every csrc/*.cu and link `lib`.  `defines` (experiments only) are passed as -D flags."""
+    os.makedirs(obj, exist_ok=True)
     hdrs = _headers()
     jobs = []
     objs = []
     for src in _sources():
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
-        objs.append(obj)
-        if force or _stale(obj, [src] + hdrs):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        o = os.path.join(obj, os.path.basename(src)[:-3] + ".o")
+        objs.append(o)
+        if force or _stale(o, [src] + hdrs):
+            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)
@@ -60,10 +61,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for out in ex.map(run, jobs):
             if verbose and out:
                 print(out, file=sys.stderr)
-    if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-lcudart_static", "-lrt", "-lpthread"]
+    if force or jobs or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-ldl", "-lcudart_static", "-lrt", "-lpthread"]
         run(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

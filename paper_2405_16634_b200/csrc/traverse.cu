@@ -86,7 +86,10 @@ __device__ __forceinline__ const float4* rec_at(const float4* base, int node) {
 }
 
 template <int OP, int EPI, bool COUNT, bool FROZEN>
-__global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
+#ifndef WN_EXP_LBMIN
+#define WN_EXP_LBMIN 1
+#endif
+__global__ void __launch_bounds__(kTravBlock, WN_EXP_LBMIN) trav_kernel(const TravArgs a) {
   extern __shared__ int2 stk_all[];
   __shared__ double red[kTravBlock / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -123,7 +126,11 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
           const float d2 = dist2(dx, dy, dz);
           const bool far = d2 > R.w;
           const bool live = mine && far && !(d2 < w2);
+#ifdef WN_EXP_NOLO
+          const float ex = dx, ey = dy, ez = dz;
+#else
           const float ex = dx + L.x, ey = dy + L.y, ez = dz + L.z;  // value at d = (hi − x_q) + lo
+#endif
           acc.term(live, ex, ey, ez, dist2(ex, ey, ez), V);
           if (COUNT && mine) {
             ++ntest;
@@ -157,8 +164,7 @@ __global__ void __launch_bounds__(kTravBlock) trav_kernel(const TravArgs a) {
           }
         }
       }
-      acc.flush();
-      __syncwarp();
+      acc.flush();  // (no trailing __syncwarp: every lane writes the same stack words and reads its own)
     }
   }
   // ---------------- epilogue ----------------

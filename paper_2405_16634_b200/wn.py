@@ -12,7 +12,7 @@ import os
 
 import torch
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwn.so")
+_LIB_PATH = os.environ.get("WN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwn.so")
 if not os.path.exists(_LIB_PATH):
     raise ImportError(f"libwn.so not built ({_LIB_PATH}); run paper_2405_16634_b200.build.build()")
 _L = C.CDLL(_LIB_PATH)

@@ -1,0 +1,16 @@
+"""Build experimental libwn variants (macros) into paper_2405_16634_b200/exp/<name>/libwn.so."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2405_16634_b200 import build as b
+VARIANTS = {
+    "base": [],
+
+    "nosync_lb2": ["WN_EXP_LBMIN=2"],
+    "nosync_lb4": ["WN_EXP_LBMIN=4"],
+    "nosync_nolo": ["WN_EXP_NOLO"],
+}
+names = sys.argv[1:] or list(VARIANTS)
+for n in names:
+    d = os.path.join(b.HERE, "exp", n)
+    b.build(lib=os.path.join(d, "libwn.so"), obj=os.path.join(d, "obj"), defines=VARIANTS[n])
+    print(n, "ok")
