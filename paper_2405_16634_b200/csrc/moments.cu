@@ -9,7 +9,8 @@
 // sums its children IN CHILD ORDER (deterministic; child sums are loaded 4 at a time so their
 // latencies overlap).  No fences, no atomics; kernel boundaries order the levels:
 //   1. one launch for every leaf at or below the cut level (the first level with ≥ 1024 nodes);
-//   2. one launch per level, deepest first, for the internal nodes at or below the cut;
+//   2. one launch per pair of levels, deepest first, for the internal nodes at or below the cut (the
+//      upper level of a pair forms its children's sums from the grandchildren in the same order);
 //   3. one single-block launch for the few levels above the cut (__syncthreads() between levels).
 // Each node writes its 64-byte traversal record (rep hi + lo, threshold, ν_B, topology code).
 // Traffic O(N + Nn): ≈ 32 B/point + 64 B fp64 sums + 64 B record per node.
@@ -76,7 +77,7 @@ __device__ __forceinline__ void write_record(int64_t i, const Sums& S, int cnt, 
 
 // one node per thread: a leaf sums its points, an internal node its children's fp64 sums in child order;
 // the children's sums are loaded 4 at a time so their L2 latencies overlap
-template <int KIND>
+template <int KIND, bool DEEP = false>
 __device__ __forceinline__ void process_node(int64_t i, int depth, const TreeView& tv, const MomentArgs& m,
                                              float alpha) {
   Sums S = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
@@ -115,6 +116,29 @@ __device__ __forceinline__ void process_node(int64_t i, int depth, const TreeVie
       S.V[0] += v0;
       S.V[1] += v1;
       S.V[2] += v2;
+    }
+  } else if (DEEP) {
+    // the children's sums are formed here from the grandchildren (same operations, same order as the
+    // child's own thread), so two levels are finished per launch
+    const int c0 = tv.cb[i];
+    for (int c = c0; c < c0 + nc; ++c) {
+      const int gn = tv.cc[c];
+      Sums C = {0.0, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+      const int g0 = gn ? tv.cb[c] : c;
+      for (int g = g0; g < g0 + (gn ? gn : 1); ++g) {  // a leaf child contributes its stored sums
+        const double2* q = reinterpret_cast<const double2*>(tv.sums + 8 * (int64_t)g);
+        const double2 a = q[0], b = q[1], d = q[2], e = q[3];
+        if (gn) {
+          C.W += a.x; C.P[0] += a.y; C.P[1] += b.x; C.P[2] += b.y; C.V[0] += d.x; C.V[1] += d.y; C.V[2] += e.x;
+        } else {
+          C.W = a.x; C.P[0] = a.y; C.P[1] = b.x; C.P[2] = b.y; C.V[0] = d.x; C.V[1] = d.y; C.V[2] = e.x;
+        }
+      }
+      S.W += C.W;
+      for (int k = 0; k < 3; ++k) {
+        S.P[k] += C.P[k];
+        S.V[k] += C.V[k];
+      }
     }
   } else {
     const double2* c = reinterpret_cast<const double2*>(tv.sums + 8 * (int64_t)tv.cb[i]);
@@ -159,15 +183,19 @@ __global__ void __launch_bounds__(kTopThreads) moments_top(TreeView tv, MomentAr
 }
 
 // leaves (MODE 0: every leaf in [i0, i1), any level) or internal nodes of one level (MODE 1)
+// MODE 0: every leaf in [i0, i1) (any level).  MODE 1: the internal nodes of levels `level` ([imid, i1))
+// and `level − 1` ([i0, imid)) — the latter from their grandchildren.
 template <int KIND, int MODE>
-__global__ void __launch_bounds__(kMomThreads) moments_range(TreeView tv, MomentArgs m, int64_t i0, int64_t i1,
-                                                             int level) {
+__global__ void __launch_bounds__(kMomThreads) moments_range(TreeView tv, MomentArgs m, int64_t i0, int64_t imid,
+                                                             int64_t i1, int level) {
   const int64_t i = i0 + blockIdx.x * (int64_t)kMomThreads + threadIdx.x;
   if (i >= i1) return;
   const bool leaf = tv.cc[i] == 0;
   if (leaf != (MODE == 0)) return;
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-  process_node<KIND>(i, MODE == 0 ? tv.depth[i] : level, tv, m, alpha);
+  if (MODE == 0) process_node<KIND>(i, tv.depth[i], tv, m, alpha);
+  else if (i >= imid) process_node<KIND>(i, level, tv, m, alpha);
+  else process_node<KIND, true>(i, level - 1, tv, m, alpha);
 }
 
 template <int KIND>
@@ -178,11 +206,12 @@ void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s, const int64_t
     // levels ≥ cut: all their leaves in one launch, then one launch per level for the internal nodes
     const int64_t i0 = t->level_off[cut], nn = t->nn;
     moments_range<KIND, 0><<<(unsigned)((nn - i0 + kMomThreads - 1) / kMomThreads), kMomThreads, 0, s>>>(
-        tv, m, i0, nn, 0);
-    for (int l = t->depth_used - 1; l >= cut; --l) {
-      const int64_t a = t->level_off[l], b = t->level_off[l + 1];
+        tv, m, i0, i0, nn, 0);
+    for (int l = t->depth_used - 1; l >= cut; l -= 2) {  // two levels per launch
+      const int lo = l - 1 >= cut ? l - 1 : l;
+      const int64_t a = t->level_off[lo], mid = t->level_off[l], b = t->level_off[l + 1];
       moments_range<KIND, 1><<<(unsigned)((b - a + kMomThreads - 1) / kMomThreads), kMomThreads, 0, s>>>(
-          tv, m, a, b, l);
+          tv, m, a, mid, b, l);
     }
   }
   // the few levels above the cut: one block, __syncthreads() between levels
@@ -208,7 +237,7 @@ wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
 }
 
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
-  ProfScope ps(WN_PROF_MOMENTS, s, (t->mom_cut <= t->depth_used ? 1 + t->depth_used - t->mom_cut : 0) + (t->mom_cut > 0));
+  ProfScope ps(WN_PROF_MOMENTS, s, (t->mom_cut <= t->depth_used ? 1 + (t->depth_used - t->mom_cut + 1) / 2 : 0) + (t->mom_cut > 0));
   switch (m.kind) {
     case ATTR_VEC: launch_all<ATTR_VEC>(t, m, s, t->mom_loff); break;
     case ATTR_SCALAR: launch_all<ATTR_SCALAR>(t, m, s, t->mom_loff); break;
