@@ -125,6 +125,7 @@ static TravArgs base_args(const wn_tree_s* t, float w2) {
   a.w2 = w2;
   a.stack_depth = stack_depth(t);
   a.root_single = t->n == 1;
+  a.qorder = t->qorder;
   return a;
 }
 
@@ -139,6 +140,8 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
   const int64_t stride = it.nblk;
   int64_t q0 = 0, q1 = t->n;
   if (comm) WN_TRY(comm_shard(comm, t->n, &q0, &q1));
+  // multi-GPU shards are contiguous Morton ranges (the exchange sends contiguous rows): no Hilbert schedule
+  const int32_t* qord = comm ? nullptr : t->qorder;
   for (int i = 0; i < p.iters; ++i) {
     const int k = p.first_iter + i;
     const float w = width_at(k, total, (double)p.w_min, (double)p.w_max);
@@ -151,6 +154,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     m1.out = transpose ? t->set[1] : t->set[0];
     WN_TRY(build_moments(t, m1, s));
     TravArgs a1 = base_args(t, w2);
+    a1.qorder = qord;
     a1.op = OP_A;
     a1.epi = EPI_S;
     a1.nodes = m1.out;
@@ -172,6 +176,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
       m2.out = t->set[0];
       WN_TRY(build_moments(t, m2, s));
       TravArgs a2 = base_args(t, w2);
+    a2.qorder = qord;
       a2.op = OP_AT;
       a2.epi = EPI_R;
       a2.nodes = t->set[0];
@@ -191,6 +196,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     m3.out = t->set[0];
     WN_TRY(build_moments(t, m3, s));
     TravArgs a3 = base_args(t, w2);
+    a3.qorder = qord;
     a3.op = OP_A;
     a3.epi = EPI_SQ;
     a3.nodes = transpose ? t->set[1] : t->set[0];
@@ -214,6 +220,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     m4.out = t->set[0];
     WN_TRY(build_moments(t, m4, s));
     TravArgs a4 = base_args(t, w2);
+    a4.qorder = qord;
     a4.op = OP_G;
     a4.epi = EPI_RESCALE;
     a4.nodes = t->set[0];
@@ -402,6 +409,7 @@ static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a,
     ta.queries = t->qbuf;
     ta.q_end = m;
     ta.out_map = nullptr;
+    ta.qorder = nullptr;
   } else {
     ta.out_map = t->perm;
   }

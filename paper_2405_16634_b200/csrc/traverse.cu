@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(kTravBlock, WN_EXP_LBMIN) trav_kernel(const Tr
   __shared__ double red[kTravBlock / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int2* stk = stk_all + warp * a.stack_depth;
-  const int64_t q = a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
-  const bool valid = q < a.q_end;
+  const int64_t kq = a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;  // schedule position
+  const bool valid = kq < a.q_end;
+  const int64_t q = (valid && a.qorder) ? (int64_t)a.qorder[kq] : kq;             // query index
   const float4 xq = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
   const uint32_t active = __ballot_sync(FULL, valid);
   const float4* __restrict__ G = a.nodes.rec;             // geometry: R (+0), L (+2)

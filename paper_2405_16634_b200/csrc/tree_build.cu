@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "wn_internal.cuh"
 
@@ -215,6 +216,39 @@ __global__ void gather_sorted(const float4* __restrict__ xn, const int32_t* __re
   int32_t j = idx[k];
   pts[k] = xn[j];
   perm[k] = j;
+}
+
+// 3-D Hilbert index of a point (Skilling's transpose algorithm) on a 2^kHilbertBits grid of [−1,1]^3
+constexpr int kHilbertBits = 10;
+__global__ void hilbert_keys(const float4* __restrict__ pts, int64_t n, uint64_t* __restrict__ hk,
+                             int32_t* __restrict__ hv) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const float4 p = pts[k];
+  uint32_t X[3] = {quantize(p.x, kHilbertBits), quantize(p.y, kHilbertBits), quantize(p.z, kHilbertBits)};
+  const uint32_t M = 1u << (kHilbertBits - 1);
+  for (uint32_t Q = M; Q > 1; Q >>= 1) {  // inverse undo
+    const uint32_t P = Q - 1;
+    for (int i = 0; i < 3; ++i) {
+      if (X[i] & Q) {
+        X[0] ^= P;
+      } else {
+        const uint32_t t = (X[0] ^ X[i]) & P;
+        X[0] ^= t;
+        X[i] ^= t;
+      }
+    }
+  }
+  for (int i = 1; i < 3; ++i) X[i] ^= X[i - 1];  // Gray encode
+  uint32_t t = 0;
+  for (uint32_t Q = M; Q > 1; Q >>= 1)
+    if (X[2] & Q) t ^= Q - 1;
+  for (int i = 0; i < 3; ++i) X[i] ^= t;
+  uint64_t h = 0;
+  for (int b = kHilbertBits - 1; b >= 0; --b)
+    h = (h << 3) | (((X[0] >> b) & 1u) << 2) | (((X[1] >> b) & 1u) << 1) | ((X[2] >> b) & 1u);
+  hk[k] = h;
+  hv[k] = (int32_t)k;
 }
 
 __device__ __forceinline__ int common_digits(uint64_t a, uint64_t b, int D) {
@@ -422,6 +456,28 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
     gather_sorted<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(xn, v0, n, t->pts, t->perm);
   }
   t->keys = k0;
+  // --- query schedule: the sorted points in Hilbert order (warps get spatially compact query sets;
+  //     a Z-order jump between diagonal octants no longer splits a warp's 32 queries) ---
+  if (!getenv("WN_EXP_NOHILBERT")) {
+    uint64_t* hk = k1;  // reuse the sort buffers
+    int32_t* hv = v0;
+    hilbert_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t->pts, n, hk, hv);
+    uint64_t *ka = hk, *kb = nullptr;
+    int32_t *va = hv, *vb = v1;
+    WN_TRY(dalloc(&kb, n, s));
+    const int hpasses = (3 * kHilbertBits + 7) / 8;
+    ProfScope ps(WN_PROF_TREE, s, 1 + 3 * hpasses);
+    for (int p = 0; p < hpasses; ++p) {
+      radix_hist<<<ntiles, kSortThreads, 0, s>>>(ka, n, 8 * p, ntiles, hist);
+      scan_excl_1block<<<1, 1024, 0, s>>>(hist, hist, (int64_t)256 * ntiles, nullptr);
+      radix_scatter<<<ntiles, kSortThreads, 0, s>>>(ka, va, kb, vb, n, 8 * p, ntiles, hist);
+      std::swap(ka, kb);
+      std::swap(va, vb);
+    }
+    WN_TRY(dalloc(&t->qorder, n, s));
+    WN_CUDA(cudaMemcpyAsync(t->qorder, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    cudaFreeAsync(hk == ka ? kb : ka, s);  // the extra key buffer (k1 is freed below)
+  }
   cudaFreeAsync(k1, s);
   cudaFreeAsync(v0, s);
   cudaFreeAsync(v1, s);
@@ -507,7 +563,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 }
 
 void free_tree(wn_tree_s* t) {
-  void* ptrs[] = {t->pts, t->perm, t->keys, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
+  void* ptrs[] = {t->pts, t->perm, t->keys, t->qorder, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
                   t->topo, t->smask, t->mom_loff, t->centroid, t->sums, t->set[0].rec, t->set[1].rec,
                   t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
                   t->qbuf, t->tvb, t->tu};

@@ -54,6 +54,7 @@ struct wn_tree_s {
   float4* pts = nullptr;        // N normalized points, Morton order (w unused)
   int32_t* perm = nullptr;      // sorted position → caller index
   uint64_t* keys = nullptr;     // sorted keys
+  int32_t* qorder = nullptr;    // query schedule: sorted point indices in Hilbert order (or null)
   int32_t* depth = nullptr;     // per node (BFS)
   int32_t* pb = nullptr;
   int32_t* pe = nullptr;
@@ -148,7 +149,8 @@ struct TravArgs {
   const int32_t* nrange_pb = nullptr;
   const int32_t* nrange_pe = nullptr;
   const float4* queries = nullptr;  // query points (normalized)
-  int64_t q_begin = 0, q_end = 0;   // query index range
+  int64_t q_begin = 0, q_end = 0;   // query index range (positions in the schedule)
+  const int32_t* qorder = nullptr;  // schedule position → query index (null: identity)
   const int32_t* out_map = nullptr; // output index = out_map[q] (perm) or q
   float* out_f = nullptr;
   float4* out_v4 = nullptr;         // float4 output (internal vectors)
