@@ -363,7 +363,6 @@ wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, fl
   }
   if (a) m.a_sorted = dim == 3 ? it.s : (const float*)it.tmp;
   WN_TRY(build_moments(t, m, s));
-  if (W) WN_TRY(export_single_leaf_sums(t, m, s));
   const size_t NN = t->nn;
   const size_t pitch = kRec * sizeof(float4);
   if (rep) WN_CUDA(cudaMemcpy2DAsync(rep, 12, t->set[0].rec, pitch, 12, NN, cudaMemcpyDeviceToDevice, s));

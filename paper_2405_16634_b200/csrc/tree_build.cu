@@ -556,7 +556,6 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   MomentArgs ma;
   ma.kind = ATTR_UNIT;
   ma.out = t->set[1];
-  ma.out2 = t->set[0];
   ma.centroid_out = t->centroid;
   ma.leaf_of_out = t->leaf_of;
   WN_TRY(build_moments(t, ma, s));

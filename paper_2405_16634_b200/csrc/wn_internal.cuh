@@ -123,13 +123,11 @@ struct MomentArgs {
   float4* axpy_out = nullptr;
   float theta = 2.0f;
   NodeSet out;
-  NodeSet out2;                     // ATTR_UNIT: second record set receiving the static one-point records
   float4* centroid_out = nullptr;   // ATTR_UNIT: writes the centroid table
   int32_t* leaf_of_out = nullptr;   // ATTR_UNIT: writes the leaf node of every sorted point
 };
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s);
 wn_status plan_moments(wn_tree_s* t, cudaStream_t s);  // once per tree, after the topology
-wn_status export_single_leaf_sums(wn_tree_s* t, const MomentArgs& m, cudaStream_t s);  // diagnostics
 
 // ---- traversal (traverse.cu) ----
 enum TravOp { OP_A = 0, OP_AT = 1, OP_G = 2 };
