@@ -87,7 +87,7 @@ __device__ __forceinline__ const float4* rec_at(const float4* base, int node) {
 
 template <int OP, int EPI, bool COUNT, bool FROZEN>
 #ifndef WN_EXP_LBMIN
-#define WN_EXP_LBMIN 1
+#define WN_EXP_LBMIN 6  // 6 resident blocks (48 warps) per SM: ≤ 42 registers, no spills; measured best
 #endif
 __global__ void __launch_bounds__(kTravBlock, WN_EXP_LBMIN) trav_kernel(const TravArgs a) {
   extern __shared__ int2 stk_all[];
@@ -117,12 +117,27 @@ __global__ void __launch_bounds__(kTravBlock, WN_EXP_LBMIN) trav_kernel(const Tr
       const int cb = code >> 4, ncc = (code & 7) + 1;
       const bool mine = ((uint32_t)e.y >> lane) & 1u;
       {
+#ifdef WN_EXP_PREFETCH
+        const float4* rp = rec_at(G, cb);
+        const float4* vp = FROZEN ? rec_at(Vr, cb) : rp;
+        float4 Rn = __ldg(rp), Vn = __ldg(vp + 1), Ln = __ldg(rp + 2);
+#endif
         for (int k = 0; k < ncc; ++k) {
           const int node = cb + k;
+#ifdef WN_EXP_PREFETCH
+          // software pipeline: child k+1's record is in flight while child k is evaluated (records padded)
+          const float4 R = Rn, V = Vn, L = Ln;
+          rp += kRec;
+          vp += kRec;
+          Rn = __ldg(rp);
+          Vn = __ldg(vp + 1);
+          Ln = __ldg(rp + 2);
+#else
           const float4* rp = rec_at(G, node);
           const float4 R = __ldg(rp);
           const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
           const float4 L = __ldg(rp + 2);
+#endif
           const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
           const float d2 = dist2(dx, dy, dz);
           const bool far = d2 > R.w;

@@ -526,8 +526,8 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   WN_TRY(dalloc(&t->leaf_of, n, s));
   WN_TRY(dalloc(&t->sums, 8 * (size_t)nn, s));
   for (int k = 0; k < 2; ++k) {
-    WN_TRY(dalloc(&t->set[k].rec, (size_t)kRec * nn, s));
-    WN_CUDA(cudaMemsetAsync(t->set[k].rec, 0, sizeof(float4) * kRec * nn, s));
+    WN_TRY(dalloc(&t->set[k].rec, (size_t)kRec * (nn + 1), s));  // +1: the traversal prefetches one past a group
+    WN_CUDA(cudaMemsetAsync(t->set[k].rec, 0, sizeof(float4) * kRec * (nn + 1), s));
   }
   int64_t* loff = nullptr;
   WN_TRY(dalloc(&loff, t->level_off.size(), s));

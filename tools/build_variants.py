@@ -4,10 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_16634_b200 import build as b
 VARIANTS = {
     "base": [],
-
-    "nosync_lb2": ["WN_EXP_LBMIN=2"],
-    "nosync_lb4": ["WN_EXP_LBMIN=4"],
-    "nosync_nolo": ["WN_EXP_NOLO"],
+    "lb6": ["WN_EXP_LBMIN=6"],
+    "lb7": ["WN_EXP_LBMIN=7"],
+    "lb8": ["WN_EXP_LBMIN=8"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
