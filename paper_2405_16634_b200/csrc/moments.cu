@@ -142,15 +142,19 @@ __device__ __forceinline__ void process_node(int64_t i, int depth, const TreeVie
     }
   } else {
     const double2* c = reinterpret_cast<const double2*>(tv.sums + 8 * (int64_t)tv.cb[i]);
-    for (int k0 = 0; k0 < nc; k0 += 4) {
-      double2 q[4][4];
+#ifndef WN_EXP_MOM_BATCH
+#define WN_EXP_MOM_BATCH 2
+#endif
+    constexpr int B = WN_EXP_MOM_BATCH;
+    for (int k0 = 0; k0 < nc; k0 += B) {
+      double2 q[B][4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < B; ++k)
         if (k0 + k < nc)
 #pragma unroll
           for (int u = 0; u < 4; ++u) q[k][u] = c[4 * (k0 + k) + u];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < B; ++k)
         if (k0 + k < nc) {
           S.W += q[k][0].x;
           S.P[0] += q[k][0].y;
@@ -186,7 +190,10 @@ __global__ void __launch_bounds__(kTopThreads) moments_top(TreeView tv, MomentAr
 // MODE 0: every leaf in [i0, i1) (any level).  MODE 1: the internal nodes of levels `level` ([imid, i1))
 // and `level − 1` ([i0, imid)) — the latter from their grandchildren.
 template <int KIND, int MODE>
-__global__ void __launch_bounds__(kMomThreads) moments_range(TreeView tv, MomentArgs m, int64_t i0, int64_t imid,
+#ifndef WN_EXP_MOM_LB
+#define WN_EXP_MOM_LB 4
+#endif
+__global__ void __launch_bounds__(kMomThreads, WN_EXP_MOM_LB) moments_range(TreeView tv, MomentArgs m, int64_t i0, int64_t imid,
                                                              int64_t i1, int level) {
   const int64_t i = i0 + blockIdx.x * (int64_t)kMomThreads + threadIdx.x;
   if (i >= i1) return;
