@@ -140,8 +140,9 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
   const int64_t stride = it.nblk;
   int64_t q0 = 0, q1 = t->n;
   if (comm) WN_TRY(comm_shard(comm, t->n, &q0, &q1));
-  // multi-GPU shards are contiguous Morton ranges (the exchange sends contiguous rows): no Hilbert schedule
-  const int32_t* qord = comm ? nullptr : t->qorder;
+  // queries follow the Hilbert schedule; multi-GPU shards are schedule ranges (exchanged via staging)
+  const int32_t* qord = t->qorder;
+  float* stage = (float*)it.tmp;  // n × 4 floats
   for (int i = 0; i < p.iters; ++i) {
     const int k = p.first_iter + i;
     const float w = width_at(k, total, (double)p.w_min, (double)p.w_max);
@@ -164,7 +165,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a1.out_f = it.s;
     a1.partial = it.part;
     WN_TRY(traverse(a1, s));
-    if (comm) WN_TRY(comm_allgather_f(comm, it.s, 1, t->n, s));
+    if (comm) WN_TRY(comm_allgather_f(comm, it.s, 1, t->n, qord, stage, s));
     // (2) r = A_wᵀ s  (+ Σ|r|² partials)
     if (transpose) {
       WN_TRY(adjoint_transpose(t, t->set[1], it.s, w2, it.r, it.part + stride, s));
@@ -186,7 +187,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
       a2.out_v4 = it.r;
       a2.partial = it.part + stride;
       WN_TRY(traverse(a2, s));
-      if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.r, 4, t->n, s));
+      if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.r, 4, t->n, qord, stage, s));
     }
     // (3) Σ (A_w r)²  — gather: r's own representatives; transpose: μ's frozen geometry
     MomentArgs m3;
@@ -230,7 +231,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a4.q_end = q1;
     a4.out_v4 = it.mu;
     WN_TRY(traverse(a4, s));
-    if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, s));
+    if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, s));
   }
   return WN_OK;
 }

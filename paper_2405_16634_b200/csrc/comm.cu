@@ -75,17 +75,47 @@ wn_status comm_shard(wn_comm c, int64_t n, int64_t* q0, int64_t* q1) {
   return wn_shard_range(n, c->rank, c->world, q0, q1);
 }
 
-wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, cudaStream_t s) {
+namespace {
+// schedule-ordered staging: stage[k] = buf[qorder[k]] (pack the owned range) and the inverse (unpack)
+__global__ void k_pack(const float* __restrict__ buf, const int32_t* __restrict__ qorder, int64_t b, int64_t e,
+                       int comps, float* __restrict__ stage) {
+  const int64_t k = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= e) return;
+  const int64_t q = qorder[k];
+  for (int c = 0; c < comps; ++c) stage[k * comps + c] = buf[q * comps + c];
+}
+__global__ void k_unpack(const float* __restrict__ stage, const int32_t* __restrict__ qorder, int64_t n, int comps,
+                         float* __restrict__ buf) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t q = qorder[k];
+  for (int c = 0; c < comps; ++c) buf[q * comps + c] = stage[k * comps + c];
+}
+}  // namespace
+
+wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, const int32_t* qorder, float* stage,
+                           cudaStream_t s) {
   Nccl& N = nccl();
+  float* x = buf;
+  if (qorder) {  // the owned rows are a schedule range: gather them into schedule order first
+    int64_t b = 0, e = 0;
+    wn_shard_range(n, c->rank, c->world, &b, &e);
+    if (e > b) k_pack<<<(unsigned)((e - b + 255) / 256), 256, 0, s>>>(buf, qorder, b, e, comps, stage);
+    count_launches(1);
+    x = stage;
+  }
   ncclResult_t r = N.GroupStart();
   for (int k = 0; k < c->world && r == ncclSuccess; ++k) {
     int64_t b = 0, e = 0;
     wn_shard_range(n, k, c->world, &b, &e);
-    if (e > b) r = N.Broadcast(buf + b * comps, buf + b * comps, (size_t)(e - b) * comps, ncclFloat32, k, c->comm, s);
+    if (e > b) r = N.Broadcast(x + b * comps, x + b * comps, (size_t)(e - b) * comps, ncclFloat32, k, c->comm, s);
   }
   ncclResult_t r2 = N.GroupEnd();
   if (r == ncclSuccess) r = r2;
-
+  if (r == ncclSuccess && qorder) {
+    k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(stage, qorder, n, comps, buf);
+    count_launches(1);
+  }
   return nccl_status(r, "ncclBroadcast (all-gather)");
 }
 

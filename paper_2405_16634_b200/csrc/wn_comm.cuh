@@ -8,8 +8,10 @@
 
 namespace wn {
 wn_status comm_shard(wn_comm c, int64_t n, int64_t* q0, int64_t* q1);
-// Every rank owns rows [q0, q1) of a sorted-order array of n rows × comps floats; make it whole on all ranks.
-wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, cudaStream_t s);
+// Every rank owns the rows of schedule positions [q0, q1) of a sorted-order array of n rows × comps floats
+// (row = qorder[k], or k when qorder is null); make it whole on all ranks.  stage: n × comps scratch.
+wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, const int32_t* qorder, float* stage,
+                           cudaStream_t s);
 // The three per-block partial arrays (stride entries each, blocks of WN_SHARD_ALIGN queries).
 wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64_t n, cudaStream_t s);
 }  // namespace wn

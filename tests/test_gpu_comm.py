@@ -1,0 +1,45 @@
+"""The NCCL exchange path of wnnc_iterate on the one GPU of this run (a world-size-1 communicator):
+every collective runs (grouped broadcasts, schedule pack / unpack, partial exchange) and the trajectory
+must be bit-identical to the single-GPU path.  Multi-rank logic: tests/test_multirank_cpu.py."""
+import numpy as np
+import pytest
+
+from paper_2405_16634_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def wn():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2405_16634_b200.wn as wn
+
+    return wn
+
+
+def test_world1_comm_matches_single_gpu(wn):
+    uid = wn.wn_comm_unique_id()
+    assert len(uid) == 128
+    comm = wn.wn_comm_init(0, 1, uid)
+    p = torch.from_numpy(synth.config("C2")["points"]).cuda()
+    outs = []
+    for c in (None, comm, comm):
+        t = wn.wn_build_tree(p)
+        mu = torch.zeros(len(p), 3, device="cuda")
+        st = wn.wnnc_iterate(t, mu, comm=c, stats=True, iters=4, total_iters=40,
+                             flags=wn.WN_FLAG_GRAPH if c is not None and outs and len(outs) == 2 else 0)
+        outs.append((mu.cpu().numpy(), [s["alpha"] for s in st]))
+    for m, a in outs[1:]:
+        np.testing.assert_array_equal(m, outs[0][0])
+        assert a == outs[0][1]
+    with pytest.raises(wn.WnError, match="ARG"):
+        t = wn.wn_build_tree(p)
+        wn.wnnc_iterate(t, torch.zeros(len(p), 3, device="cuda"), comm=comm, adjoint_mode=wn.WN_ADJ_TRANSPOSE)
+    comm.close()
+
+
+def test_comm_init_errors(wn):
+    with pytest.raises(wn.WnError, match="ARG"):
+        wn.wn_comm_init(2, 2, bytes(128))
