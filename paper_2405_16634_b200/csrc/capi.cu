@@ -403,14 +403,17 @@ static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a,
     if (m == 0) return WN_OK;
     if (t->qcap < m) {
       if (t->qbuf) cudaFreeAsync(t->qbuf, s);
+      if (t->qbuf_order) cudaFreeAsync(t->qbuf_order, s);
       WN_CUDA(cudaMallocAsync((void**)&t->qbuf, m * sizeof(float4), s));
+      WN_CUDA(cudaMallocAsync((void**)&t->qbuf_order, m * sizeof(int32_t), s));
       t->qcap = m;
     }
     normalize_queries(m, q, t->xf, t->qbuf, s);
+    WN_TRY(hilbert_schedule(t->qbuf, m, t->qbuf_order, s));  // coherent warps for arbitrary queries (f1)
     ta.queries = t->qbuf;
     ta.q_end = m;
     ta.out_map = nullptr;
-    ta.qorder = nullptr;
+    ta.qorder = t->qbuf_order;
   } else {
     ta.out_map = t->perm;
   }

@@ -398,6 +398,39 @@ wn_status dalloc(T** p, size_t count, cudaStream_t s) {
     if (st_ != WN_OK) return st_;       \
   } while (0)
 
+wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s) {
+  if (n <= 0) return WN_OK;
+  const int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+  uint64_t *ka = nullptr, *kb = nullptr;
+  int32_t *va = nullptr, *vb = nullptr;
+  uint32_t* hist = nullptr;
+  WN_TRY(dalloc(&ka, n, s));
+  WN_TRY(dalloc(&kb, n, s));
+  WN_TRY(dalloc(&va, n, s));
+  WN_TRY(dalloc(&vb, n, s));
+  WN_TRY(dalloc(&hist, (size_t)256 * ntiles, s));
+  const int hpasses = (3 * kHilbertBits + 7) / 8;
+  {
+    ProfScope ps(WN_PROF_TREE, s, 1 + 3 * hpasses);
+    hilbert_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pts, n, ka, va);
+    for (int p = 0; p < hpasses; ++p) {
+      radix_hist<<<ntiles, kSortThreads, 0, s>>>(ka, n, 8 * p, ntiles, hist);
+      scan_excl_1block<<<1, 1024, 0, s>>>(hist, hist, (int64_t)256 * ntiles, nullptr);
+      radix_scatter<<<ntiles, kSortThreads, 0, s>>>(ka, va, kb, vb, n, 8 * p, ntiles, hist);
+      std::swap(ka, kb);
+      std::swap(va, vb);
+    }
+  }
+  WN_CUDA(cudaMemcpyAsync(order, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  cudaFreeAsync(ka, s);
+  cudaFreeAsync(kb, s);
+  cudaFreeAsync(va, s);
+  cudaFreeAsync(vb, s);
+  cudaFreeAsync(hist, s);
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
 wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree_s* t) {
   t->n = n;
   t->D = D;
@@ -459,24 +492,8 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   // --- query schedule: the sorted points in Hilbert order (warps get spatially compact query sets;
   //     a Z-order jump between diagonal octants no longer splits a warp's 32 queries) ---
   if (!getenv("WN_EXP_NOHILBERT")) {
-    uint64_t* hk = k1;  // reuse the sort buffers
-    int32_t* hv = v0;
-    hilbert_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t->pts, n, hk, hv);
-    uint64_t *ka = hk, *kb = nullptr;
-    int32_t *va = hv, *vb = v1;
-    WN_TRY(dalloc(&kb, n, s));
-    const int hpasses = (3 * kHilbertBits + 7) / 8;
-    ProfScope ps(WN_PROF_TREE, s, 1 + 3 * hpasses);
-    for (int p = 0; p < hpasses; ++p) {
-      radix_hist<<<ntiles, kSortThreads, 0, s>>>(ka, n, 8 * p, ntiles, hist);
-      scan_excl_1block<<<1, 1024, 0, s>>>(hist, hist, (int64_t)256 * ntiles, nullptr);
-      radix_scatter<<<ntiles, kSortThreads, 0, s>>>(ka, va, kb, vb, n, 8 * p, ntiles, hist);
-      std::swap(ka, kb);
-      std::swap(va, vb);
-    }
     WN_TRY(dalloc(&t->qorder, n, s));
-    WN_CUDA(cudaMemcpyAsync(t->qorder, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    cudaFreeAsync(hk == ka ? kb : ka, s);  // the extra key buffer (k1 is freed below)
+    WN_TRY(hilbert_schedule(t->pts, n, t->qorder, s));
   }
   cudaFreeAsync(k1, s);
   cudaFreeAsync(v0, s);
@@ -566,7 +583,7 @@ void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->qorder, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
                   t->topo, t->smask, t->mom_loff, t->centroid, t->sums, t->set[0].rec, t->set[1].rec,
                   t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
-                  t->qbuf, t->tvb, t->tu};
+                  t->qbuf, t->qbuf_order, t->tvb, t->tu};
   // stream-ordered frees on the legacy stream: no device-wide synchronization, memory returns to the pool
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, 0);

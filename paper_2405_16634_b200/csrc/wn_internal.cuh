@@ -72,6 +72,7 @@ struct wn_tree_s {
   std::vector<int64_t> level_off;  // host: BFS offset of each level, size depth_used + 2
   wn::IterScratch it;
   float4* qbuf = nullptr;       // normalized arbitrary queries
+  int32_t* qbuf_order = nullptr;  // their Hilbert schedule
   int64_t qcap = 0;
   // transpose-mode accumulators
   double* tvb = nullptr;        // node accumulators V_B (Nn×3, fp64)
@@ -108,6 +109,8 @@ int64_t* work_counters(int cls);  // device counters of a traversal class, or nu
 // ---- tree build (tree_build.cu) ----
 wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree_s* t);
 void free_tree(wn_tree_s* t);
+// order[k] = index of the k-th of n points along a 3-D Hilbert curve of [−1,1]^3 (query schedule)
+wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s);
 
 // ---- moments (moments.cu) ----
 // Build node records for attribute `kind` into `out`.  vec: float4 ν (sorted order), scal: float s.
