@@ -293,7 +293,8 @@ wn_status wn_build_tree(const float* pts, int64_t n, int32_t max_depth, void* st
   if (n < 1) return set_error(WN_ERR_EMPTY, "empty point set (n < 1)");
   if (!pts) return set_error(WN_ERR_ARG, "pts is NULL");
   if (max_depth < 1 || max_depth > kMaxDepth) return set_error(WN_ERR_ARG, "max_depth must be in [1, 21]");
-  if (n > (int64_t)1 << 27) return set_error(WN_ERR_ARG, "n > 2^27 points is not supported");
+  // 32-bit node byte offsets in the traversal (64-B records) bound the node count: n ≤ 2^25 points
+  if (n > (int64_t)1 << 25) return set_error(WN_ERR_ARG, "n > 2^25 points is not supported");
   WN_TRY(check_device());
   wn_tree_s* t = new (std::nothrow) wn_tree_s();
   if (!t) return set_error(WN_ERR_OOM, "host allocation failed");
