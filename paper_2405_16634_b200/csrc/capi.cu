@@ -364,6 +364,7 @@ wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, fl
     m.scal = it.s;
   }
   if (a) m.a_sorted = dim == 3 ? it.s : (const float*)it.tmp;
+  m.write_W = W != nullptr;
   WN_TRY(build_moments(t, m, s));
   const size_t NN = t->nn;
   const size_t pitch = kRec * sizeof(float4);

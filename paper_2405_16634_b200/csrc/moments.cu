@@ -205,6 +205,272 @@ __global__ void __launch_bounds__(kMomThreads, WN_EXP_MOM_LB) moments_range(Tree
   else process_node<KIND, true>(i, level - 1, tv, m, alpha);
 }
 
+// ---------------- prefix-difference builds (per-iteration attributes: ATTR_VEC, ATTR_SCALAR) ----------------
+// Every node B covers a contiguous range [pb, pe) of the Morton-sorted points, so its sums are
+// E[pe] − E[pb] of one exclusive prefix E over the points' (|ν|, |ν|x, ν) — no level-by-level chain:
+// one scan (3 launches) and one fully parallel node launch.  E is double-double (hi + lo, error-free
+// two-sum adds; lo stored in fp32), so a difference keeps ≈ 2^-77·|Σ_all| accuracy — far below the bottom-up fp64
+// rounding — and an exact integer count of the points with |ν| > 0 decides Σ|ν| = 0 (⇒ centroid)
+// exactly.  One-point nodes take their point's own values (exact: rep = the point).  DESIGN.md §Moments.
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+constexpr int kScanTopThreads = 256;
+// prefix entry j (exclusive: points [0, j)): hi[8] = (W, P, V, count) fp64 in E_hi, lo[8] = the
+// double-double low parts rounded to fp32 in E_lo (|lo| ≤ ulp(hi)/2, so fp32 keeps ≈ 2^-77 relative)
+
+struct DD {
+  double hi, lo;
+};
+
+// two-sum based double-double addition (adds only: nothing for the compiler to contract)
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  const double s = __dadd_rn(a.hi, b.hi);
+  const double bb = __dsub_rn(s, a.hi);
+  double e = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(s, bb)), __dsub_rn(b.hi, bb));
+  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
+  const double h = __dadd_rn(s, e);
+  return DD{h, __dsub_rn(e, __dsub_rn(h, s))};
+}
+
+template <int KIND>
+__device__ __forceinline__ void point_vals(int64_t j, const float4* __restrict__ pts, const MomentArgs& m, float alpha,
+                                           double o[7]) {
+  const float4 x = pts[j];
+  double a, v0, v1 = 0.0, v2 = 0.0;
+  if (KIND == ATTR_VEC) {
+    float4 v = m.vec[j];
+    if (m.axpy_r) {  // μ' = μ + α r (Alg. 2 line 3) — the same fmaf as the record's one-point branch
+      const float4 r = m.axpy_r[j];
+      v = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
+    }
+    v0 = v.x; v1 = v.y; v2 = v.z;
+    if (m.a_sorted) {
+      const double f = m.a_sorted[j];
+      v0 *= f; v1 *= f; v2 *= f;
+    }
+    a = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+  } else {
+    v0 = m.scal[j];
+    if (m.a_sorted) v0 *= (double)m.a_sorted[j];
+    a = fabs(v0);
+  }
+  o[0] = a;
+  o[1] = a * (double)x.x;
+  o[2] = a * (double)x.y;
+  o[3] = a * (double)x.z;
+  o[4] = v0;
+  o[5] = v1;
+  o[6] = v2;
+}
+
+// scan element: 7 double-double sums + the number of points with |ν| > 0 (an exact integer)
+struct Elt {
+  DD v[7];
+  double cnt;
+};
+
+__device__ __forceinline__ void elt_zero(Elt& e) {
+#pragma unroll
+  for (int c = 0; c < 7; ++c) e.v[c] = DD{0.0, 0.0};
+  e.cnt = 0.0;
+}
+__device__ __forceinline__ void elt_add(Elt& e, const Elt& f) {
+#pragma unroll
+  for (int c = 0; c < 7; ++c) e.v[c] = dd_add(e.v[c], f.v[c]);
+  e.cnt += f.cnt;
+}
+__device__ __forceinline__ void elt_add_point(Elt& e, const double o[7]) {
+#pragma unroll
+  for (int c = 0; c < 7; ++c) e.v[c] = dd_add(e.v[c], DD{o[c], 0.0});
+  e.cnt += o[0] > 0.0 ? 1.0 : 0.0;
+}
+__device__ __forceinline__ Elt elt_shfl_up(const Elt& e, int d) {
+  Elt r;
+#pragma unroll
+  for (int c = 0; c < 7; ++c) {
+    r.v[c].hi = __shfl_up_sync(0xffffffffu, e.v[c].hi, d);
+    r.v[c].lo = __shfl_up_sync(0xffffffffu, e.v[c].lo, d);
+  }
+  r.cnt = __shfl_up_sync(0xffffffffu, e.cnt, d);
+  return r;
+}
+// inclusive warp scan over the first `width` lanes (fixed order)
+__device__ __forceinline__ void warp_inscan(Elt& x, int lane, int width) {
+  for (int o = 1; o < width; o <<= 1) {
+    const Elt y = elt_shfl_up(x, o);
+    if (lane >= o) {
+      Elt z = y;
+      elt_add(z, x);
+      x = z;
+    }
+  }
+}
+
+// block-wide exclusive scan (fixed order: deterministic); e becomes the exclusive prefix, tot the total
+template <int NT>
+__device__ __forceinline__ void block_exscan(Elt& e, Elt& tot) {
+  constexpr int NW = NT / 32;
+  __shared__ Elt ws[NW + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Elt inc = e;
+  warp_inscan(inc, lane, 32);
+  if (lane == 31) ws[warp] = inc;
+  Elt prev = elt_shfl_up(inc, 1);
+  if (lane == 0) elt_zero(prev);
+  __syncthreads();
+  if (warp == 0) {  // scan of the warp totals by one warp
+    Elt x;
+    if (lane < NW) x = ws[lane];
+    else elt_zero(x);
+    warp_inscan(x, lane, NW);
+    Elt xp = elt_shfl_up(x, 1);
+    if (lane == 0) elt_zero(xp);
+    __syncwarp();
+    if (lane < NW) ws[lane] = xp;
+    if (lane == NW - 1) ws[NW] = x;
+  }
+  __syncthreads();
+  e = ws[warp];
+  elt_add(e, prev);
+  tot = ws[NW];
+  __syncthreads();
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kScanThreads) mom_tile_sum(const float4* __restrict__ pts, MomentArgs m, int64_t n,
+                                                             Elt* __restrict__ tile_tot) {
+  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
+  Elt t, tot;
+  elt_zero(t);
+  // coalesced: item k of thread x is point tile·T + k·256 + x (totals need no ownership order)
+  const int64_t j0 = blockIdx.x * (int64_t)kScanTile + threadIdx.x;
+#pragma unroll 2
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t j = j0 + k * kScanThreads;
+    if (j < n) {
+      double o[7];
+      point_vals<KIND>(j, pts, m, alpha, o);
+      elt_add_point(t, o);
+    }
+  }
+  block_exscan<kScanThreads>(t, tot);
+  if (threadIdx.x == 0) tile_tot[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanTopThreads) mom_tile_scan(const Elt* __restrict__ tile_tot, int64_t ntiles,
+                                                                 Elt* __restrict__ tile_off) {
+  const int64_t per = (ntiles + kScanTopThreads - 1) / kScanTopThreads;
+  const int64_t t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
+  Elt v, tot;
+  elt_zero(v);
+  for (int64_t t = t0; t < t1; ++t) elt_add(v, tile_tot[t]);
+  block_exscan<kScanTopThreads>(v, tot);
+  for (int64_t t = t0; t < t1; ++t) {
+    tile_off[t] = v;
+    elt_add(v, tile_tot[t]);
+  }
+}
+
+__device__ __forceinline__ void store_pre(double* __restrict__ Eh, float* __restrict__ El, int64_t j, const Elt& t) {
+  double2* h = reinterpret_cast<double2*>(Eh + 8 * j);
+  h[0] = make_double2(t.v[0].hi, t.v[1].hi);
+  h[1] = make_double2(t.v[2].hi, t.v[3].hi);
+  h[2] = make_double2(t.v[4].hi, t.v[5].hi);
+  h[3] = make_double2(t.v[6].hi, t.cnt);
+  float4* l = reinterpret_cast<float4*>(El + 8 * j);
+  l[0] = make_float4((float)t.v[0].lo, (float)t.v[1].lo, (float)t.v[2].lo, (float)t.v[3].lo);
+  l[1] = make_float4((float)t.v[4].lo, (float)t.v[5].lo, (float)t.v[6].lo, 0.f);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __restrict__ pts, MomentArgs m,
+                                                                int64_t n, const Elt* __restrict__ tile_off,
+                                                                double* __restrict__ Eh, float* __restrict__ El) {
+  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
+  Elt t, tot;
+  elt_zero(t);
+  const int64_t j0 = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanItems;  // consecutive ownership
+  for (int k = 0; k < kScanItems; ++k)
+    if (j0 + k < n) {
+      double o[7];
+      point_vals<KIND>(j0 + k, pts, m, alpha, o);
+      elt_add_point(t, o);
+    }
+  block_exscan<kScanThreads>(t, tot);
+  {
+    Elt z = tile_off[blockIdx.x];
+    elt_add(z, t);
+    t = z;
+  }
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t j = j0 + k;
+    if (j < n) {
+      store_pre(Eh, El, j, t);
+      double o[7];
+      point_vals<KIND>(j, pts, m, alpha, o);
+      elt_add_point(t, o);
+      if (KIND == ATTR_VEC && m.axpy_r) {  // μ' written once here, read by the G traversal
+        const float4 v = m.vec[j], r = m.axpy_r[j];
+        m.axpy_out[j] = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
+      }
+      if (j == n - 1) store_pre(Eh, El, n, t);
+    }
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int64_t nn, const double* __restrict__ Eh,
+                                                 const float* __restrict__ El) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  const int j0 = tv.pb[i], j1 = tv.pe[i];
+  Sums S;
+  float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j1 - j0 == 1) {
+    const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
+    double o[7];
+    point_vals<KIND>(j0, tv.pts, m, alpha, o);
+    S.W = o[0];
+    S.P[0] = o[1]; S.P[1] = o[2]; S.P[2] = o[3];
+    S.V[0] = o[4]; S.V[1] = o[5]; S.V[2] = o[6];
+    p0 = tv.pts[j0];
+  } else {
+    const double2* a = reinterpret_cast<const double2*>(Eh + 8 * (int64_t)j0);
+    const double2* b = reinterpret_cast<const double2*>(Eh + 8 * (int64_t)j1);
+    const double2 a0 = a[0], a1 = a[1], a2 = a[2], a3 = a[3], b0 = b[0], b1 = b[1], b2 = b[2], b3 = b[3];
+    double d[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (b3.y != a3.y) {  // else no point has |ν| > 0: Σ|ν| = 0 and every ν_j = 0, exactly
+      const float4* al = reinterpret_cast<const float4*>(El + 8 * (int64_t)j0);
+      const float4* bl = reinterpret_cast<const float4*>(El + 8 * (int64_t)j1);
+      const float4 la0 = al[0], la1 = al[1], lb0 = bl[0], lb1 = bl[1];
+      const double ah[7] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x};
+      const double bh[7] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y, b3.x};
+      const float alo[7] = {la0.x, la0.y, la0.z, la0.w, la1.x, la1.y, la1.z};
+      const float blo[7] = {lb0.x, lb0.y, lb0.z, lb0.w, lb1.x, lb1.y, lb1.z};
+#pragma unroll
+      for (int c = 0; c < 7; ++c) d[c] = dd_add(DD{bh[c], (double)blo[c]}, DD{-ah[c], -(double)alo[c]}).hi;
+    }
+    S.W = d[0];
+    S.P[0] = d[1]; S.P[1] = d[2]; S.P[2] = d[3];
+    S.V[0] = d[4]; S.V[1] = d[5]; S.V[2] = d[6];
+  }
+  if (m.write_W) tv.sums[8 * i] = S.W;
+  write_record<KIND>(i, S, j1 - j0, p0, tv.depth[i], tv.topo[i], tv.smask[i], m.theta, tv.centroid, m);
+}
+
+template <int KIND>
+void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
+  TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->topo, t->smask, t->sums, t->centroid};
+  const int64_t nt = t->mom_ntiles;
+  Elt* tot = reinterpret_cast<Elt*>(t->mom_tile);
+  Elt* off = tot + nt;
+  double* Eh = t->mom_pre;
+  float* El = reinterpret_cast<float*>(t->mom_pre + 8 * (t->n + 1));
+  mom_tile_sum<KIND><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, tot);
+  mom_tile_scan<<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
+  mom_tile_prefix<KIND><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, off, Eh, El);
+  mom_nodes<KIND><<<(unsigned)((t->nn + 255) / 256), 256, 0, s>>>(tv, m, t->nn, Eh, El);
+}
+
 template <int KIND>
 void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s, const int64_t* loff_dev) {
   TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->topo, t->smask, t->sums, t->centroid};
@@ -240,10 +506,22 @@ wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
   WN_CUDA(cudaMallocAsync((void**)&t->mom_loff, t->level_off.size() * sizeof(int64_t), s));
   WN_CUDA(cudaMemcpyAsync(t->mom_loff, t->level_off.data(), t->level_off.size() * sizeof(int64_t),
                           cudaMemcpyHostToDevice, s));
+  t->mom_ntiles = (t->n + kScanTile - 1) / kScanTile;
+  WN_CUDA(cudaMallocAsync((void**)&t->mom_pre, 12 * (size_t)(t->n + 1) * sizeof(double), s));
+  WN_CUDA(cudaMallocAsync((void**)&t->mom_tile, 2 * (size_t)t->mom_ntiles * sizeof(Elt), s));
   return WN_OK;
 }
 
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
+#ifndef WN_EXP_OLD_MOM
+  if (m.kind != ATTR_UNIT) {  // per-iteration attributes: prefix differences
+    ProfScope ps(WN_PROF_MOMENTS, s, 4);
+    if (m.kind == ATTR_VEC) launch_prefix<ATTR_VEC>(t, m, s);
+    else launch_prefix<ATTR_SCALAR>(t, m, s);
+    WN_CUDA(cudaGetLastError());
+    return WN_OK;
+  }
+#endif
   ProfScope ps(WN_PROF_MOMENTS, s, (t->mom_cut <= t->depth_used ? 1 + (t->depth_used - t->mom_cut + 1) / 2 : 0) + (t->mom_cut > 0));
   switch (m.kind) {
     case ATTR_VEC: launch_all<ATTR_VEC>(t, m, s, t->mom_loff); break;

@@ -68,6 +68,9 @@ struct wn_tree_s {
   double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
   int mom_cut = 0;              // moment builds: levels < mom_cut run in one block
   int64_t* mom_loff = nullptr;  //   level offsets on the device
+  double* mom_pre = nullptr;    // (N+1) × 8 fp64 exclusive prefix of the point sums (moments.cu)
+  double* mom_tile = nullptr;   // 2 × tiles × 8 fp64: per-tile totals, per-tile offsets
+  int64_t mom_ntiles = 0;
   wn::NodeSet set[2];           // [0] = current attribute, [1] = frozen geometry (transpose mode)
   std::vector<int64_t> level_off;  // host: BFS offset of each level, size depth_used + 2
   wn::IterScratch it;
@@ -128,6 +131,7 @@ struct MomentArgs {
   NodeSet out;
   float4* centroid_out = nullptr;   // ATTR_UNIT: writes the centroid table
   int32_t* leaf_of_out = nullptr;   // ATTR_UNIT: writes the leaf node of every sorted point
+  bool write_W = false;             // also store each node's Σ|ν| in tree sums[8·i] (wn_moments export)
 };
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s);
 wn_status plan_moments(wn_tree_s* t, cudaStream_t s);  // once per tree, after the topology

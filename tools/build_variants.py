@@ -4,10 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_16634_b200 import build as b
 VARIANTS = {
     "base": [],
-    "mlb4": ["WN_EXP_MOM_LB=4"],
-    "mlb4_b2": ["WN_EXP_MOM_LB=4", "WN_EXP_MOM_BATCH=2"],
-    "mlb8_b1": ["WN_EXP_MOM_LB=8", "WN_EXP_MOM_BATCH=1"],
-    "mlb6_b2": ["WN_EXP_MOM_LB=6", "WN_EXP_MOM_BATCH=2"],
+    "oldmom": ["WN_EXP_OLD_MOM"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
