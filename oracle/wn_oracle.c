@@ -39,6 +39,12 @@ static float d2_f32(const float a[3], const float b[3]) {
   float dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
   return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
 }
+/* distance² to a representative held as fp32 hi + lo (lo = fp32 rounding of rep − hi):
+   e = (hi − y) + lo per axis, all in fp32 — the fp32 evaluation of |x_B − y| (R-prec) */
+static float d2_rep_f32(const float hi[3], const float lo[3], const float y[3]) {
+  float ex = (hi[0] - y[0]) + lo[0], ey = (hi[1] - y[1]) + lo[1], ez = (hi[2] - y[2]) + lo[2];
+  return fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+}
 
 /* ------------------------------------------------------------------------------------------ */
 /* Normalization: PAPER.md:L419 (§5.1.1) "normalized to fit into the cube [−1,1]^3 with a margin */
@@ -219,7 +225,8 @@ void wo_tree_export(const wo_tree* t, int32_t* perm, int32_t* depth, int32_t* pb
 /* ------------------------------------------------------------------------------------------ */
 typedef struct {
   double* rep;   /* nn×3 (node id order) */
-  float* repf;   /* nn×3 fp32 rounding of rep (decision operand) */
+  float* repf;   /* nn×3 fp32 rounding of rep: hi (decision operand) */
+  float* lof;    /* nn×3 fp32 rounding of rep − hi: lo (decision operand) */
   double* V;     /* nn×dim */
   double* W;     /* nn */
   float* thrf;   /* nn: (c·width)^2 in fp32 */
@@ -264,18 +271,24 @@ static void reps_compute(const wo_tree* t, const double* nu, int dim, double the
   r->dim = dim;
   r->rep = (double*)malloc((size_t)t->nn * 3 * sizeof(double));
   r->repf = (float*)malloc((size_t)t->nn * 3 * sizeof(float));
+  r->lof = (float*)malloc((size_t)t->nn * 3 * sizeof(float));
   r->V = (double*)malloc((size_t)t->nn * dim * sizeof(double));
   r->W = (double*)malloc((size_t)t->nn * sizeof(double));
   r->thrf = (float*)malloc((size_t)t->nn * sizeof(float));
 #pragma omp parallel for schedule(dynamic, 256)
   for (int64_t id = 0; id < t->nn; ++id) {
     node_moment(t, id, nu, dim, r->rep + 3 * id, r->V + (size_t)dim * id, r->W + id);
-    for (int c = 0; c < 3; ++c) r->repf[3 * id + c] = (float)r->rep[3 * id + c];
+    for (int c = 0; c < 3; ++c) {
+      r->repf[3 * id + c] = (float)r->rep[3 * id + c];
+      r->lof[3 * id + c] = (float)(r->rep[3 * id + c] - (double)r->repf[3 * id + c]);
+    }
     r->thrf[id] = thr_f32(theta, t->nodes[id].depth);
   }
 }
 
-static void reps_free(wo_reps* r) { free(r->rep); free(r->repf); free(r->V); free(r->W); free(r->thrf); }
+static void reps_free(wo_reps* r) {
+  free(r->rep); free(r->repf); free(r->lof); free(r->V); free(r->W); free(r->thrf);
+}
 
 void wo_moments(const wo_tree* t, const double* nu, int dim, double* rep, double* attr, double* W) {
   wo_reps r;
@@ -368,8 +381,7 @@ static int near_tie(float d2, float thr) { return isfinite(thr) && thr > 0 && fa
 
 static void trav(const trav_ctx* c, int64_t id, const double y[3], const float yf[3], double* acc, wo_cnt* k) {
   const wo_node* nd = &c->t->nodes[id];
-  const float* rf = c->geo->repf + 3 * id;
-  float d2 = d2_f32(rf, yf);
+  float d2 = d2_rep_f32(c->geo->repf + 3 * id, c->geo->lof + 3 * id, yf);
   k->tests++;
   if (near_tie(d2, c->geo->thrf[id])) k->ties++;
   if (d2 > c->geo->thrf[id]) {                                  /* far: representative */
@@ -442,8 +454,7 @@ void wo_tree_A_frozen(const wo_tree* t, const double* mu_geom, const double* nu,
 static void trav_T(const trav_ctx* c, int64_t id, const double y[3], const float yf[3], double s, double* VB,
                    double* U) {
   const wo_node* nd = &c->t->nodes[id];
-  const float* rf = c->geo->repf + 3 * id;
-  float d2 = d2_f32(rf, yf);
+  float d2 = d2_rep_f32(c->geo->repf + 3 * id, c->geo->lof + 3 * id, yf);
   if (d2 > c->geo->thrf[id]) {
     if (!(d2 < c->w2f)) {
       const double* x = c->geo->rep + 3 * id;

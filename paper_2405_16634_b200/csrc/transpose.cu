@@ -61,16 +61,17 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
     for (int k = 0; k < ncc; ++k) {
       const int node = cb + k;
       const float4 R = __ldg(G + kRec * (int64_t)node);
-      const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
-      const float d2 = dist2(dx, dy, dz);
+      const float4 Lo = __ldg(G + kRec * (int64_t)node + 2);
+      // d = (hi − x_q) + lo: the decisions of the frozen-geometry A traversal (R-prec)
+      const float ex = __fadd_rn(__fsub_rn(R.x, xq.x), Lo.x), ey = __fadd_rn(__fsub_rn(R.y, xq.y), Lo.y),
+                  ez = __fadd_rn(__fsub_rn(R.z, xq.z), Lo.z);
+      const float d2 = dist2(ex, ey, ez);
       const bool far = d2 > R.w;
       // s_i ∇Φ(x_i − x_B) = s_i d / (4π r³), d = x_B − x_i
       float cx = 0.f, cy = 0.f, cz = 0.f;
       const bool live = mine && far && !(d2 < w2);
-      if (live) {  // value at d = (hi − x_q) + lo
-        const float4 Lo = __ldg(G + kRec * (int64_t)node + 2);
-        const float ex = dx + Lo.x, ey = dy + Lo.y, ez = dz + Lo.z;
-        const float inv = rsqrtf(dist2(ex, ey, ez));
+      if (live) {
+        const float inv = rsqrtf(d2);
         const float c = sq * inv * inv * inv;
         cx = c * ex; cy = c * ey; cz = c * ez;
       }

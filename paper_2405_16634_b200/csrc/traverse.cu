@@ -19,8 +19,8 @@
 //   * one-point nodes carry thr = −1, so they always take the representative branch (which equals
 //     the leaf branch: rep = the point, ν_B = ν_j) and are never opened;
 //   * the kernel term is branch-free (predicated by `live`), rsqrt is one MUFU op (ftz; r ≥ w > 0);
-//   * decisions and cutoff are fp32 on d = hi − x_q, d² = fma(dx,dx, fma(dy,dy, dz·dz))
-//     (DESIGN.md R-prec); the term value uses d = (hi − x_q) + lo; A accumulates per child group in
+//   * decisions, cutoff and term value all use the fp32 offset d = (hi − x_q) + lo to the representative,
+//     d² = fma(dx,dx, fma(dy,dy, dz·dz)) (DESIGN.md R-prec); A accumulates per child group in
 //     fp32 and across groups in fp64 (s = ½ − Aμ cancels near convergence);
 //   * epilogues fuse the solver's elementwise work (s = ½ − Aμ, Σ partials, rescale).
 #include <cuda_runtime.h>
@@ -117,37 +117,19 @@ __global__ void __launch_bounds__(kTravBlock, WN_EXP_LBMIN) trav_kernel(const Tr
       const int cb = code >> 4, ncc = (code & 7) + 1;
       const bool mine = ((uint32_t)e.y >> lane) & 1u;
       {
-#ifdef WN_EXP_PREFETCH
-        const float4* rp = rec_at(G, cb);
-        const float4* vp = FROZEN ? rec_at(Vr, cb) : rp;
-        float4 Rn = __ldg(rp), Vn = __ldg(vp + 1), Ln = __ldg(rp + 2);
-#endif
         for (int k = 0; k < ncc; ++k) {
           const int node = cb + k;
-#ifdef WN_EXP_PREFETCH
-          // software pipeline: child k+1's record is in flight while child k is evaluated (records padded)
-          const float4 R = Rn, V = Vn, L = Ln;
-          rp += kRec;
-          vp += kRec;
-          Rn = __ldg(rp);
-          Vn = __ldg(vp + 1);
-          Ln = __ldg(rp + 2);
-#else
           const float4* rp = rec_at(G, node);
           const float4 R = __ldg(rp);
           const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
           const float4 L = __ldg(rp + 2);
-#endif
-          const float dx = __fsub_rn(R.x, xq.x), dy = __fsub_rn(R.y, xq.y), dz = __fsub_rn(R.z, xq.z);
-          const float d2 = dist2(dx, dy, dz);
+          // d = (hi − x_q) + lo: decisions and value on the same fp32 offset (R-prec)
+          const float ex = __fadd_rn(__fsub_rn(R.x, xq.x), L.x), ey = __fadd_rn(__fsub_rn(R.y, xq.y), L.y),
+                      ez = __fadd_rn(__fsub_rn(R.z, xq.z), L.z);
+          const float d2 = dist2(ex, ey, ez);
           const bool far = d2 > R.w;
           const bool live = mine && far && !(d2 < w2);
-#ifdef WN_EXP_NOLO
-          const float ex = dx, ey = dy, ez = dz;
-#else
-          const float ex = dx + L.x, ey = dy + L.y, ez = dz + L.z;  // value at d = (hi − x_q) + lo
-#endif
-          acc.term(live, ex, ey, ez, dist2(ex, ey, ez), V);
+          acc.term(live, ex, ey, ez, d2, V);
           if (COUNT && mine) {
             ++ntest;
             nfar += far;

@@ -4,7 +4,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_16634_b200 import build as b
 VARIANTS = {
     "base": [],
-    "oldmom": ["WN_EXP_OLD_MOM"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
