@@ -72,14 +72,26 @@ __global__ void bbox_partial(const float* __restrict__ p, int64_t n, float* __re
 }
 
 // xf = (c, scale): c = (lo + hi)/2, half = max_a (hi − lo)/2, scale = (10/11)/half  (fp64)
-__global__ void bbox_final(const float* __restrict__ part, int nb, const int* bad, BBox* out) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(1024) bbox_final(const float* __restrict__ part, int nb, const int* bad, BBox* out) {
+  __shared__ float slo[3][32], shi[3][32];
   float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int b = 0; b < nb; ++b)
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
     for (int a = 0; a < 3; ++a) {
       lo[a] = fminf(lo[a], part[6 * b + a]);
       hi[a] = fmaxf(hi[a], part[6 * b + 3 + a]);
     }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o; o >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+    if (lane == 0) { slo[a][w] = lo[a]; shi[a][w] = hi[a]; }
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int a = 0; a < 3; ++a)
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { lo[a] = fminf(lo[a], slo[a][k]); hi[a] = fmaxf(hi[a], shi[a][k]); }
   double half = 0.0;
   for (int a = 0; a < 3; ++a) {
     out->lo[a] = lo[a];
@@ -184,29 +196,81 @@ __global__ void radix_scatter(const uint64_t* __restrict__ kin, const int32_t* _
   }
 }
 
-// exclusive scan of m uint32 with one block of 1024 threads; total → *total
-__global__ void scan_excl_1block(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t m,
-                                 uint32_t* total) {
-  __shared__ uint32_t sh[1024];
-  int64_t chunk = (m + 1023) / 1024;
-  int64_t b = threadIdx.x * chunk, e = min(b + chunk, m);
-  uint32_t sum = 0;
-  for (int64_t i = b; i < e; ++i) sum += in[i];
-  sh[threadIdx.x] = sum;
+// exclusive scan of m uint32 (exact integer sums: any association gives the same result), three launches:
+// per-block totals (4096 elements per block), one-block scan of the totals, per-block scan + offset
+constexpr int kScanT = 1024, kScanPer = 4, kScanBlk = kScanT * kScanPer;
+
+__device__ __forceinline__ uint32_t block_exscan_u32(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t ws[kScanT / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[w] = x;
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    uint32_t v = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
-    __syncthreads();
-    sh[threadIdx.x] += v;
-    __syncthreads();
+  if (w == 0) {
+    uint32_t t = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    ws[lane] = t;  // inclusive over warps
   }
-  uint32_t run = sh[threadIdx.x] - sum;
-  for (int64_t i = b; i < e; ++i) {
-    uint32_t v = in[i];
-    out[i] = run;
-    run += v;
+  __syncthreads();
+  const uint32_t r = (w ? ws[w - 1] : 0u) + x - v;
+  if (total) *total = ws[kScanT / 32 - 1];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ void load4(const uint32_t* __restrict__ in, int64_t i, int64_t m, uint32_t v[4]) {
+  if (i + 3 < m && ((reinterpret_cast<uintptr_t>(in + i) & 15) == 0)) {
+    const uint4 q = *reinterpret_cast<const uint4*>(in + i);
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = i + k < m ? in[i + k] : 0u;
   }
-  if (threadIdx.x == 1023 && total) *total = sh[1023];
+}
+
+__global__ void __launch_bounds__(kScanT) scan_blocks(const uint32_t* __restrict__ in, int64_t m,
+                                                      uint32_t* __restrict__ bsum) {
+  uint32_t v[4];
+  load4(in, (int64_t)blockIdx.x * kScanBlk + kScanPer * threadIdx.x, m, v);
+  uint32_t tot;
+  block_exscan_u32(v[0] + v[1] + v[2] + v[3], &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanT) scan_top(uint32_t* __restrict__ bsum, int nb, uint32_t* total) {
+  uint32_t run = 0;
+  for (int b0 = 0; b0 < nb; b0 += kScanT) {  // nb ≤ a few thousand
+    const int b = b0 + threadIdx.x;
+    const uint32_t v = b < nb ? bsum[b] : 0u;
+    uint32_t tot;
+    const uint32_t e = block_exscan_u32(v, &tot);
+    if (b < nb) bsum[b] = run + e;
+    run += tot;
+  }
+  if (threadIdx.x == 0 && total) *total = run;
+}
+
+__global__ void __launch_bounds__(kScanT) scan_apply(const uint32_t* in, uint32_t* out, int64_t m,
+                                                     const uint32_t* __restrict__ boff) {
+  const int64_t i = (int64_t)blockIdx.x * kScanBlk + kScanPer * threadIdx.x;
+  uint32_t v[4];
+  load4(in, i, m, v);
+  uint32_t run = boff[blockIdx.x] + block_exscan_u32(v[0] + v[1] + v[2] + v[3], nullptr);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (i + k < m) {
+      out[i + k] = run;
+      run += v[k];
+    }
 }
 
 __global__ void gather_sorted(const float4* __restrict__ xn, const int32_t* __restrict__ idx, int64_t n,
@@ -390,6 +454,19 @@ wn_status dalloc(T** p, size_t count, cudaStream_t s) {
   return WN_OK;
 }
 
+// exclusive scan (in may equal out); total (device) optional
+wn_status scan_excl(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* total, cudaStream_t s) {
+  const int nb = (int)((m + kScanBlk - 1) / kScanBlk);
+  uint32_t* bsum = nullptr;
+  wn_status st = dalloc(&bsum, (size_t)nb, s);
+  if (st != WN_OK) return st;
+  scan_blocks<<<nb, kScanT, 0, s>>>(in, m, bsum);
+  scan_top<<<1, kScanT, 0, s>>>(bsum, nb, total);
+  scan_apply<<<nb, kScanT, 0, s>>>(in, out, m, bsum);
+  cudaFreeAsync(bsum, s);
+  return WN_OK;
+}
+
 }  // namespace
 
 #define WN_TRY(x)                       \
@@ -411,11 +488,11 @@ wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStr
   WN_TRY(dalloc(&hist, (size_t)256 * ntiles, s));
   const int hpasses = (3 * kHilbertBits + 7) / 8;
   {
-    ProfScope ps(WN_PROF_TREE, s, 1 + 3 * hpasses);
+    ProfScope ps(WN_PROF_TREE, s, 1 + 5 * hpasses);
     hilbert_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pts, n, ka, va);
     for (int p = 0; p < hpasses; ++p) {
       radix_hist<<<ntiles, kSortThreads, 0, s>>>(ka, n, 8 * p, ntiles, hist);
-      scan_excl_1block<<<1, 1024, 0, s>>>(hist, hist, (int64_t)256 * ntiles, nullptr);
+      WN_TRY(scan_excl(hist, hist, (int64_t)256 * ntiles, nullptr, s));
       radix_scatter<<<ntiles, kSortThreads, 0, s>>>(ka, va, kb, vb, n, 8 * p, ntiles, hist);
       std::swap(ka, kb);
       std::swap(va, vb);
@@ -446,7 +523,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   {
     ProfScope ps(WN_PROF_TREE, s, 2);
     bbox_partial<<<nb, 256, 0, s>>>(pts, n, part, bad);
-    bbox_final<<<1, 32, 0, s>>>(part, nb, bad, bb);
+    bbox_final<<<1, 1024, 0, s>>>(part, nb, bad, bb);
   }
   BBox hb;
   WN_CUDA(cudaMemcpyAsync(&hb, bb, sizeof(BBox), cudaMemcpyDeviceToHost, s));
@@ -475,11 +552,11 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   WN_TRY(dalloc(&hist, (size_t)256 * ntiles, s));
   int passes = (3 * D + 7) / 8;
   {
-    ProfScope ps(WN_PROF_TREE, s, 1 + 3 * passes + 1);
+    ProfScope ps(WN_PROF_TREE, s, 1 + 5 * passes + 1);
     normalize_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pts, n, bb, D, xn, k0, v0);
     for (int p = 0; p < passes; ++p) {
       radix_hist<<<ntiles, kSortThreads, 0, s>>>(k0, n, 8 * p, ntiles, hist);
-      scan_excl_1block<<<1, 1024, 0, s>>>(hist, hist, (int64_t)256 * ntiles, nullptr);
+      WN_TRY(scan_excl(hist, hist, (int64_t)256 * ntiles, nullptr, s));
       radix_scatter<<<ntiles, kSortThreads, 0, s>>>(k0, v0, k1, v1, n, 8 * p, ntiles, hist);
       std::swap(k0, k1);
       std::swap(v0, v1);
@@ -511,9 +588,9 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   WN_TRY(dalloc(&cnt, m + 1, s));
   WN_TRY(dalloc(&offs, m + 1, s));
   {
-    ProfScope ps(WN_PROF_TREE, s, 2);
+    ProfScope ps(WN_PROF_TREE, s, 4);
     level_counts<<<etiles, kEmitThreads, 0, s>>>(t->keys, n, D, etiles, cnt);
-    scan_excl_1block<<<1, 1024, 0, s>>>(cnt, offs, m, offs + m);
+    WN_TRY(scan_excl(cnt, offs, m, offs + m, s));
   }
   std::vector<uint32_t> hoffs(m + 1);
   WN_CUDA(cudaMemcpyAsync(hoffs.data(), offs, (m + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
