@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "wn_oracle.c")
 _LIB = os.path.join(_HERE, "libwn_oracle.so")
 
-OP_A, OP_G, OP_AT, ABS = 0, 1, 2, 8
+OP_A, OP_G, OP_AT, ABS, ORDER1 = 0, 1, 2, 8, 16
 
 
 def build(force: bool = False) -> str:
@@ -61,7 +61,7 @@ def lib():
         L.wo_tree_op.argtypes = [P, I32, P, I32, P, P, I64, D, D, P, P]
         L.wo_tree_A_frozen.argtypes = [P, P, P, D, D, P]
         L.wo_tree_AT_transpose.argtypes = [P, P, P, D, D, P]
-        L.wo_solve.argtypes = [P, P, D, D, I32, I32, I32, D, I32, I32, I32, P]
+        L.wo_solve.argtypes = [P, P, D, D, I32, I32, I32, D, I32, I32, I32, I32, P]
         L.wo_solve.restype = I32
         L.wo_num_threads.restype = I32
         _lib = L
@@ -167,13 +167,16 @@ class Tree:
         lib().wo_dense_op(self._h, op, _p(nu), dim, None if q is None else _p(q), m, float(w), _p(out))
         return out[:, 0] if od == 1 else out
 
-    def tree(self, op, nu, w, theta=2.0, queries=None, qidx=None, counters=False):
+    def tree(self, op, nu, w, theta=2.0, queries=None, qidx=None, counters=False, order=0):
+        """Alg. 4 treecode; order=1: first-order far field (not the paper's)."""
+        if order == 1:
+            op |= ORDER1
         nu = _f64(nu)
         dim = 1 if nu.ndim == 1 else 3
         q = None if queries is None else _f32(queries).reshape(-1, 3)
         qi = None if qidx is None else np.ascontiguousarray(qidx, dtype=np.int64)
         m = q.shape[0] if q is not None else (qi.shape[0] if qi is not None else self.n)
-        od = 1 if (op == OP_A or op & ABS) else 3
+        od = 1 if ((op & ~ORDER1) == OP_A or op & ABS) else 3
         out = np.empty((m, od))
         cnt = np.empty((m, 4), np.int64) if counters else None
         lib().wo_tree_op(self._h, op, _p(nu), dim, None if q is None else _p(q),
@@ -193,14 +196,14 @@ class Tree:
         return out
 
     def solve(self, mu0=None, w1=0.002, w2=0.016, iters=40, theta=2.0, backend="tree", mode="gather",
-              wnnc=True, first_iter=1, total_iters=None):
+              wnnc=True, first_iter=1, total_iters=None, order=0):
         """Alg. 3 in the normalized frame; returns (mu_norm n×3, stats iters×5)."""
         mu = np.zeros((self.n, 3)) if mu0 is None else _f64(mu0).copy()
         stats = np.empty((iters, 5))
         total = iters if total_iters is None else total_iters
         lib().wo_solve(self._h, _p(mu), float(w1), float(w2), int(iters), int(first_iter), int(total),
                        float(theta), 0 if backend == "tree" else 1, 0 if mode == "gather" else 1,
-                       1 if wnnc else 0, _p(stats))
+                       1 if wnnc else 0, int(order), _p(stats))
         return mu, stats
 
 
@@ -230,35 +233,35 @@ class Cloud:
     def _q(self, queries):
         return None if queries is None else normalize_apply(self.xf, queries)
 
-    def F(self, mu, w, theta=2.0, a=None, queries=None, dense=False, qidx=None, counters=False):
+    def F(self, mu, w, theta=2.0, a=None, queries=None, dense=False, qidx=None, counters=False, order=0):
         if dense:
             return self.t.dense(OP_A, self._mu_norm(mu, a), w, self._q(queries))
-        return self.t.tree(OP_A, self._mu_norm(mu, a), w, theta, self._q(queries), qidx, counters)
+        return self.t.tree(OP_A, self._mu_norm(mu, a), w, theta, self._q(queries), qidx, counters, order)
 
-    def gradF(self, mu, w, theta=2.0, a=None, queries=None, dense=False, qidx=None, counters=False):
+    def gradF(self, mu, w, theta=2.0, a=None, queries=None, dense=False, qidx=None, counters=False, order=0):
         """∇F in the input frame (= −G scaled by `scale`)."""
         if dense:
             g = self.t.dense(OP_G, self._mu_norm(mu, a), w, self._q(queries))
             return -g * self.scale
-        r = self.t.tree(OP_G, self._mu_norm(mu, a), w, theta, self._q(queries), qidx, counters)
+        r = self.t.tree(OP_G, self._mu_norm(mu, a), w, theta, self._q(queries), qidx, counters, order)
         if counters:
             return -r[0] * self.scale, r[1]
         return -r * self.scale
 
-    def AT(self, s, w, theta=2.0, dense=False, qidx=None, counters=False):
+    def AT(self, s, w, theta=2.0, dense=False, qidx=None, counters=False, order=0):
         if dense:
             return self.t.dense(OP_AT, _f64(s), w) * self.scale ** 2
-        r = self.t.tree(OP_AT, _f64(s), w, theta, None, qidx, counters)
+        r = self.t.tree(OP_AT, _f64(s), w, theta, None, qidx, counters, order)
         if counters:
             return r[0] * self.scale ** 2, r[1]
         return r * self.scale ** 2
 
-    def abs_scale(self, op, nu_in, w, theta=2.0, a=None, queries=None, qidx=None):
+    def abs_scale(self, op, nu_in, w, theta=2.0, a=None, queries=None, qidx=None, order=0):
         """S_i = Σ_j |term_ij| of the treecode sum at query i, in the output's frame (the conditioning
         scale of a cancelling sum; used for the parity error floor)."""
         if op == OP_AT:
-            return self.t.tree(OP_AT | ABS, _f64(nu_in), w, theta, None, qidx) * self.scale ** 2
-        S = self.t.tree(op | ABS, self._mu_norm(nu_in, a), w, theta, self._q(queries), qidx)
+            return self.t.tree(OP_AT | ABS, _f64(nu_in), w, theta, None, qidx, order=order) * self.scale ** 2
+        S = self.t.tree(op | ABS, self._mu_norm(nu_in, a), w, theta, self._q(queries), qidx, order=order)
         return S * (self.scale if op == OP_G else 1.0)
 
     def AT_transpose(self, s, mu_geom, w, theta=2.0):

@@ -11,15 +11,18 @@
  *
  * Precision: fp64 for every value.  The two decisions that turn floating point into a branch —
  * the opening test |x_i − x_B| > c·width(B) (Alg. 4) and the smoothing cutoff |y| < w (§4.4) —
- * are taken in fp32 on fp32 operands (the kernel's precision; the paper fixes none), with the
- * operation sequence d = a − b per axis, d² = fma(dx,dx, fma(dy,dy, dz·dz)), so that both sides
- * decide identically on identical operands (reading R-prec).
+ * are taken in fp32 (the kernel's precision; the paper fixes none): for a node on the offset
+ * d = (hi − y) + lo to its representative held as fp32 hi + lo, for a point on d = x_j − y, with
+ * d² = fma(dx,dx, fma(dy,dy, dz·dz)), so that both sides decide identically on identical operands
+ * (reading R-prec).
  *
  * Pins (tests/test_oracle_*.py): kernel identities and finite differences; Theorem-1 indicator
  * values; sphere closed forms for A, Aᵀ, G; dense adjointness / symmetry; treecode(c=∞) == dense;
  * treecode error decreasing in c; transpose-mode exact adjointness; tree invariants and SPEC
  * examples; the paper's Table 5 (mean / total solved area, level-7 icosphere); solver energy
- * monotonicity, sphere trajectory and WNNC ablation.  No function is "parity unpinned".
+ * monotonicity, sphere trajectory and WNNC ablation; the first-order far field (WO_ORDER1, SURVEY
+ * §8 row f2 — an extension, not the paper's method) by Taylor decay rates, one-point-node identity,
+ * c = ∞ and its error reduction (tests/test_oracle_order1.py).  No function is "parity unpinned".
  */
 #include "wn_oracle.h"
 
@@ -230,6 +233,8 @@ typedef struct {
   double* V;     /* nn×dim */
   double* W;     /* nn */
   float* thrf;   /* nn: (c·width)^2 in fp32 */
+  double* X;     /* first-order moments (WO_ORDER1) or NULL: dim 3: M (nn×9, row-major M_ab =
+                    Σ_j ν_j,a (x_j − x_B)_b); dim 1: D (nn×3, D = Σ_j s_j (x_j − x_B)) */
   int dim;
 } wo_reps;
 
@@ -267,8 +272,32 @@ static float thr_f32(double theta, int depth) {
   return cw * cw;
 }
 
+/* first-order moments of node id about its representative, from the definition (row f2) */
+static void node_moment1(const wo_tree* t, int64_t id, const double* nu, int dim, const double rep[3], double* X) {
+  const wo_node* nd = &t->nodes[id];
+  int nx = dim == 3 ? 9 : 3;
+  for (int c = 0; c < nx; ++c) X[c] = 0;
+  for (int64_t k = nd->pb; k < nd->pe; ++k) {
+    int64_t j = t->order[k];
+    const double* v = nu + (size_t)dim * j;
+    double d[3];
+    for (int c = 0; c < 3; ++c) d[c] = (double)t->xn[3 * j + c] - rep[c];
+    if (dim == 3) {
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) X[3 * a + b] += v[a] * d[b];
+    } else {
+      for (int c = 0; c < 3; ++c) X[c] += v[0] * d[c];
+    }
+  }
+}
+
+static void reps_compute_o(const wo_tree* t, const double* nu, int dim, double theta, int order1, wo_reps* r);
 static void reps_compute(const wo_tree* t, const double* nu, int dim, double theta, wo_reps* r) {
+  reps_compute_o(t, nu, dim, theta, 0, r);
+}
+static void reps_compute_o(const wo_tree* t, const double* nu, int dim, double theta, int order1, wo_reps* r) {
   r->dim = dim;
+  r->X = order1 ? (double*)malloc((size_t)t->nn * (dim == 3 ? 9 : 3) * sizeof(double)) : NULL;
   r->rep = (double*)malloc((size_t)t->nn * 3 * sizeof(double));
   r->repf = (float*)malloc((size_t)t->nn * 3 * sizeof(float));
   r->lof = (float*)malloc((size_t)t->nn * 3 * sizeof(float));
@@ -283,11 +312,12 @@ static void reps_compute(const wo_tree* t, const double* nu, int dim, double the
       r->lof[3 * id + c] = (float)(r->rep[3 * id + c] - (double)r->repf[3 * id + c]);
     }
     r->thrf[id] = thr_f32(theta, t->nodes[id].depth);
+    if (order1) node_moment1(t, id, nu, dim, r->rep + 3 * id, r->X + (size_t)(dim == 3 ? 9 : 3) * id);
   }
 }
 
 static void reps_free(wo_reps* r) {
-  free(r->rep); free(r->repf); free(r->lof); free(r->V); free(r->W); free(r->thrf);
+  free(r->rep); free(r->repf); free(r->lof); free(r->V); free(r->W); free(r->thrf); free(r->X);
 }
 
 void wo_moments(const wo_tree* t, const double* nu, int dim, double* rep, double* attr, double* W) {
@@ -311,7 +341,7 @@ void wo_moments(const wo_tree* t, const double* nu, int dim, double* rep, double
 static void term(int op, const double y[3], const double x[3], const double* nu, double* acc) {
   /* op | WO_ABS: accumulate |contribution| instead (the per-query conditioning scale Σ_j |term_j|) */
   int absm = op & WO_ABS;
-  op &= ~WO_ABS;
+  op &= ~(WO_ABS | WO_ORDER1);
   double t[3] = {0, 0, 0};
   double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};     /* d = y − x */
   double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
@@ -333,7 +363,51 @@ static void term(int op, const double y[3], const double x[3], const double* nu,
   else for (int c = 0; c < 3; ++c) acc[c] += t[c];
 }
 
-static int out_dim(int op) { return (op == WO_OP_A || (op & WO_ABS)) ? 1 : 3; }
+/* First-order far field (the paper uses order 0 only, and
+   cites Barill et al. for expansions, L409).  For a far node B with sources x_j = x_B + d_j, the
+   contribution Σ_j f(x_j) of op's kernel f is expanded to first order in d_j about x_B:
+   Σ_j f(x_j) ≈ f(x_B)·(ν_B) + Σ_j ∇_x f(x_B)·d_j.  With u = x_B − y, r = |u|, M_ab = Σ_j ν_j,a d_j,b
+   (vector attribute) or D = Σ_j s_j d_j (scalar):
+     A : f = u·ν/(4πr³)                    → [tr M − 3 uᵀMu/r²] / (4π r³)
+     G : f = [ν − 3(u·ν)u/r²]/(4πr³)       → [−3(Mu + u tr M + Mᵀu) + 15 (uᵀMu) u/r²] / (4π r⁵)
+     Aᵀ: f = −s u/(4πr³)                   → −[D − 3 u (u·D)/r²] / (4π r³)
+   Adds the correction for source (x_B, X) at query y into t[3]. */
+static void term1(int op, const double y[3], const double xB[3], const double* X, double t[3]) {
+  double u[3] = {xB[0] - y[0], xB[1] - y[1], xB[2] - y[2]};
+  double r2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+  double r = sqrt(r2);
+  double k3 = 1.0 / (WO_4PI * r2 * r);
+  if (op == WO_OP_AT) {
+    double uD = u[0] * X[0] + u[1] * X[1] + u[2] * X[2];
+    for (int c = 0; c < 3; ++c) t[c] += -(X[c] - 3.0 * u[c] * uD / r2) * k3;
+    return;
+  }
+  double Mu[3], MTu[3], tr = X[0] + X[4] + X[8];
+  for (int a = 0; a < 3; ++a) {
+    Mu[a] = X[3 * a] * u[0] + X[3 * a + 1] * u[1] + X[3 * a + 2] * u[2];
+    MTu[a] = X[a] * u[0] + X[3 + a] * u[1] + X[6 + a] * u[2];
+  }
+  double uMu = u[0] * Mu[0] + u[1] * Mu[1] + u[2] * Mu[2];
+  if (op == WO_OP_A) {
+    t[0] += (tr - 3.0 * uMu / r2) * k3;
+  } else {
+    double k5 = k3 / r2;
+    for (int c = 0; c < 3; ++c) t[c] += (-3.0 * (Mu[c] + u[c] * tr + MTu[c]) + 15.0 * uMu * u[c] / r2) * k5;
+  }
+}
+
+/* far-node contribution: order 0 (term) plus, if X, the first-order correction; |·| under WO_ABS */
+static void term_far(int op, const double y[3], const double xB[3], const double* nuB, const double* X,
+                     double* acc) {
+  int absm = op & WO_ABS, base = op & ~(WO_ABS | WO_ORDER1);
+  double t[3] = {0, 0, 0};
+  term(base, y, xB, nuB, t);
+  if (X) term1(base, y, xB, X, t);
+  if (absm) acc[0] += sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
+  else for (int c = 0; c < 3; ++c) acc[c] += t[c];
+}
+
+static int out_dim(int op) { return ((op & ~WO_ORDER1) == WO_OP_A || (op & WO_ABS)) ? 1 : 3; }
 
 /* ------------------------------------------------------------------------------------------ */
 /* Dense operators: the O(N^2) definitions.              */
@@ -387,7 +461,10 @@ static void trav(const trav_ctx* c, int64_t id, const double y[3], const float y
   if (d2 > c->geo->thrf[id]) {                                  /* far: representative */
     k->far++;
     if (near_tie(d2, c->w2f)) k->ties++;
-    if (!(d2 < c->w2f)) term(c->op, y, c->geo->rep + 3 * id, c->Vattr + (size_t)c->dim * id, acc);
+    if (!(d2 < c->w2f)) {
+      const double* X = c->geo->X ? c->geo->X + (size_t)(c->dim == 3 ? 9 : 3) * id : NULL;
+      term_far(c->op, y, c->geo->rep + 3 * id, c->Vattr + (size_t)c->dim * id, X, acc);
+    }
   } else if (nd->nchild) {
     for (int ch = 0; ch < nd->nchild; ++ch) trav(c, nd->child[ch], y, yf, acc, k);
   } else {                                                      /* leaf: direct sum */
@@ -427,7 +504,7 @@ static void run_queries(const trav_ctx* c, const float* qf, const int64_t* qidx,
 void wo_tree_op(const wo_tree* t, int op, const double* nu, int dim, const float* qf, const int64_t* qidx,
                 int64_t m, double w, double theta, double* out, int64_t* counters) {
   wo_reps r;
-  reps_compute(t, nu, dim, theta, &r);
+  reps_compute_o(t, nu, dim, theta, (op & WO_ORDER1) != 0, &r);
   float wf = (float)w;
   trav_ctx c = {t, &r, r.V, nu, dim, op, wf * wf};
   run_queries(&c, qf, qidx, m, out, counters);
@@ -541,7 +618,8 @@ static void apply(const wo_tree* t, int backend, int op, const double* nu, int d
 }
 
 int wo_solve(const wo_tree* t, double* mu, double w1, double w2, int iters, int first_iter, int total_iters,
-             double theta, int backend, int mode, int wnnc, double* stats) {
+             double theta, int backend, int mode, int wnnc, int order, double* stats) {
+  const int o1 = (order == 1 && backend == 0) ? WO_ORDER1 : 0;
   int64_t n = t->n;
   double* s = (double*)malloc((size_t)n * sizeof(double));
   double* r = (double*)malloc((size_t)n * 3 * sizeof(double));
@@ -554,13 +632,13 @@ int wo_solve(const wo_tree* t, double* mu, double w1, double w2, int iters, int 
     /* the width is handed to the kernels as fp32; both sides use the same rounding */
     double w = (double)(float)width_at(k, total_iters, w1, w2);
     /* grad step */
-    apply(t, backend, WO_OP_A, mu, 3, w, theta, s);
+    apply(t, backend, WO_OP_A | o1, mu, 3, w, theta, s);
     double E = 0;
     for (int64_t i = 0; i < n; ++i) { s[i] = 0.5 - s[i]; E += s[i] * s[i]; }
     if (transpose) wo_tree_AT_transpose(t, mu, s, w, theta, r);
-    else apply(t, backend, WO_OP_AT, s, 1, w, theta, r);
+    else apply(t, backend, WO_OP_AT | o1, s, 1, w, theta, r);
     if (transpose) wo_tree_A_frozen(t, mu, r, w, theta, q);
-    else apply(t, backend, WO_OP_A, r, 3, w, theta, q);
+    else apply(t, backend, WO_OP_A | o1, r, 3, w, theta, q);
     double rr = 0, qq = 0;
     for (int64_t i = 0; i < n; ++i) {
       rr += r[3 * i] * r[3 * i] + r[3 * i + 1] * r[3 * i + 1] + r[3 * i + 2] * r[3 * i + 2];
@@ -570,7 +648,7 @@ int wo_solve(const wo_tree* t, double* mu, double w1, double w2, int iters, int 
     for (int64_t i = 0; i < 3 * n; ++i) mp[i] = mu[i] + alpha * r[i];
     /* WNNC update + rescale */
     if (wnnc) {
-      apply(t, backend, WO_OP_G, mp, 3, w, theta, mh);
+      apply(t, backend, WO_OP_G | o1, mp, 3, w, theta, mh);
       for (int64_t i = 0; i < n; ++i) {
         double a = sqrt(mp[3 * i] * mp[3 * i] + mp[3 * i + 1] * mp[3 * i + 1] + mp[3 * i + 2] * mp[3 * i + 2]);
         double h = sqrt(mh[3 * i] * mh[3 * i] + mh[3 * i + 1] * mh[3 * i + 1] + mh[3 * i + 2] * mh[3 * i + 2]);

@@ -24,7 +24,9 @@ typedef struct wo_tree wo_tree;
 enum { WO_OP_A = 0,   /* Σ ∇Φ(y−x_j)·ν_j          (A, and the field F at arbitrary y) */
        WO_OP_G = 1,   /* −Σ HΦ(y−x_j) ν_j         (G, and −∇F at arbitrary y)         */
        WO_OP_AT = 2,  /* Σ ν_i ∇Φ(x_i−y), ν scalar (Aᵀ, gather form)                  */
-       WO_ABS = 8     /* modifier: accumulate |term| (conditioning scale S = Σ_j |term_j|)  */ };
+       WO_ABS = 8,    /* modifier: accumulate |term| (conditioning scale S = Σ_j |term_j|)  */
+       WO_ORDER1 = 16 /* modifier: first-order far field (not the paper's):   */
+                      /* a far node adds the first-order Taylor term of its sources about x_B  */ };
 
 /* §5.1.1 normalization; returns 0, 1 (empty), 2 (non-finite), 3 (zero extent). */
 int wo_normalize(const float* raw, int64_t n, float* xn, double xf[4]);
@@ -63,7 +65,7 @@ void wo_tree_AT_transpose(const wo_tree* t, const double* mu_geom, const double*
    wnnc: 1 normal, 0 ablation (skip the WNNC update + rescale).
    stats (iters×5 or NULL): E_before, alpha, Σr², Σ(Ar)², w. */
 int wo_solve(const wo_tree* t, double* mu, double w1, double w2, int iters, int first_iter,
-             int total_iters, double theta, int backend, int mode, int wnnc, double* stats);
+             int total_iters, double theta, int backend, int mode, int wnnc, int order, double* stats);
 
 int wo_num_threads(void);
 
