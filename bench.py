@@ -45,6 +45,8 @@ CONFIG_TEXT = {
 #     G : rsqrt 1 + r⁻², r⁻³ 2 + d·ν 5 + 3(d·ν)r⁻² 2 + ν − t d 6 + accumulate 6            = 22
 FLOPS_TEST = 8
 FLOPS_TERM = {"A": 10, "AT": 10, "G": 22}
+# first-order far field (--order 1): the order-0 term plus M e / eᵀMe / D·e (traverse.cu term1)
+FLOPS_TERM1 = {"A": 34, "AT": 23, "G": 55}
 
 
 class ClockSampler:
@@ -173,6 +175,8 @@ def run_ours(args):
 
     def step(**over):
         tree = wn.wn_build_tree(pts)
+        if args.order:
+            wn.wn_tree_set_far_order(tree, args.order)
         mu = torch.zeros(n, 3, dtype=torch.float32, device=dev)
         wn.wnnc_iterate(tree, mu, comm=comm, **{**params, **over})
         return tree, mu
@@ -237,7 +241,8 @@ def run_ours(args):
     # ---- roofline of the dominant kernel class (the treecode traversals) ----
     trav_ms = sum(prof[k][0] for k in ("trav_A", "trav_AT", "trav_G")) / args.prof_steps
     trav_launches = sum(prof[k][1] for k in ("trav_A", "trav_AT", "trav_G")) / args.prof_steps
-    flops = sum(FLOPS_TEST * work[c]["tests"] + FLOPS_TERM[c] * work[c]["live"] for c in ("A", "AT", "G"))
+    fterm = FLOPS_TERM1 if args.order == 1 else FLOPS_TERM
+    flops = sum(FLOPS_TEST * work[c]["tests"] + fterm[c] * work[c]["live"] for c in ("A", "AT", "G"))
     achieved = flops / (trav_ms / 1e3) / 1e12
     props = torch.cuda.get_device_properties(dev)
     sm_count = props.multi_processor_count
@@ -261,7 +266,8 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": CONFIG_TEXT[args.config], "n_points": n, "iters_per_step": ITERS,
-                   "theta": args.theta, "max_depth": 15, "depth_used": depth_used, "num_nodes": num_nodes,
+                   "theta": args.theta, "far_order": args.order, "max_depth": 15, "depth_used": depth_used,
+                   "num_nodes": num_nodes,
                    "adjoint": "transpose" if args.transpose else "gather",
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
                    "parallelism": f"query-sharded x{world}" if world > 1 else "1 GPU",
@@ -305,6 +311,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--theta", type=float, default=2.0)
     ap.add_argument("--transpose", action="store_true", help="north-star exact-transpose adjoint")
+    ap.add_argument("--order", type=int, default=0, choices=[0, 1],
+                    help="far-field order: 0 = the paper's Alg. 4 (headline), 1 = first-order (SURVEY §8 row f2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-iters", type=int, default=3, help="oracle iterations per sample / reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -112,6 +112,16 @@ wn_status wn_tree_destroy(wn_tree t);
 /* (host outputs) sizes and the similarity transform: xn = (x − xform[0:3]) · xform[3]. */
 wn_status wn_tree_info(wn_tree t, int64_t* num_points, int64_t* num_nodes, int32_t* depth_used,
                        double xform[4]);
+/* Far-field order used by every later wn_eval / wn_eval_grad / wn_query_work / wn_eval_adjoint
+   (gather) / wnnc_iterate call on t.  0 (default): the paper's Alg. 4 — a far node B contributes its
+   representative term K(x_i − x_B)·ν_B.  1: first-order far field (SURVEY §8
+   row f2, an extension; the paper points to expansions via Barill et al., L409): the far term also
+   includes Σ_{j∈B} ∇_x K(x_i − x)|_{x_B}·(x_j − x_B) ν_j, from per-node first moments (symmetric
+   M = Σ_j ν_j (x_j − x_B)ᵀ for vector ν, D = Σ_j s_j (x_j − x_B) for scalar s).  Opening decisions
+   and near-field terms are unchanged.  Order 1 is not defined for the transpose-mode adjoint
+   (WN_ADJ_TRANSPOSE ⇒ WN_ERR_ARG).  The first call with order 1 allocates its scratch (stream-ordered
+   on `stream`; ≈ 200 B per point).  WN_ERR_ARG for order ∉ {0, 1}. */
+wn_status wn_tree_set_far_order(wn_tree t, int32_t order, void* stream);
 /* Export the structure (device outputs, any may be NULL): keys[N] uint64 Morton keys in sorted order
    (3·D bits, level-1 octant digit most significant, digit = 4·x + 2·y + z); perm[N] caller index of
    the k-th sorted point; xn[N×3] normalized coordinates in sorted order; per node in BFS order

@@ -153,6 +153,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     m1.vec = it.mu;
     m1.theta = p.theta;
     m1.out = transpose ? t->set[1] : t->set[0];
+    m1.order1 = t->far_order == 1;
     WN_TRY(build_moments(t, m1, s));
     TravArgs a1 = base_args(t, w2);
     a1.qorder = qord;
@@ -164,6 +165,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a1.q_end = q1;
     a1.out_f = it.s;
     a1.partial = it.part;
+    a1.order1 = t->far_order;
     WN_TRY(traverse(a1, s));
     if (comm) WN_TRY(comm_allgather_f(comm, it.s, 1, t->n, qord, stage, s));
     // (2) r = A_wᵀ s  (+ Σ|r|² partials)
@@ -175,7 +177,8 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
       m2.scal = it.s;
       m2.theta = p.theta;
       m2.out = t->set[0];
-      WN_TRY(build_moments(t, m2, s));
+      m2.order1 = t->far_order == 1;
+    WN_TRY(build_moments(t, m2, s));
       TravArgs a2 = base_args(t, w2);
     a2.qorder = qord;
       a2.op = OP_AT;
@@ -186,7 +189,8 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
       a2.q_end = q1;
       a2.out_v4 = it.r;
       a2.partial = it.part + stride;
-      WN_TRY(traverse(a2, s));
+      a2.order1 = t->far_order;
+    WN_TRY(traverse(a2, s));
       if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.r, 4, t->n, qord, stage, s));
     }
     // (3) Σ (A_w r)²  — gather: r's own representatives; transpose: μ's frozen geometry
@@ -195,6 +199,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     m3.vec = it.r;
     m3.theta = p.theta;
     m3.out = t->set[0];
+    m3.order1 = t->far_order == 1;
     WN_TRY(build_moments(t, m3, s));
     TravArgs a3 = base_args(t, w2);
     a3.qorder = qord;
@@ -206,6 +211,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a3.q_begin = q0;
     a3.q_end = q1;
     a3.partial = it.part + 2 * stride;
+    a3.order1 = t->far_order;
     WN_TRY(traverse(a3, s));
     if (comm) WN_TRY(comm_allgather_partials(comm, it.part, stride, t->n, s));
     // α = Σr² / Σ(Ar)²  (Alg. 2), fixed-order reduction of the partials
@@ -219,6 +225,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     m4.axpy_out = it.mup;
     m4.theta = p.theta;
     m4.out = t->set[0];
+    m4.order1 = t->far_order == 1;
     WN_TRY(build_moments(t, m4, s));
     TravArgs a4 = base_args(t, w2);
     a4.qorder = qord;
@@ -230,6 +237,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a4.q_begin = q0;
     a4.q_end = q1;
     a4.out_v4 = it.mu;
+    a4.order1 = t->far_order;
     WN_TRY(traverse(a4, s));
     if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, s));
   }
@@ -317,6 +325,14 @@ wn_status wn_tree_destroy(wn_tree t) {
   return WN_OK;
 }
 
+wn_status wn_tree_set_far_order(wn_tree t, int32_t order, void* stream) {
+  if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
+  if (order != 0 && order != 1) return set_error(WN_ERR_ARG, "far-field order must be 0 or 1");
+  if (order == 1) WN_TRY(enable_order1(t, (cudaStream_t)stream));
+  t->far_order = order;
+  return WN_OK;
+}
+
 wn_status wn_tree_info(wn_tree t, int64_t* num_points, int64_t* num_nodes, int32_t* depth_used, double xform[4]) {
   if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
   if (num_points) *num_points = t->n;
@@ -392,8 +408,10 @@ static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a,
   mm.a_sorted = a ? (const float*)it.tmp : nullptr;
   mm.theta = theta;
   mm.out = t->set[0];
+  mm.order1 = t->far_order == 1;
   WN_TRY(build_moments(t, mm, s));
   TravArgs ta = base_args(t, width * width);
+  ta.order1 = t->far_order;
   ta.op = op;
   ta.epi = EPI_PLAIN;
   ta.nodes = t->set[0];
@@ -452,6 +470,8 @@ wn_status wn_eval_adjoint(wn_tree t, const float* sv, float width, float theta, 
   if (bad_theta(theta)) return set_error(WN_ERR_ARG, "theta must be > 0");
   if (mode != WN_ADJ_GATHER && mode != WN_ADJ_TRANSPOSE) return set_error(WN_ERR_ARG, "bad adjoint mode");
   if (mode == WN_ADJ_TRANSPOSE && !mu_geom) return set_error(WN_ERR_ARG, "transpose mode needs mu_geom");
+  if (mode == WN_ADJ_TRANSPOSE && t->far_order != 0)
+    return set_error(WN_ERR_ARG, "transpose-mode adjoint is defined for the order-0 far field only");
   cudaStream_t s = (cudaStream_t)stream;
   WN_TRY(ensure_scratch(t, s));
   IterScratch& it = t->it;
@@ -464,8 +484,10 @@ wn_status wn_eval_adjoint(wn_tree t, const float* sv, float width, float theta, 
     m.scal = it.s;
     m.theta = theta;
     m.out = t->set[0];
+    m.order1 = t->far_order == 1;
     WN_TRY(build_moments(t, m, s));
     TravArgs ta = base_args(t, w2);
+    ta.order1 = t->far_order;
     ta.op = OP_AT;
     ta.epi = EPI_PLAIN;
     ta.nodes = t->set[0];
@@ -506,6 +528,8 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
   WN_TRY(check_params(p));
   if (comm && p->adjoint_mode == WN_ADJ_TRANSPOSE)
     return set_error(WN_ERR_ARG, "transpose-mode adjoint is single-GPU only in this build");
+  if (t->far_order != 0 && p->adjoint_mode == WN_ADJ_TRANSPOSE)
+    return set_error(WN_ERR_ARG, "transpose-mode adjoint is defined for the order-0 far field only");
   cudaStream_t s = (cudaStream_t)stream;
   WN_TRY(ensure_scratch(t, s));
   IterScratch& it = t->it;
@@ -518,9 +542,10 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
   gather_vec(t->n, t->perm, mu, sc2, t->it.mu, s);        // μ_norm = scale²·μ
   if (p->flags & WN_FLAG_GRAPH) {
     // the whole iteration loop as one CUDA graph: captured on a private stream, cached per parameters
-    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm));
+    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm) + sizeof(int));
     memcpy(key.data(), p, sizeof(wnnc_params));
     memcpy(key.data() + sizeof(wnnc_params), &comm, sizeof(comm));
+    memcpy(key.data() + sizeof(wnnc_params) + sizeof(comm), &t->far_order, sizeof(int));
     if (!t->graph_exec || key != t->graph_key) {
       if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
       t->graph_exec = nullptr;

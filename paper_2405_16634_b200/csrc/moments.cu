@@ -212,10 +212,21 @@ __global__ void __launch_bounds__(kMomThreads, WN_EXP_MOM_LB) moments_range(Tree
 // two-sum adds; lo stored in fp32), so a difference keeps ≈ 2^-77·|Σ_all| accuracy — far below the bottom-up fp64
 // rounding — and an exact integer count of the points with |ν| > 0 decides Σ|ν| = 0 (⇒ centroid)
 // exactly.  One-point nodes take their point's own values (exact: rep = the point).  DESIGN.md §Moments.
+// First-order far field (ORD = 1): the prefix also carries sym(Σ ν_j x_jᵀ) (vector ν,
+// 6 terms) or Σ s_j x_j (scalar, 3), and each node stores its first moment about the representative,
+// sym M = sym(Σ ν_j x_jᵀ) − sym(ν_B x_Bᵀ) or D = Σ s_j x_j − s_B x_B, in NodeSet::ext.
 constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
 constexpr int kScanTopThreads = 256;
-// prefix entry j (exclusive: points [0, j)): hi[8] = (W, P, V, count) fp64 in E_hi, lo[8] = the
-// double-double low parts rounded to fp32 in E_lo (|lo| ≤ ulp(hi)/2, so fp32 keeps ≈ 2^-77 relative)
+
+// components per prefix entry; entry j (exclusive: points [0, j)) = hi[EH] fp64 (the NC sums, the count,
+// padding) in E_hi and lo[EL] = the double-double low parts rounded to fp32 in E_lo
+template <int KIND, int ORD>
+struct PreLayout {
+  static constexpr int NC = ORD == 0 ? 7 : (KIND == ATTR_VEC ? 13 : 10);
+  static constexpr int EH = (NC + 2) & ~1;
+  static constexpr int EL = (NC + 3) & ~3;
+};
+constexpr int kPreDoublesMax = 14 + 8;  // EH + EL/2 of the largest layout (vector, ORD 1)
 
 struct DD {
   double hi, lo;
@@ -231,9 +242,10 @@ __device__ __forceinline__ DD dd_add(DD a, DD b) {
   return DD{h, __dsub_rn(e, __dsub_rn(h, s))};
 }
 
-template <int KIND>
+// per-point terms: (|ν|, |ν|x, |ν|y, |ν|z, ν) and, for ORD 1, sym(ν xᵀ) (xx, yy, zz, xy, xz, yz) or s x
+template <int KIND, int ORD>
 __device__ __forceinline__ void point_vals(int64_t j, const float4* __restrict__ pts, const MomentArgs& m, float alpha,
-                                           double o[7]) {
+                                           double* o) {
   const float4 x = pts[j];
   double a, v0, v1 = 0.0, v2 = 0.0;
   if (KIND == ATTR_VEC) {
@@ -253,40 +265,60 @@ __device__ __forceinline__ void point_vals(int64_t j, const float4* __restrict__
     if (m.a_sorted) v0 *= (double)m.a_sorted[j];
     a = fabs(v0);
   }
+  const double px = x.x, py = x.y, pz = x.z;
   o[0] = a;
-  o[1] = a * (double)x.x;
-  o[2] = a * (double)x.y;
-  o[3] = a * (double)x.z;
+  o[1] = a * px;
+  o[2] = a * py;
+  o[3] = a * pz;
   o[4] = v0;
   o[5] = v1;
   o[6] = v2;
+  if (ORD == 1) {
+    if (KIND == ATTR_VEC) {
+      o[7] = v0 * px;
+      o[8] = v1 * py;
+      o[9] = v2 * pz;
+      o[10] = 0.5 * (v0 * py + v1 * px);
+      o[11] = 0.5 * (v0 * pz + v2 * px);
+      o[12] = 0.5 * (v1 * pz + v2 * py);
+    } else {
+      o[7] = v0 * px;
+      o[8] = v0 * py;
+      o[9] = v0 * pz;
+    }
+  }
 }
 
-// scan element: 7 double-double sums + the number of points with |ν| > 0 (an exact integer)
+// scan element: NC double-double sums + the number of points with |ν| > 0 (an exact integer)
+template <int NC>
 struct Elt {
-  DD v[7];
+  DD v[NC];
   double cnt;
 };
 
-__device__ __forceinline__ void elt_zero(Elt& e) {
+template <int NC>
+__device__ __forceinline__ void elt_zero(Elt<NC>& e) {
 #pragma unroll
-  for (int c = 0; c < 7; ++c) e.v[c] = DD{0.0, 0.0};
+  for (int c = 0; c < NC; ++c) e.v[c] = DD{0.0, 0.0};
   e.cnt = 0.0;
 }
-__device__ __forceinline__ void elt_add(Elt& e, const Elt& f) {
+template <int NC>
+__device__ __forceinline__ void elt_add(Elt<NC>& e, const Elt<NC>& f) {
 #pragma unroll
-  for (int c = 0; c < 7; ++c) e.v[c] = dd_add(e.v[c], f.v[c]);
+  for (int c = 0; c < NC; ++c) e.v[c] = dd_add(e.v[c], f.v[c]);
   e.cnt += f.cnt;
 }
-__device__ __forceinline__ void elt_add_point(Elt& e, const double o[7]) {
+template <int NC>
+__device__ __forceinline__ void elt_add_point(Elt<NC>& e, const double* o) {
 #pragma unroll
-  for (int c = 0; c < 7; ++c) e.v[c] = dd_add(e.v[c], DD{o[c], 0.0});
+  for (int c = 0; c < NC; ++c) e.v[c] = dd_add(e.v[c], DD{o[c], 0.0});
   e.cnt += o[0] > 0.0 ? 1.0 : 0.0;
 }
-__device__ __forceinline__ Elt elt_shfl_up(const Elt& e, int d) {
-  Elt r;
+template <int NC>
+__device__ __forceinline__ Elt<NC> elt_shfl_up(const Elt<NC>& e, int d) {
+  Elt<NC> r;
 #pragma unroll
-  for (int c = 0; c < 7; ++c) {
+  for (int c = 0; c < NC; ++c) {
     r.v[c].hi = __shfl_up_sync(0xffffffffu, e.v[c].hi, d);
     r.v[c].lo = __shfl_up_sync(0xffffffffu, e.v[c].lo, d);
   }
@@ -294,11 +326,12 @@ __device__ __forceinline__ Elt elt_shfl_up(const Elt& e, int d) {
   return r;
 }
 // inclusive warp scan over the first `width` lanes (fixed order)
-__device__ __forceinline__ void warp_inscan(Elt& x, int lane, int width) {
+template <int NC>
+__device__ __forceinline__ void warp_inscan(Elt<NC>& x, int lane, int width) {
   for (int o = 1; o < width; o <<= 1) {
-    const Elt y = elt_shfl_up(x, o);
+    const Elt<NC> y = elt_shfl_up(x, o);
     if (lane >= o) {
-      Elt z = y;
+      Elt<NC> z = y;
       elt_add(z, x);
       x = z;
     }
@@ -306,23 +339,23 @@ __device__ __forceinline__ void warp_inscan(Elt& x, int lane, int width) {
 }
 
 // block-wide exclusive scan (fixed order: deterministic); e becomes the exclusive prefix, tot the total
-template <int NT>
-__device__ __forceinline__ void block_exscan(Elt& e, Elt& tot) {
+template <int NT, int NC>
+__device__ __forceinline__ void block_exscan(Elt<NC>& e, Elt<NC>& tot) {
   constexpr int NW = NT / 32;
-  __shared__ Elt ws[NW + 1];
+  __shared__ Elt<NC> ws[NW + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Elt inc = e;
+  Elt<NC> inc = e;
   warp_inscan(inc, lane, 32);
   if (lane == 31) ws[warp] = inc;
-  Elt prev = elt_shfl_up(inc, 1);
+  Elt<NC> prev = elt_shfl_up(inc, 1);
   if (lane == 0) elt_zero(prev);
   __syncthreads();
   if (warp == 0) {  // scan of the warp totals by one warp
-    Elt x;
+    Elt<NC> x;
     if (lane < NW) x = ws[lane];
     else elt_zero(x);
     warp_inscan(x, lane, NW);
-    Elt xp = elt_shfl_up(x, 1);
+    Elt<NC> xp = elt_shfl_up(x, 1);
     if (lane == 0) elt_zero(xp);
     __syncwarp();
     if (lane < NW) ws[lane] = xp;
@@ -335,11 +368,12 @@ __device__ __forceinline__ void block_exscan(Elt& e, Elt& tot) {
   __syncthreads();
 }
 
-template <int KIND>
+template <int KIND, int ORD>
 __global__ void __launch_bounds__(kScanThreads) mom_tile_sum(const float4* __restrict__ pts, MomentArgs m, int64_t n,
-                                                             Elt* __restrict__ tile_tot) {
+                                                             Elt<PreLayout<KIND, ORD>::NC>* __restrict__ tile_tot) {
+  constexpr int NC = PreLayout<KIND, ORD>::NC;
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-  Elt t, tot;
+  Elt<NC> t, tot;
   elt_zero(t);
   // coalesced: item k of thread x is point tile·T + k·256 + x (totals need no ownership order)
   const int64_t j0 = blockIdx.x * (int64_t)kScanTile + threadIdx.x;
@@ -347,8 +381,8 @@ __global__ void __launch_bounds__(kScanThreads) mom_tile_sum(const float4* __res
   for (int k = 0; k < kScanItems; ++k) {
     const int64_t j = j0 + k * kScanThreads;
     if (j < n) {
-      double o[7];
-      point_vals<KIND>(j, pts, m, alpha, o);
+      double o[NC];
+      point_vals<KIND, ORD>(j, pts, m, alpha, o);
       elt_add_point(t, o);
     }
   }
@@ -356,11 +390,12 @@ __global__ void __launch_bounds__(kScanThreads) mom_tile_sum(const float4* __res
   if (threadIdx.x == 0) tile_tot[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(kScanTopThreads) mom_tile_scan(const Elt* __restrict__ tile_tot, int64_t ntiles,
-                                                                 Elt* __restrict__ tile_off) {
+template <int NC>
+__global__ void __launch_bounds__(kScanTopThreads) mom_tile_scan(const Elt<NC>* __restrict__ tile_tot, int64_t ntiles,
+                                                                 Elt<NC>* __restrict__ tile_off) {
   const int64_t per = (ntiles + kScanTopThreads - 1) / kScanTopThreads;
   const int64_t t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
-  Elt v, tot;
+  Elt<NC> v, tot;
   elt_zero(v);
   for (int64_t t = t0; t < t1; ++t) elt_add(v, tile_tot[t]);
   block_exscan<kScanTopThreads>(v, tot);
@@ -370,105 +405,141 @@ __global__ void __launch_bounds__(kScanTopThreads) mom_tile_scan(const Elt* __re
   }
 }
 
-__device__ __forceinline__ void store_pre(double* __restrict__ Eh, float* __restrict__ El, int64_t j, const Elt& t) {
-  double2* h = reinterpret_cast<double2*>(Eh + 8 * j);
-  h[0] = make_double2(t.v[0].hi, t.v[1].hi);
-  h[1] = make_double2(t.v[2].hi, t.v[3].hi);
-  h[2] = make_double2(t.v[4].hi, t.v[5].hi);
-  h[3] = make_double2(t.v[6].hi, t.cnt);
-  float4* l = reinterpret_cast<float4*>(El + 8 * j);
-  l[0] = make_float4((float)t.v[0].lo, (float)t.v[1].lo, (float)t.v[2].lo, (float)t.v[3].lo);
-  l[1] = make_float4((float)t.v[4].lo, (float)t.v[5].lo, (float)t.v[6].lo, 0.f);
+template <int KIND, int ORD>
+__device__ __forceinline__ void store_pre(double* __restrict__ Eh, float* __restrict__ El, int64_t j,
+                                          const Elt<PreLayout<KIND, ORD>::NC>& t) {
+  using Lay = PreLayout<KIND, ORD>;
+  double h[Lay::EH];
+  float l[Lay::EL];
+#pragma unroll
+  for (int c = 0; c < Lay::EH; ++c) h[c] = c < Lay::NC ? t.v[c].hi : (c == Lay::NC ? t.cnt : 0.0);
+#pragma unroll
+  for (int c = 0; c < Lay::EL; ++c) l[c] = c < Lay::NC ? (float)t.v[c].lo : 0.f;
+  double2* hp = reinterpret_cast<double2*>(Eh + Lay::EH * j);
+#pragma unroll
+  for (int c = 0; c < Lay::EH / 2; ++c) hp[c] = make_double2(h[2 * c], h[2 * c + 1]);
+  float4* lp = reinterpret_cast<float4*>(El + Lay::EL * j);
+#pragma unroll
+  for (int c = 0; c < Lay::EL / 4; ++c) lp[c] = make_float4(l[4 * c], l[4 * c + 1], l[4 * c + 2], l[4 * c + 3]);
 }
 
-template <int KIND>
+template <int KIND, int ORD>
 __global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __restrict__ pts, MomentArgs m,
-                                                                int64_t n, const Elt* __restrict__ tile_off,
+                                                                int64_t n,
+                                                                const Elt<PreLayout<KIND, ORD>::NC>* __restrict__ tile_off,
                                                                 double* __restrict__ Eh, float* __restrict__ El) {
+  constexpr int NC = PreLayout<KIND, ORD>::NC;
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-  Elt t, tot;
+  Elt<NC> t, tot;
   elt_zero(t);
   const int64_t j0 = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanItems;  // consecutive ownership
   for (int k = 0; k < kScanItems; ++k)
     if (j0 + k < n) {
-      double o[7];
-      point_vals<KIND>(j0 + k, pts, m, alpha, o);
+      double o[NC];
+      point_vals<KIND, ORD>(j0 + k, pts, m, alpha, o);
       elt_add_point(t, o);
     }
   block_exscan<kScanThreads>(t, tot);
   {
-    Elt z = tile_off[blockIdx.x];
+    Elt<NC> z = tile_off[blockIdx.x];
     elt_add(z, t);
     t = z;
   }
   for (int k = 0; k < kScanItems; ++k) {
     const int64_t j = j0 + k;
     if (j < n) {
-      store_pre(Eh, El, j, t);
-      double o[7];
-      point_vals<KIND>(j, pts, m, alpha, o);
+      store_pre<KIND, ORD>(Eh, El, j, t);
+      double o[NC];
+      point_vals<KIND, ORD>(j, pts, m, alpha, o);
       elt_add_point(t, o);
       if (KIND == ATTR_VEC && m.axpy_r) {  // μ' written once here, read by the G traversal
         const float4 v = m.vec[j], r = m.axpy_r[j];
         m.axpy_out[j] = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
       }
-      if (j == n - 1) store_pre(Eh, El, n, t);
+      if (j == n - 1) store_pre<KIND, ORD>(Eh, El, n, t);
     }
   }
 }
 
-template <int KIND>
+template <int KIND, int ORD>
 __global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int64_t nn, const double* __restrict__ Eh,
                                                  const float* __restrict__ El) {
+  using Lay = PreLayout<KIND, ORD>;
+  constexpr int NC = Lay::NC;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nn) return;
   const int j0 = tv.pb[i], j1 = tv.pe[i];
-  Sums S;
+  double d[NC];
   float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
   if (j1 - j0 == 1) {
     const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-    double o[7];
-    point_vals<KIND>(j0, tv.pts, m, alpha, o);
-    S.W = o[0];
-    S.P[0] = o[1]; S.P[1] = o[2]; S.P[2] = o[3];
-    S.V[0] = o[4]; S.V[1] = o[5]; S.V[2] = o[6];
+    point_vals<KIND, ORD>(j0, tv.pts, m, alpha, d);
     p0 = tv.pts[j0];
   } else {
-    const double2* a = reinterpret_cast<const double2*>(Eh + 8 * (int64_t)j0);
-    const double2* b = reinterpret_cast<const double2*>(Eh + 8 * (int64_t)j1);
-    const double2 a0 = a[0], a1 = a[1], a2 = a[2], a3 = a[3], b0 = b[0], b1 = b[1], b2 = b[2], b3 = b[3];
-    double d[7] = {0, 0, 0, 0, 0, 0, 0};
-    if (b3.y != a3.y) {  // else no point has |ν| > 0: Σ|ν| = 0 and every ν_j = 0, exactly
-      const float4* al = reinterpret_cast<const float4*>(El + 8 * (int64_t)j0);
-      const float4* bl = reinterpret_cast<const float4*>(El + 8 * (int64_t)j1);
-      const float4 la0 = al[0], la1 = al[1], lb0 = bl[0], lb1 = bl[1];
-      const double ah[7] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x};
-      const double bh[7] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y, b3.x};
-      const float alo[7] = {la0.x, la0.y, la0.z, la0.w, la1.x, la1.y, la1.z};
-      const float blo[7] = {lb0.x, lb0.y, lb0.z, lb0.w, lb1.x, lb1.y, lb1.z};
+    const double2* a = reinterpret_cast<const double2*>(Eh + Lay::EH * (int64_t)j0);
+    const double2* b = reinterpret_cast<const double2*>(Eh + Lay::EH * (int64_t)j1);
+    double ah[Lay::EH], bh[Lay::EH];
 #pragma unroll
-      for (int c = 0; c < 7; ++c) d[c] = dd_add(DD{bh[c], (double)blo[c]}, DD{-ah[c], -(double)alo[c]}).hi;
+    for (int c = 0; c < Lay::EH / 2; ++c) {
+      const double2 x = a[c], y = b[c];
+      ah[2 * c] = x.x; ah[2 * c + 1] = x.y;
+      bh[2 * c] = y.x; bh[2 * c + 1] = y.y;
     }
-    S.W = d[0];
-    S.P[0] = d[1]; S.P[1] = d[2]; S.P[2] = d[3];
-    S.V[0] = d[4]; S.V[1] = d[5]; S.V[2] = d[6];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) d[c] = 0.0;
+    if (bh[NC] != ah[NC]) {  // else no point has |ν| > 0: Σ|ν| = 0 and every ν_j = 0, exactly
+      const float4* al = reinterpret_cast<const float4*>(El + Lay::EL * (int64_t)j0);
+      const float4* bl = reinterpret_cast<const float4*>(El + Lay::EL * (int64_t)j1);
+      float alo[Lay::EL], blo[Lay::EL];
+#pragma unroll
+      for (int c = 0; c < Lay::EL / 4; ++c) {
+        const float4 x = al[c], y = bl[c];
+        alo[4 * c] = x.x; alo[4 * c + 1] = x.y; alo[4 * c + 2] = x.z; alo[4 * c + 3] = x.w;
+        blo[4 * c] = y.x; blo[4 * c + 1] = y.y; blo[4 * c + 2] = y.z; blo[4 * c + 3] = y.w;
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) d[c] = dd_add(DD{bh[c], (double)blo[c]}, DD{-ah[c], -(double)alo[c]}).hi;
+    }
   }
+  Sums S;
+  S.W = d[0];
+  S.P[0] = d[1]; S.P[1] = d[2]; S.P[2] = d[3];
+  S.V[0] = d[4]; S.V[1] = d[5]; S.V[2] = d[6];
   if (m.write_W) tv.sums[8 * i] = S.W;
   write_record<KIND>(i, S, j1 - j0, p0, tv.depth[i], tv.topo[i], tv.smask[i], m.theta, tv.centroid, m);
+  if (ORD == 1) {  // first moment about the fp64 representative (0 for one-point nodes and Σ|ν| = 0)
+    float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f), e1 = e0;
+    if (j1 - j0 > 1 && S.W > 0.0) {
+      const double X = S.P[0] / S.W, Y = S.P[1] / S.W, Z = S.P[2] / S.W;
+      if (KIND == ATTR_VEC) {
+        const double mxx = d[7] - S.V[0] * X, myy = d[8] - S.V[1] * Y, mzz = d[9] - S.V[2] * Z;
+        const double mxy = d[10] - 0.5 * (S.V[0] * Y + S.V[1] * X);
+        const double mxz = d[11] - 0.5 * (S.V[0] * Z + S.V[2] * X);
+        const double myz = d[12] - 0.5 * (S.V[1] * Z + S.V[2] * Y);
+        e0 = make_float4((float)mxx, (float)myy, (float)mzz, (float)(mxx + myy + mzz));
+        e1 = make_float4((float)mxy, (float)mxz, (float)myz, 0.f);
+      } else {
+        e0 = make_float4((float)(d[7] - S.V[0] * X), (float)(d[8] - S.V[0] * Y), (float)(d[9] - S.V[0] * Z), 0.f);
+      }
+    }
+    m.out.ext[2 * i] = e0;
+    m.out.ext[2 * i + 1] = e1;
+  }
 }
 
-template <int KIND>
+template <int KIND, int ORD>
 void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
+  using Lay = PreLayout<KIND, ORD>;
   TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->topo, t->smask, t->sums, t->centroid};
   const int64_t nt = t->mom_ntiles;
-  Elt* tot = reinterpret_cast<Elt*>(t->mom_tile);
-  Elt* off = tot + nt;
+  Elt<Lay::NC>* tot = reinterpret_cast<Elt<Lay::NC>*>(t->mom_tile);
+  Elt<Lay::NC>* off = tot + nt;
   double* Eh = t->mom_pre;
-  float* El = reinterpret_cast<float*>(t->mom_pre + 8 * (t->n + 1));
-  mom_tile_sum<KIND><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, tot);
-  mom_tile_scan<<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
-  mom_tile_prefix<KIND><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, off, Eh, El);
-  mom_nodes<KIND><<<(unsigned)((t->nn + 255) / 256), 256, 0, s>>>(tv, m, t->nn, Eh, El);
+  float* El = reinterpret_cast<float*>(t->mom_pre + Lay::EH * (t->n + 1));
+  mom_tile_sum<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, tot);
+  mom_tile_scan<Lay::NC><<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
+  mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, off, Eh, El);
+  mom_nodes<KIND, ORD><<<(unsigned)((t->nn + 255) / 256), 256, 0, s>>>(tv, m, t->nn, Eh, El);
 }
 
 template <int KIND>
@@ -508,7 +579,7 @@ wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
                           cudaMemcpyHostToDevice, s));
   t->mom_ntiles = (t->n + kScanTile - 1) / kScanTile;
   WN_CUDA(cudaMallocAsync((void**)&t->mom_pre, 12 * (size_t)(t->n + 1) * sizeof(double), s));
-  WN_CUDA(cudaMallocAsync((void**)&t->mom_tile, 2 * (size_t)t->mom_ntiles * sizeof(Elt), s));
+  WN_CUDA(cudaMallocAsync((void**)&t->mom_tile, 2 * (size_t)t->mom_ntiles * sizeof(Elt<7>), s));
   return WN_OK;
 }
 
@@ -516,8 +587,14 @@ wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
 #ifndef WN_EXP_OLD_MOM
   if (m.kind != ATTR_UNIT) {  // per-iteration attributes: prefix differences
     ProfScope ps(WN_PROF_MOMENTS, s, 4);
-    if (m.kind == ATTR_VEC) launch_prefix<ATTR_VEC>(t, m, s);
-    else launch_prefix<ATTR_SCALAR>(t, m, s);
+    if (m.order1 && !(m.out.ext && t->mom_order1_ready)) return set_error(WN_ERR_ARG, "internal: order-1 scratch");
+    if (m.kind == ATTR_VEC) {
+      if (m.order1) launch_prefix<ATTR_VEC, 1>(t, m, s);
+      else launch_prefix<ATTR_VEC, 0>(t, m, s);
+    } else {
+      if (m.order1) launch_prefix<ATTR_SCALAR, 1>(t, m, s);
+      else launch_prefix<ATTR_SCALAR, 0>(t, m, s);
+    }
     WN_CUDA(cudaGetLastError());
     return WN_OK;
   }
@@ -529,6 +606,21 @@ wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
     default: launch_all<ATTR_UNIT>(t, m, s, t->mom_loff); break;
   }
   WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
+// order-1 far field (row f2): larger prefix entries and tile totals, the node sets' ext arrays
+wn_status enable_order1(wn_tree_s* t, cudaStream_t s) {
+  if (t->mom_order1_ready) return WN_OK;
+  cudaFreeAsync(t->mom_pre, s);
+  cudaFreeAsync(t->mom_tile, s);
+  t->mom_pre = nullptr;
+  t->mom_tile = nullptr;
+  WN_CUDA(cudaMallocAsync((void**)&t->mom_pre, kPreDoublesMax * (size_t)(t->n + 1) * sizeof(double), s));
+  WN_CUDA(cudaMallocAsync((void**)&t->mom_tile, 2 * (size_t)t->mom_ntiles * sizeof(Elt<13>), s));
+  WN_CUDA(cudaMallocAsync((void**)&t->set[0].ext, 2 * (size_t)(t->nn + 1) * sizeof(float4), s));
+  WN_CUDA(cudaMemsetAsync(t->set[0].ext, 0, 2 * (size_t)(t->nn + 1) * sizeof(float4), s));
+  t->mom_order1_ready = true;
   return WN_OK;
 }
 

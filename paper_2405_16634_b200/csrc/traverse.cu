@@ -66,6 +66,40 @@ struct Acc {
       z = fmaf(inv3, fmaf(-t, ez, V.z), z);
     }
   }
+  // first-order far field (row f2): the order-0 term plus Σ_j ∇f(x_B)·d_j from the node's first moments,
+  // X0 = (Mxx, Myy, Mzz, tr M), X1 = (Mxy, Mxz, Myz, ·) (sym M, vector ν) or X0 = (D, ·) (scalar s):
+  //   A : (e·ν + tr M − 3 eᵀMe/r²) / r³
+  //   Aᵀ: −(s e + D − 3 e (e·D)/r²) / r³
+  //   G : (ν − 3(e·ν) e/r² − 6 M e/r² + (15 eᵀMe/r² − 3 tr M) e/r²) / r³       (e = x_B − x_q, ×1/(4π) later)
+  __device__ __forceinline__ void term1(bool live, float ex, float ey, float ez, float e2, const float4& V,
+                                        const float4& X0, const float4& X1) {
+    const float inv = rsqrt_ftz(live ? e2 : 1.0f);
+    const float inv2 = inv * inv;
+    const float inv3 = live ? inv2 * inv : 0.0f;
+    if (OP == OP_AT) {
+      const float eD = fmaf(ex, X0.x, fmaf(ey, X0.y, ez * X0.z));
+      const float k = fmaf(-3.0f * eD, inv2, V.x);
+      x = fmaf(-inv3, fmaf(k, ex, X0.x), x);
+      y = fmaf(-inv3, fmaf(k, ey, X0.y), y);
+      z = fmaf(-inv3, fmaf(k, ez, X0.z), z);
+      return;
+    }
+    const float mx = fmaf(X0.x, ex, fmaf(X1.x, ey, X1.y * ez));
+    const float my = fmaf(X1.x, ex, fmaf(X0.y, ey, X1.z * ez));
+    const float mz = fmaf(X1.y, ex, fmaf(X1.z, ey, X0.z * ez));
+    const float uMu = fmaf(ex, mx, fmaf(ey, my, ez * mz));
+    const float eV = fmaf(ex, V.x, fmaf(ey, V.y, ez * V.z));
+    if (OP == OP_A) {
+      x = fmaf(fmaf(-3.0f * uMu, inv2, eV + X0.w), inv3, x);
+    } else {
+      const float t = 3.0f * eV * inv2;
+      const float k = fmaf(inv2, fmaf(15.0f * uMu, inv2, -3.0f * X0.w), -t);
+      const float m6 = -6.0f * inv2;
+      x = fmaf(inv3, fmaf(k, ex, fmaf(m6, mx, V.x)), x);
+      y = fmaf(inv3, fmaf(k, ey, fmaf(m6, my, V.y)), y);
+      z = fmaf(inv3, fmaf(k, ez, fmaf(m6, mz, V.z)), z);
+    }
+  }
   __device__ __forceinline__ void flush() {
     if (OP == OP_A) {
       d += (double)x;
@@ -85,11 +119,11 @@ __device__ __forceinline__ const float4* rec_at(const float4* base, int node) {
   return reinterpret_cast<const float4*>(reinterpret_cast<const char*>(base) + ((uint32_t)node << 6));
 }
 
-template <int OP, int EPI, bool COUNT, bool FROZEN>
+template <int OP, int EPI, bool COUNT, bool FROZEN, int ORD>
 #ifndef WN_EXP_LBMIN
 #define WN_EXP_LBMIN 6  // 6 resident blocks (48 warps) per SM: ≤ 42 registers, no spills; measured best
 #endif
-__global__ void __launch_bounds__(kTravBlock, WN_EXP_LBMIN) trav_kernel(const TravArgs a) {
+__global__ void __launch_bounds__(kTravBlock, ORD == 1 ? 5 : WN_EXP_LBMIN) trav_kernel(const TravArgs a) {
   extern __shared__ int2 stk_all[];
   __shared__ double red[kTravBlock / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -129,7 +163,13 @@ __global__ void __launch_bounds__(kTravBlock, WN_EXP_LBMIN) trav_kernel(const Tr
           const float d2 = dist2(ex, ey, ez);
           const bool far = d2 > R.w;
           const bool live = mine && far && !(d2 < w2);
-          acc.term(live, ex, ey, ez, d2, V);
+          if (ORD == 1) {
+            const float4 X0 = __ldg(a.nodes.ext + 2 * node);
+            const float4 X1 = OP == OP_AT ? X0 : __ldg(a.nodes.ext + 2 * node + 1);
+            acc.term1(live, ex, ey, ez, d2, V, X0, X1);
+          } else {
+            acc.term(live, ex, ey, ez, d2, V);
+          }
           if (COUNT && mine) {
             ++ntest;
             nfar += far;
@@ -236,13 +276,18 @@ __global__ void __launch_bounds__(kTravBlock, WN_EXP_LBMIN) trav_kernel(const Tr
 template <int OP, int EPI>
 void launch(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
   const bool cnt = a.work || a.qcounts;
-  if (OP == OP_A && EPI == EPI_SQ && a.attr) {  // frozen geometry (transpose-mode A(r))
-    if (cnt) trav_kernel<OP, EPI, true, true><<<grid, kTravBlock, smem, s>>>(a);
-    else trav_kernel<OP, EPI, false, true><<<grid, kTravBlock, smem, s>>>(a);
+  if (OP == OP_A && EPI == EPI_SQ && a.attr) {  // frozen geometry (transpose-mode A(r)); order 0 only
+    if (cnt) trav_kernel<OP, EPI, true, true, 0><<<grid, kTravBlock, smem, s>>>(a);
+    else trav_kernel<OP, EPI, false, true, 0><<<grid, kTravBlock, smem, s>>>(a);
     return;
   }
-  if (cnt) trav_kernel<OP, EPI, true, false><<<grid, kTravBlock, smem, s>>>(a);
-  else trav_kernel<OP, EPI, false, false><<<grid, kTravBlock, smem, s>>>(a);
+  if (a.order1) {
+    if (cnt) trav_kernel<OP, EPI, true, false, 1><<<grid, kTravBlock, smem, s>>>(a);
+    else trav_kernel<OP, EPI, false, false, 1><<<grid, kTravBlock, smem, s>>>(a);
+    return;
+  }
+  if (cnt) trav_kernel<OP, EPI, true, false, 0><<<grid, kTravBlock, smem, s>>>(a);
+  else trav_kernel<OP, EPI, false, false, 0><<<grid, kTravBlock, smem, s>>>(a);
 }
 
 }  // namespace
@@ -256,6 +301,7 @@ wn_status traverse(const TravArgs& a, cudaStream_t s) {
   ProfScope ps(cls, s);
   TravArgs b = a;
   b.work = work_counters(cls);
+  if (a.order1 && (!a.nodes.ext || a.attr)) return set_error(WN_ERR_ARG, "internal: order-1 traversal setup");
   switch (a.op * 8 + a.epi) {
     case OP_A * 8 + EPI_PLAIN: launch<OP_A, EPI_PLAIN>(b, s, grid, smem); break;
     case OP_A * 8 + EPI_S: launch<OP_A, EPI_S>(b, s, grid, smem); break;

@@ -658,7 +658,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 
 void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->qorder, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
-                  t->topo, t->smask, t->mom_loff, t->mom_pre, t->mom_tile, t->centroid, t->sums, t->set[0].rec, t->set[1].rec,
+                  t->topo, t->smask, t->mom_loff, t->mom_pre, t->mom_tile, t->centroid, t->sums, t->set[0].rec, t->set[1].rec, t->set[0].ext,
                   t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
                   t->qbuf, t->qbuf_order, t->tvb, t->tu};
   // stream-ordered frees on the legacy stream: no device-wide synchronization, memory returns to the pool

@@ -21,13 +21,16 @@ enum AttrKind { ATTR_VEC = 0, ATTR_SCALAR = 1, ATTR_UNIT = 2 };
 //   R = (x_B, y_B, z_B, thr)   thr = (c·edge)² in fp32, or −1 for a one-point node (always "far":
 //                               rep = the point, ν_B = ν_j, so far and leaf terms coincide)
 //   V = (ν_B.x, ν_B.y, ν_B.z, topo) for vector ν, (s_B, 0, 0, topo) for scalar ν
-//   L = (x_B − hi, y_B − hi, z_B − hi, 0): the fp32 remainder of the fp64 representative, so a far term is
-//       evaluated at d = (hi − x_q) + lo (error ~1e-7·|d| instead of ulp(x_B)/|d|); decisions use hi only.
+//   L = (x_B − hi, y_B − hi, z_B − hi, 0): the fp32 remainder of the fp64 representative; decisions and the
+//       far term use d = (hi − x_q) + lo (error ~1e-7·|d| instead of ulp(x_B)/|d|), DESIGN.md R-prec.
 //   X = unused (pads the record to one aligned 64-byte half line)
 // topo (int bits): leaf = 0; internal = (child_begin << 4) | (count − 1); L.w = one-point-leaf child mask
 constexpr int kRec = 4;  // float4 per record
 struct NodeSet {
   float4* rec = nullptr;
+  // order-1 far field, 2 float4 per node: vector ν: (Mxx, Myy, Mzz, tr M), (Mxy, Mxz,
+  // Myz, 0) with M = sym Σ_j ν_j (x_j − x_B)ᵀ; scalar s: (D, 0), D = Σ_j s_j (x_j − x_B); null for order 0
+  float4* ext = nullptr;
 };
 
 struct IterScratch {
@@ -71,6 +74,8 @@ struct wn_tree_s {
   double* mom_pre = nullptr;    // (N+1) × 8 fp64 exclusive prefix of the point sums (moments.cu)
   double* mom_tile = nullptr;   // 2 × tiles × 8 fp64: per-tile totals, per-tile offsets
   int64_t mom_ntiles = 0;
+  bool mom_order1_ready = false;  // prefix scratch + set[0].ext sized for the first-order far field
+  int far_order = 0;              // wn_tree_set_far_order: 0 (the paper's Alg. 4) or 1 (row f2)
   wn::NodeSet set[2];           // [0] = current attribute, [1] = frozen geometry (transpose mode)
   std::vector<int64_t> level_off;  // host: BFS offset of each level, size depth_used + 2
   wn::IterScratch it;
@@ -132,9 +137,11 @@ struct MomentArgs {
   float4* centroid_out = nullptr;   // ATTR_UNIT: writes the centroid table
   int32_t* leaf_of_out = nullptr;   // ATTR_UNIT: writes the leaf node of every sorted point
   bool write_W = false;             // also store each node's Σ|ν| in tree sums[8·i] (wn_moments export)
+  bool order1 = false;              // also the first moments (out.ext), row f2
 };
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s);
 wn_status plan_moments(wn_tree_s* t, cudaStream_t s);  // once per tree, after the topology
+wn_status enable_order1(wn_tree_s* t, cudaStream_t s);  // first wn_tree_set_far_order(t, 1)
 
 // ---- traversal (traverse.cu) ----
 enum TravOp { OP_A = 0, OP_AT = 1, OP_G = 2 };
@@ -168,6 +175,7 @@ struct TravArgs {
   float w2 = 0.0f;
   int stack_depth = 128;
   int root_single = 0;              // 1 iff the root is a one-point leaf (n = 1)
+  int order1 = 0;                   // first-order far field (nodes.ext), row f2
   int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
   int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order
 };

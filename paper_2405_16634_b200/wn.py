@@ -26,7 +26,8 @@ STATUS_NAMES = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_EMPTY", 3: "WN_ERR_NONFI
 EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", "wn_prof_read", "wn_build_tree",
             "wn_tree_destroy", "wn_tree_info", "wn_tree_export", "wn_moments", "wn_eval", "wn_eval_grad",
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
-            "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work")
+            "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work",
+            "wn_tree_set_far_order")
 
 
 class wnnc_params(C.Structure):
@@ -54,6 +55,7 @@ _sig = {
     "wn_shard_range": ([I64, I32, I32, P, P], I32),
     "wn_work_count_enable": ([I32], I32), "wn_work_count_read": ([P], I32),
     "wn_query_work": ([P, I32, P, P, I64, F32, F32, P, P], I32),
+    "wn_tree_set_far_order": ([P, I32, P], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -169,6 +171,11 @@ def wn_build_tree(pts: torch.Tensor, max_depth: int = 15) -> Tree:
 
 def wn_tree_destroy(tree: Tree):
     tree.close()
+
+
+def wn_tree_set_far_order(tree: Tree, order: int):
+    """0: the paper's representative far term (Alg. 4); 1: first-order far field."""
+    _check(_L.wn_tree_set_far_order(tree.handle, int(order), _stream()))
 
 
 def wn_tree_export(tree: Tree):
