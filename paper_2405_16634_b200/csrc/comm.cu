@@ -126,7 +126,7 @@ wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64
     for (int k = 0; k < c->world && r == ncclSuccess; ++k) {
       int64_t b = 0, e = 0;
       wn_shard_range(n, k, c->world, &b, &e);
-      const int64_t b0 = b / WN_SHARD_ALIGN, b1 = (e + WN_SHARD_ALIGN - 1) / WN_SHARD_ALIGN;
+      const int64_t b0 = b / kTravBlock, b1 = (e + kTravBlock - 1) / kTravBlock;  // partials per traversal block
       if (b1 > b0) {
         double* p = part + a * stride + b0;
         r = N.Broadcast(p, p, (size_t)(b1 - b0), ncclFloat64, k, c->comm, s);

@@ -63,15 +63,16 @@ __global__ void k_normalize_queries(int64_t m, const float* __restrict__ q, doub
 }
 
 // α = Σr² / Σ(Ar)² from fixed-order block partials (0 if the denominator is 0)
-__global__ void k_alpha(const double* __restrict__ part, int nblk, int64_t stride, double w, double* alpha,
-                        double* stats) {
-  __shared__ double sh[3][256];
+constexpr int kAlphaThreads = 1024;
+__global__ void __launch_bounds__(kAlphaThreads) k_alpha(const double* __restrict__ part, int nblk, int64_t stride,
+                                                         double w, double* alpha, double* stats) {
+  __shared__ double sh[3][kAlphaThreads];
   double acc[3] = {0.0, 0.0, 0.0};
-  for (int b = threadIdx.x; b < nblk; b += 256)
+  for (int b = threadIdx.x; b < nblk; b += kAlphaThreads)
     for (int c = 0; c < 3; ++c) acc[c] += part[c * stride + b];
   for (int c = 0; c < 3; ++c) sh[c][threadIdx.x] = acc[c];
   __syncthreads();
-  for (int o = 128; o; o >>= 1) {
+  for (int o = kAlphaThreads / 2; o; o >>= 1) {
     if (threadIdx.x < o)
       for (int c = 0; c < 3; ++c) sh[c][threadIdx.x] += sh[c][threadIdx.x + o];
     __syncthreads();
@@ -123,7 +124,7 @@ void normalize_queries(int64_t m, const float* q, const double xf[4], float4* ou
 }
 void alpha_step(const double* part, int nblk, int64_t stride, double w, double* alpha, double* stats, cudaStream_t s) {
   ProfScope ps(WN_PROF_OTHER, s);
-  k_alpha<<<1, 256, 0, s>>>(part, nblk, stride, w, alpha, stats);
+  k_alpha<<<1, kAlphaThreads, 0, s>>>(part, nblk, stride, w, alpha, stats);
 }
 void unit_normals(int64_t n, const float* mu, float* out, cudaStream_t s) {
   k_unit<<<g256(n), 256, 0, s>>>(n, mu, out);

@@ -123,7 +123,7 @@ template <int OP, int EPI, bool COUNT, bool FROZEN, int ORD>
 #ifndef WN_EXP_LBMIN
 #define WN_EXP_LBMIN 6  // 6 resident blocks (48 warps) per SM: ≤ 42 registers, no spills; measured best
 #endif
-__global__ void __launch_bounds__(kTravBlock, ORD == 1 ? 5 : WN_EXP_LBMIN) trav_kernel(const TravArgs a) {
+__global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 256 / kTravBlock) trav_kernel(const TravArgs a) {
   extern __shared__ int2 stk_all[];
   __shared__ double red[kTravBlock / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

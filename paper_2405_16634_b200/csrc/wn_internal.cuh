@@ -186,7 +186,11 @@ wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sor
                             float4* r_out, double* partial, cudaStream_t st);
 
 // ---- small utility kernels (iterate.cu) ----
-constexpr int kTravBlock = 256;  // queries per block (8 warps)
+#ifndef WN_EXP_TRAVBLOCK
+#define WN_EXP_TRAVBLOCK 128
+#endif
+constexpr int kTravBlock = WN_EXP_TRAVBLOCK;  // queries per block (4 warps: the block tail holds an SM slot for less; 256: +0.8 %)
+static_assert(WN_SHARD_ALIGN % kTravBlock == 0, "rank shards must hold whole traversal blocks (Σ partials)");
 inline int trav_blocks(int64_t nq) { return (int)((nq + kTravBlock - 1) / kTravBlock); }
 
 }  // namespace wn
