@@ -165,7 +165,7 @@ def run_ours(args):
     n = len(pts_h)
     pts = torch.from_numpy(pts_h).to(dev)
     params = dict(iters=ITERS, theta=args.theta, adjoint_mode=wn.WN_ADJ_TRANSPOSE if args.transpose else 0,
-                  flags=0 if args.no_graph else wn.WN_FLAG_GRAPH)
+                  flags=(0 if args.no_graph else wn.WN_FLAG_GRAPH) | (wn.WN_FLAG_COMM_NCCL if args.comm == "nccl" else 0))
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
@@ -271,6 +271,8 @@ def run_ours(args):
                    "adjoint": "transpose" if args.transpose else "gather",
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
                    "parallelism": f"query-sharded x{world}" if world > 1 else "1 GPU",
+                   "exchange": ("peer-memory stores in the traversal epilogues" if args.comm == "peer"
+                                else "NCCL broadcasts") if world > 1 else None,
                    "step": "wn_build_tree + 40 x (4 moment builds + 4 traversals + alpha)"},
         "interactions_per_s": {"counted": interactions * 1e3 / ms, "effective_dense": 4.0 * n * n * ITERS * 1e3 / ms,
                                "unit": "source-query interactions/s",
@@ -311,6 +313,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--theta", type=float, default=2.0)
     ap.add_argument("--transpose", action="store_true", help="north-star exact-transpose adjoint")
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                    help="multi-GPU exchange: peer-memory stores fused into the traversals (default) or NCCL")
     ap.add_argument("--order", type=int, default=0, choices=[0, 1],
                     help="far-field order: 0 = the paper's Alg. 4 (headline), 1 = first-order (SURVEY §8 row f2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -59,7 +59,11 @@ enum { WN_ADJ_GATHER = 0,    /* Aᵀ by its own traversal with |s|-weighted reps
        WN_ADJ_TRANSPOSE = 1  /* exact transpose of treecode A at frozen geometry g(μ): scatter into node
                                 accumulators, then push down the tree (BASELINE north star)           */ };
 
-enum { WN_FLAG_GRAPH = 1 };  /* wnnc_params.flags: capture the iteration loop in a CUDA graph */
+enum {
+  WN_FLAG_GRAPH = 1,      /* wnnc_params.flags: capture the iteration loop in a CUDA graph */
+  WN_FLAG_COMM_NCCL = 2   /* multi-GPU: exchange with NCCL broadcasts instead of the default peer-memory
+                             stores fused into the traversal epilogues (see wnnc_iterate) */
+};
 
 typedef struct {
   float w_min;          /* w1, final smoothing width (PAPER.md:L419 default 0.002)             */
@@ -162,7 +166,13 @@ wn_status wn_eval_adjoint(wn_tree t, const float* s, float width, float theta, i
    μ' = μ + α r; μ̂ = G_w(μ'); μ_i = μ̂_i |μ'_i| / |μ̂_i| (μ'_i kept if |μ̂_i| = 0).
    mu[N×3] caller order, input frame, in/out; zeros ⇒ the paper's initialization (L301).
    comm NULL ⇒ one GPU; otherwise queries are sharded over the communicator's ranks (every rank passes
-   the full mu and receives the full, rank-identical result).  stats (host, p->iters records) may be
+   the full mu and receives the full, rank-identical result).  Exchange (multi-GPU): by default each
+   traversal's epilogue stores its owned rows and Σ partials straight into every rank's replica through
+   CUDA IPC peer mappings (NVLink / NVSwitch), the last block of the launch signals every rank and a
+   device-side wait orders the next step — no separate collective; the first call per communicator (and
+   any call with a larger N) sets up the per-rank arena collectively (≈ 52 B per point, synchronizes
+   `stream`).  WN_FLAG_COMM_NCCL selects grouped ncclBroadcasts instead.  Both give the single-GPU
+   trajectory bit for bit.  At most 8 ranks in peer mode (WN_ERR_ARG beyond).  stats (host, p->iters records) may be
    NULL; when given the call synchronizes `stream` before returning. */
 wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm, wnnc_iter_stats* stats,
                        void* stream);

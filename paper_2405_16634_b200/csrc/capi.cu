@@ -132,14 +132,37 @@ static TravArgs base_args(const wn_tree_s* t, float w2) {
 static bool bad_width(float w) { return !(w > 0.f) || std::isnan(w); }
 static bool bad_theta(float c) { return !(c > 0.f) || std::isnan(c); }
 
+// route a traversal's outputs into every rank's replica (peer-memory exchange); none when P is null
+static void peer_route(TravArgs& ta, const PeerArena* P, float* const* f, float4* const* v4, int part_slot) {
+  if (!P) return;
+  ta.world = P->world;
+  for (int r = 0; r < P->world; ++r) {
+    if (f) ta.peer_f[r] = f[r];
+    if (v4) ta.peer_v4[r] = v4[r];
+    ta.peer_part[r] = P->part[r] + part_slot * P->part_stride;
+    ta.peer_sig[r] = P->sig[r];
+  }
+  ta.done = P->done;
+}
+
 // ---- Alg. 3 loop over a query range [q0, q1) of the sorted points (multi-GPU: this rank's shard) ----
-static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm, cudaStream_t s) {
+// Exchanges (multi-GPU): with P (peer-memory arena) the traversal epilogues store into every rank's
+// replica and a device-side wait follows each exchanging traversal; μ ping-pongs between the arena's two
+// buffers (iteration i reads μ[i % 2], its G epilogue writes μ[(i + 1) % 2]).  Without P but with comm:
+// NCCL broadcasts after each traversal.
+static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm, const PeerArena* P,
+                                cudaStream_t s) {
   IterScratch& it = t->it;
   const int total = p.total_iters > 0 ? p.total_iters : p.iters;
   const bool transpose = p.adjoint_mode == WN_ADJ_TRANSPOSE;
-  const int64_t stride = it.nblk;
   int64_t q0 = 0, q1 = t->n;
   if (comm) WN_TRY(comm_shard(comm, t->n, &q0, &q1));
+  const bool nccl = comm && !P;
+  const int me = P ? P->rank : 0;
+  float* sb = P ? P->s[me] : it.s;
+  float4* rb = P ? P->r[me] : it.r;
+  double* part = P ? P->part[me] : it.part;
+  const int64_t stride = P ? P->part_stride : it.nblk;
   // queries follow the Hilbert schedule; multi-GPU shards are schedule ranges (exchanged via staging)
   const int32_t* qord = t->qorder;
   float* stage = (float*)it.tmp;  // n × 4 floats
@@ -147,10 +170,11 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     const int k = p.first_iter + i;
     const float w = width_at(k, total, (double)p.w_min, (double)p.w_max);
     const float w2 = w * w;
+    float4* mu_cur = P ? P->mu[i & 1][me] : it.mu;
     // (1) s = ½ − A_w μ  (+ Σ s² partials)
     MomentArgs m1;
     m1.kind = ATTR_VEC;
-    m1.vec = it.mu;
+    m1.vec = mu_cur;
     m1.theta = p.theta;
     m1.out = transpose ? t->set[1] : t->set[0];
     m1.order1 = t->far_order == 1;
@@ -160,43 +184,47 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a1.op = OP_A;
     a1.epi = EPI_S;
     a1.nodes = m1.out;
-    a1.vec = it.mu;
+    a1.vec = mu_cur;
     a1.q_begin = q0;
     a1.q_end = q1;
-    a1.out_f = it.s;
-    a1.partial = it.part;
+    a1.out_f = sb;
+    a1.partial = part;
     a1.order1 = t->far_order;
+    peer_route(a1, P, P ? P->s : nullptr, nullptr, 0);
     WN_TRY(traverse(a1, s));
-    if (comm) WN_TRY(comm_allgather_f(comm, it.s, 1, t->n, qord, stage, s));
+    if (P) comm_peer_wait(*P, s);
+    if (nccl) WN_TRY(comm_allgather_f(comm, sb, 1, t->n, qord, stage, s));
     // (2) r = A_wᵀ s  (+ Σ|r|² partials)
     if (transpose) {
-      WN_TRY(adjoint_transpose(t, t->set[1], it.s, w2, it.r, it.part + stride, s));
+      WN_TRY(adjoint_transpose(t, t->set[1], sb, w2, rb, part + stride, s));
     } else {
       MomentArgs m2;
       m2.kind = ATTR_SCALAR;
-      m2.scal = it.s;
+      m2.scal = sb;
       m2.theta = p.theta;
       m2.out = t->set[0];
       m2.order1 = t->far_order == 1;
-    WN_TRY(build_moments(t, m2, s));
+      WN_TRY(build_moments(t, m2, s));
       TravArgs a2 = base_args(t, w2);
-    a2.qorder = qord;
+      a2.qorder = qord;
       a2.op = OP_AT;
       a2.epi = EPI_R;
       a2.nodes = t->set[0];
-      a2.scal = it.s;
+      a2.scal = sb;
       a2.q_begin = q0;
       a2.q_end = q1;
-      a2.out_v4 = it.r;
-      a2.partial = it.part + stride;
+      a2.out_v4 = rb;
+      a2.partial = part + stride;
       a2.order1 = t->far_order;
-    WN_TRY(traverse(a2, s));
-      if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.r, 4, t->n, qord, stage, s));
+      peer_route(a2, P, nullptr, P ? P->r : nullptr, 1);
+      WN_TRY(traverse(a2, s));
+      if (P) comm_peer_wait(*P, s);
+      if (nccl) WN_TRY(comm_allgather_f(comm, (float*)rb, 4, t->n, qord, stage, s));
     }
     // (3) Σ (A_w r)²  — gather: r's own representatives; transpose: μ's frozen geometry
     MomentArgs m3;
     m3.kind = ATTR_VEC;
-    m3.vec = it.r;
+    m3.vec = rb;
     m3.theta = p.theta;
     m3.out = t->set[0];
     m3.order1 = t->far_order == 1;
@@ -207,20 +235,23 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a3.epi = EPI_SQ;
     a3.nodes = transpose ? t->set[1] : t->set[0];
     a3.attr = transpose ? t->set[0].rec : nullptr;
-    a3.vec = it.r;
+    a3.vec = rb;
     a3.q_begin = q0;
     a3.q_end = q1;
-    a3.partial = it.part + 2 * stride;
+    a3.partial = part + 2 * stride;
     a3.order1 = t->far_order;
+    peer_route(a3, P, nullptr, nullptr, 2);
     WN_TRY(traverse(a3, s));
-    if (comm) WN_TRY(comm_allgather_partials(comm, it.part, stride, t->n, s));
+    if (P) comm_peer_wait(*P, s);
+    if (nccl) WN_TRY(comm_allgather_partials(comm, part, stride, t->n, s));
     // α = Σr² / Σ(Ar)²  (Alg. 2), fixed-order reduction of the partials
-    alpha_step(it.part, (int)stride, stride, (double)w, it.alpha, it.dstats + 5 * i, s);
+    // (the partial arrays' stride may exceed this cloud's block count: a peer arena sized for a larger N)
+    alpha_step(part, trav_blocks(t->n), stride, (double)w, it.alpha, it.dstats + 5 * i, s);
     // (4) μ' = μ + α r (fused into the moment build), μ̂ = G_w(μ'), μ = μ̂ |μ'|/|μ̂|
     MomentArgs m4;
     m4.kind = ATTR_VEC;
-    m4.vec = it.mu;
-    m4.axpy_r = it.r;
+    m4.vec = mu_cur;
+    m4.axpy_r = rb;
     m4.alpha = it.alpha;
     m4.axpy_out = it.mup;
     m4.theta = p.theta;
@@ -238,8 +269,10 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a4.q_end = q1;
     a4.out_v4 = it.mu;
     a4.order1 = t->far_order;
+    peer_route(a4, P, nullptr, P ? P->mu[(i + 1) & 1] : nullptr, 0);
     WN_TRY(traverse(a4, s));
-    if (comm) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, s));
+    if (P) comm_peer_wait(*P, s);
+    if (nccl) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, s));
   }
   return WN_OK;
 }
@@ -539,20 +572,26 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
     it.stats_cap = p->iters;
   }
   const double sc2 = t->xf[3] * t->xf[3];
-  gather_vec(t->n, t->perm, mu, sc2, t->it.mu, s);        // μ_norm = scale²·μ
+  // multi-GPU exchange: peer-memory stores fused into the traversal epilogues (default), or NCCL
+  const PeerArena* P = nullptr;
+  if (comm && !(p->flags & WN_FLAG_COMM_NCCL)) WN_TRY(comm_peer_arena(comm, t->n, s, &P));
+  float4* mu0 = P ? P->mu[0][P->rank] : t->it.mu;
+  gather_vec(t->n, t->perm, mu, sc2, mu0, s);             // μ_norm = scale²·μ
   if (p->flags & WN_FLAG_GRAPH) {
     // the whole iteration loop as one CUDA graph: captured on a private stream, cached per parameters
-    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm) + sizeof(int));
+    const void* arena = P ? P->own : nullptr;
+    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm) + sizeof(int) + sizeof(arena));
     memcpy(key.data(), p, sizeof(wnnc_params));
     memcpy(key.data() + sizeof(wnnc_params), &comm, sizeof(comm));
     memcpy(key.data() + sizeof(wnnc_params) + sizeof(comm), &t->far_order, sizeof(int));
+    memcpy(key.data() + sizeof(wnnc_params) + sizeof(comm) + sizeof(int), &arena, sizeof(arena));
     if (!t->graph_exec || key != t->graph_key) {
       if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
       t->graph_exec = nullptr;
       if (!t->cap_stream) WN_CUDA(cudaStreamCreateWithFlags(&t->cap_stream, cudaStreamNonBlocking));
       WN_CUDA(cudaStreamBeginCapture(t->cap_stream, cudaStreamCaptureModeThreadLocal));
       g_capturing = true;
-      wn_status st = run_iterations(t, *p, comm, t->cap_stream);
+      wn_status st = run_iterations(t, *p, comm, P, t->cap_stream);
       g_capturing = false;
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaStreamEndCapture(t->cap_stream, &graph);
@@ -580,9 +619,10 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
     count_launches((int)t->graph_launches);
     WN_CUDA(cudaGraphLaunch(t->graph_exec, s));
   } else {
-    WN_TRY(run_iterations(t, *p, comm, s));
+    WN_TRY(run_iterations(t, *p, comm, P, s));
   }
-  scatter_vec(t->n, t->perm, t->it.mu, 1.0 / sc2, mu, s);  // back to the input frame
+  const float4* mu_end = P ? P->mu[p->iters & 1][P->rank] : t->it.mu;
+  scatter_vec(t->n, t->perm, mu_end, 1.0 / sc2, mu, s);  // back to the input frame
   if (stats) {
     std::vector<double> h(5 * (size_t)p->iters);
     WN_CUDA(cudaMemcpyAsync(h.data(), t->it.dstats, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -21,6 +21,7 @@
 struct wn_comm_s {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  wn::PeerArena arena;  // peer-memory exchange (fused into the traversal epilogues), built on first use
 };
 
 namespace wn {
@@ -33,6 +34,7 @@ struct Nccl {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -53,11 +55,13 @@ Nccl& nccl() {
     SYM(CommInitRank, "ncclCommInitRank");
     SYM(CommDestroy, "ncclCommDestroy");
     SYM(Broadcast, "ncclBroadcast");
+    SYM(AllGather, "ncclAllGather");
     SYM(GroupStart, "ncclGroupStart");
     SYM(GroupEnd, "ncclGroupEnd");
     SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
-    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Broadcast && n.GroupStart && n.GroupEnd;
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Broadcast && n.AllGather && n.GroupStart &&
+           n.GroupEnd;
     if (!n.ok) n.err = "libnccl.so.2 lacks required symbols";
   });
   return n;
@@ -138,6 +142,102 @@ wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64
   return nccl_status(r, "ncclBroadcast (partials)");
 }
 
+// ---------------- peer-memory exchange (B200-native form of the per-traversal all-gather) ----------------
+// Every rank allocates one IPC-capable block (cudaMalloc) holding the exchanged arrays — s (N fp32),
+// r (N float4), μ (2 × N float4: ping-pong, so a fast rank's G epilogue never overwrites the μ a slow
+// rank's axpy still reads), the Σ partials (3 × blocks fp64) — and a signal word.  The handles are
+// all-gathered once (NCCL) and opened with cudaIpcOpenMemHandle, so every rank holds a device pointer
+// to every replica; the traversal epilogues then store each owned row into all replicas over NVLink
+// and the last block of each launch signals every rank (system-scope fence + remote atomic add).
+// A one-thread wait kernel on each rank spins on its own signal word until all ranks have signalled
+// that exchange — its target advances on the device, so a captured CUDA graph can be replayed.
+namespace {
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+__global__ void k_peer_wait(unsigned long long* sig, unsigned long long* expected, int world) {
+  const unsigned long long target = *expected + (unsigned long long)world;
+  *expected = target;
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sig) : "memory");
+  } while (v < target);
+  __threadfence_system();
+}
+}  // namespace
+
+static void arena_release(PeerArena& A) {
+  for (int r = 0; r < A.world; ++r)
+    if (A.opened[r] && A.base[r]) cudaIpcCloseMemHandle(A.base[r]);
+  if (A.own) cudaFree(A.own);
+  A = PeerArena();
+}
+
+wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena** out) {
+  PeerArena& A = c->arena;
+  if (c->world > kMaxPeers) return set_error(WN_ERR_ARG, "peer-memory exchange supports at most 8 ranks");
+  if (A.own && A.cap >= n) {
+    *out = &A;
+    return WN_OK;
+  }
+  // (re)build, collectively: every rank reaches this point in the same wnnc_iterate call
+  arena_release(A);
+  const int64_t nb = trav_blocks(n);
+  const size_t o_s = 0, o_r = align256(o_s + n * sizeof(float)), o_mu0 = align256(o_r + n * sizeof(float4));
+  const size_t o_mu1 = align256(o_mu0 + n * sizeof(float4)), o_part = align256(o_mu1 + n * sizeof(float4));
+  const size_t o_sig = align256(o_part + 3 * nb * sizeof(double)), bytes = align256(o_sig + 4 * sizeof(uint64_t));
+  WN_CUDA(cudaStreamSynchronize(s));
+  WN_CUDA(cudaMalloc(&A.own, bytes));
+  WN_CUDA(cudaMemset(A.own, 0, bytes));
+  cudaIpcMemHandle_t mine;
+  WN_CUDA(cudaIpcGetMemHandle(&mine, A.own));
+  cudaIpcMemHandle_t* dh = nullptr;
+  WN_CUDA(cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * c->world));
+  WN_CUDA(cudaMemcpy(dh + c->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  Nccl& N = nccl();
+  wn_status st = nccl_status(N.AllGather(dh + c->rank, dh, sizeof(mine), ncclUint8, c->comm, s), "ncclAllGather (IPC handles)");
+  cudaIpcMemHandle_t hs[kMaxPeers];
+  if (st == WN_OK) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMemcpy(hs, dh, sizeof(mine) * c->world, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = cuda_status(e, "IPC handle exchange");
+  }
+  cudaFree(dh);
+  if (st != WN_OK) return st;
+  A.world = c->world;
+  A.rank = c->rank;
+  A.cap = n;
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) {
+      A.base[r] = A.own;
+    } else {
+      cudaError_t e = cudaIpcOpenMemHandle(&A.base[r], hs[r], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        arena_release(A);
+        return cuda_status(e, "cudaIpcOpenMemHandle (peer arena)");
+      }
+      A.opened[r] = true;
+    }
+    char* b = static_cast<char*>(A.base[r]);
+    A.s[r] = reinterpret_cast<float*>(b + o_s);
+    A.r[r] = reinterpret_cast<float4*>(b + o_r);
+    A.mu[0][r] = reinterpret_cast<float4*>(b + o_mu0);
+    A.mu[1][r] = reinterpret_cast<float4*>(b + o_mu1);
+    A.part[r] = reinterpret_cast<double*>(b + o_part);
+    A.sig[r] = reinterpret_cast<unsigned long long*>(b + o_sig);
+  }
+  char* own = static_cast<char*>(A.own);
+  A.expected = reinterpret_cast<unsigned long long*>(own + o_sig) + 1;  // local: next wait target
+  A.done = reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(own + o_sig) + 2);
+  A.part_stride = nb;
+  *out = &A;
+  return WN_OK;
+}
+
+void comm_peer_wait(const PeerArena& A, cudaStream_t s) {
+  k_peer_wait<<<1, 1, 0, s>>>(A.sig[A.rank], A.expected, A.world);
+  count_launches(1);
+}
+
 }  // namespace wn
 
 using namespace wn;
@@ -178,6 +278,10 @@ wn_status wn_comm_init(int32_t rank, int32_t world, const uint8_t id[128], wn_co
 
 wn_status wn_comm_destroy(wn_comm c) {
   if (!c) return WN_OK;
+  if (c->arena.own) {
+    cudaDeviceSynchronize();
+    arena_release(c->arena);
+  }
   if (c->comm) nccl().CommDestroy(c->comm);
   delete c;
   return WN_OK;

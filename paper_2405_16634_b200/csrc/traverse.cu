@@ -214,7 +214,11 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
       if (EPI == EPI_PLAIN && a.out_f) a.out_f[oq] = (float)(val * (double)a.scale_out);
       if (EPI == EPI_S) {
         const double sv = 0.5 - val;
-        a.out_f[q] = (float)sv;
+        if (a.world) {  // peer-memory exchange: this row into every rank's replica (NVLink stores)
+          for (int r = 0; r < a.world; ++r) a.peer_f[r][q] = (float)sv;
+        } else {
+          a.out_f[q] = (float)sv;
+        }
         part = sv * sv;
       }
       if (EPI == EPI_SQ) part = val * val;
@@ -226,7 +230,12 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
         a.out_v3[3 * oq + 2] = vz * a.scale_out;
       }
       if (EPI == EPI_R) {
-        a.out_v4[q] = make_float4(vx, vy, vz, 0.f);
+        const float4 o = make_float4(vx, vy, vz, 0.f);
+        if (a.world) {
+          for (int r = 0; r < a.world; ++r) a.peer_v4[r][q] = o;
+        } else {
+          a.out_v4[q] = o;
+        }
         part = (double)vx * vx + (double)vy * vy + (double)vz * vz;
       }
       if (EPI == EPI_RESCALE) {  // μ_i = μ̂_i |μ'_i| / |μ̂_i|, μ'_i kept if |μ̂_i| = 0 (Alg. 3)
@@ -238,7 +247,11 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
           const double f = mm / hm;
           o = make_float4((float)(vx * f), (float)(vy * f), (float)(vz * f), 0.f);
         }
-        a.out_v4[q] = o;
+        if (a.world) {
+          for (int r = 0; r < a.world; ++r) a.peer_v4[r][q] = o;
+        } else {
+          a.out_v4[q] = o;
+        }
       }
     }
   }
@@ -268,7 +281,24 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
     if (threadIdx.x == 0) {
       double b = 0.0;
       for (int k = 0; k < kTravBlock / 32; ++k) b += red[k];
-      a.partial[(a.q_begin / kTravBlock) + blockIdx.x] = b;
+      const int64_t ib = (a.q_begin / kTravBlock) + blockIdx.x;
+      if (a.world) {
+        for (int r = 0; r < a.world; ++r) a.peer_part[r][ib] = b;
+      } else {
+        a.partial[ib] = b;
+      }
+    }
+  }
+  if (a.world) {  // signal: every thread's remote stores, then one count per block, the last block tells every rank
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int prev = atomicAdd(a.done, 1u);
+      if (prev == gridDim.x - 1) {
+        __threadfence_system();
+        *a.done = 0u;  // ready for the next exchange (stream-ordered)
+        for (int r = 0; r < a.world; ++r) atomicAdd_system(a.peer_sig[r], 1ull);
+      }
     }
   }
 }
@@ -292,9 +322,22 @@ void launch(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
 
 }  // namespace
 
+// an empty shard still takes part in the peer-memory exchange: signal every rank
+__global__ void k_peer_signal(TravArgs a) {
+  __threadfence_system();
+  for (int r = 0; r < a.world; ++r) atomicAdd_system(a.peer_sig[r], 1ull);
+}
+
 wn_status traverse(const TravArgs& a, cudaStream_t s) {
   const int64_t nq = a.q_end - a.q_begin;
-  if (nq <= 0) return WN_OK;
+  if (nq <= 0) {
+    if (a.world) {
+      k_peer_signal<<<1, 1, 0, s>>>(a);
+      count_launches(1);
+      WN_CUDA(cudaGetLastError());
+    }
+    return WN_OK;
+  }
   const unsigned grid = (unsigned)trav_blocks(nq);
   const size_t smem = (size_t)(kTravBlock / 32) * a.stack_depth * sizeof(int2);
   const int cls = a.op == OP_A ? WN_PROF_TRAV_A : a.op == OP_AT ? WN_PROF_TRAV_AT : WN_PROF_TRAV_G;

@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "../../include/wn.h"
+#include "wn_internal.cuh"
 
 namespace wn {
 wn_status comm_shard(wn_comm c, int64_t n, int64_t* q0, int64_t* q1);
@@ -12,6 +13,10 @@ wn_status comm_shard(wn_comm c, int64_t n, int64_t* q0, int64_t* q1);
 // (row = qorder[k], or k when qorder is null); make it whole on all ranks.  stage: n × comps scratch.
 wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, const int32_t* qorder, float* stage,
                            cudaStream_t s);
-// The three per-block partial arrays (stride entries each, blocks of WN_SHARD_ALIGN queries).
+// The three per-block partial arrays (stride entries each, blocks of kTravBlock queries).
 wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64_t n, cudaStream_t s);
+// Peer-memory exchange: the communicator's arena (collective on first use or growth; synchronizes s),
+// and the per-exchange device-side wait for every rank's signal.
+wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena** out);
+void comm_peer_wait(const PeerArena& A, cudaStream_t s);
 }  // namespace wn

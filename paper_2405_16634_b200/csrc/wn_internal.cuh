@@ -152,6 +152,7 @@ enum Epi {
   EPI_R = 3,         // r = Σ/(4π); partial Σ|r|²
   EPI_RESCALE = 4    // μ_out = μ̂ |μ'| / |μ̂| (μ̂ = Σ/(4π)); keep μ' if |μ̂| = 0
 };
+constexpr int kMaxPeers = 8;  // ranks of the peer-memory exchange (one NVLink / NVSwitch node)
 struct TravArgs {
   int op = OP_A;
   int epi = EPI_PLAIN;
@@ -178,8 +179,32 @@ struct TravArgs {
   int order1 = 0;                   // first-order far field (nodes.ext), row f2
   int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
   int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order
+  // peer-memory exchange (multi-GPU, fused): the epilogue stores its row / block partial into every rank's
+  // replica and the last block signals every rank; world = 0 ⇒ local outputs only
+  int world = 0;
+  float* peer_f[kMaxPeers] = {};
+  float4* peer_v4[kMaxPeers] = {};
+  double* peer_part[kMaxPeers] = {};
+  unsigned long long* peer_sig[kMaxPeers] = {};
+  unsigned int* done = nullptr;
 };
 wn_status traverse(const TravArgs& a, cudaStream_t s);
+
+// ---- peer-memory exchange arena (comm.cu): every rank's replicas of the exchanged arrays ----
+struct PeerArena {
+  int world = 0, rank = 0;
+  int64_t cap = 0, part_stride = 0;
+  void* own = nullptr;                 // this rank's cudaMalloc block (IPC-exported)
+  void* base[kMaxPeers] = {};          // every rank's block, mapped here (own or IPC-opened)
+  bool opened[kMaxPeers] = {};
+  float* s[kMaxPeers] = {};            // s = ½ − Aμ            (N)
+  float4* r[kMaxPeers] = {};           // r = Aᵀ s              (N)
+  float4* mu[2][kMaxPeers] = {};       // μ, ping-pong by iteration parity (N each)
+  double* part[kMaxPeers] = {};        // Σ partials [3][blocks]
+  unsigned long long* sig[kMaxPeers] = {};  // signal words (remote atomic adds)
+  unsigned long long* expected = nullptr;   // local: next wait target (advanced by the wait kernel)
+  unsigned int* done = nullptr;             // local: finished blocks of the running traversal
+};
 
 // ---- transpose-mode adjoint (transpose.cu) ----
 wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sorted, float w2,

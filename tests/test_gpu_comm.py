@@ -20,16 +20,18 @@ def wn():
 
 
 def test_world1_comm_matches_single_gpu(wn):
+    # single GPU; peer-memory exchange (default: epilogue stores into every replica + signal / wait),
+    # with and without the CUDA graph; NCCL broadcasts, with and without the graph — one trajectory
     uid = wn.wn_comm_unique_id()
     assert len(uid) == 128
     comm = wn.wn_comm_init(0, 1, uid)
     p = torch.from_numpy(synth.config("C2")["points"]).cuda()
     outs = []
-    for c in (None, comm, comm):
+    G, NC = wn.WN_FLAG_GRAPH, wn.WN_FLAG_COMM_NCCL
+    for c, flags in ((None, 0), (comm, 0), (comm, G), (comm, NC), (comm, NC | G), (comm, G)):
         t = wn.wn_build_tree(p)
         mu = torch.zeros(len(p), 3, device="cuda")
-        st = wn.wnnc_iterate(t, mu, comm=c, stats=True, iters=4, total_iters=40,
-                             flags=wn.WN_FLAG_GRAPH if c is not None and outs and len(outs) == 2 else 0)
+        st = wn.wnnc_iterate(t, mu, comm=c, stats=True, iters=5, total_iters=40, flags=flags)
         outs.append((mu.cpu().numpy(), [s["alpha"] for s in st]))
     for m, a in outs[1:]:
         np.testing.assert_array_equal(m, outs[0][0])
@@ -37,6 +39,23 @@ def test_world1_comm_matches_single_gpu(wn):
     with pytest.raises(wn.WnError, match="ARG"):
         t = wn.wn_build_tree(p)
         wn.wnnc_iterate(t, torch.zeros(len(p), 3, device="cuda"), comm=comm, adjoint_mode=wn.WN_ADJ_TRANSPOSE)
+    comm.close()
+
+
+def test_peer_arena_grows_with_n(wn):
+    # one communicator, clouds of increasing size: the peer-memory arena is rebuilt (collectively) and the
+    # cached graph re-captured; every run still equals the single-GPU trajectory
+    comm = wn.wn_comm_init(0, 1, wn.wn_comm_unique_id())
+    for cfg, n in (("C1", None), ("C2", 20000), ("C2", None), ("C1", None)):
+        pts = synth.config(cfg)["points"]
+        p = torch.from_numpy(pts[:n] if n else pts).cuda()
+        res = []
+        for c in (None, comm):
+            t = wn.wn_build_tree(p)
+            mu = torch.zeros(len(p), 3, device="cuda")
+            wn.wnnc_iterate(t, mu, comm=c, iters=3, total_iters=40, flags=wn.WN_FLAG_GRAPH)
+            res.append(mu.cpu().numpy())
+        np.testing.assert_array_equal(res[1], res[0])
     comm.close()
 
 
