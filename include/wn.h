@@ -176,6 +176,13 @@ wn_status wn_eval_adjoint(wn_tree t, const float* s, float width, float theta, i
    NULL; when given the call synchronizes `stream` before returning. */
 wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm, wnnc_iter_stats* stats,
                        void* stream);
+/* Diagnostic: the peer-memory exchange of `world` (1..8) ranks emulated on this one GPU, serialized on
+   `stream` — every rank's traversal over its shard reads its own replica and stores into all replicas,
+   every wait is issued after all signals (none ever spins).  mu as in wnnc_iterate (rank 0's result);
+   replicas (device, world×N×3, may be NULL) receives every rank's final μ.  No CUDA graph; synchronizes
+   `stream`; gather-mode adjoint only. */
+wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int32_t world, float* replicas,
+                                void* stream);
 /* End-to-end convenience for HOST buffers: copies pts_host (N×3) to the device, builds the tree,
    runs wnnc_iterate from μ = 0, copies the unit-normalized result (zero rows stay zero) to
    normals_host (N×3, host) and, if mu_host ≠ NULL, the raw μ (input frame).  Synchronizes `stream`.

@@ -146,17 +146,20 @@ static void peer_route(TravArgs& ta, const PeerArena* P, float* const* f, float4
 }
 
 // ---- Alg. 3 loop over a query range [q0, q1) of the sorted points (multi-GPU: this rank's shard) ----
-// Exchanges (multi-GPU): with P (peer-memory arena) the traversal epilogues store into every rank's
-// replica and a device-side wait follows each exchanging traversal; μ ping-pongs between the arena's two
-// buffers (iteration i reads μ[i % 2], its G epilogue writes μ[(i + 1) % 2]).  Without P but with comm:
-// NCCL broadcasts after each traversal.
-static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm, const PeerArena* P,
-                                cudaStream_t s) {
+// Exchanges (multi-GPU): with peer-memory arenas the traversal epilogues store into every rank's replica
+// and a device-side wait follows each exchanging traversal; μ ping-pongs between the arena's two buffers
+// (iteration i reads μ[i % 2], its G epilogue writes μ[(i + 1) % 2]).  `views` are the ranks this process
+// drives: normally one (its own rank; moments, α and μ' from its replica); several when W ranks are
+// emulated on one GPU (wnnc_iterate_emulated: each rank's traversal over its shard and its own replica,
+// serialized on one stream, all waits after all signals).  No views but a comm: NCCL broadcasts.
+static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm, const PeerArena* const* views,
+                                int nviews, cudaStream_t s) {
   IterScratch& it = t->it;
   const int total = p.total_iters > 0 ? p.total_iters : p.iters;
   const bool transpose = p.adjoint_mode == WN_ADJ_TRANSPOSE;
+  const PeerArena* P = nviews > 0 ? views[0] : nullptr;
   int64_t q0 = 0, q1 = t->n;
-  if (comm) WN_TRY(comm_shard(comm, t->n, &q0, &q1));
+  if (comm && !P) WN_TRY(comm_shard(comm, t->n, &q0, &q1));
   const bool nccl = comm && !P;
   const int me = P ? P->rank : 0;
   float* sb = P ? P->s[me] : it.s;
@@ -166,11 +169,35 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
   // queries follow the Hilbert schedule; multi-GPU shards are schedule ranges (exchanged via staging)
   const int32_t* qord = t->qorder;
   float* stage = (float*)it.tmp;  // n × 4 floats
+  // one exchanging traversal: every view's shard (inputs from its own replica), then every view's wait
+  enum Rows { NONE, S, R, MU0, MU1 };
+  auto run_traversal = [&](const TravArgs& ta, int slot, Rows in, Rows out) -> wn_status {
+    if (!P) {
+      TravArgs tv = ta;
+      tv.q_begin = q0;
+      tv.q_end = q1;
+      return traverse(tv, s);
+    }
+    for (int v = 0; v < nviews; ++v) {
+      const PeerArena& A = *views[v];
+      TravArgs tv = ta;
+      wn_shard_range(t->n, A.rank, A.world, &tv.q_begin, &tv.q_end);
+      if (in == S) tv.scal = A.s[A.rank];
+      if (in == R) tv.vec = A.r[A.rank];
+      if (in == MU0 || in == MU1) tv.vec = A.mu[in == MU1][A.rank];
+      peer_route(tv, &A, out == S ? A.s : nullptr,
+                 out == R ? A.r : (out == MU0 || out == MU1) ? A.mu[out == MU1] : nullptr, slot);
+      WN_TRY(traverse(tv, s));
+    }
+    for (int v = 0; v < nviews; ++v) comm_peer_wait(*views[v], s);
+    return WN_OK;
+  };
   for (int i = 0; i < p.iters; ++i) {
     const int k = p.first_iter + i;
     const float w = width_at(k, total, (double)p.w_min, (double)p.w_max);
     const float w2 = w * w;
-    float4* mu_cur = P ? P->mu[i & 1][me] : it.mu;
+    const int cur = i & 1;
+    float4* mu_cur = P ? P->mu[cur][me] : it.mu;
     // (1) s = ½ − A_w μ  (+ Σ s² partials)
     MomentArgs m1;
     m1.kind = ATTR_VEC;
@@ -185,14 +212,10 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a1.epi = EPI_S;
     a1.nodes = m1.out;
     a1.vec = mu_cur;
-    a1.q_begin = q0;
-    a1.q_end = q1;
     a1.out_f = sb;
     a1.partial = part;
     a1.order1 = t->far_order;
-    peer_route(a1, P, P ? P->s : nullptr, nullptr, 0);
-    WN_TRY(traverse(a1, s));
-    if (P) comm_peer_wait(*P, s);
+    WN_TRY(run_traversal(a1, 0, cur ? MU1 : MU0, S));
     if (nccl) WN_TRY(comm_allgather_f(comm, sb, 1, t->n, qord, stage, s));
     // (2) r = A_wᵀ s  (+ Σ|r|² partials)
     if (transpose) {
@@ -211,14 +234,10 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
       a2.epi = EPI_R;
       a2.nodes = t->set[0];
       a2.scal = sb;
-      a2.q_begin = q0;
-      a2.q_end = q1;
       a2.out_v4 = rb;
       a2.partial = part + stride;
       a2.order1 = t->far_order;
-      peer_route(a2, P, nullptr, P ? P->r : nullptr, 1);
-      WN_TRY(traverse(a2, s));
-      if (P) comm_peer_wait(*P, s);
+      WN_TRY(run_traversal(a2, 1, S, R));
       if (nccl) WN_TRY(comm_allgather_f(comm, (float*)rb, 4, t->n, qord, stage, s));
     }
     // (3) Σ (A_w r)²  — gather: r's own representatives; transpose: μ's frozen geometry
@@ -236,13 +255,9 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a3.nodes = transpose ? t->set[1] : t->set[0];
     a3.attr = transpose ? t->set[0].rec : nullptr;
     a3.vec = rb;
-    a3.q_begin = q0;
-    a3.q_end = q1;
     a3.partial = part + 2 * stride;
     a3.order1 = t->far_order;
-    peer_route(a3, P, nullptr, nullptr, 2);
-    WN_TRY(traverse(a3, s));
-    if (P) comm_peer_wait(*P, s);
+    WN_TRY(run_traversal(a3, 2, R, NONE));
     if (nccl) WN_TRY(comm_allgather_partials(comm, part, stride, t->n, s));
     // α = Σr² / Σ(Ar)²  (Alg. 2), fixed-order reduction of the partials
     // (the partial arrays' stride may exceed this cloud's block count: a peer arena sized for a larger N)
@@ -265,13 +280,9 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a4.nodes = t->set[0];
     a4.vec = it.mup;
     a4.mup = it.mup;
-    a4.q_begin = q0;
-    a4.q_end = q1;
     a4.out_v4 = it.mu;
     a4.order1 = t->far_order;
-    peer_route(a4, P, nullptr, P ? P->mu[(i + 1) & 1] : nullptr, 0);
-    WN_TRY(traverse(a4, s));
-    if (P) comm_peer_wait(*P, s);
+    WN_TRY(run_traversal(a4, 0, NONE, cur ? MU0 : MU1));
     if (nccl) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, s));
   }
   return WN_OK;
@@ -555,6 +566,47 @@ static wn_status check_params(const wnnc_params* p) {
   return WN_OK;
 }
 
+wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int32_t world, float* replicas,
+                                void* stream) {
+  if (!t || !mu) return set_error(WN_ERR_ARG, "tree or mu is NULL");
+  WN_TRY(check_params(p));
+  if (world < 1 || world > kMaxPeers) return set_error(WN_ERR_ARG, "world must be 1..8");
+  if (p->adjoint_mode == WN_ADJ_TRANSPOSE) return set_error(WN_ERR_ARG, "transpose-mode adjoint is single-GPU only");
+  cudaStream_t s = (cudaStream_t)stream;
+  WN_TRY(ensure_scratch(t, s));
+  IterScratch& it = t->it;
+  if (it.stats_cap < p->iters) {
+    if (it.dstats) cudaFreeAsync(it.dstats, s);
+    WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)p->iters, s));
+    it.stats_cap = p->iters;
+  }
+  PeerArena arenas[kMaxPeers];
+  void* blocks[kMaxPeers] = {};
+  wn_status st = emulated_arenas(world, t->n, arenas, blocks);
+  const double sc2 = t->xf[3] * t->xf[3];
+  if (st == WN_OK) {
+    const PeerArena* views[kMaxPeers];
+    for (int v = 0; v < world; ++v) {
+      views[v] = &arenas[v];
+      gather_vec(t->n, t->perm, mu, sc2, arenas[0].mu[0][v], s);  // every rank's replica of μ⁰
+    }
+    st = run_iterations(t, *p, nullptr, views, world, s);
+  }
+  if (st == WN_OK) {
+    const int e = p->iters & 1;
+    scatter_vec(t->n, t->perm, arenas[0].mu[e][0], 1.0 / sc2, mu, s);
+    if (replicas)
+      for (int v = 0; v < world; ++v) scatter_vec(t->n, t->perm, arenas[0].mu[e][v], 1.0 / sc2, replicas + 3 * t->n * v, s);
+    cudaError_t ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) st = cuda_status(ce, "wnnc_iterate_emulated");
+  } else {
+    cudaStreamSynchronize(s);
+  }
+  for (int v = 0; v < world; ++v)
+    if (blocks[v]) cudaFree(blocks[v]);
+  return st;
+}
+
 wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm, wnnc_iter_stats* stats,
                        void* stream) {
   if (!t || !mu) return set_error(WN_ERR_ARG, "tree or mu is NULL");
@@ -591,7 +643,7 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
       if (!t->cap_stream) WN_CUDA(cudaStreamCreateWithFlags(&t->cap_stream, cudaStreamNonBlocking));
       WN_CUDA(cudaStreamBeginCapture(t->cap_stream, cudaStreamCaptureModeThreadLocal));
       g_capturing = true;
-      wn_status st = run_iterations(t, *p, comm, P, t->cap_stream);
+      wn_status st = run_iterations(t, *p, comm, &P, P ? 1 : 0, t->cap_stream);
       g_capturing = false;
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaStreamEndCapture(t->cap_stream, &graph);
@@ -619,7 +671,7 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
     count_launches((int)t->graph_launches);
     WN_CUDA(cudaGraphLaunch(t->graph_exec, s));
   } else {
-    WN_TRY(run_iterations(t, *p, comm, P, s));
+    WN_TRY(run_iterations(t, *p, comm, &P, P ? 1 : 0, s));
   }
   const float4* mu_end = P ? P->mu[p->iters & 1][P->rank] : t->it.mu;
   scatter_vec(t->n, t->perm, mu_end, 1.0 / sc2, mu, s);  // back to the input frame

@@ -172,6 +172,44 @@ static void arena_release(PeerArena& A) {
   A = PeerArena();
 }
 
+// the arena's layout inside one block of `arena_bytes(n)` bytes
+struct ArenaLayout {
+  size_t o_s, o_r, o_mu0, o_mu1, o_part, o_sig, bytes;
+  int64_t nb;
+  explicit ArenaLayout(int64_t n) {
+    nb = trav_blocks(n);
+    o_s = 0;
+    o_r = align256(o_s + n * sizeof(float));
+    o_mu0 = align256(o_r + n * sizeof(float4));
+    o_mu1 = align256(o_mu0 + n * sizeof(float4));
+    o_part = align256(o_mu1 + n * sizeof(float4));
+    o_sig = align256(o_part + 3 * nb * sizeof(double));
+    bytes = align256(o_sig + 4 * sizeof(uint64_t));
+  }
+};
+
+// point A (rank `rank` of `world`) at every rank's block; blocks[r] mapped in this process
+static void arena_bind(PeerArena& A, void* const* blocks, int world, int rank, int64_t n) {
+  const ArenaLayout L(n);
+  A.world = world;
+  A.rank = rank;
+  A.cap = n;
+  A.part_stride = L.nb;
+  for (int r = 0; r < world; ++r) {
+    char* b = static_cast<char*>(blocks[r]);
+    A.base[r] = blocks[r];
+    A.s[r] = reinterpret_cast<float*>(b + L.o_s);
+    A.r[r] = reinterpret_cast<float4*>(b + L.o_r);
+    A.mu[0][r] = reinterpret_cast<float4*>(b + L.o_mu0);
+    A.mu[1][r] = reinterpret_cast<float4*>(b + L.o_mu1);
+    A.part[r] = reinterpret_cast<double*>(b + L.o_part);
+    A.sig[r] = reinterpret_cast<unsigned long long*>(b + L.o_sig);
+  }
+  char* own = static_cast<char*>(blocks[rank]);
+  A.expected = reinterpret_cast<unsigned long long*>(own + L.o_sig) + 1;  // local: next wait target
+  A.done = reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(own + L.o_sig) + 2);
+}
+
 wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena** out) {
   PeerArena& A = c->arena;
   if (c->world > kMaxPeers) return set_error(WN_ERR_ARG, "peer-memory exchange supports at most 8 ranks");
@@ -181,20 +219,19 @@ wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena*
   }
   // (re)build, collectively: every rank reaches this point in the same wnnc_iterate call
   arena_release(A);
-  const int64_t nb = trav_blocks(n);
-  const size_t o_s = 0, o_r = align256(o_s + n * sizeof(float)), o_mu0 = align256(o_r + n * sizeof(float4));
-  const size_t o_mu1 = align256(o_mu0 + n * sizeof(float4)), o_part = align256(o_mu1 + n * sizeof(float4));
-  const size_t o_sig = align256(o_part + 3 * nb * sizeof(double)), bytes = align256(o_sig + 4 * sizeof(uint64_t));
+  const ArenaLayout L(n);
   WN_CUDA(cudaStreamSynchronize(s));
-  WN_CUDA(cudaMalloc(&A.own, bytes));
-  WN_CUDA(cudaMemset(A.own, 0, bytes));
+  void* own = nullptr;
+  WN_CUDA(cudaMalloc(&own, L.bytes));
+  WN_CUDA(cudaMemset(own, 0, L.bytes));
   cudaIpcMemHandle_t mine;
-  WN_CUDA(cudaIpcGetMemHandle(&mine, A.own));
+  WN_CUDA(cudaIpcGetMemHandle(&mine, own));
   cudaIpcMemHandle_t* dh = nullptr;
   WN_CUDA(cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * c->world));
   WN_CUDA(cudaMemcpy(dh + c->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice));
   Nccl& N = nccl();
-  wn_status st = nccl_status(N.AllGather(dh + c->rank, dh, sizeof(mine), ncclUint8, c->comm, s), "ncclAllGather (IPC handles)");
+  wn_status st = nccl_status(N.AllGather(dh + c->rank, dh, sizeof(mine), ncclUint8, c->comm, s),
+                             "ncclAllGather (IPC handles)");
   cudaIpcMemHandle_t hs[kMaxPeers];
   if (st == WN_OK) {
     cudaError_t e = cudaStreamSynchronize(s);
@@ -202,34 +239,41 @@ wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena*
     if (e != cudaSuccess) st = cuda_status(e, "IPC handle exchange");
   }
   cudaFree(dh);
-  if (st != WN_OK) return st;
-  A.world = c->world;
-  A.rank = c->rank;
-  A.cap = n;
+  if (st != WN_OK) {
+    cudaFree(own);
+    return st;
+  }
+  void* blocks[kMaxPeers] = {};
+  bool opened[kMaxPeers] = {};
   for (int r = 0; r < c->world; ++r) {
     if (r == c->rank) {
-      A.base[r] = A.own;
-    } else {
-      cudaError_t e = cudaIpcOpenMemHandle(&A.base[r], hs[r], cudaIpcMemLazyEnablePeerAccess);
-      if (e != cudaSuccess) {
-        arena_release(A);
-        return cuda_status(e, "cudaIpcOpenMemHandle (peer arena)");
-      }
-      A.opened[r] = true;
+      blocks[r] = own;
+      continue;
     }
-    char* b = static_cast<char*>(A.base[r]);
-    A.s[r] = reinterpret_cast<float*>(b + o_s);
-    A.r[r] = reinterpret_cast<float4*>(b + o_r);
-    A.mu[0][r] = reinterpret_cast<float4*>(b + o_mu0);
-    A.mu[1][r] = reinterpret_cast<float4*>(b + o_mu1);
-    A.part[r] = reinterpret_cast<double*>(b + o_part);
-    A.sig[r] = reinterpret_cast<unsigned long long*>(b + o_sig);
+    cudaError_t e = cudaIpcOpenMemHandle(&blocks[r], hs[r], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int q = 0; q < r; ++q)
+        if (opened[q]) cudaIpcCloseMemHandle(blocks[q]);
+      cudaFree(own);
+      return cuda_status(e, "cudaIpcOpenMemHandle (peer arena)");
+    }
+    opened[r] = true;
   }
-  char* own = static_cast<char*>(A.own);
-  A.expected = reinterpret_cast<unsigned long long*>(own + o_sig) + 1;  // local: next wait target
-  A.done = reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(own + o_sig) + 2);
-  A.part_stride = nb;
+  arena_bind(A, blocks, c->world, c->rank, n);
+  A.own = own;
+  for (int r = 0; r < c->world; ++r) A.opened[r] = opened[r];
   *out = &A;
+  return WN_OK;
+}
+
+// W ranks in this process on this GPU (wnnc_iterate_emulated): one plain block per rank
+wn_status emulated_arenas(int world, int64_t n, PeerArena* arenas, void** blocks) {
+  const ArenaLayout L(n);
+  for (int r = 0; r < world; ++r) {
+    WN_CUDA(cudaMalloc(&blocks[r], L.bytes));
+    WN_CUDA(cudaMemset(blocks[r], 0, L.bytes));
+  }
+  for (int r = 0; r < world; ++r) arena_bind(arenas[r], blocks, world, r, n);
   return WN_OK;
 }
 

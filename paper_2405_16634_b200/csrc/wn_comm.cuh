@@ -19,4 +19,6 @@ wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64
 // and the per-exchange device-side wait for every rank's signal.
 wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena** out);
 void comm_peer_wait(const PeerArena& A, cudaStream_t s);
+// W emulated ranks in one process (diagnostic): plain blocks[W] bound as each other's replicas
+wn_status emulated_arenas(int world, int64_t n, PeerArena* arenas, void** blocks);
 }  // namespace wn

@@ -28,7 +28,7 @@ EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", 
             "wn_tree_destroy", "wn_tree_info", "wn_tree_export", "wn_moments", "wn_eval", "wn_eval_grad",
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
             "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work",
-            "wn_tree_set_far_order")
+            "wn_tree_set_far_order", "wnnc_iterate_emulated")
 
 
 class wnnc_params(C.Structure):
@@ -57,6 +57,7 @@ _sig = {
     "wn_work_count_enable": ([I32], I32), "wn_work_count_read": ([P], I32),
     "wn_query_work": ([P, I32, P, P, I64, F32, F32, P, P], I32),
     "wn_tree_set_far_order": ([P, I32, P], I32),
+    "wnnc_iterate_emulated": ([P, P, P, I32, P, P], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -289,6 +290,15 @@ def wn_comm_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(_L.wn_comm_unique_id(buf))
     return bytes(buf)
+
+
+def wnnc_iterate_emulated(tree: Tree, mu: torch.Tensor, world: int, **params):
+    """Diagnostic: `world` ranks of the peer-memory exchange emulated on this GPU; returns every rank's μ."""
+    _dev_f32(mu, 3)
+    p = make_params(**params)
+    reps = torch.empty(world, tree.n, 3, dtype=torch.float32, device=tree.device)
+    _check(_L.wnnc_iterate_emulated(tree.handle, _ptr(mu), C.byref(p), int(world), _ptr(reps), _stream()))
+    return reps
 
 
 def wn_comm_init(rank: int, world: int, uid: bytes) -> Comm:

@@ -59,6 +59,22 @@ def test_peer_arena_grows_with_n(wn):
     comm.close()
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_emulated_ranks_match_single_gpu(wn, world):
+    # W ranks of the peer-memory exchange emulated on this GPU (each rank's shard reads its own replica
+    # and stores into all W replicas; signals / waits with world-W targets; ping-pong μ): every replica
+    # must hold the single-GPU trajectory bit for bit
+    p = torch.from_numpy(synth.config("C2")["points"][:30011]).cuda()
+    t = wn.wn_build_tree(p)
+    ref = torch.zeros(len(p), 3, device="cuda")
+    wn.wnnc_iterate(t, ref, iters=5, total_iters=40)
+    mu = torch.zeros(len(p), 3, device="cuda")
+    reps = wn.wnnc_iterate_emulated(t, mu, world, iters=5, total_iters=40)
+    np.testing.assert_array_equal(mu.cpu().numpy(), ref.cpu().numpy())
+    for r in range(world):
+        np.testing.assert_array_equal(reps[r].cpu().numpy(), ref.cpu().numpy())
+
+
 def test_comm_init_errors(wn):
     with pytest.raises(wn.WnError, match="ARG"):
         wn.wn_comm_init(2, 2, bytes(128))
