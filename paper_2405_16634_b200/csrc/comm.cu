@@ -35,6 +35,8 @@ struct Nccl {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -56,12 +58,13 @@ Nccl& nccl() {
     SYM(CommDestroy, "ncclCommDestroy");
     SYM(Broadcast, "ncclBroadcast");
     SYM(AllGather, "ncclAllGather");
+    SYM(AllReduce, "ncclAllReduce");
     SYM(GroupStart, "ncclGroupStart");
     SYM(GroupEnd, "ncclGroupEnd");
     SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
-    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Broadcast && n.AllGather && n.GroupStart &&
-           n.GroupEnd;
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Broadcast && n.AllGather && n.AllReduce &&
+           n.GroupStart && n.GroupEnd;
     if (!n.ok) n.err = "libnccl.so.2 lacks required symbols";
   });
   return n;
@@ -154,13 +157,29 @@ wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64
 namespace {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// a rank that never signals (a crashed peer) must not hang the GPU: give up after 10 s and trap
+constexpr unsigned long long kPeerWaitTimeoutNs = 10ull * 1000 * 1000 * 1000;
+
 __global__ void k_peer_wait(unsigned long long* sig, unsigned long long* expected, int world) {
   const unsigned long long target = *expected + (unsigned long long)world;
   *expected = target;
+  const unsigned long long t0 = globaltimer_ns();
   unsigned long long v;
-  do {
+  for (;;) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sig) : "memory");
-  } while (v < target);
+    if (v >= target) break;
+    if (globaltimer_ns() - t0 > kPeerWaitTimeoutNs) {
+      printf("libwn: peer-memory exchange timed out (signal %llu of %llu)\n", v, target);
+      __trap();
+    }
+    __nanosleep(200);
+  }
   __threadfence_system();
 }
 }  // namespace
@@ -245,19 +264,35 @@ wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena*
   }
   void* blocks[kMaxPeers] = {};
   bool opened[kMaxPeers] = {};
-  for (int r = 0; r < c->world; ++r) {
+  cudaError_t oe = cudaSuccess;
+  for (int r = 0; r < c->world && oe == cudaSuccess; ++r) {
     if (r == c->rank) {
       blocks[r] = own;
       continue;
     }
-    cudaError_t e = cudaIpcOpenMemHandle(&blocks[r], hs[r], cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) {
-      for (int q = 0; q < r; ++q)
-        if (opened[q]) cudaIpcCloseMemHandle(blocks[q]);
-      cudaFree(own);
-      return cuda_status(e, "cudaIpcOpenMemHandle (peer arena)");
-    }
-    opened[r] = true;
+    oe = cudaIpcOpenMemHandle(&blocks[r], hs[r], cudaIpcMemLazyEnablePeerAccess);
+    opened[r] = oe == cudaSuccess;
+  }
+  // every rank must agree before anyone stores into a peer: min over ranks of "all opens succeeded"
+  int32_t* flag = nullptr;
+  int32_t ok = oe == cudaSuccess ? 1 : 0, all_ok = 0;
+  WN_CUDA(cudaMalloc(&flag, sizeof(int32_t)));
+  WN_CUDA(cudaMemcpy(flag, &ok, sizeof(ok), cudaMemcpyHostToDevice));
+  st = nccl_status(N.AllReduce(flag, flag, 1, ncclInt32, ncclMin, c->comm, s), "ncclAllReduce (peer arena)");
+  if (st == WN_OK) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMemcpy(&all_ok, flag, sizeof(all_ok), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = cuda_status(e, "peer arena agreement");
+  }
+  cudaFree(flag);
+  if (st == WN_OK && !all_ok)
+    st = oe != cudaSuccess ? cuda_status(oe, "cudaIpcOpenMemHandle (peer arena)")
+                           : set_error(WN_ERR_CUDA, "peer arena: another rank could not map the replicas");
+  if (st != WN_OK) {
+    for (int r = 0; r < c->world; ++r)
+      if (opened[r]) cudaIpcCloseMemHandle(blocks[r]);
+    cudaFree(own);
+    return st;
   }
   arena_bind(A, blocks, c->world, c->rank, n);
   A.own = own;
