@@ -38,12 +38,13 @@ CONFIG_TEXT = {
     "C5": "C5: 8-shape scene, N=4,000,000, 0.25% noise, 40 WNNC iterations, theta=2, D=15",
 }
 # Algorithmic FP32 operations per unit of work (FMA = 2 flops, rsqrt = 1):
-#   opening test: d = x_B − x_q (3) + d² (1 mul + 2 fma = 5)                               = 8
+#   opening test: d = (hi − x_q) + lo (3 sub + 3 add, DESIGN.md R-prec) + d² (1 mul + 2 fma = 5)
+#                 + far compare (1) + cutoff compare (1)                                      = 13
 #   live kernel evaluation, on top of its d²:
 #     A : rsqrt 1 + r⁻³ 2 + d·ν 5 + accumulate 2                                           = 10
 #     Aᵀ: rsqrt 1 + r⁻³ 2 + s·r⁻³ 1 + accumulate 6                                         = 10
 #     G : rsqrt 1 + r⁻², r⁻³ 2 + d·ν 5 + 3(d·ν)r⁻² 2 + ν − t d 6 + accumulate 6            = 22
-FLOPS_TEST = 8
+FLOPS_TEST = 13
 FLOPS_TERM = {"A": 10, "AT": 10, "G": 22}
 # first-order far field (--order 1): the order-0 term plus M e / eᵀMe / D·e (traverse.cu term1)
 FLOPS_TERM1 = {"A": 34, "AT": 23, "G": 55}
