@@ -596,6 +596,11 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   WN_CUDA(cudaMemcpyAsync(hoffs.data(), offs, (m + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   WN_CUDA(cudaStreamSynchronize(s));
   t->nn = hoffs[m];
+  if (t->nn + 1 > ((int64_t)1 << 26)) {  // the traversal addresses 64-byte records with 32-bit byte offsets
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(offs, s);
+    return set_error(WN_ERR_ARG, "octree with more than 2^26 - 1 nodes (deep chains of close points)");
+  }
   t->level_off.assign(D + 2, t->nn);
   int used = 0;
   for (int l = 0; l <= D; ++l) {
