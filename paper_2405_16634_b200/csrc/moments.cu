@@ -470,11 +470,29 @@ __global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int6
   if (i >= nn) return;
   const int j0 = tv.pb[i], j1 = tv.pe[i];
   double d[NC];
-  float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (j1 - j0 == 1) {
+  const float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j1 - j0 == 1) {  // one-point node: R = (x_j, −1), L and ext (= 0) are fixed per tree — only V = ν_j
     const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-    point_vals<KIND, ORD>(j0, tv.pts, m, alpha, d);
-    p0 = tv.pts[j0];
+    double v0, v1 = 0.0, v2 = 0.0;
+    if (KIND == ATTR_VEC) {
+      float4 v = m.vec[j0];
+      if (m.axpy_r) {
+        const float4 r = m.axpy_r[j0];
+        v = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
+      }
+      v0 = v.x; v1 = v.y; v2 = v.z;
+      if (m.a_sorted) {
+        const double f = m.a_sorted[j0];
+        v0 *= f; v1 *= f; v2 *= f;
+      }
+      if (m.write_W) tv.sums[8 * i] = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+    } else {
+      v0 = m.scal[j0];
+      if (m.a_sorted) v0 *= (double)m.a_sorted[j0];
+      if (m.write_W) tv.sums[8 * i] = fabs(v0);
+    }
+    m.out.rec[kRec * i + 1] = make_float4((float)v0, (float)v1, (float)v2, __int_as_float(tv.topo[i]));
+    return;
   } else {
     const double2* a = reinterpret_cast<const double2*>(Eh + Lay::EH * (int64_t)j0);
     const double2* b = reinterpret_cast<const double2*>(Eh + Lay::EH * (int64_t)j1);
@@ -507,9 +525,9 @@ __global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int6
   S.V[0] = d[4]; S.V[1] = d[5]; S.V[2] = d[6];
   if (m.write_W) tv.sums[8 * i] = S.W;
   write_record<KIND>(i, S, j1 - j0, p0, tv.depth[i], tv.topo[i], tv.smask[i], m.theta, tv.centroid, m);
-  if (ORD == 1) {  // first moment about the fp64 representative (0 for one-point nodes and Σ|ν| = 0)
+  if (ORD == 1) {  // first moment about the fp64 representative (0 for Σ|ν| = 0)
     float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f), e1 = e0;
-    if (j1 - j0 > 1 && S.W > 0.0) {
+    if (S.W > 0.0) {
       const double X = S.P[0] / S.W, Y = S.P[1] / S.W, Z = S.P[2] / S.W;
       if (KIND == ATTR_VEC) {
         const double mxx = d[7] - S.V[0] * X, myy = d[8] - S.V[1] * Y, mzz = d[9] - S.V[2] * Z;

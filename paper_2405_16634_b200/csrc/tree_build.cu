@@ -658,6 +658,8 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   ma.centroid_out = t->centroid;
   ma.leaf_of_out = t->leaf_of;
   WN_TRY(build_moments(t, ma, s));
+  // the per-iteration builds rewrite only V of one-point nodes: their R = (x_j, −1) and L are fixed here
+  WN_CUDA(cudaMemcpyAsync(t->set[0].rec, t->set[1].rec, sizeof(float4) * kRec * (nn + 1), cudaMemcpyDeviceToDevice, s));
   return WN_OK;
 }
 
