@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __
       elt_add_point(t, o);
     }
   block_exscan<kScanThreads>(t, tot);
-  {
+  if (tile_off) {  // null: a single tile, offset 0
     Elt<NC> z = tile_off[blockIdx.x];
     elt_add(z, t);
     t = z;
@@ -554,9 +554,11 @@ void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
   Elt<Lay::NC>* off = tot + nt;
   double* Eh = t->mom_pre;
   float* El = reinterpret_cast<float*>(t->mom_pre + Lay::EH * (t->n + 1));
-  mom_tile_sum<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, tot);
-  mom_tile_scan<Lay::NC><<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
-  mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, off, Eh, El);
+  if (nt > 1) {  // a single tile needs no tile totals
+    mom_tile_sum<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, tot);
+    mom_tile_scan<Lay::NC><<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
+  }
+  mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, nt > 1 ? off : nullptr, Eh, El);
   mom_nodes<KIND, ORD><<<(unsigned)((t->nn + 255) / 256), 256, 0, s>>>(tv, m, t->nn, Eh, El);
 }
 
@@ -604,7 +606,7 @@ wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
 #ifndef WN_EXP_OLD_MOM
   if (m.kind != ATTR_UNIT) {  // per-iteration attributes: prefix differences
-    ProfScope ps(WN_PROF_MOMENTS, s, 4);
+    ProfScope ps(WN_PROF_MOMENTS, s, t->mom_ntiles > 1 ? 4 : 2);
     if (m.order1 && !(m.out.ext && t->mom_order1_ready)) return set_error(WN_ERR_ARG, "internal: order-1 scratch");
     if (m.kind == ATTR_VEC) {
       if (m.order1) launch_prefix<ATTR_VEC, 1>(t, m, s);
