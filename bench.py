@@ -166,7 +166,8 @@ def run_ours(args):
     n = len(pts_h)
     pts = torch.from_numpy(pts_h).to(dev)
     params = dict(iters=ITERS, theta=args.theta, adjoint_mode=wn.WN_ADJ_TRANSPOSE if args.transpose else 0,
-                  flags=(0 if args.no_graph else wn.WN_FLAG_GRAPH) | (wn.WN_FLAG_COMM_NCCL if args.comm == "nccl" else 0))
+                  flags=(0 if args.no_graph else wn.WN_FLAG_GRAPH) | (wn.WN_FLAG_COMM_NCCL if args.comm == "nccl" else 0)
+                  | wn.WN_FLAG_MU_ZERO)  # every step starts from the paper's μ = 0: iteration 1 takes A(0) = 0
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
@@ -196,7 +197,7 @@ def run_ours(args):
 
     # ---- algorithmic work of one step (counting variant, same decisions; untimed) ----
     wn.wn_work_count_enable(True)
-    tree, mu = step(flags=0)
+    tree, mu = step(flags=params["flags"] & ~wn.WN_FLAG_GRAPH)
     work = wn.wn_work_count_read()
     wn.wn_work_count_enable(False)
     depth_used, num_nodes = tree.depth_used, tree.num_nodes
@@ -206,7 +207,7 @@ def run_ours(args):
     wn.wn_prof_enable(True)
     for _ in range(args.prof_steps):
         flush.zero_()
-        step(flags=0)
+        step(flags=params["flags"] & ~wn.WN_FLAG_GRAPH)
     prof = wn.wn_prof_read()
     wn.wn_prof_enable(False)
 

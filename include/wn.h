@@ -61,8 +61,11 @@ enum { WN_ADJ_GATHER = 0,    /* Aᵀ by its own traversal with |s|-weighted reps
 
 enum {
   WN_FLAG_GRAPH = 1,      /* wnnc_params.flags: capture the iteration loop in a CUDA graph */
-  WN_FLAG_COMM_NCCL = 2   /* multi-GPU: exchange with NCCL broadcasts instead of the default peer-memory
+  WN_FLAG_COMM_NCCL = 2,  /* multi-GPU: exchange with NCCL broadcasts instead of the default peer-memory
                              stores fused into the traversal epilogues (see wnnc_iterate) */
+  WN_FLAG_MU_ZERO = 4     /* the caller's mu is all zeros (the paper's initialization) and
+                             first_iter = 1: iteration 1 takes A(0) = 0, i.e. s = ½ exactly, without a
+                             moment build and traversal (bit-identical to computing it) */
 };
 
 typedef struct {

@@ -199,24 +199,32 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     const int cur = i & 1;
     float4* mu_cur = P ? P->mu[cur][me] : it.mu;
     // (1) s = ½ − A_w μ  (+ Σ s² partials)
-    MomentArgs m1;
-    m1.kind = ATTR_VEC;
-    m1.vec = mu_cur;
-    m1.theta = p.theta;
-    m1.out = transpose ? t->set[1] : t->set[0];
-    m1.order1 = t->far_order == 1;
-    WN_TRY(build_moments(t, m1, s));
-    TravArgs a1 = base_args(t, w2);
-    a1.qorder = qord;
-    a1.op = OP_A;
-    a1.epi = EPI_S;
-    a1.nodes = m1.out;
-    a1.vec = mu_cur;
-    a1.out_f = sb;
-    a1.partial = part;
-    a1.order1 = t->far_order;
-    WN_TRY(run_traversal(a1, 0, cur ? MU1 : MU0, S));
-    if (nccl) WN_TRY(comm_allgather_f(comm, sb, 1, t->n, qord, stage, s));
+    if (i == 0 && k == 1 && (p.flags & WN_FLAG_MU_ZERO) && !transpose) {
+      // μ⁰ = 0: A(0) = 0 term by term, s = ½ exactly — every rank fills its whole replica
+      if (P)
+        for (int v = 0; v < nviews; ++v) s_half(t->n, views[v]->s[views[v]->rank], views[v]->part[views[v]->rank], s);
+      else
+        s_half(t->n, sb, part, s);
+    } else {
+      MomentArgs m1;
+      m1.kind = ATTR_VEC;
+      m1.vec = mu_cur;
+      m1.theta = p.theta;
+      m1.out = transpose ? t->set[1] : t->set[0];
+      m1.order1 = t->far_order == 1;
+      WN_TRY(build_moments(t, m1, s));
+      TravArgs a1 = base_args(t, w2);
+      a1.qorder = qord;
+      a1.op = OP_A;
+      a1.epi = EPI_S;
+      a1.nodes = m1.out;
+      a1.vec = mu_cur;
+      a1.out_f = sb;
+      a1.partial = part;
+      a1.order1 = t->far_order;
+      WN_TRY(run_traversal(a1, 0, cur ? MU1 : MU0, S));
+      if (nccl) WN_TRY(comm_allgather_f(comm, sb, 1, t->n, qord, stage, s));
+    }
     // (2) r = A_wᵀ s  (+ Σ|r|² partials)
     if (transpose) {
       WN_TRY(adjoint_transpose(t, t->set[1], sb, w2, rb, part + stride, s));
@@ -702,7 +710,9 @@ wn_status wnnc_solve_host(const float* pts_host, int64_t n, int32_t max_depth, c
   WN_CUDA(cudaMemsetAsync(dmu, 0, bytes, s));
   wn_tree t = nullptr;
   wn_status st = wn_build_tree(dp, n, max_depth, stream, &t);
-  if (st == WN_OK) st = wnnc_iterate(t, dmu, p, nullptr, stats, stream);
+  wnnc_params pz = *p;
+  if (pz.first_iter == 1) pz.flags |= WN_FLAG_MU_ZERO;  // μ⁰ = 0 here by construction
+  if (st == WN_OK) st = wnnc_iterate(t, dmu, &pz, nullptr, stats, stream);
   if (st == WN_OK) {
     unit_normals(n, dmu, dn, s);
     cudaMemcpyAsync(normals_host, dn, bytes, cudaMemcpyDeviceToHost, s);

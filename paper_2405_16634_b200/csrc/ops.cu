@@ -85,6 +85,17 @@ __global__ void __launch_bounds__(kAlphaThreads) k_alpha(const double* __restric
   }
 }
 
+// s = ½ − A(0) = ½ for every query and the block partials Σ s² = 0.25 · (queries in the block) — exactly the
+// values the A traversal's EPI_S epilogue produces for μ = 0 (every term 0), without the traversal
+__global__ void k_s_half(int64_t n, float* __restrict__ s, double* __restrict__ part, int block) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) s[i] = 0.5f;
+  if (i * block < n) {
+    const int64_t cnt = n - i * block < block ? n - i * block : block;
+    part[i] = 0.25 * (double)cnt;
+  }
+}
+
 // final "Normalize" step of the pipeline figure: n_i = μ_i/|μ_i|, zero stays zero
 __global__ void k_unit(int64_t n, const float* __restrict__ mu, float* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -125,6 +136,10 @@ void normalize_queries(int64_t m, const float* q, const double xf[4], float4* ou
 void alpha_step(const double* part, int nblk, int64_t stride, double w, double* alpha, double* stats, cudaStream_t s) {
   ProfScope ps(WN_PROF_OTHER, s);
   k_alpha<<<1, kAlphaThreads, 0, s>>>(part, nblk, stride, w, alpha, stats);
+}
+void s_half(int64_t n, float* s_out, double* part, cudaStream_t s) {
+  k_s_half<<<g256(n), 256, 0, s>>>(n, s_out, part, kTravBlock);
+  count_launches(1);
 }
 void unit_normals(int64_t n, const float* mu, float* out, cudaStream_t s) {
   k_unit<<<g256(n), 256, 0, s>>>(n, mu, out);

@@ -21,6 +21,7 @@ WN_OK, WN_ERR_ARG, WN_ERR_EMPTY, WN_ERR_NONFINITE, WN_ERR_DEGENERATE, WN_ERR_CUD
 WN_ADJ_GATHER, WN_ADJ_TRANSPOSE = 0, 1
 WN_FLAG_GRAPH = 1
 WN_FLAG_COMM_NCCL = 2
+WN_FLAG_MU_ZERO = 4
 PROF_CLASSES = ("trav_A", "trav_AT", "trav_G", "moments", "tree", "other")
 STATUS_NAMES = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_EMPTY", 3: "WN_ERR_NONFINITE", 4: "WN_ERR_DEGENERATE",
                 5: "WN_ERR_CUDA", 6: "WN_ERR_OOM", 7: "WN_ERR_NCCL"}

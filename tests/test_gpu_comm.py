@@ -75,6 +75,32 @@ def test_emulated_ranks_match_single_gpu(wn, world):
         np.testing.assert_array_equal(reps[r].cpu().numpy(), ref.cpu().numpy())
 
 
+@pytest.mark.parametrize("order", [0, 1])
+def test_mu_zero_flag_is_exact(wn, order):
+    # WN_FLAG_MU_ZERO (iteration 1 takes A(0) = 0, s = ½, without the traversal) reproduces the computed
+    # first iteration bit for bit: single GPU (stream and graph), NCCL world 1, 3 emulated ranks
+    p = torch.from_numpy(synth.config("C2")["points"][:20011]).cuda()
+    t = wn.wn_build_tree(p)
+    wn.wn_tree_set_far_order(t, order)
+    Z, G = wn.WN_FLAG_MU_ZERO, wn.WN_FLAG_GRAPH
+    out = []
+    for flags in (0, Z, Z | G):
+        mu = torch.zeros(len(p), 3, device="cuda")
+        st = wn.wnnc_iterate(t, mu, stats=True, iters=4, total_iters=40, flags=flags)
+        out.append((mu.cpu().numpy(), [(x["E"], x["alpha"]) for x in st]))
+    comm = wn.wn_comm_init(0, 1, wn.wn_comm_unique_id())
+    mu = torch.zeros(len(p), 3, device="cuda")
+    wn.wnnc_iterate(t, mu, comm=comm, iters=4, total_iters=40, flags=Z | wn.WN_FLAG_COMM_NCCL)
+    out.append((mu.cpu().numpy(), out[0][1]))
+    comm.close()
+    mu = torch.zeros(len(p), 3, device="cuda")
+    reps = wn.wnnc_iterate_emulated(t, mu, 3, iters=4, total_iters=40, flags=Z)
+    out.append((reps[2].cpu().numpy(), out[0][1]))
+    for m, st in out[1:]:
+        np.testing.assert_array_equal(m, out[0][0])
+        assert st == out[0][1]
+
+
 def test_comm_init_errors(wn):
     with pytest.raises(wn.WnError, match="ARG"):
         wn.wn_comm_init(2, 2, bytes(128))
