@@ -32,7 +32,7 @@ struct Sums {
 
 struct TreeView {
   const float4* pts;
-  const int32_t *pb, *pe, *cb, *cc, *depth, *topo, *smask;
+  const int32_t *pb, *pe, *cb, *cc, *depth, *topo, *smask;  // depth: the threshold depth (tdepth)
   double* sums;
   const float4* centroid;
 };
@@ -172,7 +172,7 @@ __device__ __forceinline__ void process_node(int64_t i, int depth, const TreeVie
   o[2] = make_double2(S.V[0], S.V[1]);
   o[3] = make_double2(S.V[2], 0.0);
   const float4 p0 = (j1 - j0 == 1) ? tv.pts[j0] : make_float4(0.f, 0.f, 0.f, 0.f);
-  write_record<KIND>(i, S, j1 - j0, p0, depth, tv.topo[i], tv.smask[i], m.theta, tv.centroid, m);
+  write_record<KIND>(i, S, j1 - j0, p0, tv.depth[i], tv.topo[i], tv.smask[i], m.theta, tv.centroid, m);
 }
 
 template <int KIND>
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int6
 template <int KIND, int ORD>
 void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
   using Lay = PreLayout<KIND, ORD>;
-  TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->topo, t->smask, t->sums, t->centroid};
+  TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->tdepth, t->topo, t->smask, t->sums, t->centroid};
   const int64_t nt = t->mom_ntiles;
   Elt<Lay::NC>* tot = reinterpret_cast<Elt<Lay::NC>*>(t->mom_tile);
   Elt<Lay::NC>* off = tot + nt;
@@ -564,7 +564,7 @@ void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
 
 template <int KIND>
 void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s, const int64_t* loff_dev) {
-  TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->depth, t->topo, t->smask, t->sums, t->centroid};
+  TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->tdepth, t->topo, t->smask, t->sums, t->centroid};
   const int cut = t->mom_cut;
   if (cut <= t->depth_used) {
     // levels ≥ cut: all their leaves in one launch, then one launch per level for the internal nodes

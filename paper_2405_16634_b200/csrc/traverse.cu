@@ -171,7 +171,19 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
             acc.term(live, ex, ey, ez, d2, V);
           }
           if (COUNT && mine) {
-            ++ntest;
+            // a collapsed chain (tree_build.cu:topo_codes): Alg. 4 tests its levels from the top until one
+            // is far — level k's threshold is the bottom's × 4^(len−1−k), exactly (powers of two)
+            const int len = (__float_as_int(L.w) >> 8) & 31;
+            int tests = 1;
+            if (len > 1) {
+              tests = len;
+              for (int kk = 0; kk < len; ++kk)
+                if (d2 > ldexpf(R.w, 2 * (len - 1 - kk))) {
+                  tests = kk + 1;
+                  break;
+                }
+            }
+            ntest += tests;
             nfar += far;
             nlive += live;
           }

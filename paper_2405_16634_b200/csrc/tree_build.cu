@@ -417,23 +417,39 @@ __global__ void child_counts(int64_t nn, const int32_t* __restrict__ depth, cons
   if (last) cc[p] = (int32_t)(i - cb[p] + 1);
 }
 
-// traversal code per node: leaf 0; internal (child_begin << 4) | all-children-one-point-leaves << 3 | (count − 1)
+// Traversal code per node: leaf 0; internal (child_begin << 4) | (count − 1).  A chain of single-child
+// nodes holds the same points at every level — the same representative and ν_B — while its threshold
+// (c·edge)² shrinks by 4 per level, so a lane is far somewhere in the chain iff it is far at the chain's
+// bottom, and the term is the same at every level: the chain's top takes the bottom's children, the
+// bottom's one-point-child mask and the bottom's depth for its threshold (tdepth), and the chain length
+// goes to smask bits 8..12 (the counting traversal re-derives Alg. 4's per-level tests from it).
+// Nodes strictly inside a chain are never visited.
 __global__ void topo_codes(int64_t nn, const int32_t* __restrict__ cb, const int32_t* __restrict__ cc,
-                           const int32_t* __restrict__ pb, const int32_t* __restrict__ pe, int32_t* __restrict__ topo,
-                           int32_t* __restrict__ smask) {
+                           const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
+                           const int32_t* __restrict__ depth, int32_t* __restrict__ topo, int32_t* __restrict__ smask,
+                           int32_t* __restrict__ tdepth) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nn) return;
-  const int nc = cc[i];
+  int64_t b = i;  // chain bottom
+  int len = 1;
+#ifndef WN_EXP_NOCHAIN
+  while (cc[b] == 1) {
+    b = cb[b];
+    ++len;
+  }
+#endif
+  tdepth[i] = depth[b];
+  const int nc = cc[b];
   if (nc == 0) {
     topo[i] = 0;
-    smask[i] = 0;
+    smask[i] = len << 8;
     return;
   }
-  const int c0 = cb[i];
+  const int c0 = cb[b];
   int single = 0;  // bit k: child k is a one-point leaf
   for (int c = c0; c < c0 + nc; ++c) single |= ((cc[c] == 0) && (pe[c] - pb[c] == 1)) << (c - c0);
   topo[i] = (c0 << 4) | (nc - 1);
-  smask[i] = single;
+  smask[i] = single | (len << 8);
 }
 
 __global__ void level_pe(int64_t i0, int64_t i1, int64_t n, const int32_t* __restrict__ parent,
@@ -621,6 +637,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   WN_TRY(dalloc(&t->parent, nn, s));
   WN_TRY(dalloc(&t->topo, nn, s));
   WN_TRY(dalloc(&t->smask, nn, s));
+  WN_TRY(dalloc(&t->tdepth, nn, s));
   WN_TRY(dalloc(&t->centroid, nn, s));
   WN_TRY(dalloc(&t->leaf_of, n, s));
   WN_TRY(dalloc(&t->sums, 8 * (size_t)nn, s));
@@ -643,7 +660,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
       int64_t i0 = t->level_off[l], i1 = t->level_off[l + 1];
       level_pe<<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, s>>>(i0, i1, n, t->parent, t->pb, t->pe);
     }
-    topo_codes<<<g, 256, 0, s>>>(nn, t->cb, t->cc, t->pb, t->pe, t->topo, t->smask);
+    topo_codes<<<g, 256, 0, s>>>(nn, t->cb, t->cc, t->pb, t->pe, t->depth, t->topo, t->smask, t->tdepth);
   }
   cudaFreeAsync(loff, s);
   cudaFreeAsync(cnt, s);
@@ -665,7 +682,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 
 void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->qorder, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
-                  t->topo, t->smask, t->mom_loff, t->mom_pre, t->mom_tile, t->centroid, t->sums, t->set[0].rec, t->set[1].rec, t->set[0].ext,
+                  t->topo, t->smask, t->tdepth, t->mom_loff, t->mom_pre, t->mom_tile, t->centroid, t->sums, t->set[0].rec, t->set[1].rec, t->set[0].ext,
                   t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
                   t->qbuf, t->qbuf_order, t->tvb, t->tu};
   // stream-ordered frees on the legacy stream: no device-wide synchronization, memory returns to the pool

@@ -66,7 +66,8 @@ struct wn_tree_s {
   int32_t* parent = nullptr;    // −1 for the root
   int32_t* leaf_of = nullptr;   // sorted point → its leaf node
   int32_t* topo = nullptr;      // per node traversal code (see NodeSet)
-  int32_t* smask = nullptr;     // per node: bit k set iff child k is a one-point leaf
+  int32_t* smask = nullptr;     // per node: bit k set iff child k is a one-point leaf; bits 8..12: chain length
+  int32_t* tdepth = nullptr;    // per node: depth whose (c·edge)² is its threshold (its chain's bottom)
   float4* centroid = nullptr;   // unweighted centroid per node (Σ|ν| = 0 fallback)
   double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
   int mom_cut = 0;              // moment builds: levels < mom_cut run in one block
