@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
                 if (COUNT && lm) {
                   ++nnear;
                   nlive += lv;
+                  ntest += (__float_as_int(L.w) >> 13) & 1;  // a node whose children are all points
                 }
               }
             }

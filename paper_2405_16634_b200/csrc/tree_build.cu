@@ -448,6 +448,17 @@ __global__ void topo_codes(int64_t nn, const int32_t* __restrict__ cb, const int
   const int c0 = cb[b];
   int single = 0;  // bit k: child k is a one-point leaf
   for (int c = c0; c < c0 + nc; ++c) single |= ((cc[c] == 0) && (pe[c] - pb[c] == 1)) << (c - c0);
+#ifndef WN_EXP_NOPSEUDO
+  if (single == (1 << nc) - 1) {
+    // every child is a one-point leaf, whose term is exactly its point's direct term (rep = the point,
+    // ν_B = ν_j, lo = 0): opening the node = a direct sum over its points, like a multi-point leaf —
+    // no child group to push and pop.  Bit 13 tells the counting traversal to count one node test per
+    // point, as Alg. 4 tests each child.
+    topo[i] = 0;
+    smask[i] = single | (len << 8) | (1 << 13);
+    return;
+  }
+#endif
   topo[i] = (c0 << 4) | (nc - 1);
   smask[i] = single | (len << 8);
 }
