@@ -433,6 +433,7 @@ wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, fl
   }
   if (a) m.a_sorted = dim == 3 ? it.s : (const float*)it.tmp;
   m.write_W = W != nullptr;
+  m.all_nodes = true;  // diagnostic export: every node's representative
   WN_TRY(build_moments(t, m, s));
   const size_t NN = t->nn;
   const size_t pitch = kRec * sizeof(float4);

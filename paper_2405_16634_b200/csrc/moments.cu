@@ -463,11 +463,12 @@ __global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __
 
 template <int KIND, int ORD>
 __global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int64_t nn, const double* __restrict__ Eh,
-                                                 const float* __restrict__ El) {
+                                                 const float* __restrict__ El, const int32_t* __restrict__ list) {
   using Lay = PreLayout<KIND, ORD>;
   constexpr int NC = Lay::NC;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nn) return;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nn) return;
+  const int64_t i = list ? (int64_t)list[k] : k;  // list: only the nodes a traversal can visit
   const int j0 = tv.pb[i], j1 = tv.pe[i];
   double d[NC];
   const float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -559,7 +560,11 @@ void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
     mom_tile_scan<Lay::NC><<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
   }
   mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, nt > 1 ? off : nullptr, Eh, El);
-  mom_nodes<KIND, ORD><<<(unsigned)((t->nn + 255) / 256), 256, 0, s>>>(tv, m, t->nn, Eh, El);
+  // per-iteration builds: only the nodes a traversal can read (chain interiors and the children of
+  // pseudo-leaves are never visited); the diagnostic export (write_W) builds every node
+  const bool all = m.all_nodes || m.write_W || !t->mom_live;
+  const int64_t cnt = all ? t->nn : t->mom_nlive;
+  mom_nodes<KIND, ORD><<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(tv, m, cnt, Eh, El, all ? nullptr : t->mom_live);
 }
 
 template <int KIND>

@@ -463,6 +463,23 @@ __global__ void topo_codes(int64_t nn, const int32_t* __restrict__ cb, const int
   smask[i] = single | (len << 8);
 }
 
+// the nodes a traversal can visit: the root and every child group referenced by an internal code
+__global__ void mark_visited(int64_t nn, const int32_t* __restrict__ topo, uint32_t* __restrict__ vis) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  if (i == 0) vis[0] = 1;
+  const int code = topo[i];
+  if (code != 0) {
+    const int c0 = code >> 4, nc = (code & 7) + 1;
+    for (int c = c0; c < c0 + nc; ++c) vis[c] = 1;
+  }
+}
+__global__ void compact_visited(int64_t nn, const uint32_t* __restrict__ vis, const uint32_t* __restrict__ pos,
+                                int32_t* __restrict__ list) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nn && vis[i]) list[pos[i]] = (int32_t)i;
+}
+
 __global__ void level_pe(int64_t i0, int64_t i1, int64_t n, const int32_t* __restrict__ parent,
                          const int32_t* __restrict__ pb, int32_t* __restrict__ pe) {
   int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -673,6 +690,24 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
     }
     topo_codes<<<g, 256, 0, s>>>(nn, t->cb, t->cc, t->pb, t->pe, t->depth, t->topo, t->smask, t->tdepth);
   }
+  {  // the visited nodes, compacted in BFS order (per-iteration moment builds skip the rest)
+    uint32_t *vis = nullptr, *pos = nullptr;
+    WN_TRY(dalloc(&vis, nn + 1, s));
+    WN_TRY(dalloc(&pos, nn + 1, s));
+    WN_CUDA(cudaMemsetAsync(vis, 0, (nn + 1) * sizeof(uint32_t), s));
+    const unsigned g = (unsigned)((nn + 255) / 256);
+    mark_visited<<<g, 256, 0, s>>>(nn, t->topo, vis);
+    WN_TRY(scan_excl(vis, pos, nn, pos + nn, s));
+    uint32_t nlive = 0;
+    WN_CUDA(cudaMemcpyAsync(&nlive, pos + nn, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaStreamSynchronize(s));
+    t->mom_nlive = nlive;
+    WN_TRY(dalloc(&t->mom_live, std::max<int64_t>(nlive, 1), s));
+    compact_visited<<<g, 256, 0, s>>>(nn, vis, pos, t->mom_live);
+    cudaFreeAsync(vis, s);
+    cudaFreeAsync(pos, s);
+    count_launches(5);
+  }
   cudaFreeAsync(loff, s);
   cudaFreeAsync(cnt, s);
   cudaFreeAsync(offs, s);
@@ -693,7 +728,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 
 void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->qorder, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
-                  t->topo, t->smask, t->tdepth, t->mom_loff, t->mom_pre, t->mom_tile, t->centroid, t->sums, t->set[0].rec, t->set[1].rec, t->set[0].ext,
+                  t->topo, t->smask, t->tdepth, t->mom_live, t->mom_loff, t->mom_pre, t->mom_tile, t->centroid, t->sums, t->set[0].rec, t->set[1].rec, t->set[0].ext,
                   t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
                   t->qbuf, t->qbuf_order, t->tvb, t->tu};
   // stream-ordered frees on the legacy stream: no device-wide synchronization, memory returns to the pool

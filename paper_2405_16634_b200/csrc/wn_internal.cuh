@@ -68,6 +68,8 @@ struct wn_tree_s {
   int32_t* topo = nullptr;      // per node traversal code (see NodeSet)
   int32_t* smask = nullptr;     // per node: bit k set iff child k is a one-point leaf; bits 8..12: chain length
   int32_t* tdepth = nullptr;    // per node: depth whose (c·edge)² is its threshold (its chain's bottom)
+  int32_t* mom_live = nullptr;  // the nodes a traversal can visit (root + the child groups of internal codes)
+  int64_t mom_nlive = 0;
   float4* centroid = nullptr;   // unweighted centroid per node (Σ|ν| = 0 fallback)
   double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
   int mom_cut = 0;              // moment builds: levels < mom_cut run in one block
@@ -139,6 +141,7 @@ struct MomentArgs {
   int32_t* leaf_of_out = nullptr;   // ATTR_UNIT: writes the leaf node of every sorted point
   bool write_W = false;             // also store each node's Σ|ν| in tree sums[8·i] (wn_moments export)
   bool order1 = false;              // also the first moments (out.ext), row f2
+  bool all_nodes = false;           // every node (wn_moments export), not only the visitable ones
 };
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s);
 wn_status plan_moments(wn_tree_s* t, cudaStream_t s);  // once per tree, after the topology
