@@ -126,6 +126,8 @@ static TravArgs base_args(const wn_tree_s* t, float w2) {
   a.stack_depth = stack_depth(t);
   a.root_single = t->n == 1;
   a.qorder = t->qorder;
+  a.nnodes = t->nn;
+  a.npts = t->n;
   return a;
 }
 

@@ -469,6 +469,7 @@ __global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int6
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nn) return;
   const int64_t i = list ? (int64_t)list[k] : k;  // list: only the nodes a traversal can visit
+  WN_DCHECK(i >= 0 && i < (list ? (int64_t)1 << 31 : nn), "moment node index");
   const int j0 = tv.pb[i], j1 = tv.pe[i];
   double d[NC];
   const float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int6
     m.out.rec[kRec * i + 1] = make_float4((float)v0, (float)v1, (float)v2, __int_as_float(tv.topo[i]));
     return;
   } else {
+    WN_DCHECK(j0 >= 0 && j0 < j1, "moment point range");
     const double2* a = reinterpret_cast<const double2*>(Eh + Lay::EH * (int64_t)j0);
     const double2* b = reinterpret_cast<const double2*>(Eh + Lay::EH * (int64_t)j1);
     double ah[Lay::EH], bh[Lay::EH];

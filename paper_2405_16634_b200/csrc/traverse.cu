@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
   const int64_t kq = a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;  // schedule position
   const bool valid = kq < a.q_end;
   const int64_t q = (valid && a.qorder) ? (int64_t)a.qorder[kq] : kq;             // query index
+  WN_DCHECK(!valid || (q >= 0 && (a.npts == 0 || a.queries != a.pts || q < a.npts)), "query index");
   const float4 xq = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
   const uint32_t active = __ballot_sync(FULL, valid);
   const float4* __restrict__ G = a.nodes.rec;             // geometry: R (+0), L (+2)
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
       {
         for (int k = 0; k < ncc; ++k) {
           const int node = cb + k;
+          WN_DCHECK(node >= 0 && node < a.nnodes, "node index");
           const float4* rp = rec_at(G, node);
           const float4 R = __ldg(rp);
           const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
@@ -191,11 +193,13 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
           if (open) {
             const int topo = __float_as_int(V.w);
             if (topo != 0) {
+              WN_DCHECK(sp < a.stack_depth, "traversal stack");
               stk[sp] = make_int2(topo, (int)open);  // every lane writes the same word: no divergence
               ++sp;
             } else {  // multi-point leaf (depth D): direct sum for the lanes that opened it
               const bool lm = (open >> lane) & 1u;
               const int j1 = a.nrange_pe[node];
+              WN_DCHECK(a.nrange_pb[node] >= 0 && j1 <= a.npts && a.nrange_pb[node] < j1, "leaf point range");
               for (int j = a.nrange_pb[node]; j < j1; ++j) {
                 const float4 P = __ldg(a.pts + j);
                 float4 Vj;
@@ -295,6 +299,7 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
       double b = 0.0;
       for (int k = 0; k < kTravBlock / 32; ++k) b += red[k];
       const int64_t ib = (a.q_begin / kTravBlock) + blockIdx.x;
+      WN_DCHECK(ib < (a.npts + kTravBlock - 1) / kTravBlock || a.queries != a.pts, "partial slot");
       if (a.world) {
         for (int r = 0; r < a.world; ++r) a.peer_part[r][ib] = b;
       } else {

@@ -11,6 +11,22 @@
 
 namespace wn {
 
+// WN_DEBUG builds (tools/build_variants.py "debug") trap on any out-of-range index the kernels compute —
+// the bounds checks stand in for compute-sanitizer, which this GPU pool does not allow
+#ifdef WN_DEBUG
+#define WN_DCHECK(cond, what)                                                                   \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("libwn WN_DEBUG check failed: %s (%s:%d)\n", what, __FILE__, __LINE__);           \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define WN_DCHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
 constexpr int kMaxDepth = 21;
 constexpr float kInv4Pi = 0.0795774715459476679f;  // 1/(4π)
 
@@ -181,6 +197,7 @@ struct TravArgs {
   int stack_depth = 128;
   int root_single = 0;              // 1 iff the root is a one-point leaf (n = 1)
   int order1 = 0;                   // first-order far field (nodes.ext), row f2
+  int64_t nnodes = 0, npts = 0;     // sizes (WN_DEBUG bounds checks)
   int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
   int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order
   // peer-memory exchange (multi-GPU, fused): the epilogue stores its row / block partial into every rank's

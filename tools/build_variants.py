@@ -4,6 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_16634_b200 import build as b
 VARIANTS = {
     "base": [],
+    "debug": ["WN_DEBUG"],  # device-side bounds checks (trap on violation)
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
