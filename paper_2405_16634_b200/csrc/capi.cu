@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -114,6 +115,16 @@ static wn_status ensure_scratch(wn_tree_s* t, cudaStream_t s) {
 
 static int stack_depth(const wn_tree_s* t) { return 8 * (t->depth_used + 2); }
 
+// several warps per query group below this many queries (too few query warps to fill the GPU otherwise);
+// decided on the whole cloud, so every rank of a sharded run picks the same kernel
+static int64_t split_max() {
+  static int64_t v = [] {
+    const char* e = getenv("WN_SPLIT_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)60000;  // measured: C2 (50k) −25 %, a 65k subset of C3 +10 %
+  }();
+  return v;
+}
+
 static TravArgs base_args(const wn_tree_s* t, float w2) {
   TravArgs a;
   a.pts = t->pts;
@@ -128,6 +139,7 @@ static TravArgs base_args(const wn_tree_s* t, float w2) {
   a.qorder = t->qorder;
   a.nnodes = t->nn;
   a.npts = t->n;
+  a.split = t->n <= split_max();
   return a;
 }
 
@@ -487,6 +499,7 @@ static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a,
     WN_TRY(hilbert_schedule(t->qbuf, m, t->qbuf_order, s));  // coherent warps for arbitrary queries (f1)
     ta.queries = t->qbuf;
     ta.q_end = m;
+    ta.split = m <= split_max();
     ta.out_map = nullptr;
     ta.qorder = t->qbuf_order;
   } else {

@@ -119,6 +119,211 @@ __device__ __forceinline__ const float4* rec_at(const float4* base, int node) {
   return reinterpret_cast<const float4*>(reinterpret_cast<const char*>(base) + ((uint32_t)node << 6));
 }
 
+struct Work {  // algorithmic work of one query (counting variant)
+  int test = 0, far = 0, near = 0, live = 0;
+};
+
+// Visit `node` for the lanes in `mine`: its term (far lanes past the cutoff) and, for the lanes that
+// open a leaf-coded node (a multi-point leaf or a pseudo-leaf), the direct sum over its points.
+// Returns the ballot of the lanes that open it; *topo_out = its traversal code (0: leaf-coded).
+template <int OP, bool COUNT, bool FROZEN, int ORD>
+__device__ __forceinline__ uint32_t trav_visit(const TravArgs& a, int node, bool mine, const float4& xq, Acc<OP>& acc,
+                                               Work& wk, int& topo_out) {
+  const int lane = threadIdx.x & 31;
+  const float4* __restrict__ G = a.nodes.rec;           // geometry: R (+0), L (+2)
+  const float4* __restrict__ Vr = FROZEN ? a.attr : G;  // attributes: V (+1)
+  const float w2 = a.w2;
+  WN_DCHECK(node >= 0 && node < a.nnodes, "node index");
+  const float4* rp = rec_at(G, node);
+  const float4 R = __ldg(rp);
+  const float4 V = FROZEN ? __ldg(rec_at(Vr, node) + 1) : __ldg(rp + 1);
+  const float4 L = __ldg(rp + 2);
+  // d = (hi − x_q) + lo: decisions and value on the same fp32 offset (R-prec)
+  const float ex = __fadd_rn(__fsub_rn(R.x, xq.x), L.x), ey = __fadd_rn(__fsub_rn(R.y, xq.y), L.y),
+              ez = __fadd_rn(__fsub_rn(R.z, xq.z), L.z);
+  const float d2 = dist2(ex, ey, ez);
+  const bool far = d2 > R.w;
+  const bool live = mine && far && !(d2 < w2);
+  if (ORD == 1) {
+    const float4 X0 = __ldg(a.nodes.ext + 2 * node);
+    const float4 X1 = OP == OP_AT ? X0 : __ldg(a.nodes.ext + 2 * node + 1);
+    acc.term1(live, ex, ey, ez, d2, V, X0, X1);
+  } else {
+    acc.term(live, ex, ey, ez, d2, V);
+  }
+  if (COUNT && mine) {
+    // a collapsed chain (tree_build.cu:topo_codes): Alg. 4 tests its levels from the top until one
+    // is far — level k's threshold is the bottom's × 4^(len−1−k), exactly (powers of two)
+    const int len = (__float_as_int(L.w) >> 8) & 31;
+    int tests = 1;
+    if (len > 1) {
+      tests = len;
+      for (int kk = 0; kk < len; ++kk)
+        if (d2 > ldexpf(R.w, 2 * (len - 1 - kk))) {
+          tests = kk + 1;
+          break;
+        }
+    }
+    wk.test += tests;
+    wk.far += far;
+    wk.live += live;
+  }
+  const uint32_t open = __ballot_sync(FULL, mine && !far);
+  const int topo = __float_as_int(V.w);
+  topo_out = topo;
+  if (open && topo == 0) {  // leaf-coded: direct sum for the lanes that opened it
+    const bool lm = (open >> lane) & 1u;
+    const int j1 = a.nrange_pe[node];
+    WN_DCHECK(a.nrange_pb[node] >= 0 && j1 <= a.npts && a.nrange_pb[node] < j1, "leaf point range");
+    for (int j = a.nrange_pb[node]; j < j1; ++j) {
+      const float4 P = __ldg(a.pts + j);
+      float4 Vj;
+      if (OP == OP_AT) Vj = make_float4(__ldg(a.scal + j), 0.f, 0.f, 0.f);
+      else Vj = __ldg(a.vec + j);
+      const float px = __fsub_rn(P.x, xq.x), py = __fsub_rn(P.y, xq.y), pz = __fsub_rn(P.z, xq.z);
+      const float p2 = dist2(px, py, pz);
+      const bool lv = lm && !(p2 < w2);
+      acc.term(lv, px, py, pz, p2, Vj);
+      if (COUNT && lm) {
+        ++wk.near;
+        wk.live += lv;
+        wk.test += (__float_as_int(L.w) >> 13) & 1;  // a node whose children are all points
+      }
+    }
+  }
+  return open;
+}
+
+// Pop child groups (code, lane mask) off this warp's stack until it is empty; every child of a popped
+// group is visited, the lanes that open an internal node push its child group.
+template <int OP, bool COUNT, bool FROZEN, int ORD>
+__device__ __forceinline__ void trav_loop(const TravArgs& a, int2* stk, int sp, const float4& xq, Acc<OP>& acc,
+                                          Work& wk) {
+  const int lane = threadIdx.x & 31;
+  while (sp > 0) {
+    --sp;
+    const int2 e = stk[sp];
+    __syncwarp();
+    const int code = e.x;
+    const int cb = code >> 4, ncc = (code & 7) + 1;
+    const bool mine = ((uint32_t)e.y >> lane) & 1u;
+    for (int k = 0; k < ncc; ++k) {
+      int topo;
+      const uint32_t open = trav_visit<OP, COUNT, FROZEN, ORD>(a, cb + k, mine, xq, acc, wk, topo);
+      if (open && topo != 0) {
+        WN_DCHECK(sp < a.stack_depth, "traversal stack");
+        stk[sp] = make_int2(topo, (int)open);  // every lane writes the same word: no divergence
+        ++sp;
+      }
+    }
+    acc.flush();  // (no trailing __syncwarp: every lane writes the same stack words and reads its own)
+  }
+}
+
+// outputs of one query (fused solver epilogues), its work counts, and the block's Σ partial (NW warps)
+template <int OP, int EPI, bool COUNT, int NW>
+__device__ __forceinline__ void trav_epilogue(const TravArgs& a, bool valid, int64_t q, const Acc<OP>& acc,
+                                              const Work& wk, double* red, int64_t ib) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double part = 0.0;
+  if (valid) {
+    const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
+    if (OP == OP_A) {
+      const double val = acc.d * 0.0795774715459476679;  // Σ / (4π)
+      if (EPI == EPI_PLAIN && a.out_f) a.out_f[oq] = (float)(val * (double)a.scale_out);
+      if (EPI == EPI_S) {
+        const double sv = 0.5 - val;
+        if (a.world) {  // peer-memory exchange: this row into every rank's replica (NVLink stores)
+          for (int r = 0; r < a.world; ++r) a.peer_f[r][q] = (float)sv;
+        } else {
+          a.out_f[q] = (float)sv;
+        }
+        part = sv * sv;
+      }
+      if (EPI == EPI_SQ) part = val * val;
+    } else {
+      const float vx = acc.x * kInv4Pi, vy = acc.y * kInv4Pi, vz = acc.z * kInv4Pi;
+      if (EPI == EPI_PLAIN && a.out_v3) {
+        a.out_v3[3 * oq + 0] = vx * a.scale_out;
+        a.out_v3[3 * oq + 1] = vy * a.scale_out;
+        a.out_v3[3 * oq + 2] = vz * a.scale_out;
+      }
+      if (EPI == EPI_R) {
+        const float4 o = make_float4(vx, vy, vz, 0.f);
+        if (a.world) {
+          for (int r = 0; r < a.world; ++r) a.peer_v4[r][q] = o;
+        } else {
+          a.out_v4[q] = o;
+        }
+        part = (double)vx * vx + (double)vy * vy + (double)vz * vz;
+      }
+      if (EPI == EPI_RESCALE) {  // μ_i = μ̂_i |μ'_i| / |μ̂_i|, μ'_i kept if |μ̂_i| = 0 (Alg. 3)
+        const float4 m = a.mup[q];
+        const double hm = sqrt((double)vx * vx + (double)vy * vy + (double)vz * vz);
+        const double mm = sqrt((double)m.x * m.x + (double)m.y * m.y + (double)m.z * m.z);
+        float4 o = m;
+        if (hm > 0.0) {
+          const double f = mm / hm;
+          o = make_float4((float)(vx * f), (float)(vy * f), (float)(vz * f), 0.f);
+        }
+        if (a.world) {
+          for (int r = 0; r < a.world; ++r) a.peer_v4[r][q] = o;
+        } else {
+          a.out_v4[q] = o;
+        }
+      }
+    }
+  }
+  if (COUNT) {  // algorithmic work: node tests, representative terms, leaf-point terms, live terms (r ≥ w)
+    if (a.qcounts && valid) {
+      const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
+      a.qcounts[4 * oq + 0] = wk.test;
+      a.qcounts[4 * oq + 1] = wk.far;
+      a.qcounts[4 * oq + 2] = wk.near;
+      a.qcounts[4 * oq + 3] = wk.live;
+    }
+    if (a.work) {
+      unsigned long long c[4] = {(unsigned long long)wk.test, (unsigned long long)wk.far,
+                                 (unsigned long long)wk.near, (unsigned long long)wk.live};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c[k] += __shfl_xor_sync(FULL, c[k], o);
+        if (lane == 0) atomicAdd((unsigned long long*)a.work + k, c[k]);
+      }
+    }
+  }
+  if (EPI == EPI_S || EPI == EPI_SQ || EPI == EPI_R) {
+    part = warp_sum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int k = 0; k < NW; ++k) b += red[k];
+      WN_DCHECK(ib < (a.npts + kTravBlock - 1) / kTravBlock || a.queries != a.pts, "partial slot");
+      if (a.world) {
+        for (int r = 0; r < a.world; ++r) a.peer_part[r][ib] = b;
+      } else {
+        a.partial[ib] = b;
+      }
+    }
+  }
+  if (a.world) {  // signal: every thread's remote stores, then one count per block, the last block tells every rank
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int prev = atomicAdd(a.done, 1u);
+      if (prev == gridDim.x - 1) {
+        __threadfence_system();
+        *a.done = 0u;  // ready for the next exchange (stream-ordered)
+        for (int r = 0; r < a.world; ++r) atomicAdd_system(a.peer_sig[r], 1ull);
+      }
+    }
+  }
+}
+
+// one warp = 32 consecutive queries of the schedule, traversing from the root (the hot kernel: its
+// loop is written out here — the same steps as trav_visit / trav_loop, which the compiler schedules worse)
 template <int OP, int EPI, bool COUNT, bool FROZEN, int ORD>
 #ifndef WN_EXP_LBMIN
 #define WN_EXP_LBMIN 6  // 6 resident blocks (48 warps) per SM: ≤ 42 registers, no spills; measured best
@@ -321,21 +526,134 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
   }
 }
 
+// Small clouds (few query warps for the GPU): kSplit warps share each group of 32 queries.  All of them
+// test the root; the root's children are split between them; the child groups of the children the lanes
+// open are dealt round-robin; each warp traverses its share; the partial accumulators are added in warp
+// order (a fixed order: deterministic), and one warp per group runs the epilogue.
+constexpr int kSplit = 4;
+constexpr int kSplitWarps = kSplit * (kTravBlock / 32);
+
+template <int OP, int EPI, bool COUNT, bool FROZEN, int ORD>
+__global__ void __launch_bounds__(kSplitWarps * 32) trav_split_kernel(const TravArgs a) {
+  constexpr int NG = kTravBlock / 32;  // query groups per block
+  extern __shared__ int2 stk_all[];
+  __shared__ double red[kSplitWarps];
+  __shared__ uint32_t sm_open[NG][8];
+  __shared__ int sm_topo[NG][8];
+  __shared__ float sm_v[kSplitWarps][3][32];
+  __shared__ double sm_d[kSplitWarps][32];
+  __shared__ int sm_w[kSplitWarps][4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = warp / kSplit, sub = warp % kSplit;
+  int2* stk = stk_all + warp * a.stack_depth;
+  const int64_t kq = a.q_begin + (int64_t)blockIdx.x * kTravBlock + g * 32 + lane;
+  const bool valid = kq < a.q_end;
+  const int64_t q = (valid && a.qorder) ? (int64_t)a.qorder[kq] : kq;
+  WN_DCHECK(!valid || (q >= 0 && (a.npts == 0 || a.queries != a.pts || q < a.npts)), "query index");
+  const float4 xq = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t active = __ballot_sync(FULL, valid);
+  if (sub == 0 && lane < 8) sm_open[g][lane] = 0u;
+  Acc<OP> acc;
+  Work wk;
+  uint32_t ropen = 0;
+  int rtopo = 0;
+  if (active) {  // the root: every warp of the group decides it, warp 0 keeps its term
+    Acc<OP> scratch;
+    Work wscratch;
+    ropen = sub == 0 ? trav_visit<OP, COUNT, FROZEN, ORD>(a, 0, valid, xq, acc, wk, rtopo)
+                     : trav_visit<OP, COUNT, FROZEN, ORD>(a, 0, valid, xq, scratch, wscratch, rtopo);
+  }
+  __syncthreads();
+  if (ropen && rtopo != 0) {  // the root's children, child k by warp k mod kSplit
+    const int c0 = rtopo >> 4, ncc = (rtopo & 7) + 1;
+    for (int k = sub; k < ncc; k += kSplit) {
+      int ctopo;
+      const uint32_t copen =
+          trav_visit<OP, COUNT, FROZEN, ORD>(a, c0 + k, (ropen >> lane) & 1u, xq, acc, wk, ctopo);
+      if (lane == 0) {
+        sm_open[g][k] = ctopo != 0 ? copen : 0u;
+        sm_topo[g][k] = ctopo;
+      }
+    }
+  }
+  __syncthreads();
+  if (ropen && rtopo != 0) {  // the opened children's groups, dealt round-robin, then this warp's share
+    const int ncc = (rtopo & 7) + 1;
+    int sp = 0, t = 0;
+    for (int k = 0; k < ncc; ++k) {
+      const uint32_t m = sm_open[g][k];
+      if (!m) continue;
+      const int tp = sm_topo[g][k];
+      const int gc0 = tp >> 4, gn = (tp & 7) + 1;
+      for (int j = 0; j < gn; ++j, ++t)
+        if (t % kSplit == sub) {
+          if (lane == 0) stk[sp] = make_int2((gc0 + j) << 4, (int)m);  // a group of one node
+          ++sp;
+        }
+    }
+    __syncwarp();
+    trav_loop<OP, COUNT, FROZEN, ORD>(a, stk, sp, xq, acc, wk);
+  }
+  acc.flush();
+  // the group's kSplit partial sums, added in warp order
+  if (OP == OP_A) {
+    sm_d[warp][lane] = acc.d;
+  } else {
+    sm_v[warp][0][lane] = acc.x;
+    sm_v[warp][1][lane] = acc.y;
+    sm_v[warp][2][lane] = acc.z;
+  }
+  if (COUNT) {
+    sm_w[warp][0][lane] = wk.test;
+    sm_w[warp][1][lane] = wk.far;
+    sm_w[warp][2][lane] = wk.near;
+    sm_w[warp][3][lane] = wk.live;
+  }
+  __syncthreads();
+  if (sub == 0) {
+    for (int s2 = 1; s2 < kSplit; ++s2) {
+      const int w2 = warp + s2;
+      if (OP == OP_A) {
+        acc.d += sm_d[w2][lane];
+      } else {
+        acc.x += sm_v[w2][0][lane];
+        acc.y += sm_v[w2][1][lane];
+        acc.z += sm_v[w2][2][lane];
+      }
+      if (COUNT) {
+        wk.test += sm_w[w2][0][lane];
+        wk.far += sm_w[w2][1][lane];
+        wk.near += sm_w[w2][2][lane];
+        wk.live += sm_w[w2][3][lane];
+      }
+    }
+  } else {
+    wk = Work();
+  }
+  trav_epilogue<OP, EPI, COUNT, kSplitWarps>(a, valid && sub == 0, q, acc, wk, red,
+                                             (a.q_begin / kTravBlock) + blockIdx.x);
+}
+
+template <int OP, int EPI, bool C, bool F, int O>
+void launch_one(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
+  if (a.split) trav_split_kernel<OP, EPI, C, F, O><<<grid, kSplitWarps * 32, smem * kSplit, s>>>(a);
+  else trav_kernel<OP, EPI, C, F, O><<<grid, kTravBlock, smem, s>>>(a);
+}
+
 template <int OP, int EPI>
 void launch(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
   const bool cnt = a.work || a.qcounts;
   if (OP == OP_A && EPI == EPI_SQ && a.attr) {  // frozen geometry (transpose-mode A(r)); order 0 only
-    if (cnt) trav_kernel<OP, EPI, true, true, 0><<<grid, kTravBlock, smem, s>>>(a);
-    else trav_kernel<OP, EPI, false, true, 0><<<grid, kTravBlock, smem, s>>>(a);
+    if (cnt) launch_one<OP, EPI, true, true, 0>(a, s, grid, smem);
+    else launch_one<OP, EPI, false, true, 0>(a, s, grid, smem);
     return;
   }
   if (a.order1) {
-    if (cnt) trav_kernel<OP, EPI, true, false, 1><<<grid, kTravBlock, smem, s>>>(a);
-    else trav_kernel<OP, EPI, false, false, 1><<<grid, kTravBlock, smem, s>>>(a);
+    if (cnt) launch_one<OP, EPI, true, false, 1>(a, s, grid, smem);
+    else launch_one<OP, EPI, false, false, 1>(a, s, grid, smem);
     return;
   }
-  if (cnt) trav_kernel<OP, EPI, true, false, 0><<<grid, kTravBlock, smem, s>>>(a);
-  else trav_kernel<OP, EPI, false, false, 0><<<grid, kTravBlock, smem, s>>>(a);
+  if (cnt) launch_one<OP, EPI, true, false, 0>(a, s, grid, smem);
+  else launch_one<OP, EPI, false, false, 0>(a, s, grid, smem);
 }
 
 }  // namespace

@@ -197,6 +197,7 @@ struct TravArgs {
   int stack_depth = 128;
   int root_single = 0;              // 1 iff the root is a one-point leaf (n = 1)
   int order1 = 0;                   // first-order far field (nodes.ext), row f2
+  int split = 0;                    // small clouds: several warps per query group (traverse.cu)
   int64_t nnodes = 0, npts = 0;     // sizes (WN_DEBUG bounds checks)
   int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
   int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order

@@ -128,3 +128,25 @@ def test_node_count_limit(wn):
     p = np.repeat(c, 2, axis=0)
     with pytest.raises(wn.WnError, match="ARG"):
         wn.wn_build_tree(_cuda(p), 21)
+
+
+def test_split_and_single_warp_kernels_agree(wn):
+    # a 70k cloud's own points take the one-warp-per-32-queries kernel; 50k of them passed as arbitrary
+    # queries take the split kernel (several warps per query group, below 60k queries): the same
+    # quantities, identical per-query work counts, values within the parity tolerance of each other
+    p = synth.config("C3")["points"][:70000]
+    n = len(p)
+    rng = np.random.default_rng(44)
+    mu = (rng.standard_normal((n, 3)) * 4 * np.pi / n).astype(np.float32)
+    t = wn.wn_build_tree(_cuda(p))
+    idx = rng.choice(n, 50000, replace=False)
+    w = float(np.float32(0.004))
+    for op, ev in ((0, wn.wn_eval), (2, wn.wn_eval_grad)):
+        full = ev(t, _cuda(mu), w).cpu().numpy()[idx]
+        part = ev(t, _cuda(mu), w, q=_cuda(p[idx])).cpu().numpy()
+        cf = wn.wn_query_work(t, _cuda(mu), w, op=op).cpu().numpy()[idx]
+        cp = wn.wn_query_work(t, _cuda(mu), w, op=op, q=_cuda(p[idx])).cpu().numpy()
+        np.testing.assert_array_equal(cp, cf)
+        ref = full.reshape(len(idx), -1)
+        err = np.linalg.norm(part.reshape(len(idx), -1) - ref, axis=1)
+        assert np.all(err <= 1e-5 * np.linalg.norm(ref, axis=1) + 1e-6 * np.sqrt(np.mean(ref ** 2))), err.max()

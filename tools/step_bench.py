@@ -6,7 +6,8 @@ from paper_2405_16634_b200 import synth
 import paper_2405_16634_b200.wn as wn
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
-p = torch.from_numpy(synth.config(cfg)["points"]).cuda()
+nmax = int(sys.argv[2]) if len(sys.argv) > 2 else None  # optional: the first nmax points (a random subset)
+p = torch.from_numpy(synth.config(cfg)["points"][:nmax]).cuda()
 t = wn.wn_build_tree(p)
 mu = torch.zeros(len(p), 3, device="cuda")
 wn.wnnc_iterate(t, mu, iters=40, flags=wn.WN_FLAG_GRAPH)
