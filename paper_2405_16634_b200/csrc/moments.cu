@@ -215,7 +215,10 @@ __global__ void __launch_bounds__(kMomThreads, WN_EXP_MOM_LB) moments_range(Tree
 // First-order far field (ORD = 1): the prefix also carries sym(Σ ν_j x_jᵀ) (vector ν,
 // 6 terms) or Σ s_j x_j (scalar, 3), and each node stores its first moment about the representative,
 // sym M = sym(Σ ν_j x_jᵀ) − sym(ν_B x_Bᵀ) or D = Σ s_j x_j − s_B x_B, in NodeSet::ext.
-constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+#ifndef WN_EXP_SCANITEMS
+#define WN_EXP_SCANITEMS 8
+#endif
+constexpr int kScanThreads = 256, kScanItems = WN_EXP_SCANITEMS, kScanTile = kScanThreads * kScanItems;
 constexpr int kScanTopThreads = 256;
 
 // components per prefix entry; entry j (exclusive: points [0, j)) = hi[EH] fp64 (the NC sums, the count,
