@@ -59,12 +59,13 @@ def test_peer_arena_grows_with_n(wn):
     comm.close()
 
 
-@pytest.mark.parametrize("world", [2, 3, 8])
-def test_emulated_ranks_match_single_gpu(wn, world):
+@pytest.mark.parametrize("world,n", [(2, 30011), (3, 30011), (8, 30011), (3, 70001)])
+def test_emulated_ranks_match_single_gpu(wn, world, n):
     # W ranks of the peer-memory exchange emulated on this GPU (each rank's shard reads its own replica
     # and stores into all W replicas; signals / waits with world-W targets; ping-pong μ): every replica
-    # must hold the single-GPU trajectory bit for bit
-    p = torch.from_numpy(synth.config("C2")["points"][:30011]).cuda()
+    # must hold the single-GPU trajectory bit for bit — below 60k queries through the split traversal,
+    # above through the one-warp kernel
+    p = torch.from_numpy(synth.config("C2" if n <= 50000 else "C3")["points"][:n]).cuda()
     t = wn.wn_build_tree(p)
     ref = torch.zeros(len(p), 3, device="cuda")
     wn.wnnc_iterate(t, ref, iters=5, total_iters=40)
