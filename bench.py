@@ -245,6 +245,50 @@ def run_ours(args):
         te = (time.perf_counter() - t0) / args.steps
         e2e = {"value": ITERS / te, "unit": "iterations/s", "h2d_bytes_per_step": int(n * 12),
                "d2h_bytes_per_step": int(n * 12), "ms_per_step": 1e3 * te}
+    else:  # N ranks through the public API: every rank H2D-copies the points (replicated sources), builds
+        # the tree and runs the sharded solve; rank 0 reads the result back; time = max over ranks
+        pts_pin = torch.from_numpy(pts_h).pin_memory()
+        mu_host = torch.empty(n, 3, dtype=torch.float32).pin_memory()
+        pts_dev = torch.empty(n, 3, dtype=torch.float32, device=dev)
+        tes = []
+        for _ in range(args.steps + 1):
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pts_dev.copy_(pts_pin, non_blocking=True)
+            tree = wn.wn_build_tree(pts_dev)
+            mu = torch.zeros(n, 3, dtype=torch.float32, device=dev)
+            wn.wnnc_iterate(tree, mu, comm=comm, **params)
+            if rank == 0:
+                mu_host.copy_(mu, non_blocking=True)
+            torch.cuda.synchronize()
+            tes.append(time.perf_counter() - t0)
+            del tree
+        t = torch.tensor([sum(tes[1:]) / args.steps], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        te = float(t.item())
+        e2e = {"value": ITERS / te, "unit": "iterations/s", "h2d_bytes_per_step": int(world * n * 12),
+               "d2h_bytes_per_step": int(n * 12), "ms_per_step": 1e3 * te,
+               "note": "every rank copies the points (replicated sources); rank 0 reads mu back"}
+    # ---- exchange check (N > 1, untimed): the peer-memory solve must equal the NCCL solve bit for bit on
+    # every rank, and all ranks must hold the same result (both equal the single-GPU trajectory) ----
+    exchange_check = None
+    if world > 1:
+        outs = []
+        for extra in (0, wn.WN_FLAG_COMM_NCCL):
+            tree = wn.wn_build_tree(pts)
+            mu = torch.zeros(n, 3, dtype=torch.float32, device=dev)
+            wn.wnnc_iterate(tree, mu, comm=comm, **{**params, "flags": params["flags"] | extra})
+            outs.append(mu)
+            del tree
+        same = int(torch.equal(outs[0], outs[1]))
+        h = outs[0].view(torch.int32).to(torch.int64).sum().reshape(1)
+        hs = [torch.zeros_like(h) for _ in range(world)]
+        torch.distributed.all_gather(hs, h)
+        ok = torch.tensor([same], device=dev)
+        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+        exchange_check = {"peer_equals_nccl_on_all_ranks": bool(ok.item()),
+                          "ranks_identical": bool(all(int(x.item()) == int(hs[0].item()) for x in hs))}
 
     if rank != 0:
         return 0
@@ -290,6 +334,7 @@ def run_ours(args):
                                "note": "counted = live kernel evaluations (far + leaf) of the traversals; "
                                        "effective_dense = 4 N^2 per iteration (the O(N^2) sums replaced)"},
         "breakdown_ms_per_step": {k: v[0] / args.prof_steps for k, v in prof.items()},
+        **({"exchange_check": exchange_check} if exchange_check else {}),
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "treecode traversals (trav_kernel A/AT/G), %.0f launches/step, %.3f ms/step"
