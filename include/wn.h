@@ -203,6 +203,14 @@ wn_status wn_comm_destroy(wn_comm c);
    partials are identical for every world size).  Pure host arithmetic. */
 enum { WN_SHARD_ALIGN = 256 };
 wn_status wn_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
+/* The query schedule (diagnostic): qorder[N] (device) = sorted-point index at each schedule position —
+   the 3-D Hilbert order the traversals and the multi-GPU shards follow. */
+wn_status wn_tree_schedule(wn_tree t, int32_t* qorder, void* stream);
+/* The shards wnnc_iterate actually uses for `world` ranks (1..64) on this tree: bounds[world + 1] (host),
+   rank r owns schedule positions [bounds[r], bounds[r+1]), multiples of WN_SHARD_ALIGN, split by
+   estimated work (the node tests of the A traversal over the unit-weight geometry) so that non-uniform
+   clouds load the ranks evenly; wn_shard_range is the equal-count split.  Synchronizes `stream`. */
+wn_status wn_shard_plan(wn_tree t, int32_t world, int64_t* bounds, void* stream);
 
 #ifdef __cplusplus
 }

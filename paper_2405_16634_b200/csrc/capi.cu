@@ -146,6 +146,77 @@ static TravArgs base_args(const wn_tree_s* t, float w2) {
 static bool bad_width(float w) { return !(w > 0.f) || std::isnan(w); }
 static bool bad_theta(float c) { return !(c > 0.f) || std::isnan(c); }
 
+// per WN_SHARD_ALIGN block of the query schedule: its queries' node tests (from a counting traversal)
+__global__ void k_block_work(int64_t n, const int32_t* __restrict__ qorder, const int32_t* __restrict__ cnt,
+                             int64_t b0, int64_t b1, int64_t* __restrict__ bw) {
+  const int64_t b = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= b1) return;
+  int64_t w = 0;
+  const int64_t k1 = std::min<int64_t>(n, (b + 1) * WN_SHARD_ALIGN);
+  for (int64_t k = b * WN_SHARD_ALIGN; k < k1; ++k) w += cnt[4 * (int64_t)(qorder ? qorder[k] : k)];
+  bw[b] = w;
+}
+
+// Work-weighted query shards for `world` ranks: the per-block node tests of the A traversal
+// over the fixed unit-weight geometry (decisions do not depend on the width; the representatives of later
+// attributes move little) — counted by each rank over its equal-count share and summed over the ranks
+// (comm), or all here (emulated ranks) — then rank r starts at the first block where the running work
+// reaches r/world of the total.  Shards only decide which rank computes which blocks: every result is
+// unchanged.  Cached on the tree per world size; computed outside any graph capture.
+static wn_status plan_shards(wn_tree_s* t, int world, wn_comm comm, cudaStream_t s) {
+  ShardPlan& P = t->shard;
+  if (world <= 1 || world > kMaxShardRanks) {
+    P.world = 0;
+    return WN_OK;
+  }
+  if (P.world == world) return WN_OK;
+  IterScratch& it = t->it;
+  const int64_t n = t->n, nb = (n + WN_SHARD_ALIGN - 1) / WN_SHARD_ALIGN;
+  int64_t q0 = 0, q1 = n;
+  if (comm) wn_shard_range(n, comm_rank(comm), world, &q0, &q1);
+  int64_t* bw = nullptr;
+  WN_CUDA(cudaMallocAsync((void**)&bw, nb * sizeof(int64_t), s));
+  WN_CUDA(cudaMemsetAsync(bw, 0, nb * sizeof(int64_t), s));
+  TravArgs ca = base_args(t, 0.0f);
+  ca.op = OP_A;
+  ca.epi = EPI_PLAIN;
+  ca.nodes = t->set[1];
+  ca.vec = it.mu;  // (values unused: only the decisions are counted)
+  ca.q_begin = q0;
+  ca.q_end = q1;
+  ca.out_map = nullptr;
+  ca.qcounts = reinterpret_cast<int32_t*>(it.tmp);  // n × 4 int32, indexed by query
+  ca.nowork = true;
+  ca.prof_cls = WN_PROF_OTHER;
+  wn_status st = traverse(ca, s);
+  if (st == WN_OK && q1 > q0) {
+    const int64_t b0 = q0 / WN_SHARD_ALIGN, b1 = (q1 + WN_SHARD_ALIGN - 1) / WN_SHARD_ALIGN;
+    k_block_work<<<(unsigned)((b1 - b0 + 255) / 256), 256, 0, s>>>(n, t->qorder, ca.qcounts, b0, b1, bw);
+    count_launches(1);
+  }
+  if (st == WN_OK && comm) st = comm_allreduce_i64(comm, bw, nb, s);
+  std::vector<int64_t> h(nb);
+  if (st == WN_OK) {
+    cudaError_t e = cudaMemcpyAsync(h.data(), bw, nb * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = cuda_status(e, "shard plan");
+  }
+  cudaFreeAsync(bw, s);
+  if (st != WN_OK) return st;
+  int64_t total = 0;
+  for (int64_t v : h) total += v + 1;  // + 1: a block costs something even when empty of tests
+  P.b[0] = 0;
+  int64_t run = 0, blk = 0;
+  for (int r = 1; r < world; ++r) {
+    const int64_t target = (total * r) / world;  // (exact integer arithmetic: identical on every rank)
+    while (blk < nb && run + h[blk] + 1 <= target) run += h[blk++] + 1;
+    P.b[r] = std::min<int64_t>(n, blk * WN_SHARD_ALIGN);
+  }
+  P.b[world] = n;
+  P.world = world;
+  return WN_OK;
+}
+
 // route a traversal's outputs into every rank's replica (peer-memory exchange); none when P is null
 static void peer_route(TravArgs& ta, const PeerArena* P, float* const* f, float4* const* v4, int part_slot) {
   if (!P) return;
@@ -173,7 +244,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
   const bool transpose = p.adjoint_mode == WN_ADJ_TRANSPOSE;
   const PeerArena* P = nviews > 0 ? views[0] : nullptr;
   int64_t q0 = 0, q1 = t->n;
-  if (comm && !P) WN_TRY(comm_shard(comm, t->n, &q0, &q1));
+  if (comm && !P) shard_of(&t->shard, t->n, comm_rank(comm), comm_world(comm), &q0, &q1);
   const bool nccl = comm && !P;
   const int me = P ? P->rank : 0;
   float* sb = P ? P->s[me] : it.s;
@@ -195,7 +266,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     for (int v = 0; v < nviews; ++v) {
       const PeerArena& A = *views[v];
       TravArgs tv = ta;
-      wn_shard_range(t->n, A.rank, A.world, &tv.q_begin, &tv.q_end);
+      shard_of(&t->shard, t->n, A.rank, A.world, &tv.q_begin, &tv.q_end);
       if (in == S) tv.scal = A.s[A.rank];
       if (in == R) tv.vec = A.r[A.rank];
       if (in == MU0 || in == MU1) tv.vec = A.mu[in == MU1][A.rank];
@@ -237,7 +308,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
       a1.partial = part;
       a1.order1 = t->far_order;
       WN_TRY(run_traversal(a1, 0, cur ? MU1 : MU0, S));
-      if (nccl) WN_TRY(comm_allgather_f(comm, sb, 1, t->n, qord, stage, s));
+      if (nccl) WN_TRY(comm_allgather_f(comm, sb, 1, t->n, qord, stage, &t->shard, s));
     }
     // (2) r = A_wᵀ s  (+ Σ|r|² partials)
     if (transpose) {
@@ -260,7 +331,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
       a2.partial = part + stride;
       a2.order1 = t->far_order;
       WN_TRY(run_traversal(a2, 1, S, R));
-      if (nccl) WN_TRY(comm_allgather_f(comm, (float*)rb, 4, t->n, qord, stage, s));
+      if (nccl) WN_TRY(comm_allgather_f(comm, (float*)rb, 4, t->n, qord, stage, &t->shard, s));
     }
     // (3) Σ (A_w r)²  — gather: r's own representatives; transpose: μ's frozen geometry
     MomentArgs m3;
@@ -280,7 +351,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a3.partial = part + 2 * stride;
     a3.order1 = t->far_order;
     WN_TRY(run_traversal(a3, 2, R, NONE));
-    if (nccl) WN_TRY(comm_allgather_partials(comm, part, stride, t->n, s));
+    if (nccl) WN_TRY(comm_allgather_partials(comm, part, stride, t->n, &t->shard, s));
     // α = Σr² / Σ(Ar)²  (Alg. 2), fixed-order reduction of the partials
     // (the partial arrays' stride may exceed this cloud's block count: a peer arena sized for a larger N)
     alpha_step(part, trav_blocks(t->n), stride, (double)w, it.alpha, it.dstats + 5 * i, s);
@@ -305,7 +376,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a4.out_v4 = it.mu;
     a4.order1 = t->far_order;
     WN_TRY(run_traversal(a4, 0, NONE, cur ? MU0 : MU1));
-    if (nccl) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, s));
+    if (nccl) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, &t->shard, s));
   }
   return WN_OK;
 }
@@ -604,6 +675,7 @@ wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int3
     WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)p->iters, s));
     it.stats_cap = p->iters;
   }
+  WN_TRY(plan_shards(t, world, nullptr, s));
   PeerArena arenas[kMaxPeers];
   void* blocks[kMaxPeers] = {};
   wn_status st = emulated_arenas(world, t->n, arenas, blocks);
@@ -651,16 +723,23 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
   // multi-GPU exchange: peer-memory stores fused into the traversal epilogues (default), or NCCL
   const PeerArena* P = nullptr;
   if (comm && !(p->flags & WN_FLAG_COMM_NCCL)) WN_TRY(comm_peer_arena(comm, t->n, s, &P));
+  if (comm) WN_TRY(plan_shards(t, comm_world(comm), comm, s));
   float4* mu0 = P ? P->mu[0][P->rank] : t->it.mu;
   gather_vec(t->n, t->perm, mu, sc2, mu0, s);             // μ_norm = scale²·μ
   if (p->flags & WN_FLAG_GRAPH) {
     // the whole iteration loop as one CUDA graph: captured on a private stream, cached per parameters
     const void* arena = P ? P->own : nullptr;
-    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm) + sizeof(int) + sizeof(arena));
-    memcpy(key.data(), p, sizeof(wnnc_params));
-    memcpy(key.data() + sizeof(wnnc_params), &comm, sizeof(comm));
-    memcpy(key.data() + sizeof(wnnc_params) + sizeof(comm), &t->far_order, sizeof(int));
-    memcpy(key.data() + sizeof(wnnc_params) + sizeof(comm) + sizeof(int), &arena, sizeof(arena));
+    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm) + sizeof(int) + sizeof(arena) + sizeof(ShardPlan));
+    uint8_t* kp = key.data();
+    memcpy(kp, p, sizeof(wnnc_params));
+    kp += sizeof(wnnc_params);
+    memcpy(kp, &comm, sizeof(comm));
+    kp += sizeof(comm);
+    memcpy(kp, &t->far_order, sizeof(int));
+    kp += sizeof(int);
+    memcpy(kp, &arena, sizeof(arena));
+    kp += sizeof(arena);
+    memcpy(kp, &t->shard, sizeof(ShardPlan));
     if (!t->graph_exec || key != t->graph_key) {
       if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
       t->graph_exec = nullptr;
@@ -741,6 +820,26 @@ wn_status wnnc_solve_host(const float* pts_host, int64_t n, int32_t max_depth, c
   if (t) wn_tree_destroy(t);
   if (st != WN_OK) return st;
   if (e != cudaSuccess) return cuda_status(e, "wnnc_solve_host");
+  return WN_OK;
+}
+
+wn_status wn_tree_schedule(wn_tree t, int32_t* qorder, void* stream) {
+  if (!t || !qorder) return set_error(WN_ERR_ARG, "tree or output is NULL");
+  WN_CUDA(cudaMemcpyAsync(qorder, t->qorder, t->n * sizeof(int32_t), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return WN_OK;
+}
+
+wn_status wn_shard_plan(wn_tree t, int32_t world, int64_t* bounds, void* stream) {
+  if (!t || !bounds || world < 1 || world > kMaxShardRanks) return set_error(WN_ERR_ARG, "bad shard-plan arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  WN_TRY(ensure_scratch(t, s));
+  WN_TRY(plan_shards(t, world, nullptr, s));
+  for (int r = 0; r < world; ++r) {
+    int64_t b = 0, e = 0;
+    shard_of(&t->shard, t->n, r, world, &b, &e);
+    bounds[r] = b;
+  }
+  bounds[world] = t->n;
   return WN_OK;
 }
 

@@ -100,13 +100,22 @@ __global__ void k_unpack(const float* __restrict__ stage, const int32_t* __restr
 }
 }  // namespace
 
+void shard_of(const ShardPlan* plan, int64_t n, int rank, int world, int64_t* b, int64_t* e) {
+  if (plan && plan->world == world) {
+    *b = plan->b[rank];
+    *e = plan->b[rank + 1];
+  } else {
+    wn_shard_range(n, rank, world, b, e);
+  }
+}
+
 wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, const int32_t* qorder, float* stage,
-                           cudaStream_t s) {
+                           const ShardPlan* plan, cudaStream_t s) {
   Nccl& N = nccl();
   float* x = buf;
   if (qorder) {  // the owned rows are a schedule range: gather them into schedule order first
     int64_t b = 0, e = 0;
-    wn_shard_range(n, c->rank, c->world, &b, &e);
+    shard_of(plan, n, c->rank, c->world, &b, &e);
     if (e > b) k_pack<<<(unsigned)((e - b + 255) / 256), 256, 0, s>>>(buf, qorder, b, e, comps, stage);
     count_launches(1);
     x = stage;
@@ -114,7 +123,7 @@ wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, const in
   ncclResult_t r = N.GroupStart();
   for (int k = 0; k < c->world && r == ncclSuccess; ++k) {
     int64_t b = 0, e = 0;
-    wn_shard_range(n, k, c->world, &b, &e);
+    shard_of(plan, n, k, c->world, &b, &e);
     if (e > b) r = N.Broadcast(x + b * comps, x + b * comps, (size_t)(e - b) * comps, ncclFloat32, k, c->comm, s);
   }
   ncclResult_t r2 = N.GroupEnd();
@@ -126,13 +135,14 @@ wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, const in
   return nccl_status(r, "ncclBroadcast (all-gather)");
 }
 
-wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64_t n, cudaStream_t s) {
+wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64_t n, const ShardPlan* plan,
+                                  cudaStream_t s) {
   Nccl& N = nccl();
   ncclResult_t r = N.GroupStart();
   for (int a = 0; a < 3 && r == ncclSuccess; ++a)
     for (int k = 0; k < c->world && r == ncclSuccess; ++k) {
       int64_t b = 0, e = 0;
-      wn_shard_range(n, k, c->world, &b, &e);
+      shard_of(plan, n, k, c->world, &b, &e);
       const int64_t b0 = b / kTravBlock, b1 = (e + kTravBlock - 1) / kTravBlock;  // partials per traversal block
       if (b1 > b0) {
         double* p = part + a * stride + b0;
@@ -144,6 +154,13 @@ wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64
 
   return nccl_status(r, "ncclBroadcast (partials)");
 }
+
+wn_status comm_allreduce_i64(wn_comm c, int64_t* buf, int64_t count, cudaStream_t s) {
+  return nccl_status(nccl().AllReduce(buf, buf, (size_t)count, ncclInt64, ncclSum, c->comm, s), "ncclAllReduce (work)");
+}
+
+int comm_rank(wn_comm c) { return c->rank; }
+int comm_world(wn_comm c) { return c->world; }
 
 // ---------------- peer-memory exchange (B200-native form of the per-traversal all-gather) ----------------
 // Every rank allocates one IPC-capable block (cudaMalloc) holding the exchanged arrays — s (N fp32),

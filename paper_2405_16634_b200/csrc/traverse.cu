@@ -677,9 +677,9 @@ wn_status traverse(const TravArgs& a, cudaStream_t s) {
   const unsigned grid = (unsigned)trav_blocks(nq);
   const size_t smem = (size_t)(kTravBlock / 32) * a.stack_depth * sizeof(int2);
   const int cls = a.op == OP_A ? WN_PROF_TRAV_A : a.op == OP_AT ? WN_PROF_TRAV_AT : WN_PROF_TRAV_G;
-  ProfScope ps(cls, s);
+  ProfScope ps(a.prof_cls >= 0 ? a.prof_cls : cls, s);
   TravArgs b = a;
-  b.work = work_counters(cls);
+  b.work = a.nowork ? nullptr : work_counters(cls);
   if (a.order1 && (!a.nodes.ext || a.attr)) return set_error(WN_ERR_ARG, "internal: order-1 traversal setup");
   switch (a.op * 8 + a.epi) {
     case OP_A * 8 + EPI_PLAIN: launch<OP_A, EPI_PLAIN>(b, s, grid, smem); break;

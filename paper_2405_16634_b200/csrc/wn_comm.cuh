@@ -12,9 +12,15 @@ wn_status comm_shard(wn_comm c, int64_t n, int64_t* q0, int64_t* q1);
 // Every rank owns the rows of schedule positions [q0, q1) of a sorted-order array of n rows × comps floats
 // (row = qorder[k], or k when qorder is null); make it whole on all ranks.  stage: n × comps scratch.
 wn_status comm_allgather_f(wn_comm c, float* buf, int comps, int64_t n, const int32_t* qorder, float* stage,
-                           cudaStream_t s);
+                           const ShardPlan* plan, cudaStream_t s);
 // The three per-block partial arrays (stride entries each, blocks of kTravBlock queries).
-wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64_t n, cudaStream_t s);
+wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64_t n, const ShardPlan* plan,
+                                  cudaStream_t s);
+// rank r's query range [*b, *e): the plan's when it is for this world size, else equal counts
+void shard_of(const ShardPlan* plan, int64_t n, int rank, int world, int64_t* b, int64_t* e);
+wn_status comm_allreduce_i64(wn_comm c, int64_t* buf, int64_t count, cudaStream_t s);
+int comm_rank(wn_comm c);
+int comm_world(wn_comm c);
 // Peer-memory exchange: the communicator's arena (collective on first use or growth; synchronizes s),
 // and the per-exchange device-side wait for every rank's signal.
 wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena** out);

@@ -62,6 +62,13 @@ struct IterScratch {
   float* tmp = nullptr;      // generic N×4 scratch
   int nblk = 0;
 };
+// Query shards of a multi-GPU solve: schedule positions [b[r], b[r+1]) for rank r, multiples of
+// WN_SHARD_ALIGN, split by estimated work (capi.cu:plan_shards); world = 0 ⇒ equal counts (wn_shard_range)
+constexpr int kMaxShardRanks = 64;
+struct ShardPlan {
+  int world = 0;
+  int64_t b[kMaxShardRanks + 1] = {};
+};
 
 }  // namespace wn
 
@@ -92,6 +99,7 @@ struct wn_tree_s {
   int64_t* mom_loff = nullptr;  //   level offsets on the device
   double* mom_pre = nullptr;    // (N+1) × 8 fp64 exclusive prefix of the point sums (moments.cu)
   double* mom_tile = nullptr;   // 2 × tiles × 8 fp64: per-tile totals, per-tile offsets
+  wn::ShardPlan shard;           // work-weighted query shards for the last world size used
   int64_t mom_ntiles = 0;
   bool mom_order1_ready = false;  // prefix scratch + set[0].ext sized for the first-order far field
   int far_order = 0;              // wn_tree_set_far_order: 0 (the paper's Alg. 4) or 1 (row f2)
@@ -198,6 +206,8 @@ struct TravArgs {
   int root_single = 0;              // 1 iff the root is a one-point leaf (n = 1)
   int order1 = 0;                   // first-order far field (nodes.ext), row f2
   int split = 0;                    // small clouds: several warps per query group (traverse.cu)
+  bool nowork = false;              // keep this launch out of the wn_work_count totals
+  int prof_cls = -1;                // profiling class override (-1: by operator)
   int64_t nnodes = 0, npts = 0;     // sizes (WN_DEBUG bounds checks)
   int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
   int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order

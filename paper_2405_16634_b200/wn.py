@@ -29,7 +29,7 @@ EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", 
             "wn_tree_destroy", "wn_tree_info", "wn_tree_export", "wn_moments", "wn_eval", "wn_eval_grad",
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
             "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work",
-            "wn_tree_set_far_order", "wnnc_iterate_emulated")
+            "wn_tree_set_far_order", "wnnc_iterate_emulated", "wn_shard_plan", "wn_tree_schedule")
 
 
 class wnnc_params(C.Structure):
@@ -59,6 +59,8 @@ _sig = {
     "wn_query_work": ([P, I32, P, P, I64, F32, F32, P, P], I32),
     "wn_tree_set_far_order": ([P, I32, P], I32),
     "wnnc_iterate_emulated": ([P, P, P, I32, P, P], I32),
+    "wn_shard_plan": ([P, I32, P, P], I32),
+    "wn_tree_schedule": ([P, P, P], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -300,6 +302,20 @@ def wnnc_iterate_emulated(tree: Tree, mu: torch.Tensor, world: int, **params):
     reps = torch.empty(world, tree.n, 3, dtype=torch.float32, device=tree.device)
     _check(_L.wnnc_iterate_emulated(tree.handle, _ptr(mu), C.byref(p), int(world), _ptr(reps), _stream()))
     return reps
+
+
+def wn_tree_schedule(tree: Tree) -> torch.Tensor:
+    """Sorted-point index at each position of the query schedule (3-D Hilbert order)."""
+    out = torch.empty(tree.n, dtype=torch.int32, device=tree.device)
+    _check(_L.wn_tree_schedule(tree.handle, _ptr(out), _stream()))
+    return out
+
+
+def wn_shard_plan(tree: Tree, world: int):
+    """The work-weighted query shards of a `world`-rank solve: list of world + 1 schedule positions."""
+    b = (C.c_int64 * (world + 1))()
+    _check(_L.wn_shard_plan(tree.handle, int(world), b, _stream()))
+    return list(b)
 
 
 def wn_comm_init(rank: int, world: int, uid: bytes) -> Comm:

@@ -102,6 +102,24 @@ def test_mu_zero_flag_is_exact(wn, order):
         assert st == out[0][1]
 
 
+def test_shard_plan_balances_work(wn):
+    # the work-weighted shards of an 8-rank solve of the non-uniform C3 cloud: block-aligned, covering,
+    # and balanced on the actual per-query work (node tests and live terms of A) where equal counts are not
+    c = synth.config("C3")
+    p = torch.from_numpy(c["points"]).cuda()
+    n = len(p)
+    t = wn.wn_build_tree(p)
+    pl = wn.wn_shard_plan(t, 8)
+    assert pl[0] == 0 and pl[-1] == n and all(b % 256 == 0 for b in pl[:-1]) and pl == sorted(pl)
+    mu = torch.from_numpy((synth.random_signs(c["normals"], 7) * (4 * np.pi / n)).astype(np.float32)).cuda()
+    cnt = wn.wn_query_work(t, mu, 0.004, op=0).cpu().numpy().astype(np.int64)
+    perm = wn.wn_tree_export(t)["perm"].cpu().numpy()
+    work = (cnt[:, 0] * 13 + cnt[:, 3] * 10)[perm[wn.wn_tree_schedule(t).cpu().numpy()]]
+    wp = np.array([work[pl[r]:pl[r + 1]].sum() for r in range(8)])
+    we = np.array([work[b:e].sum() for b, e in (wn.wn_shard_range(n, r, 8) for r in range(8))])
+    assert wp.max() / wp.mean() < 1.02 < we.max() / we.mean()
+
+
 def test_comm_init_errors(wn):
     with pytest.raises(wn.WnError, match="ARG"):
         wn.wn_comm_init(2, 2, bytes(128))
