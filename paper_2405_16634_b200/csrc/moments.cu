@@ -220,6 +220,10 @@ __global__ void __launch_bounds__(kMomThreads, WN_EXP_MOM_LB) moments_range(Tree
 #endif
 constexpr int kScanThreads = 256, kScanItems = WN_EXP_SCANITEMS, kScanTile = kScanThreads * kScanItems;
 constexpr int kScanTopThreads = 256;
+#ifndef WN_EXP_FEWTILES
+#define WN_EXP_FEWTILES 512
+#endif
+constexpr int kFewTiles = WN_EXP_FEWTILES;  // up to this many tiles the prefix blocks sum earlier totals themselves
 
 // components per prefix entry; entry j (exclusive: points [0, j)) = hi[EH] fp64 (the NC sums, the count,
 // padding) in E_hi and lo[EL] = the double-double low parts rounded to fp32 in E_lo
@@ -430,6 +434,7 @@ template <int KIND, int ORD>
 __global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __restrict__ pts, MomentArgs m,
                                                                 int64_t n,
                                                                 const Elt<PreLayout<KIND, ORD>::NC>* __restrict__ tile_off,
+                                                                const Elt<PreLayout<KIND, ORD>::NC>* __restrict__ tile_tot,
                                                                 double* __restrict__ Eh, float* __restrict__ El) {
   constexpr int NC = PreLayout<KIND, ORD>::NC;
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
@@ -443,11 +448,18 @@ __global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __
       elt_add_point(t, o);
     }
   block_exscan<kScanThreads>(t, tot);
-  if (tile_off) {  // null: a single tile, offset 0
+  if (tile_off) {  // the tile offsets of mom_tile_scan
     Elt<NC> z = tile_off[blockIdx.x];
     elt_add(z, t);
     t = z;
-  }
+  } else if (tile_tot && blockIdx.x > 0) {  // few tiles: this tile's offset = Σ of the earlier totals, here
+    Elt<NC> v, z;
+    elt_zero(v);
+    for (int64_t k = threadIdx.x; k < blockIdx.x; k += kScanThreads) elt_add(v, tile_tot[k]);
+    block_exscan<kScanThreads>(v, z);  // z: the block total, a fixed-order reduction
+    elt_add(z, t);
+    t = z;
+  }  // (neither: a single tile, offset 0)
   for (int k = 0; k < kScanItems; ++k) {
     const int64_t j = j0 + k;
     if (j < n) {
@@ -560,11 +572,15 @@ void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
   Elt<Lay::NC>* off = tot + nt;
   double* Eh = t->mom_pre;
   float* El = reinterpret_cast<float*>(t->mom_pre + Lay::EH * (t->n + 1));
-  if (nt > 1) {  // a single tile needs no tile totals
+  // a single tile needs no tile totals; up to kFewTiles tiles each prefix block sums the earlier tile
+  // totals itself (no one-block scan launch); more tiles go through mom_tile_scan
+  const bool scan = nt > kFewTiles;
+  if (nt > 1) {
     mom_tile_sum<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, tot);
-    mom_tile_scan<Lay::NC><<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
+    if (scan) mom_tile_scan<Lay::NC><<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
   }
-  mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, nt > 1 ? off : nullptr, Eh, El);
+  mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, scan ? off : nullptr,
+                                                                    nt > 1 ? tot : nullptr, Eh, El);
   // per-iteration builds: only the nodes a traversal can read (chain interiors and the children of
   // pseudo-leaves are never visited); the diagnostic export (write_W) builds every node
   const bool all = m.all_nodes || m.write_W || !t->mom_live;
@@ -616,7 +632,7 @@ wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
 #ifndef WN_EXP_OLD_MOM
   if (m.kind != ATTR_UNIT) {  // per-iteration attributes: prefix differences
-    ProfScope ps(WN_PROF_MOMENTS, s, t->mom_ntiles > 1 ? 4 : 2);
+    ProfScope ps(WN_PROF_MOMENTS, s, t->mom_ntiles > 1 ? (t->mom_ntiles > kFewTiles ? 4 : 3) : 2);
     if (m.order1 && !(m.out.ext && t->mom_order1_ready)) return set_error(WN_ERR_ARG, "internal: order-1 scratch");
     if (m.kind == ATTR_VEC) {
       if (m.order1) launch_prefix<ATTR_VEC, 1>(t, m, s);
