@@ -1,4 +1,6 @@
-"""Small workload touching every kernel path, for compute-sanitizer (memcheck / racecheck / synccheck)."""
+"""Small workload touching every kernel path (tree, moments, A/G/Aᵀ at sources and queries, graph iteration,
+transpose adjoint, order 1, world-1 communicator, emulated ranks) — run it against the WN_DEBUG build
+(WN_LIB=paper_2405_16634_b200/exp/debug/libwn.so) to exercise the device-side bounds checks."""
 import sys
 import numpy as np
 import torch
