@@ -283,7 +283,10 @@ __global__ void gather_sorted(const float4* __restrict__ xn, const int32_t* __re
 }
 
 // 3-D Hilbert index of a point (Skilling's transpose algorithm) on a 2^kHilbertBits grid of [−1,1]^3
-constexpr int kHilbertBits = 10;
+#ifndef WN_EXP_HBITS
+#define WN_EXP_HBITS 10
+#endif
+constexpr int kHilbertBits = WN_EXP_HBITS;
 __global__ void hilbert_keys(const float4* __restrict__ pts, int64_t n, uint64_t* __restrict__ hk,
                              int32_t* __restrict__ hv) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
