@@ -522,37 +522,62 @@ wn_status scan_excl(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* tota
     if (st_ != WN_OK) return st_;       \
   } while (0)
 
-wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s) {
-  if (n <= 0) return WN_OK;
+// stable LSD radix sort of (key, value) pairs on the low `bits` bits of the keys; ka / va are consumed,
+// the values in key order are copied to out
+static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int32_t* out, cudaStream_t s) {
   const int ntiles = (int)((n + kSortTile - 1) / kSortTile);
-  uint64_t *ka = nullptr, *kb = nullptr;
-  int32_t *va = nullptr, *vb = nullptr;
+  uint64_t* kb = nullptr;
+  int32_t* vb = nullptr;
   uint32_t* hist = nullptr;
-  WN_TRY(dalloc(&ka, n, s));
   WN_TRY(dalloc(&kb, n, s));
-  WN_TRY(dalloc(&va, n, s));
   WN_TRY(dalloc(&vb, n, s));
   WN_TRY(dalloc(&hist, (size_t)256 * ntiles, s));
-  const int hpasses = (3 * kHilbertBits + 7) / 8;
-  {
-    ProfScope ps(WN_PROF_TREE, s, 1 + 5 * hpasses);
-    hilbert_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pts, n, ka, va);
-    for (int p = 0; p < hpasses; ++p) {
-      radix_hist<<<ntiles, kSortThreads, 0, s>>>(ka, n, 8 * p, ntiles, hist);
-      WN_TRY(scan_excl(hist, hist, (int64_t)256 * ntiles, nullptr, s));
-      radix_scatter<<<ntiles, kSortThreads, 0, s>>>(ka, va, kb, vb, n, 8 * p, ntiles, hist);
-      std::swap(ka, kb);
-      std::swap(va, vb);
-    }
+  uint64_t* const own_k = kb;  // freed here whatever the parity of the passes
+  int32_t* const own_v = vb;
+  const int passes = (bits + 7) / 8;
+  for (int p = 0; p < passes; ++p) {
+    radix_hist<<<ntiles, kSortThreads, 0, s>>>(ka, n, 8 * p, ntiles, hist);
+    WN_TRY(scan_excl(hist, hist, (int64_t)256 * ntiles, nullptr, s));
+    radix_scatter<<<ntiles, kSortThreads, 0, s>>>(ka, va, kb, vb, n, 8 * p, ntiles, hist);
+    std::swap(ka, kb);
+    std::swap(va, vb);
   }
-  WN_CUDA(cudaMemcpyAsync(order, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-  cudaFreeAsync(ka, s);
-  cudaFreeAsync(kb, s);
-  cudaFreeAsync(va, s);
-  cudaFreeAsync(vb, s);
+  WN_CUDA(cudaMemcpyAsync(out, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  cudaFreeAsync(own_k, s);
+  cudaFreeAsync(own_v, s);
   cudaFreeAsync(hist, s);
+  count_launches(5 * passes);
   WN_CUDA(cudaGetLastError());
   return WN_OK;
+}
+
+wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s) {
+  if (n <= 0) return WN_OK;
+  uint64_t* ka = nullptr;
+  int32_t* va = nullptr;
+  WN_TRY(dalloc(&ka, n, s));
+  WN_TRY(dalloc(&va, n, s));
+  const int hbits = 3 * kHilbertBits;
+  {
+    ProfScope ps(WN_PROF_TREE, s, 0);
+    hilbert_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pts, n, ka, va);
+    count_launches(1);
+    WN_TRY(sort_pairs(ka, va, n, hbits, order, s));
+  }
+  cudaFreeAsync(ka, s);
+  cudaFreeAsync(va, s);
+  return WN_OK;
+}
+
+// keys of the visitable-node list: each node's first sorted point (the moment pass then reads the
+// prefix entries in point order)
+__global__ void live_keys(int64_t m, const int32_t* __restrict__ list, const int32_t* __restrict__ pb,
+                          uint64_t* __restrict__ k, int32_t* __restrict__ v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int32_t node = list[i];
+  k[i] = (uint64_t)pb[node];
+  v[i] = node;
 }
 
 wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree_s* t) {
@@ -710,6 +735,21 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
     cudaFreeAsync(vis, s);
     cudaFreeAsync(pos, s);
     count_launches(5);
+#ifndef WN_EXP_LIVE_BFS
+    if (nlive > 1) {  // in point order: neighbouring threads read neighbouring (often shared) prefix entries
+      uint64_t* k = nullptr;
+      int32_t* v = nullptr;
+      WN_TRY(dalloc(&k, nlive, s));
+      WN_TRY(dalloc(&v, nlive, s));
+      live_keys<<<(unsigned)((nlive + 255) / 256), 256, 0, s>>>(nlive, t->mom_live, t->pb, k, v);
+      count_launches(1);
+      int bits = 1;
+      while (bits < 62 && ((int64_t)1 << bits) <= n) ++bits;
+      WN_TRY(sort_pairs(k, v, nlive, bits, t->mom_live, s));
+      cudaFreeAsync(k, s);
+      cudaFreeAsync(v, s);
+    }
+#endif
   }
   cudaFreeAsync(loff, s);
   cudaFreeAsync(cnt, s);
