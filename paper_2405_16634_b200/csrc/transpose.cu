@@ -5,8 +5,9 @@
 // is linear in the attribute ν:  (T_g ν)_i = Σ_{far B} ∇Φ_w(x_i − x_B)·Σ_{j∈B} ν_j + Σ_{near j} ∇Φ_w(x_i − x_j)·ν_j.
 // Its exact transpose is  (T_gᵀ s)_j = U_j + Σ_{B ∋ j} V_B  with
 //     V_B = Σ_{i: B far for i} s_i ∇Φ_w(x_i − x_B),   U_j = Σ_{i: j near for i} s_i ∇Φ_w(x_i − x_j).
-// Kernel 1 runs the same warp-cooperative traversal as A (same fp32 decisions); for every node the
-// warp sums its lanes' contributions with shuffles and lane 0 issues one fp64 atomic per component.
+// Kernel 1 runs the same warp-cooperative traversal as A (same fp32 decisions, Hilbert query schedule);
+// the lanes' contributions to up to four nodes (or leaf points) at a time are summed with one warp
+// reduce-scatter, after which different lanes issue the fp64 atomics (one per node and component).
 // Kernel 2 pushes down: r_j = U_j + Σ over the ancestors of j's leaf, and emits Σ|r|² block partials.
 #include <cuda_runtime.h>
 
@@ -35,15 +36,46 @@ __device__ __forceinline__ void warp_add3(float x, float y, float z, double* dst
   }
 }
 
+// Reduce-scatter of 16 per-lane values (four targets × (x, y, z, ·)) over the warp: 8 + 4 + 2 + 1 + 1
+// shuffles; afterwards lane l holds the total of value 8·l₄ + 4·l₃ + 2·l₂ + l₁, i.e. target 2·l₄ + l₃,
+// component 2·l₂ + l₁ (lanes l and l ^ 1 hold the same total).  A per-target butterfly would take 15.
+__device__ __forceinline__ float reduce_scatter16(const float (&v)[16], int lane, int& target, int& comp) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  float w8[8], w4[4], w2v[2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float send = b4 ? v[i] : v[8 + i];
+    w8[i] = (b4 ? v[8 + i] : v[i]) + __shfl_xor_sync(FULL, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b3 ? w8[i] : w8[4 + i];
+    w4[i] = (b3 ? w8[4 + i] : w8[i]) + __shfl_xor_sync(FULL, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b2 ? w4[i] : w4[2 + i];
+    w2v[i] = (b2 ? w4[2 + i] : w4[i]) + __shfl_xor_sync(FULL, send, 4);
+  }
+  const float send = b1 ? w2v[0] : w2v[1];
+  float tot = (b1 ? w2v[1] : w2v[0]) + __shfl_xor_sync(FULL, send, 2);
+  tot += __shfl_xor_sync(FULL, tot, 1);
+  target = (b4 ? 2 : 0) + (b3 ? 1 : 0);
+  comp = (b2 ? 2 : 0) + (b1 ? 1 : 0);
+  return tot;
+}
+
 __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
     const float4* __restrict__ G, const float4* __restrict__ pts,
     const int32_t* __restrict__ npb, const int32_t* __restrict__ npe, const float* __restrict__ s_sorted,
-    int64_t n, float w2, int stack_depth, double* __restrict__ VB, double* __restrict__ U) {
+    int64_t n, float w2, int stack_depth, double* __restrict__ VB, double* __restrict__ U,
+    const int32_t* __restrict__ qorder) {
   extern __shared__ int2 stk_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int2* stk = stk_all + warp * stack_depth;
-  const int64_t q = (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
-  const bool valid = q < n;
+  const int64_t kq = (int64_t)blockIdx.x * kTravBlock + threadIdx.x;  // schedule position (Hilbert order)
+  const bool valid = kq < n;
+  const int64_t q = (valid && qorder) ? (int64_t)qorder[kq] : kq;
   const float4 xq = valid ? pts[q] : make_float4(0.f, 0.f, 0.f, 0.f);
   const float sq = valid ? s_sorted[q] * kInv4Pi : 0.f;
   const uint32_t active = __ballot_sync(FULL, valid);
@@ -58,48 +90,66 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
     __syncwarp();
     const int cb = e.x >> 4, ncc = (e.x & 7) + 1;
     const bool mine = ((uint32_t)e.y >> lane) & 1u;
-    for (int k = 0; k < ncc; ++k) {
-      const int node = cb + k;
-      const float4 R = __ldg(G + kRec * (int64_t)node);
-      const float4 Lo = __ldg(G + kRec * (int64_t)node + 2);
-      // d = (hi − x_q) + lo: the decisions of the frozen-geometry A traversal (R-prec)
-      const float ex = __fadd_rn(__fsub_rn(R.x, xq.x), Lo.x), ey = __fadd_rn(__fsub_rn(R.y, xq.y), Lo.y),
-                  ez = __fadd_rn(__fsub_rn(R.z, xq.z), Lo.z);
-      const float d2 = dist2(ex, ey, ez);
-      const bool far = d2 > R.w;
-      // s_i ∇Φ(x_i − x_B) = s_i d / (4π r³), d = x_B − x_i
-      float cx = 0.f, cy = 0.f, cz = 0.f;
-      const bool live = mine && far && !(d2 < w2);
-      if (live) {
-        const float inv = rsqrtf(d2);
-        const float c = sq * inv * inv * inv;
-        cx = c * ex; cy = c * ey; cz = c * ez;
-      }
-      if (__any_sync(FULL, live)) warp_add3(cx, cy, cz, VB + 3 * (int64_t)node, lane);
-      const uint32_t open = __ballot_sync(FULL, mine && !far);
-      if (open) {
-        const int topo = __float_as_int(__ldg(G + kRec * (int64_t)node + 1).w);
-        if (topo != 0) {
-          if (lane == 0) stk[sp] = make_int2(topo, (int)open);
-          ++sp;
-        } else {
-          const bool lm = (open >> lane) & 1u;
-          const int j1 = npe[node];
-          for (int j = npb[node]; j < j1; ++j) {
-            const float4 P = __ldg(pts + j);
-            const float ex = __fsub_rn(P.x, xq.x), ey = __fsub_rn(P.y, xq.y), ez = __fsub_rn(P.z, xq.z);
-            const float e2 = dist2(ex, ey, ez);
-            float ux = 0.f, uy = 0.f, uz = 0.f;
-            const bool lv = lm && !(e2 < w2);
-            if (lv) {
-              const float inv = rsqrtf(e2);
-              const float c = sq * inv * inv * inv;
-              ux = c * ex; uy = c * ey; uz = c * ez;
+    for (int k0 = 0; k0 < ncc; k0 += 4) {
+      // up to four children: each lane's contributions v[4·kk + (x, y, z, ·)], then one reduce-scatter
+      float v[16];
+      bool anylive = false;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = k0 + kk;
+        float cx = 0.f, cy = 0.f, cz = 0.f;
+        if (k < ncc) {
+          const int node = cb + k;
+          const float4 R = __ldg(G + kRec * (int64_t)node);
+          const float4 Lo = __ldg(G + kRec * (int64_t)node + 2);
+          // d = (hi − x_q) + lo: the decisions of the frozen-geometry A traversal (R-prec)
+          const float ex = __fadd_rn(__fsub_rn(R.x, xq.x), Lo.x), ey = __fadd_rn(__fsub_rn(R.y, xq.y), Lo.y),
+                      ez = __fadd_rn(__fsub_rn(R.z, xq.z), Lo.z);
+          const float d2 = dist2(ex, ey, ez);
+          const bool far = d2 > R.w;
+          // s_i ∇Φ(x_i − x_B) = s_i d / (4π r³), d = x_B − x_i
+          const bool live = mine && far && !(d2 < w2);
+          if (live) {
+            const float inv = rsqrtf(d2);
+            const float c = sq * inv * inv * inv;
+            cx = c * ex; cy = c * ey; cz = c * ez;
+          }
+          anylive |= live;
+          const uint32_t open = __ballot_sync(FULL, mine && !far);
+          if (open) {
+            const int topo = __float_as_int(__ldg(G + kRec * (int64_t)node + 1).w);
+            if (topo != 0) {
+              if (lane == 0) stk[sp] = make_int2(topo, (int)open);
+              ++sp;
+            } else {  // leaf-coded node: its points, one butterfly per point into U (grouping: no gain)
+              const bool lm = (open >> lane) & 1u;
+              const int j1 = npe[node];
+              for (int j = npb[node]; j < j1; ++j) {
+                const float4 P = __ldg(pts + j);
+                const float px = __fsub_rn(P.x, xq.x), py = __fsub_rn(P.y, xq.y), pz = __fsub_rn(P.z, xq.z);
+                const float e2 = dist2(px, py, pz);
+                float ux = 0.f, uy = 0.f, uz = 0.f;
+                const bool lv = lm && !(e2 < w2);
+                if (lv) {
+                  const float inv = rsqrtf(e2);
+                  const float c = sq * inv * inv * inv;
+                  ux = c * px; uy = c * py; uz = c * pz;
+                }
+                if (__any_sync(FULL, lv)) warp_add3(ux, uy, uz, U + 3 * (int64_t)j, lane);
+              }
             }
-            if (__any_sync(FULL, lv)) warp_add3(ux, uy, uz, U + 3 * (int64_t)j, lane);
           }
         }
+        v[4 * kk + 0] = cx;
+        v[4 * kk + 1] = cy;
+        v[4 * kk + 2] = cz;
+        v[4 * kk + 3] = 0.f;
       }
+      if (!__any_sync(FULL, anylive)) continue;
+      int child, comp;
+      const float tot = reduce_scatter16(v, lane, child, comp);
+      if (!(lane & 1) && comp < 3 && k0 + child < ncc && tot != 0.f)
+        atomicAdd(VB + 3 * (int64_t)(cb + k0 + child) + comp, (double)tot);
     }
     __syncwarp();
   }
@@ -150,7 +200,7 @@ wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sor
   {
     ProfScope ps(WN_PROF_TRAV_AT, st, 2);
     scatter_kernel<<<grid, kTravBlock, (size_t)(kTravBlock / 32) * stack_depth * sizeof(int2), st>>>(
-        geo.rec, t->pts, t->pb, t->pe, s_sorted, t->n, w2, stack_depth, t->tvb, t->tu);
+        geo.rec, t->pts, t->pb, t->pe, s_sorted, t->n, w2, stack_depth, t->tvb, t->tu, t->qorder);
     pushdown_kernel<<<grid, kTravBlock, 0, st>>>(t->n, t->leaf_of, t->parent, t->tvb, t->tu, 1.0f, r_out, partial);
   }
   WN_CUDA(cudaGetLastError());
