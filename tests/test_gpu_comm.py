@@ -102,6 +102,19 @@ def test_mu_zero_flag_is_exact(wn, order):
         assert st == out[0][1]
 
 
+def test_emulated_ranks_first_order(wn):
+    # the first-order far field (row f2) through the sharded peer exchange: 3 emulated ranks, one trajectory
+    p = torch.from_numpy(synth.config("C2")["points"][:30011]).cuda()
+    t = wn.wn_build_tree(p)
+    wn.wn_tree_set_far_order(t, 1)
+    ref = torch.zeros(len(p), 3, device="cuda")
+    wn.wnnc_iterate(t, ref, iters=4, total_iters=40)
+    mu = torch.zeros(len(p), 3, device="cuda")
+    reps = wn.wnnc_iterate_emulated(t, mu, 3, iters=4, total_iters=40)
+    for r in range(3):
+        np.testing.assert_array_equal(reps[r].cpu().numpy(), ref.cpu().numpy())
+
+
 def test_shard_plan_balances_work(wn):
     # the work-weighted shards of an 8-rank solve of the non-uniform C3 cloud: block-aligned, covering,
     # and balanced on the actual per-query work (node tests and live terms of A) where equal counts are not
