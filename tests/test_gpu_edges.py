@@ -150,3 +150,34 @@ def test_split_and_single_warp_kernels_agree(wn):
         ref = full.reshape(len(idx), -1)
         err = np.linalg.norm(part.reshape(len(idx), -1) - ref, axis=1)
         assert np.all(err <= 1e-5 * np.linalg.norm(ref, axis=1) + 1e-6 * np.sqrt(np.mean(ref ** 2))), err.max()
+
+
+@pytest.mark.parametrize("shape", ["planar", "collinear"])
+def test_flat_clouds(wn, shape):
+    # zero extent along one (planar) or two (collinear) axes: the normalization uses the longest half-extent
+    # (§5.1.1), the tree degenerates to quadtree / binary splits — structure bit-exact, operators at parity
+    rng = np.random.default_rng(45)
+    n = 3000
+    p = np.zeros((n, 3), np.float32)
+    if shape == "planar":
+        p[:, :2] = rng.uniform(-1, 1, (n, 2))
+    else:
+        p[:, 0] = rng.uniform(-1, 1, n)
+    p += np.float32(0.25)
+    mu = (rng.standard_normal((n, 3)) * 4 * np.pi / n).astype(np.float32)
+    t = wn.wn_build_tree(_cuda(p))
+    e = {k: v.cpu().numpy() for k, v in wn.wn_tree_export(t).items()}
+    cl = oracle.Cloud(p)
+    o = cl.t.export()
+    for k in ("perm", "depth", "pb", "pe", "child_begin", "child_count"):
+        np.testing.assert_array_equal(e[k], o[k], err_msg=k)
+    w = float(np.float32(0.01))
+    F = wn.wn_eval(t, _cuda(mu), w).cpu().numpy()
+    Fo, cnt = cl.F(mu, w, counters=True)
+    _check_queries(F, Fo, cnt, cl.abs_scale(oracle.OP_A, mu, w), name=f"F {shape}")
+    G = wn.wn_eval_grad(t, _cuda(mu), w).cpu().numpy()
+    Go, cnt = cl.gradF(mu, w, counters=True)
+    _check_queries(G, Go, cnt, cl.abs_scale(oracle.OP_G, mu, w), name=f"gradF {shape}")
+    m = torch.zeros(n, 3, device="cuda")
+    wn.wnnc_iterate(t, m, iters=3, total_iters=40)
+    assert np.isfinite(m.cpu().numpy()).all()
