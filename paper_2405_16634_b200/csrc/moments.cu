@@ -249,27 +249,23 @@ __device__ __forceinline__ DD dd_add(DD a, DD b) {
   return DD{h, __dsub_rn(e, __dsub_rn(h, s))};
 }
 
-// per-point terms: (|ν|, |ν|x, |ν|y, |ν|z, ν) and, for ORD 1, sym(ν xᵀ) (xx, yy, zz, xy, xz, yz) or s x
+// per-point terms: (|ν|, |ν|x, |ν|y, |ν|z, ν) and, for ORD 1, sym(ν xᵀ) (xx, yy, zz, xy, xz, yz) or s x;
+// v: the attribute (vector: μ, or μ + α r when r is given; scalar: v.x), f: the per-point factor a (or 1)
 template <int KIND, int ORD>
-__device__ __forceinline__ void point_vals(int64_t j, const float4* __restrict__ pts, const MomentArgs& m, float alpha,
-                                           double* o) {
-  const float4 x = pts[j];
+__device__ __forceinline__ void point_terms(float4 x, float4 v, const float4* r, float alpha, double f,
+                                            bool scaled, double* o) {
   double a, v0, v1 = 0.0, v2 = 0.0;
   if (KIND == ATTR_VEC) {
-    float4 v = m.vec[j];
-    if (m.axpy_r) {  // μ' = μ + α r (Alg. 2 line 3) — the same fmaf as the record's one-point branch
-      const float4 r = m.axpy_r[j];
-      v = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
-    }
+    if (r)  // μ' = μ + α r (Alg. 2 line 3) — the same fmaf as the record's one-point branch
+      v = make_float4(fmaf(alpha, r->x, v.x), fmaf(alpha, r->y, v.y), fmaf(alpha, r->z, v.z), 0.f);
     v0 = v.x; v1 = v.y; v2 = v.z;
-    if (m.a_sorted) {
-      const double f = m.a_sorted[j];
+    if (scaled) {
       v0 *= f; v1 *= f; v2 *= f;
     }
     a = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
   } else {
-    v0 = m.scal[j];
-    if (m.a_sorted) v0 *= (double)m.a_sorted[j];
+    v0 = v.x;
+    if (scaled) v0 *= f;
     a = fabs(v0);
   }
   const double px = x.x, py = x.y, pz = x.z;
@@ -294,6 +290,22 @@ __device__ __forceinline__ void point_vals(int64_t j, const float4* __restrict__
       o[9] = v0 * pz;
     }
   }
+}
+
+template <int KIND, int ORD>
+__device__ __forceinline__ void point_vals(int64_t j, const float4* __restrict__ pts, const MomentArgs& m, float alpha,
+                                           double* o) {
+  float4 v;
+  float4 r;
+  if (KIND == ATTR_VEC) {
+    v = m.vec[j];
+    if (m.axpy_r) r = m.axpy_r[j];
+  } else {
+    v = make_float4(m.scal[j], 0.f, 0.f, 0.f);
+  }
+  const bool scaled = m.a_sorted != nullptr;
+  point_terms<KIND, ORD>(pts[j], v, KIND == ATTR_VEC && m.axpy_r ? &r : nullptr, alpha,
+                         scaled ? (double)m.a_sorted[j] : 1.0, scaled, o);
 }
 
 // scan element: NC double-double sums + the number of points with |ν| > 0 (an exact integer)
@@ -430,6 +442,16 @@ __device__ __forceinline__ void store_pre(double* __restrict__ Eh, float* __rest
   for (int c = 0; c < Lay::EL / 4; ++c) lp[c] = make_float4(l[4 * c], l[4 * c + 1], l[4 * c + 2], l[4 * c + 3]);
 }
 
+// the prefix stages its tile's inputs in shared memory with coalesced loads (points, attribute, r) and the
+// threads then read their consecutive items from there: padded one float4 (float) per 8 so that the
+// stride-8 item reads of a warp are free of bank conflicts
+constexpr int kStageN = kScanTile + kScanTile / 8;
+__device__ __forceinline__ int stage_ix(int jl) { return jl + (jl >> 3); }
+template <int KIND>
+constexpr size_t stage_bytes() {  // points, attribute (float4 / float), r (vector only)
+  return KIND == ATTR_VEC ? 3 * kStageN * sizeof(float4) : kStageN * (sizeof(float4) + sizeof(float));
+}
+
 template <int KIND, int ORD>
 __global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __restrict__ pts, MomentArgs m,
                                                                 int64_t n,
@@ -437,14 +459,47 @@ __global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __
                                                                 const Elt<PreLayout<KIND, ORD>::NC>* __restrict__ tile_tot,
                                                                 double* __restrict__ Eh, float* __restrict__ El) {
   constexpr int NC = PreLayout<KIND, ORD>::NC;
+  extern __shared__ float4 stage[];
+  float4* sp = stage;
+  float4* sv = stage + kStageN;                                   // vector attribute
+  float4* sr = stage + 2 * kStageN;                               // r (μ' = μ + α r)
+  float* ss = reinterpret_cast<float*>(stage + kStageN);          // scalar attribute
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
+  const bool axpy = KIND == ATTR_VEC && m.axpy_r;
+  const bool scaled = m.a_sorted != nullptr;
+  const int64_t base = blockIdx.x * (int64_t)kScanTile;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {  // coalesced staging
+    const int jl = threadIdx.x + k * kScanThreads;
+    const int64_t j = base + jl;
+    if (j < n) {
+      const int x = stage_ix(jl);
+      sp[x] = pts[j];
+      if (KIND == ATTR_VEC) {
+        sv[x] = m.vec[j];
+        if (axpy) sr[x] = m.axpy_r[j];
+      } else {
+        ss[x] = m.scal[j];
+      }
+    }
+  }
+  __syncthreads();
+  auto vals = [&](int jl, double* o) {
+    const int x = stage_ix(jl);
+    const float4 v = KIND == ATTR_VEC ? sv[x] : make_float4(ss[x], 0.f, 0.f, 0.f);
+    float4 r;
+    if (axpy) r = sr[x];
+    point_terms<KIND, ORD>(sp[x], v, axpy ? &r : nullptr, alpha, scaled ? (double)m.a_sorted[base + jl] : 1.0,
+                           scaled, o);
+  };
   Elt<NC> t, tot;
   elt_zero(t);
-  const int64_t j0 = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanItems;  // consecutive ownership
+  const int jl0 = threadIdx.x * kScanItems;  // consecutive ownership
+  const int64_t j0 = base + jl0;
   for (int k = 0; k < kScanItems; ++k)
     if (j0 + k < n) {
       double o[NC];
-      point_vals<KIND, ORD>(j0 + k, pts, m, alpha, o);
+      vals(jl0 + k, o);
       elt_add_point(t, o);
     }
   block_exscan<kScanThreads>(t, tot);
@@ -465,13 +520,20 @@ __global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __
     if (j < n) {
       store_pre<KIND, ORD>(Eh, El, j, t);
       double o[NC];
-      point_vals<KIND, ORD>(j, pts, m, alpha, o);
+      vals(jl0 + k, o);
       elt_add_point(t, o);
-      if (KIND == ATTR_VEC && m.axpy_r) {  // μ' written once here, read by the G traversal
-        const float4 v = m.vec[j], r = m.axpy_r[j];
-        m.axpy_out[j] = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
-      }
       if (j == n - 1) store_pre<KIND, ORD>(Eh, El, n, t);
+    }
+  }
+  if (axpy) {  // μ' written once here (coalesced), read by the G traversal
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const int jl = threadIdx.x + k * kScanThreads;
+      if (base + jl < n) {
+        const int x = stage_ix(jl);
+        const float4 v = sv[x], r = sr[x];
+        m.axpy_out[base + jl] = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
+      }
     }
   }
 }
@@ -579,8 +641,14 @@ void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
     mom_tile_sum<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, tot);
     if (scan) mom_tile_scan<Lay::NC><<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
   }
-  mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, scan ? off : nullptr,
-                                                                    nt > 1 ? tot : nullptr, Eh, El);
+  static bool smem_set = false;  // per instantiation: the staging buffer exceeds the 48 KB default
+  if (!smem_set) {
+    cudaFuncSetAttribute(mom_tile_prefix<KIND, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stage_bytes<KIND>());
+    smem_set = true;
+  }
+  mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, stage_bytes<KIND>(), s>>>(
+      t->pts, m, t->n, scan ? off : nullptr, nt > 1 ? tot : nullptr, Eh, El);
   // per-iteration builds: only the nodes a traversal can read (chain interiors and the children of
   // pseudo-leaves are never visited); the diagnostic export (write_W) builds every node
   const bool all = m.all_nodes || m.write_W || !t->mom_live;
