@@ -36,9 +36,13 @@ __device__ __forceinline__ float dist2(float dx, float dy, float dz) {
   return __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
 }
 
-__device__ __forceinline__ float rsqrt_ftz(float x) {
+// 1/r for a live term, +0 for a dead one (rsqrt(+∞) = +0): live is evaluated as one predicate
+__device__ __forceinline__ float inv_live(bool live, float e2) {
   float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.f32 %0, %2, 0f7F800000, p;\n\t"
+      "rsqrt.approx.ftz.f32 %0, %0;\n\t}"
+      : "=f"(r)
+      : "r"((unsigned)live), "f"(e2));
   return r;
 }
 
@@ -47,19 +51,21 @@ struct Acc {
   float x = 0.f, y = 0.f, z = 0.f;
   double d = 0.0;
   // source at offset e = x_src − x_q (|e|² = e2), attribute V; contributes only if `live`
+  // a dead term takes rsqrt(+∞) = +0, so every factor below is 0 and the accumulators are unchanged
+  // (x + (±0) = x, all other operands finite): one select per term instead of two
   __device__ __forceinline__ void term(bool live, float ex, float ey, float ez, float e2, const float4& V) {
-    const float inv = rsqrt_ftz(live ? e2 : 1.0f);
+    const float inv = inv_live(live, e2);
     if (OP == OP_A) {
-      const float inv3 = live ? inv * inv * inv : 0.0f;
+      const float inv3 = inv * inv * inv;
       x = fmaf(fmaf(ex, V.x, fmaf(ey, V.y, ez * V.z)), inv3, x);
     } else if (OP == OP_AT) {
-      const float c = live ? -V.x * (inv * inv * inv) : 0.0f;
+      const float c = -V.x * (inv * inv * inv);
       x = fmaf(c, ex, x);
       y = fmaf(c, ey, y);
       z = fmaf(c, ez, z);
     } else {
       const float inv2 = inv * inv;
-      const float inv3 = live ? inv2 * inv : 0.0f;
+      const float inv3 = inv2 * inv;
       const float t = 3.0f * fmaf(ex, V.x, fmaf(ey, V.y, ez * V.z)) * inv2;
       x = fmaf(inv3, fmaf(-t, ex, V.x), x);
       y = fmaf(inv3, fmaf(-t, ey, V.y), y);
@@ -73,9 +79,9 @@ struct Acc {
   //   G : (ν − 3(e·ν) e/r² − 6 M e/r² + (15 eᵀMe/r² − 3 tr M) e/r²) / r³       (e = x_B − x_q, ×1/(4π) later)
   __device__ __forceinline__ void term1(bool live, float ex, float ey, float ez, float e2, const float4& V,
                                         const float4& X0, const float4& X1) {
-    const float inv = rsqrt_ftz(live ? e2 : 1.0f);
+    const float inv = inv_live(live, e2);
     const float inv2 = inv * inv;
-    const float inv3 = live ? inv2 * inv : 0.0f;
+    const float inv3 = inv2 * inv;
     if (OP == OP_AT) {
       const float eD = fmaf(ex, X0.x, fmaf(ey, X0.y, ez * X0.z));
       const float k = fmaf(-3.0f * eD, inv2, V.x);
