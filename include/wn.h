@@ -204,8 +204,13 @@ wn_status wn_comm_destroy(wn_comm c);
 enum { WN_SHARD_ALIGN = 256 };
 wn_status wn_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
 /* The query schedule (diagnostic): qorder[N] (device) = sorted-point index at each schedule position —
-   the 3-D Hilbert order the traversals and the multi-GPU shards follow. */
+   the order the traversals (32 consecutive positions per warp) and the multi-GPU shards follow. */
 wn_status wn_tree_schedule(wn_tree t, int32_t* qorder, void* stream);
+/* Which schedule wn_build_tree chose (host outputs, either may be NULL): *kind = 0 Hilbert-curve runs,
+   1 k-d boxes of 32 queries (recursive median splits); stats = warp-level visits of the A traversal over
+   the unit-weight geometry used for the choice: {Hilbert total, Hilbert heaviest warp, k-d total, k-d
+   heaviest warp} (all 0 when no choice was made: N < 4096).  The schedule never changes a result. */
+wn_status wn_tree_schedule_stats(wn_tree t, int32_t* kind, int64_t stats[4]);
 /* The shards wnnc_iterate actually uses for `world` ranks (1..64) on this tree: bounds[world + 1] (host),
    rank r owns schedule positions [bounds[r], bounds[r+1]), multiples of WN_SHARD_ALIGN, split by
    estimated work (the node tests of the A traversal over the unit-weight geometry) so that non-uniform

@@ -217,6 +217,98 @@ static wn_status plan_shards(wn_tree_s* t, int world, wn_comm comm, cudaStream_t
   return WN_OK;
 }
 
+// ---- query schedule: k-d boxes or Hilbert runs (tree_build.cu:kd_schedule / hilbert_schedule) ----
+// Both are permutations of the same queries, so every result is unchanged; what differs is the work of
+// each warp. k-d boxes are more compact (fewer visits in total) but put isolated queries (outliers)
+// together, and a warp of mutually distant queries is a long serial chain that can outlast the rest of
+// the launch (C4: the heaviest warp 1.4× Hilbert's, the A traversal 1.4× slower). The choice counts the
+// warp-level visits of the A traversal over the unit-weight geometry (no cutoff: the shard planner's
+// estimate) under both and keeps k-d only if it visits less in total and its heaviest warp is no heavier
+// than Hilbert's (C4 with k-d: 5 % fewer visits, heaviest warp +7 %, solve +5 %). Deterministic (integer
+// counts): every rank takes the same schedule.
+#ifndef WN_EXP_QSCHED
+#define WN_EXP_QSCHED 2  // 0: Hilbert, 1: k-d, 2: chosen per tree
+#endif
+constexpr int64_t kKdMinPoints = 4096;  // below: Hilbert (the choice would cost more than it saves)
+
+__global__ void __launch_bounds__(1024) k_sum_max(const int32_t* __restrict__ v, int64_t m, long long* __restrict__ out) {
+  __shared__ long long ss[32], sx[32];
+  long long sm = 0, mx = 0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    sm += v[i];
+    mx = max(mx, (long long)v[i]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    ss[threadIdx.x >> 5] = sm;
+    sx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      sm += ss[k];
+      mx = max(mx, sx[k]);
+    }
+    out[0] = sm;
+    out[1] = mx;
+  }
+}
+
+static wn_status schedule_cost(wn_tree_s* t, const int32_t* order, int32_t* wv, long long* dev2, cudaStream_t s) {
+  TravArgs ca = base_args(t, 0.0f);
+  ca.op = OP_A;
+  ca.epi = EPI_PLAIN;
+  ca.nodes = t->set[1];
+  ca.vec = t->it.mu;  // (values unused: only the visits are counted)
+  ca.qorder = order;
+  ca.out_map = nullptr;
+  ca.wvisits = wv;
+  ca.nowork = true;
+  ca.prof_cls = WN_PROF_OTHER;
+  WN_TRY(traverse_visits(ca, s));
+  k_sum_max<<<1, 1024, 0, s>>>(wv, (t->n + 31) / 32, dev2);
+  count_launches(1);
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
+static wn_status choose_schedule(wn_tree_s* t, cudaStream_t s) {
+  t->sched_kind = 0;
+  if (WN_EXP_QSCHED == 0 || t->n < kKdMinPoints) return WN_OK;
+  WN_TRY(ensure_scratch(t, s));
+  const int64_t nw = (t->n + 31) / 32;
+  int32_t *kd = nullptr, *wv = nullptr;
+  long long* dev = nullptr;
+  WN_CUDA(cudaMallocAsync((void**)&kd, t->n * sizeof(int32_t), s));
+  WN_CUDA(cudaMallocAsync((void**)&wv, nw * sizeof(int32_t), s));
+  WN_CUDA(cudaMallocAsync((void**)&dev, 4 * sizeof(long long), s));
+  wn_status st = kd_schedule(t->pts, t->n, kd, s);
+  if (st == WN_OK) st = schedule_cost(t, t->qorder, wv, dev, s);
+  if (st == WN_OK) st = schedule_cost(t, kd, wv, dev + 2, s);
+  long long h[4] = {};
+  if (st == WN_OK) {
+    cudaError_t e = cudaMemcpyAsync(h, dev, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = cuda_status(e, "schedule choice");
+  }
+  if (st == WN_OK) {
+    for (int k = 0; k < 4; ++k) t->sched_stats[k] = h[k];
+    const bool use_kd = WN_EXP_QSCHED == 1 || (h[2] < h[0] && h[3] <= h[1]);
+    if (use_kd) {
+      cudaError_t e = cudaMemcpyAsync(t->qorder, kd, t->n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) st = cuda_status(e, "schedule copy");
+      else t->sched_kind = 1;
+    }
+  }
+  cudaFreeAsync(kd, s);
+  cudaFreeAsync(wv, s);
+  cudaFreeAsync(dev, s);
+  return st;
+}
+
 // route a traversal's outputs into every rank's replica (peer-memory exchange); none when P is null
 static void peer_route(TravArgs& ta, const PeerArena* P, float* const* f, float4* const* v4, int part_slot) {
   if (!P) return;
@@ -445,6 +537,7 @@ wn_status wn_build_tree(const float* pts, int64_t n, int32_t max_depth, void* st
   if (!t) return set_error(WN_ERR_OOM, "host allocation failed");
   cudaGetDevice(&t->device);
   wn_status st = build_tree(pts, n, max_depth, (cudaStream_t)stream, t);
+  if (st == WN_OK) st = choose_schedule(t, (cudaStream_t)stream);
   if (st != WN_OK) {
     cudaStreamSynchronize((cudaStream_t)stream);
     free_tree(t);
@@ -829,6 +922,14 @@ wn_status wn_tree_schedule(wn_tree t, int32_t* qorder, void* stream) {
   return WN_OK;
 }
 
+wn_status wn_tree_schedule_stats(wn_tree t, int32_t* kind, int64_t stats[4]) {
+  if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
+  if (kind) *kind = t->sched_kind;
+  if (stats)
+    for (int k = 0; k < 4; ++k) stats[k] = t->sched_stats[k];
+  return WN_OK;
+}
+
 wn_status wn_shard_plan(wn_tree t, int32_t world, int64_t* bounds, void* stream) {
   if (!t || !bounds || world < 1 || world > kMaxShardRanks) return set_error(WN_ERR_ARG, "bad shard-plan arguments");
   cudaStream_t s = (cudaStream_t)stream;
@@ -854,3 +955,12 @@ wn_status wn_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin,
 }
 
 }  // extern "C"
+
+#ifdef WN_EXP_SETSCHED
+// experiment hook (variant builds only): replace the tree's query schedule with qorder[N] (device)
+extern "C" wn_status wn_exp_set_schedule(wn_tree t, const int32_t* qorder, void* stream) {
+  if (!t || !qorder) return wn::set_error(WN_ERR_ARG, "tree or schedule is NULL");
+  WN_CUDA(cudaMemcpyAsync(t->qorder, qorder, t->n * sizeof(int32_t), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return WN_OK;
+}
+#endif

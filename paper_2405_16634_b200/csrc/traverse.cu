@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
   const float4* __restrict__ Vr = FROZEN ? a.attr : G;    // attributes: V (+1)
   const float w2 = a.w2;
   Acc<OP> acc;
-  int ntest = 0, nfar = 0, nnear = 0, nlive = 0;
+  int ntest = 0, nfar = 0, nnear = 0, nlive = 0, wvis = 0;  // wvis: warp-level visits (counting variant)
   if (active) {
     int sp = 0;
     if (lane == 0) stk[0] = make_int2(0, (int)active);  // the root as a group of one
@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
       const int code = e.x;
       const int cb = code >> 4, ncc = (code & 7) + 1;
       const bool mine = ((uint32_t)e.y >> lane) & 1u;
+      if (COUNT) wvis += ncc;
       {
         for (int k = 0; k < ncc; ++k) {
           const int node = cb + k;
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
               const bool lm = (open >> lane) & 1u;
               const int j1 = a.nrange_pe[node];
               WN_DCHECK(a.nrange_pb[node] >= 0 && j1 <= a.npts && a.nrange_pb[node] < j1, "leaf point range");
+              if (COUNT) wvis += j1 - a.nrange_pb[node];
               for (int j = a.nrange_pb[node]; j < j1; ++j) {
                 const float4 P = __ldg(a.pts + j);
                 float4 Vj;
@@ -484,6 +486,7 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
     }
   }
   if (COUNT) {  // algorithmic work: node tests, representative terms, leaf-point terms, live terms (r ≥ w)
+    if (a.wvisits && active && lane == 0) a.wvisits[kq >> 5] = wvis;  // (lane 0's schedule position / 32)
     if (a.qcounts && valid) {
       const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
       a.qcounts[4 * oq + 0] = ntest;
@@ -647,7 +650,7 @@ void launch_one(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
 
 template <int OP, int EPI>
 void launch(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
-  const bool cnt = a.work || a.qcounts;
+  const bool cnt = a.work || a.qcounts || a.wvisits;
   if (OP == OP_A && EPI == EPI_SQ && a.attr) {  // frozen geometry (transpose-mode A(r)); order 0 only
     if (cnt) launch_one<OP, EPI, true, true, 0>(a, s, grid, smem);
     else launch_one<OP, EPI, false, true, 0>(a, s, grid, smem);
@@ -668,6 +671,61 @@ void launch(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
 __global__ void k_peer_signal(TravArgs a) {
   __threadfence_system();
   for (int r = 0; r < a.world; ++r) atomicAdd_system(a.peer_sig[r], 1ull);
+}
+
+// Warp-level visits of a traversal under a query schedule (the schedule choice's estimate, capi.cu): the
+// same walk as trav_kernel — decisions on the same offset, chains and pseudo-leaves as coded — without
+// terms or leaf-point loads; per 32-query warp, child visits + the points of the leaves it opens.
+__global__ void __launch_bounds__(kTravBlock) trav_visits_kernel(const TravArgs a) {
+  extern __shared__ int2 stk_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int2* stk = stk_all + warp * a.stack_depth;
+  const int64_t kq = a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
+  const bool valid = kq < a.q_end;
+  const int64_t q = (valid && a.qorder) ? (int64_t)a.qorder[kq] : kq;
+  const float4 xq = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t active = __ballot_sync(FULL, valid);
+  if (!active) return;
+  const float4* __restrict__ G = a.nodes.rec;
+  int wv = 0, sp = 1;
+  if (lane == 0) stk[0] = make_int2(0, (int)active);
+  __syncwarp();
+  while (sp > 0) {
+    --sp;
+    const int2 e = stk[sp];
+    __syncwarp();
+    const int cb = e.x >> 4, ncc = (e.x & 7) + 1;
+    const bool mine = ((uint32_t)e.y >> lane) & 1u;
+    wv += ncc;
+    for (int k = 0; k < ncc; ++k) {
+      const int node = cb + k;
+      const float4* rp = rec_at(G, node);
+      const float4 R = __ldg(rp), L = __ldg(rp + 2);
+      const float ex = __fadd_rn(__fsub_rn(R.x, xq.x), L.x), ey = __fadd_rn(__fsub_rn(R.y, xq.y), L.y),
+                  ez = __fadd_rn(__fsub_rn(R.z, xq.z), L.z);
+      const uint32_t open = __ballot_sync(FULL, mine && !(dist2(ex, ey, ez) > R.w));
+      if (open) {
+        const int topo = __float_as_int(__ldg(rp + 1).w);
+        if (topo != 0) {
+          stk[sp] = make_int2(topo, (int)open);
+          ++sp;
+        } else {
+          wv += a.nrange_pe[node] - a.nrange_pb[node];
+        }
+      }
+    }
+  }
+  if (lane == 0) a.wvisits[kq >> 5] = wv;
+}
+
+wn_status traverse_visits(const TravArgs& a, cudaStream_t s) {
+  const int64_t nq = a.q_end - a.q_begin;
+  if (nq <= 0) return WN_OK;
+  const size_t smem = (size_t)(kTravBlock / 32) * a.stack_depth * sizeof(int2);
+  trav_visits_kernel<<<(unsigned)trav_blocks(nq), kTravBlock, smem, s>>>(a);
+  count_launches(1);
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
 }
 
 wn_status traverse(const TravArgs& a, cudaStream_t s) {

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "wn_internal.cuh"
 
@@ -524,7 +525,8 @@ wn_status scan_excl(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* tota
 
 // stable LSD radix sort of (key, value) pairs on the low `bits` bits of the keys; ka / va are consumed,
 // the values in key order are copied to out
-static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int32_t* out, cudaStream_t s) {
+static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int32_t* out, cudaStream_t s,
+                            uint64_t* kout = nullptr) {
   const int ntiles = (int)((n + kSortTile - 1) / kSortTile);
   uint64_t* kb = nullptr;
   int32_t* vb = nullptr;
@@ -543,6 +545,7 @@ static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int3
     std::swap(va, vb);
   }
   WN_CUDA(cudaMemcpyAsync(out, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  if (kout) WN_CUDA(cudaMemcpyAsync(kout, ka, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
   cudaFreeAsync(own_k, s);
   cudaFreeAsync(own_v, s);
   cudaFreeAsync(hist, s);
@@ -566,6 +569,154 @@ wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStr
   }
   cudaFreeAsync(ka, s);
   cudaFreeAsync(va, s);
+  return WN_OK;
+}
+
+// ---- k-d query schedule -----------------------------------------------------------------------------
+// A warp takes 32 consecutive schedule positions. Grouping them by recursive median splits — k-d boxes of
+// 32 queries — instead of Hilbert-curve runs makes a warp's queries more compact, so fewer child groups
+// are visited with a partial lane mask (C3: −9 % warp-level visits). Level-synchronous on the GPU: every
+// segment of the current order holding more than 32 queries is stably sorted along the axis of its
+// largest robust extent and split at a multiple of 32 (left part: ⌊⌈m/32⌉/2⌋·32 queries).
+constexpr int kKdQBits = 16;  // coordinate quantization of the sort keys (ties keep the previous order)
+
+__global__ void kd_iota(int64_t n, int32_t* __restrict__ order, int32_t* __restrict__ seg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  order[i] = (int32_t)i;
+  seg[i] = 0;
+}
+
+// split axis of each segment: the extent of a 16-point sample (evenly spaced in the current order) without
+// its two extremes per side — robust to the few far outliers that would otherwise select the normal axis
+// of a thin surface patch; 3 = no split (≤ 32 queries)
+__global__ void kd_axes(const float4* __restrict__ pts, const int32_t* __restrict__ order,
+                        const int32_t* __restrict__ sb, const int32_t* __restrict__ se, int nseg,
+                        uint8_t* __restrict__ axis) {
+  const int sg = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sg >= nseg) return;
+  const int b = sb[sg], m = se[sg] - b;
+  if (m <= 32) {
+    axis[sg] = 3;
+    return;
+  }
+  float best = -1.f;
+  int ax = 0;
+  for (int c = 0; c < 3; ++c) {
+    float v[16];
+    for (int k = 0; k < 16; ++k) {
+      const float4 p = pts[order[b + (int)(((int64_t)k * m) / 16)]];
+      v[k] = c == 0 ? p.x : (c == 1 ? p.y : p.z);
+    }
+    for (int i = 1; i < 16; ++i) {  // insertion sort of the sample
+      const float x = v[i];
+      int j = i - 1;
+      while (j >= 0 && v[j] > x) {
+        v[j + 1] = v[j];
+        --j;
+      }
+      v[j + 1] = x;
+    }
+    const float e = v[13] - v[2];
+    if (e > best) {
+      best = e;
+      ax = c;
+    }
+  }
+  axis[sg] = (uint8_t)ax;
+}
+
+__global__ void kd_keys(const float4* __restrict__ pts, const int32_t* __restrict__ order,
+                        const int32_t* __restrict__ seg, const uint8_t* __restrict__ axis, int64_t n,
+                        uint64_t* __restrict__ key, int32_t* __restrict__ val) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int sg = seg[i], ax = axis[sg];
+  const int32_t q = order[i];
+  uint32_t c = 0;
+  if (ax < 3) {
+    const float4 p = pts[q];
+    c = quantize(ax == 0 ? p.x : (ax == 1 ? p.y : p.z), kKdQBits);
+  }
+  key[i] = ((uint64_t)sg << kKdQBits) | c;
+  val[i] = q;
+}
+
+// after the sort: each query's half of its segment, and the children's ranges (segment 2s: left, 2s+1: right)
+__global__ void kd_split(const uint64_t* __restrict__ skey, int64_t n, const int32_t* __restrict__ sb,
+                         const int32_t* __restrict__ se, int32_t* __restrict__ seg, int32_t* __restrict__ sb2,
+                         int32_t* __restrict__ se2) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int sg = (int)(skey[i] >> kKdQBits);
+  const int b = sb[sg], e = se[sg], m = e - b;
+  const int left = m > 32 ? (((m + 31) / 32) / 2) * 32 : m;
+  seg[i] = 2 * sg + ((int)i - b >= left ? 1 : 0);
+  if (i == b) {
+    sb2[2 * sg] = b;
+    se2[2 * sg] = b + left;
+    sb2[2 * sg + 1] = b + left;
+    se2[2 * sg + 1] = e;
+  }
+}
+
+wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s) {
+  if (n <= 0) return WN_OK;
+  int levels = 0;  // splits until every segment holds ≤ 32 queries (from the sizes alone)
+  {
+    std::vector<int64_t> sz{n};
+    while (*std::max_element(sz.begin(), sz.end()) > 32) {
+      std::vector<int64_t> nx;
+      for (int64_t m : sz) {
+        if (m <= 32) continue;
+        const int64_t left = (((m + 31) / 32) / 2) * 32;
+        nx.push_back(left);
+        nx.push_back(m - left);
+      }
+      std::sort(nx.begin(), nx.end());
+      nx.erase(std::unique(nx.begin(), nx.end()), nx.end());
+      sz.swap(nx);
+      ++levels;
+    }
+  }
+  const int64_t maxseg = (int64_t)1 << levels;
+  uint64_t *key = nullptr, *skey = nullptr;
+  int32_t *val = nullptr, *seg = nullptr, *sb = nullptr, *se = nullptr, *sb2 = nullptr, *se2 = nullptr;
+  uint8_t* axis = nullptr;
+  WN_TRY(dalloc(&key, n, s));
+  WN_TRY(dalloc(&skey, n, s));
+  WN_TRY(dalloc(&val, n, s));
+  WN_TRY(dalloc(&seg, n, s));
+  WN_TRY(dalloc(&sb, maxseg, s));
+  WN_TRY(dalloc(&se, maxseg, s));
+  WN_TRY(dalloc(&sb2, maxseg, s));
+  WN_TRY(dalloc(&se2, maxseg, s));
+  WN_TRY(dalloc(&axis, maxseg, s));
+  const unsigned g = (unsigned)((n + 255) / 256);
+  {
+    ProfScope ps(WN_PROF_TREE, s, 0);
+    kd_iota<<<g, 256, 0, s>>>(n, order, seg);
+    const int32_t init[2] = {0, (int32_t)n};
+    WN_CUDA(cudaMemcpyAsync(sb, &init[0], sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    WN_CUDA(cudaMemcpyAsync(se, &init[1], sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    for (int L = 0; L < levels; ++L) {
+      const int nseg = 1 << L;
+      kd_axes<<<(nseg + 127) / 128, 128, 0, s>>>(pts, order, sb, se, nseg, axis);
+      kd_keys<<<g, 256, 0, s>>>(pts, order, seg, axis, n, key, val);
+      WN_TRY(sort_pairs(key, val, n, kKdQBits + L, order, s, skey));
+      WN_CUDA(cudaMemsetAsync(sb2, 0, 2 * (size_t)nseg * sizeof(int32_t), s));
+      WN_CUDA(cudaMemsetAsync(se2, 0, 2 * (size_t)nseg * sizeof(int32_t), s));
+      kd_split<<<g, 256, 0, s>>>(skey, n, sb, se, seg, sb2, se2);
+      std::swap(sb, sb2);
+      std::swap(se, se2);
+      count_launches(3);
+    }
+    count_launches(1);
+    WN_CUDA(cudaGetLastError());
+  }
+  for (void* p : {(void*)key, (void*)skey, (void*)val, (void*)seg, (void*)sb, (void*)se, (void*)sb2, (void*)se2,
+                  (void*)axis})
+    cudaFreeAsync(p, s);
   return WN_OK;
 }
 

@@ -80,7 +80,9 @@ struct wn_tree_s {
   float4* pts = nullptr;        // N normalized points, Morton order (w unused)
   int32_t* perm = nullptr;      // sorted position → caller index
   uint64_t* keys = nullptr;     // sorted keys
-  int32_t* qorder = nullptr;    // query schedule: sorted point indices in Hilbert order (or null)
+  int32_t* qorder = nullptr;    // query schedule: sorted point indices in k-d or Hilbert order (or null)
+  int sched_kind = 0;           // 0: Hilbert runs, 1: k-d boxes (capi.cu:choose_schedule)
+  long long sched_stats[4] = {};  // warp-level visits of the estimate: Hilbert total, max; k-d total, max
   int32_t* depth = nullptr;     // per node (BFS)
   int32_t* pb = nullptr;
   int32_t* pe = nullptr;
@@ -146,6 +148,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 void free_tree(wn_tree_s* t);
 // order[k] = index of the k-th of n points along a 3-D Hilbert curve of [−1,1]^3 (query schedule)
 wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s);
+wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s);
 
 // ---- moments (moments.cu) ----
 // Build node records for attribute `kind` into `out`.  vec: float4 ν (sorted order), scal: float s.
@@ -211,6 +214,7 @@ struct TravArgs {
   int64_t nnodes = 0, npts = 0;     // sizes (WN_DEBUG bounds checks)
   int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
   int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order
+  int32_t* wvisits = nullptr;       // optional (counting variant, one-warp kernel): per schedule warp, child visits + leaf points
   // peer-memory exchange (multi-GPU, fused): the epilogue stores its row / block partial into every rank's
   // replica and the last block signals every rank; world = 0 ⇒ local outputs only
   int world = 0;
@@ -221,6 +225,7 @@ struct TravArgs {
   unsigned int* done = nullptr;
 };
 wn_status traverse(const TravArgs& a, cudaStream_t s);
+wn_status traverse_visits(const TravArgs& a, cudaStream_t s);  // per-warp visits only (a.wvisits)
 
 // ---- peer-memory exchange arena (comm.cu): every rank's replicas of the exchanged arrays ----
 struct PeerArena {

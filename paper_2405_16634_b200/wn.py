@@ -29,7 +29,8 @@ EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", 
             "wn_tree_destroy", "wn_tree_info", "wn_tree_export", "wn_moments", "wn_eval", "wn_eval_grad",
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
             "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work",
-            "wn_tree_set_far_order", "wnnc_iterate_emulated", "wn_shard_plan", "wn_tree_schedule")
+            "wn_tree_set_far_order", "wnnc_iterate_emulated", "wn_shard_plan", "wn_tree_schedule",
+            "wn_tree_schedule_stats")
 
 
 class wnnc_params(C.Structure):
@@ -61,6 +62,7 @@ _sig = {
     "wnnc_iterate_emulated": ([P, P, P, I32, P, P], I32),
     "wn_shard_plan": ([P, I32, P, P], I32),
     "wn_tree_schedule": ([P, P, P], I32),
+    "wn_tree_schedule_stats": ([P, P, P], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -305,10 +307,19 @@ def wnnc_iterate_emulated(tree: Tree, mu: torch.Tensor, world: int, **params):
 
 
 def wn_tree_schedule(tree: Tree) -> torch.Tensor:
-    """Sorted-point index at each position of the query schedule (3-D Hilbert order)."""
+    """Sorted-point index at each position of the query schedule (k-d boxes or Hilbert runs)."""
     out = torch.empty(tree.n, dtype=torch.int32, device=tree.device)
     _check(_L.wn_tree_schedule(tree.handle, _ptr(out), _stream()))
     return out
+
+
+def wn_tree_schedule_stats(tree: Tree):
+    """("kd" | "hilbert", {hilbert_total, hilbert_max, kd_total, kd_max}) — the estimate behind the choice."""
+    kind = C.c_int32(0)
+    st = (C.c_int64 * 4)()
+    _check(_L.wn_tree_schedule_stats(tree.handle, C.byref(kind), st))
+    keys = ("hilbert_total", "hilbert_max", "kd_total", "kd_max")
+    return ("kd" if kind.value == 1 else "hilbert"), dict(zip(keys, list(st)))
 
 
 def wn_shard_plan(tree: Tree, world: int):

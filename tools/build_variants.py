@@ -4,7 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_16634_b200 import build as b
 VARIANTS = {
     "base": [],
-    "debug": ["WN_DEBUG"],  # device-side bounds checks (trap on violation)
+    "debug": ["WN_DEBUG"],
+    "setsched": ["WN_EXP_SETSCHED"],  # wn_exp_set_schedule hook for tools/sched_exp.py  # device-side bounds checks (trap on violation)
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
