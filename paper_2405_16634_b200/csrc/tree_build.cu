@@ -660,12 +660,150 @@ __global__ void kd_split(const uint64_t* __restrict__ skey, int64_t n, const int
   }
 }
 
+// the last levels of a segment of ≤ kKdLocal queries inside one block: the same splits, the sort a bitonic
+// sort in shared memory on unique keys (sub-segment, coordinate, position): equal coordinates keep the
+// previous order, as in the global levels
+constexpr int kKdLocal = 2048;
+__device__ __forceinline__ unsigned long long kd_fkey(float f) {  // order-preserving float → 32-bit key
+  const uint32_t u = __float_as_uint(f);
+  return (unsigned long long)((u & 0x80000000u) ? ~u : (u | 0x80000000u));
+}
+
+__global__ void __launch_bounds__(1024) kd_local(const float4* __restrict__ pts, int32_t* __restrict__ order,
+                                                 const int32_t* __restrict__ sb, const int32_t* __restrict__ se) {
+  __shared__ unsigned long long key[kKdLocal];
+  __shared__ int32_t id[kKdLocal];  // (coordinates re-read from pts: L1/L2-resident)
+  __shared__ uint8_t sid[kKdLocal];
+  __shared__ int16_t ssb[128], sse[128], nsb[128], nse[128];
+  __shared__ uint8_t sax[128];
+  __shared__ int nsub, more;
+  const int b = sb[blockIdx.x], m = se[blockIdx.x] - b, tid = threadIdx.x;
+  if (m <= 32) return;  // (uniform: one segment per block)
+  for (int i = tid; i < m; i += 1024) {
+    id[i] = order[b + i];
+    sid[i] = 0;
+  }
+  if (tid == 0) {
+    nsub = 1;
+    ssb[0] = 0;
+    sse[0] = (int16_t)m;
+  }
+  __syncthreads();
+  int M = 32;
+  while (M < m) M <<= 1;
+  for (;;) {
+    if (tid == 0) {
+      int mo = 0;
+      for (int k = 0; k < nsub; ++k) mo |= (sse[k] - ssb[k]) > 32;
+      more = mo;
+    }
+    __syncthreads();
+    if (!more) break;
+    if (tid < nsub) {  // split axis (as kd_axes: robust extent of a 16-point sample)
+      const int bb = ssb[tid], mm = sse[tid] - bb;
+      int ax = 3;
+      if (mm > 32) {
+        float best = -1.f;
+        for (int c = 0; c < 3; ++c) {
+          float v[16];
+          for (int k = 0; k < 16; ++k) {
+            const float4 p = pts[id[bb + (k * mm) / 16]];
+            v[k] = c == 0 ? p.x : (c == 1 ? p.y : p.z);
+          }
+          for (int i = 1; i < 16; ++i) {
+            const float x = v[i];
+            int j = i - 1;
+            while (j >= 0 && v[j] > x) {
+              v[j + 1] = v[j];
+              --j;
+            }
+            v[j + 1] = x;
+          }
+          const float e = v[13] - v[2];
+          if (e > best) {
+            best = e;
+            ax = c;
+          }
+        }
+      }
+      sax[tid] = (uint8_t)ax;
+    }
+    __syncthreads();
+    for (int i = tid; i < M; i += 1024) {
+      if (i < m) {
+        const int g = sid[i], ax = sax[g];
+        unsigned long long c = 0ull;
+        if (ax < 3) {
+          const float4 p = pts[id[i]];
+          c = kd_fkey(ax == 0 ? p.x : (ax == 1 ? p.y : p.z));
+        }
+        key[i] = ((unsigned long long)g << 43) | (c << 11) | (unsigned long long)i;
+      } else {
+        key[i] = ~0ull;
+      }
+    }
+    __syncthreads();
+    for (int k = 2; k <= M; k <<= 1)  // bitonic sort, ascending
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < M; i += 1024) {
+          const int l = i ^ j;
+          if (l > i) {
+            const unsigned long long x = key[i], y = key[l];
+            if (((i & k) == 0) == (x > y)) {
+              key[i] = y;
+              key[l] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    // gather into the new order, then the children's ranges and each query's child
+    int32_t rid[2];
+    uint8_t rs[2];
+    for (int r = 0; r < 2; ++r) {
+      const int i = tid + r * 1024;
+      if (i < m) {
+        const int src = (int)(key[i] & 0x7FFull);
+        rid[r] = id[src];
+        rs[r] = (uint8_t)(key[i] >> 43);
+      }
+    }
+    __syncthreads();
+    for (int r = 0; r < 2; ++r) {
+      const int i = tid + r * 1024;
+      if (i < m) {
+        id[i] = rid[r];
+        const int g = rs[r], bb = ssb[g], mm = sse[g] - bb;
+        const int left = mm > 32 ? (((mm + 31) / 32) / 2) * 32 : mm;
+        sid[i] = (uint8_t)(2 * g + (i - bb >= left ? 1 : 0));
+      }
+    }
+    if (tid < nsub) {
+      const int bb = ssb[tid], mm = sse[tid] - bb;
+      const int left = mm > 32 ? (((mm + 31) / 32) / 2) * 32 : mm;
+      nsb[2 * tid] = (int16_t)bb;
+      nse[2 * tid] = (int16_t)(bb + left);
+      nsb[2 * tid + 1] = (int16_t)(bb + left);
+      nse[2 * tid + 1] = (int16_t)(bb + mm);
+    }
+    __syncthreads();
+    if (tid < 2 * nsub) {
+      ssb[tid] = nsb[tid];
+      sse[tid] = nse[tid];
+    }
+    __syncthreads();
+    if (tid == 0) nsub *= 2;
+    __syncthreads();
+  }
+  for (int i = tid; i < m; i += 1024) order[b + i] = id[i];
+}
+
 wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s) {
   if (n <= 0) return WN_OK;
-  int levels = 0;  // splits until every segment holds ≤ 32 queries (from the sizes alone)
+  int levels = 0;  // global splits until every segment holds ≤ kKdLocal queries (from the sizes alone)
   {
     std::vector<int64_t> sz{n};
-    while (*std::max_element(sz.begin(), sz.end()) > 32) {
+    while (*std::max_element(sz.begin(), sz.end()) > kKdLocal) {
       std::vector<int64_t> nx;
       for (int64_t m : sz) {
         if (m <= 32) continue;
@@ -711,7 +849,8 @@ wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t
       std::swap(se, se2);
       count_launches(3);
     }
-    count_launches(1);
+    kd_local<<<(unsigned)(1u << levels), 1024, 0, s>>>(pts, order, sb, se);
+    count_launches(2);
     WN_CUDA(cudaGetLastError());
   }
   for (void* p : {(void*)key, (void*)skey, (void*)val, (void*)seg, (void*)sb, (void*)se, (void*)sb2, (void*)se2,
