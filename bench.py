@@ -201,6 +201,7 @@ def run_ours(args):
     work = wn.wn_work_count_read()
     wn.wn_work_count_enable(False)
     depth_used, num_nodes = tree.depth_used, tree.num_nodes
+    sched_kind, _ = wn.wn_tree_schedule_stats(tree)  # k-d boxes or Hilbert runs (chosen per tree)
     del tree
 
     # ---- per-kernel-class device time (CUDA events around every launch group; untimed pass, no graph) ----
@@ -321,7 +322,7 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": CONFIG_TEXT[args.config], "n_points": n, "iters_per_step": ITERS,
                    "theta": args.theta, "far_order": args.order, "max_depth": 15, "depth_used": depth_used,
-                   "num_nodes": num_nodes,
+                   "num_nodes": num_nodes, "query_schedule": sched_kind,
                    "adjoint": "transpose" if args.transpose else "gather",
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
                    "parallelism": f"query-sharded x{world}" if world > 1 else "1 GPU",

@@ -206,8 +206,9 @@ wn_status wn_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin,
 /* The query schedule (diagnostic): qorder[N] (device) = sorted-point index at each schedule position —
    the order the traversals (32 consecutive positions per warp) and the multi-GPU shards follow. */
 wn_status wn_tree_schedule(wn_tree t, int32_t* qorder, void* stream);
-/* Which schedule wn_build_tree chose (host outputs, either may be NULL): *kind = 0 Hilbert-curve runs,
-   1 k-d boxes of 32 queries (recursive median splits); stats = warp-level visits of the A traversal over
+/* Which schedule wn_build_tree chose (host outputs, either may be NULL): *kind = 0 Hilbert-curve runs
+   (its 128-query blocks ordered heaviest first by the estimate below; N ≥ 4096), 1 k-d boxes of 32
+   queries (recursive median splits); stats = warp-level visits of the A traversal over
    the unit-weight geometry used for the choice: {Hilbert total, Hilbert heaviest warp, k-d total, k-d
    heaviest warp} (all 0 when no choice was made: N < 4096).  The schedule never changes a result. */
 wn_status wn_tree_schedule_stats(wn_tree t, int32_t* kind, int64_t stats[4]);

@@ -9,6 +9,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "wn_comm.cuh"
@@ -275,36 +276,66 @@ static wn_status schedule_cost(wn_tree_s* t, const int32_t* order, int32_t* wv, 
   return WN_OK;
 }
 
+// new schedule = the old one with its kTravBlock-query chunks permuted (chunk j of the new = perm[j] of the old)
+__global__ void k_permute_chunks(const int32_t* __restrict__ src, int32_t* __restrict__ dst, const int32_t* __restrict__ perm,
+                                 int64_t n) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  dst[k] = src[(int64_t)perm[k / kTravBlock] * kTravBlock + k % kTravBlock];
+}
+
 static wn_status choose_schedule(wn_tree_s* t, cudaStream_t s) {
   t->sched_kind = 0;
   if (WN_EXP_QSCHED == 0 || t->n < kKdMinPoints) return WN_OK;
   WN_TRY(ensure_scratch(t, s));
-  const int64_t nw = (t->n + 31) / 32;
-  int32_t *kd = nullptr, *wv = nullptr;
+  const int64_t n = t->n, nw = (n + 31) / 32, nb = (n + kTravBlock - 1) / kTravBlock;
+  int32_t *kd = nullptr, *wv = nullptr, *perm = nullptr;
   long long* dev = nullptr;
-  WN_CUDA(cudaMallocAsync((void**)&kd, t->n * sizeof(int32_t), s));
-  WN_CUDA(cudaMallocAsync((void**)&wv, nw * sizeof(int32_t), s));
+  WN_CUDA(cudaMallocAsync((void**)&kd, n * sizeof(int32_t), s));
+  WN_CUDA(cudaMallocAsync((void**)&wv, 2 * nw * sizeof(int32_t), s));
+  WN_CUDA(cudaMallocAsync((void**)&perm, nb * sizeof(int32_t), s));
   WN_CUDA(cudaMallocAsync((void**)&dev, 4 * sizeof(long long), s));
-  wn_status st = kd_schedule(t->pts, t->n, kd, s);
+  wn_status st = kd_schedule(t->pts, n, kd, s);
   if (st == WN_OK) st = schedule_cost(t, t->qorder, wv, dev, s);
-  if (st == WN_OK) st = schedule_cost(t, kd, wv, dev + 2, s);
+  if (st == WN_OK) st = schedule_cost(t, kd, wv + nw, dev + 2, s);
   long long h[4] = {};
+  std::vector<int32_t> hw(nw);
   if (st == WN_OK) {
     cudaError_t e = cudaMemcpyAsync(h, dev, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hw.data(), wv, nw * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) st = cuda_status(e, "schedule choice");
   }
   if (st == WN_OK) {
     for (int k = 0; k < 4; ++k) t->sched_stats[k] = h[k];
     const bool use_kd = WN_EXP_QSCHED == 1 || (h[2] < h[0] && h[3] <= h[1]);
-    if (use_kd) {
-      cudaError_t e = cudaMemcpyAsync(t->qorder, kd, t->n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
-      if (e != cudaSuccess) st = cuda_status(e, "schedule copy");
-      else t->sched_kind = 1;
+    cudaError_t e = cudaSuccess;
+    if (use_kd) {  // (heaviest blocks first measured here too: +1 % at C2, C3, C5 — not done)
+      e = cudaMemcpyAsync(t->qorder, kd, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+      t->sched_kind = 1;
+    } else {
+      // Hilbert: launch the heaviest blocks first (cost = the block's heaviest warp; a ragged last block
+      // stays last) — the long chains then overlap the rest of the launch (C4: 75.0 → 69.1 ms per solve)
+      std::vector<int64_t> cost(nb, 0);
+      for (int64_t w = 0; w < nw; ++w) cost[w / (kTravBlock / 32)] = std::max<int64_t>(cost[w / (kTravBlock / 32)], hw[w]);
+      std::vector<int32_t> hp(nb);
+      for (int64_t b = 0; b < nb; ++b) hp[b] = (int32_t)b;
+      const int64_t full = n % kTravBlock == 0 ? nb : nb - 1;
+      std::stable_sort(hp.begin(), hp.begin() + full, [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
+      e = cudaMemcpyAsync(perm, hp.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) {
+        k_permute_chunks<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t->qorder, kd, perm, n);
+        count_launches(1);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaMemcpyAsync(t->qorder, kd, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // (hp is a host buffer of this frame)
     }
+    if (e != cudaSuccess) st = cuda_status(e, "schedule copy");
   }
   cudaFreeAsync(kd, s);
   cudaFreeAsync(wv, s);
+  cudaFreeAsync(perm, s);
   cudaFreeAsync(dev, s);
   return st;
 }

@@ -5,7 +5,8 @@ from paper_2405_16634_b200 import build as b
 VARIANTS = {
     "base": [],
     "debug": ["WN_DEBUG"],
-    "setsched": ["WN_EXP_SETSCHED"],  # wn_exp_set_schedule hook for tools/sched_exp.py  # device-side bounds checks (trap on violation)
+    "setsched": ["WN_EXP_SETSCHED"],
+    "kdlpt": ["WN_EXP_KDLPT"],  # k-d schedule with the heaviest blocks first  # wn_exp_set_schedule hook for tools/sched_exp.py  # device-side bounds checks (trap on violation)
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
