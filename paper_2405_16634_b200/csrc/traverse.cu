@@ -707,6 +707,7 @@ __global__ void __launch_bounds__(kTravBlock) trav_visits_kernel(const TravArgs 
       if (open) {
         const int topo = __float_as_int(__ldg(rp + 1).w);
         if (topo != 0) {
+          WN_DCHECK(sp < a.stack_depth, "visit-count stack");
           stk[sp] = make_int2(topo, (int)open);
           ++sp;
         } else {

@@ -650,6 +650,7 @@ __global__ void kd_split(const uint64_t* __restrict__ skey, int64_t n, const int
   if (i >= n) return;
   const int sg = (int)(skey[i] >> kKdQBits);
   const int b = sb[sg], e = se[sg], m = e - b;
+  WN_DCHECK(b <= i && i < e, "k-d segment of a query");
   const int left = m > 32 ? (((m + 31) / 32) / 2) * 32 : m;
   seg[i] = 2 * sg + ((int)i - b >= left ? 1 : 0);
   if (i == b) {
@@ -678,6 +679,7 @@ __global__ void __launch_bounds__(1024) kd_local(const float4* __restrict__ pts,
   __shared__ uint8_t sax[128];
   __shared__ int nsub, more;
   const int b = sb[blockIdx.x], m = se[blockIdx.x] - b, tid = threadIdx.x;
+  WN_DCHECK(b >= 0 && m >= 0 && m <= kKdLocal, "k-d local segment");
   if (m <= 32) return;  // (uniform: one segment per block)
   for (int i = tid; i < m; i += 1024) {
     id[i] = order[b + i];
