@@ -209,8 +209,9 @@ wn_status wn_tree_schedule(wn_tree t, int32_t* qorder, void* stream);
 /* Which schedule wn_build_tree chose (host outputs, either may be NULL): *kind = 0 Hilbert-curve runs
    (its 128-query blocks ordered heaviest first by the estimate below; N ≥ 4096), 1 k-d boxes of 32
    queries (recursive median splits); stats = warp-level visits of the A traversal over
-   the unit-weight geometry used for the choice: {Hilbert total, Hilbert heaviest warp, k-d total, k-d
-   heaviest warp} (all 0 when no choice was made: N < 4096).  The schedule never changes a result. */
+   the unit-weight geometry, counted on every 4th warp of each schedule, used for the choice: {Hilbert
+   total, Hilbert heaviest warp, k-d total, k-d heaviest warp} (all 0 when no choice was made:
+   N < 4096).  The schedule never changes a result. */
 wn_status wn_tree_schedule_stats(wn_tree t, int32_t* kind, int64_t stats[4]);
 /* The shards wnnc_iterate actually uses for `world` ranks (1..64) on this tree: bounds[world + 1] (host),
    rank r owns schedule positions [bounds[r], bounds[r+1]), multiples of WN_SHARD_ALIGN, split by

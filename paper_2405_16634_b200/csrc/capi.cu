@@ -231,6 +231,7 @@ static wn_status plan_shards(wn_tree_s* t, int world, wn_comm comm, cudaStream_t
 #define WN_EXP_QSCHED 2  // 0: Hilbert, 1: k-d, 2: chosen per tree
 #endif
 constexpr int64_t kKdMinPoints = 4096;  // below: Hilbert (the choice would cost more than it saves)
+constexpr int kSampleStride = 4;        // the choice counts every 4th warp of each schedule
 
 __global__ void __launch_bounds__(1024) k_sum_max(const int32_t* __restrict__ v, int64_t m, long long* __restrict__ out) {
   __shared__ long long ss[32], sx[32];
@@ -258,7 +259,8 @@ __global__ void __launch_bounds__(1024) k_sum_max(const int32_t* __restrict__ v,
   }
 }
 
-static wn_status schedule_cost(wn_tree_s* t, const int32_t* order, int32_t* wv, long long* dev2, cudaStream_t s) {
+static wn_status schedule_cost(wn_tree_s* t, const int32_t* order, int stride, int32_t* wv, long long* dev2,
+                               cudaStream_t s) {
   TravArgs ca = base_args(t, 0.0f);
   ca.op = OP_A;
   ca.epi = EPI_PLAIN;
@@ -267,10 +269,11 @@ static wn_status schedule_cost(wn_tree_s* t, const int32_t* order, int32_t* wv, 
   ca.qorder = order;
   ca.out_map = nullptr;
   ca.wvisits = wv;
+  ca.wstride = stride;
   ca.nowork = true;
   ca.prof_cls = WN_PROF_OTHER;
   WN_TRY(traverse_visits(ca, s));
-  k_sum_max<<<1, 1024, 0, s>>>(wv, (t->n + 31) / 32, dev2);
+  k_sum_max<<<1, 1024, 0, s>>>(wv, ((t->n + 31) / 32 + stride - 1) / stride, dev2);
   count_launches(1);
   WN_CUDA(cudaGetLastError());
   return WN_OK;
@@ -295,20 +298,28 @@ static wn_status choose_schedule(wn_tree_s* t, cudaStream_t s) {
   WN_CUDA(cudaMallocAsync((void**)&wv, 2 * nw * sizeof(int32_t), s));
   WN_CUDA(cudaMallocAsync((void**)&perm, nb * sizeof(int32_t), s));
   WN_CUDA(cudaMallocAsync((void**)&dev, 4 * sizeof(long long), s));
+  // the choice compares every kSampleStride-th warp of both schedules (the sample total, its heaviest warp);
+  // the heaviest-first Hilbert order below counts every warp
   wn_status st = kd_schedule(t->pts, n, kd, s);
-  if (st == WN_OK) st = schedule_cost(t, t->qorder, wv, dev, s);
-  if (st == WN_OK) st = schedule_cost(t, kd, wv + nw, dev + 2, s);
+  if (st == WN_OK) st = schedule_cost(t, t->qorder, kSampleStride, wv, dev, s);
+  if (st == WN_OK) st = schedule_cost(t, kd, kSampleStride, wv + nw, dev + 2, s);
   long long h[4] = {};
-  std::vector<int32_t> hw(nw);
   if (st == WN_OK) {
     cudaError_t e = cudaMemcpyAsync(h, dev, sizeof(h), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hw.data(), wv, nw * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) st = cuda_status(e, "schedule choice");
   }
+  const bool use_kd = WN_EXP_QSCHED == 1 || (h[2] < h[0] && h[3] <= h[1]);
+  std::vector<int32_t> hw(nw);
+  if (st == WN_OK && !use_kd) {
+    st = schedule_cost(t, t->qorder, 1, wv, dev, s);
+    cudaError_t e = st == WN_OK ? cudaMemcpyAsync(hw.data(), wv, nw * sizeof(int32_t), cudaMemcpyDeviceToHost, s)
+                                : cudaSuccess;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = cuda_status(e, "schedule costs");
+  }
   if (st == WN_OK) {
     for (int k = 0; k < 4; ++k) t->sched_stats[k] = h[k];
-    const bool use_kd = WN_EXP_QSCHED == 1 || (h[2] < h[0] && h[3] <= h[1]);
     cudaError_t e = cudaSuccess;
     if (use_kd) {  // (heaviest blocks first measured here too: +1 % at C2, C3, C5 — not done)
       e = cudaMemcpyAsync(t->qorder, kd, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);

@@ -675,12 +675,14 @@ __global__ void k_peer_signal(TravArgs a) {
 
 // Warp-level visits of a traversal under a query schedule (the schedule choice's estimate, capi.cu): the
 // same walk as trav_kernel — decisions on the same offset, chains and pseudo-leaves as coded — without
-// terms or leaf-point loads; per 32-query warp, child visits + the points of the leaves it opens.
+// terms or leaf-point loads; per 32-query warp (every wstride-th warp of the schedule), child visits + the
+// points of the leaves it opens.
 __global__ void __launch_bounds__(kTravBlock) trav_visits_kernel(const TravArgs a) {
   extern __shared__ int2 stk_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int2* stk = stk_all + warp * a.stack_depth;
-  const int64_t kq = a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
+  const int64_t g = (int64_t)blockIdx.x * (kTravBlock / 32) + warp;  // counted warp → schedule warp g·wstride
+  const int64_t kq = a.q_begin + g * a.wstride * 32 + lane;
   const bool valid = kq < a.q_end;
   const int64_t q = (valid && a.qorder) ? (int64_t)a.qorder[kq] : kq;
   const float4 xq = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -716,14 +718,15 @@ __global__ void __launch_bounds__(kTravBlock) trav_visits_kernel(const TravArgs 
       }
     }
   }
-  if (lane == 0) a.wvisits[kq >> 5] = wv;
+  if (lane == 0) a.wvisits[g] = wv;
 }
 
 wn_status traverse_visits(const TravArgs& a, cudaStream_t s) {
   const int64_t nq = a.q_end - a.q_begin;
   if (nq <= 0) return WN_OK;
   const size_t smem = (size_t)(kTravBlock / 32) * a.stack_depth * sizeof(int2);
-  trav_visits_kernel<<<(unsigned)trav_blocks(nq), kTravBlock, smem, s>>>(a);
+  const int64_t nw = ((nq + 31) / 32 + a.wstride - 1) / a.wstride;  // counted warps
+  trav_visits_kernel<<<(unsigned)((nw + kTravBlock / 32 - 1) / (kTravBlock / 32)), kTravBlock, smem, s>>>(a);
   count_launches(1);
   WN_CUDA(cudaGetLastError());
   return WN_OK;

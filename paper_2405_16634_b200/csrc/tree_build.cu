@@ -600,14 +600,15 @@ __global__ void kd_axes(const float4* __restrict__ pts, const int32_t* __restric
     axis[sg] = 3;
     return;
   }
+  float4 smp[16];  // the 16 sample points, loaded together
+#pragma unroll
+  for (int k = 0; k < 16; ++k) smp[k] = pts[order[b + (int)(((int64_t)k * m) / 16)]];
   float best = -1.f;
   int ax = 0;
   for (int c = 0; c < 3; ++c) {
     float v[16];
-    for (int k = 0; k < 16; ++k) {
-      const float4 p = pts[order[b + (int)(((int64_t)k * m) / 16)]];
-      v[k] = c == 0 ? p.x : (c == 1 ? p.y : p.z);
-    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = c == 0 ? smp[k].x : (c == 1 ? smp[k].y : smp[k].z);
     for (int i = 1; i < 16; ++i) {  // insertion sort of the sample
       const float x = v[i];
       int j = i - 1;
@@ -705,13 +706,14 @@ __global__ void __launch_bounds__(1024) kd_local(const float4* __restrict__ pts,
       const int bb = ssb[tid], mm = sse[tid] - bb;
       int ax = 3;
       if (mm > 32) {
+        float4 smp[16];  // the 16 sample points, loaded together
+#pragma unroll
+        for (int k = 0; k < 16; ++k) smp[k] = pts[id[bb + (k * mm) / 16]];
         float best = -1.f;
         for (int c = 0; c < 3; ++c) {
           float v[16];
-          for (int k = 0; k < 16; ++k) {
-            const float4 p = pts[id[bb + (k * mm) / 16]];
-            v[k] = c == 0 ? p.x : (c == 1 ? p.y : p.z);
-          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = c == 0 ? smp[k].x : (c == 1 ? smp[k].y : smp[k].z);
           for (int i = 1; i < 16; ++i) {
             const float x = v[i];
             int j = i - 1;

@@ -215,6 +215,7 @@ struct TravArgs {
   int64_t* work = nullptr;          // set by traverse(): counting variant accumulates 4 totals
   int32_t* qcounts = nullptr;       // optional per-query (tests, far, leaf points, live terms), output order
   int32_t* wvisits = nullptr;       // optional (counting variant, one-warp kernel): per schedule warp, child visits + leaf points
+  int wstride = 1;                  // traverse_visits: count every wstride-th warp of the schedule (wvisits compact)
   // peer-memory exchange (multi-GPU, fused): the epilogue stores its row / block partial into every rank's
   // replica and the last block signals every rank; world = 0 ⇒ local outputs only
   int world = 0;

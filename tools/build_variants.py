@@ -6,6 +6,8 @@ VARIANTS = {
     "base": [],
     "debug": ["WN_DEBUG"],
     "setsched": ["WN_EXP_SETSCHED"],
+    "tb64": ["WN_EXP_TRAVBLOCK=64"],  # 64-query traversal blocks
+    "tb256": ["WN_EXP_TRAVBLOCK=256"],
     "kdlpt": ["WN_EXP_KDLPT"],  # k-d schedule with the heaviest blocks first  # wn_exp_set_schedule hook for tools/sched_exp.py  # device-side bounds checks (trap on violation)
 }
 names = sys.argv[1:] or list(VARIANTS)
