@@ -539,11 +539,10 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
 // test the root; the root's children are split between them; the child groups of the children the lanes
 // open are dealt round-robin; each warp traverses its share; the partial accumulators are added in warp
 // order (a fixed order: deterministic), and one warp per group runs the epilogue.
-constexpr int kSplit = 4;
-constexpr int kSplitWarps = kSplit * (kTravBlock / 32);
-
-template <int OP, int EPI, bool COUNT, bool FROZEN, int ORD>
-__global__ void __launch_bounds__(kSplitWarps * 32) trav_split_kernel(const TravArgs a) {
+// kSplit = KS ∈ {4, 8}: 8 for ≤ 512 query groups (capi.cu:split_factor; 2k points: −19 % per solve vs 4)
+template <int OP, int EPI, bool COUNT, bool FROZEN, int ORD, int KS>
+__global__ void __launch_bounds__(KS * (kTravBlock / 32) * 32) trav_split_kernel(const TravArgs a) {
+  constexpr int kSplit = KS, kSplitWarps = KS * (kTravBlock / 32);
   constexpr int NG = kTravBlock / 32;  // query groups per block
   extern __shared__ int2 stk_all[];
   __shared__ double red[kSplitWarps];
@@ -644,7 +643,19 @@ __global__ void __launch_bounds__(kSplitWarps * 32) trav_split_kernel(const Trav
 
 template <int OP, int EPI, bool C, bool F, int O>
 void launch_one(const TravArgs& a, cudaStream_t s, unsigned grid, size_t smem) {
-  if (a.split) trav_split_kernel<OP, EPI, C, F, O><<<grid, kSplitWarps * 32, smem * kSplit, s>>>(a);
+  if (a.split == 8) {
+    // eight warps' stacks per group plus the static combine arrays can pass the 48 KB default
+    static const cudaError_t opt = cudaFuncSetAttribute(trav_split_kernel<OP, EPI, C, F, O, 8>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    (void)opt;
+    trav_split_kernel<OP, EPI, C, F, O, 8><<<grid, 8 * kTravBlock, smem * 8, s>>>(a);
+  }
+  else if (a.split) {
+    static const cudaError_t opt = cudaFuncSetAttribute(trav_split_kernel<OP, EPI, C, F, O, 4>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    (void)opt;
+    trav_split_kernel<OP, EPI, C, F, O, 4><<<grid, 4 * kTravBlock, smem * 4, s>>>(a);
+  }
   else trav_kernel<OP, EPI, C, F, O><<<grid, kTravBlock, smem, s>>>(a);
 }
 

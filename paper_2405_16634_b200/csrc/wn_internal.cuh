@@ -208,7 +208,7 @@ struct TravArgs {
   int stack_depth = 128;
   int root_single = 0;              // 1 iff the root is a one-point leaf (n = 1)
   int order1 = 0;                   // first-order far field (nodes.ext), row f2
-  int split = 0;                    // small clouds: several warps per query group (traverse.cu)
+  int split = 0;                    // small clouds: warps per query group (0: one-warp kernel; 4 or 8, traverse.cu)
   bool nowork = false;              // keep this launch out of the wn_work_count totals
   int prof_cls = -1;                // profiling class override (-1: by operator)
   int64_t nnodes = 0, npts = 0;     // sizes (WN_DEBUG bounds checks)
