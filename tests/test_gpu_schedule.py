@@ -99,3 +99,54 @@ def test_small_cloud_no_choice(wn):
     t = wn.wn_build_tree(torch.from_numpy(p).cuda())
     kind, st = wn.wn_tree_schedule_stats(t)
     assert kind == "hilbert" and all(v == 0 for v in st.values())
+
+
+def _hilbert_keys(xn, b=10):  # tree_build.cu:hilbert_keys (Skilling's transform, 10 bits per axis)
+    q = np.clip(np.floor((xn.astype(np.float64) + 1.0) * 2.0 ** (b - 1)), 0, 2 ** b - 1).astype(np.int64)
+    X = [q[:, 0].copy(), q[:, 1].copy(), q[:, 2].copy()]
+    Q = 1 << (b - 1)
+    while Q > 1:
+        P = Q - 1
+        for i in range(3):
+            hit = (X[i] & Q) != 0
+            tt = (X[0] ^ X[i]) & P
+            x0 = np.where(hit, X[0] ^ P, X[0] ^ tt)
+            if i:
+                X[i] = np.where(hit, X[i], X[i] ^ tt)
+            X[0] = x0
+        Q >>= 1
+    for i in (1, 2):
+        X[i] ^= X[i - 1]
+    t = np.zeros_like(X[0])
+    Q = 1 << (b - 1)
+    while Q > 1:
+        t = np.where((X[2] & Q) != 0, t ^ (Q - 1), t)
+        Q >>= 1
+    for i in range(3):
+        X[i] ^= t
+    key = np.zeros(len(xn), np.int64)
+    for bit in range(b - 1, -1, -1):
+        for i in range(3):
+            key = (key << 1) | ((X[i] >> bit) & 1)
+    return key
+
+
+def test_hilbert_schedule_blocks_heaviest_first(wn):
+    # when Hilbert is kept (C4), the schedule is the Hilbert order with its 128-query blocks permuted
+    # (heaviest first by the visit estimate); the ragged last block stays last
+    p = synth.config("C4")["points"]
+    t = wn.wn_build_tree(torch.from_numpy(p).cuda())
+    kind, _ = wn.wn_tree_schedule_stats(t)
+    assert kind == "hilbert"
+    xn = wn.wn_tree_export(t)["xn"].cpu().numpy()
+    ref = np.argsort(_hilbert_keys(xn), kind="stable")
+    got = wn.wn_tree_schedule(t).cpu().numpy()
+    n, B = len(p), 128
+    full = n // B
+    np.testing.assert_array_equal(got[full * B:], ref[full * B:])
+    gb = got[:full * B].reshape(full, B)
+    rb = ref[:full * B].reshape(full, B)
+    key = {tuple(r): k for k, r in enumerate(rb)}
+    idx = [key.get(tuple(g), -1) for g in gb]
+    assert min(idx) >= 0 and sorted(idx) == list(range(full))
+    assert idx != list(range(full))  # (the estimate does reorder the blocks)
