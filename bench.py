@@ -342,6 +342,10 @@ def run_ours(args):
                                % (trav_launches, trav_ms),
                      "peak_note": f"FP32 FMA pipe: {sm_count} SMs x 128 lanes x 2 flop x {fmax:.0f} MHz "
                                   "(sm_max_mhz of MEASURED_PEAKS.json; derived, DESIGN.md §Roofline)",
+                     "bound_note": "the traversals are instruction-issue bound, not FP32-throughput bound: "
+                                   "ncu shows 72-81 % issue-slot utilization with ~37 instructions per "
+                                   "warp-level node visit, of which 13 flops are the algorithmic node test "
+                                   "(profiles/r01_ncu_trav_v9.txt, DESIGN.md §6)",
                      "work": work},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
