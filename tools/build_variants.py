@@ -8,7 +8,8 @@ VARIANTS = {
     "setsched": ["WN_EXP_SETSCHED"],
     "tb64": ["WN_EXP_TRAVBLOCK=64"],  # 64-query traversal blocks
     "tb256": ["WN_EXP_TRAVBLOCK=256"],
-    "lb5": ["WN_EXP_LBMIN=5"],  # resident 256-thread-equivalents per SM of the one-warp traversal
+    "lb5": ["WN_EXP_LBMIN=5"],
+    "few4k": ["WN_EXP_FEWTILES=4096"],  # moments: prefix blocks sum the earlier tile totals up to 4096 tiles  # resident 256-thread-equivalents per SM of the one-warp traversal
     "kdlpt": ["WN_EXP_KDLPT"],  # k-d schedule with the heaviest blocks first  # wn_exp_set_schedule hook for tools/sched_exp.py  # device-side bounds checks (trap on violation)
 }
 names = sys.argv[1:] or list(VARIANTS)
