@@ -299,13 +299,13 @@ static wn_status choose_schedule(wn_tree_s* t, cudaStream_t s) {
   const int64_t n = t->n, nw = (n + 31) / 32, nb = (n + kTravBlock - 1) / kTravBlock;
   int32_t *kd = nullptr, *wv = nullptr, *perm = nullptr;
   long long* dev = nullptr;
-  WN_CUDA(cudaMallocAsync((void**)&kd, n * sizeof(int32_t), s));
-  WN_CUDA(cudaMallocAsync((void**)&wv, 2 * nw * sizeof(int32_t), s));
-  WN_CUDA(cudaMallocAsync((void**)&perm, nb * sizeof(int32_t), s));
-  WN_CUDA(cudaMallocAsync((void**)&dev, 4 * sizeof(long long), s));
+  cudaError_t ae = cudaMallocAsync((void**)&kd, n * sizeof(int32_t), s);
+  if (ae == cudaSuccess) ae = cudaMallocAsync((void**)&wv, 2 * nw * sizeof(int32_t), s);
+  if (ae == cudaSuccess) ae = cudaMallocAsync((void**)&perm, nb * sizeof(int32_t), s);
+  if (ae == cudaSuccess) ae = cudaMallocAsync((void**)&dev, 4 * sizeof(long long), s);
   // the choice compares every kSampleStride-th warp of both schedules (the sample total, its heaviest warp);
   // the heaviest-first Hilbert order below counts every warp
-  wn_status st = kd_schedule(t->pts, n, kd, s);
+  wn_status st = ae == cudaSuccess ? kd_schedule(t->pts, n, kd, s) : cuda_status(ae, "schedule scratch");
   if (st == WN_OK) st = schedule_cost(t, t->qorder, kSampleStride, wv, dev, s);
   if (st == WN_OK) st = schedule_cost(t, kd, kSampleStride, wv + nw, dev + 2, s);
   long long h[4] = {};
@@ -349,10 +349,8 @@ static wn_status choose_schedule(wn_tree_s* t, cudaStream_t s) {
     }
     if (e != cudaSuccess) st = cuda_status(e, "schedule copy");
   }
-  cudaFreeAsync(kd, s);
-  cudaFreeAsync(wv, s);
-  cudaFreeAsync(perm, s);
-  cudaFreeAsync(dev, s);
+  for (void* p : {(void*)kd, (void*)wv, (void*)perm, (void*)dev})
+    if (p) cudaFreeAsync(p, s);
   return st;
 }
 

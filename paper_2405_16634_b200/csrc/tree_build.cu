@@ -802,6 +802,10 @@ __global__ void __launch_bounds__(1024) kd_local(const float4* __restrict__ pts,
   for (int i = tid; i < m; i += 1024) order[b + i] = id[i];
 }
 
+wn_status kd_levels(const float4* pts, int64_t n, int levels, int32_t* order, uint64_t* key, uint64_t* skey,
+                    int32_t* val, int32_t* seg, int32_t* sb, int32_t* se, int32_t* sb2, int32_t* se2, uint8_t* axis,
+                    cudaStream_t s);
+
 wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s) {
   if (n <= 0) return WN_OK;
   int levels = 0;  // global splits until every segment holds ≤ kKdLocal queries (from the sizes alone)
@@ -825,15 +829,25 @@ wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t
   uint64_t *key = nullptr, *skey = nullptr;
   int32_t *val = nullptr, *seg = nullptr, *sb = nullptr, *se = nullptr, *sb2 = nullptr, *se2 = nullptr;
   uint8_t* axis = nullptr;
-  WN_TRY(dalloc(&key, n, s));
-  WN_TRY(dalloc(&skey, n, s));
-  WN_TRY(dalloc(&val, n, s));
-  WN_TRY(dalloc(&seg, n, s));
-  WN_TRY(dalloc(&sb, maxseg, s));
-  WN_TRY(dalloc(&se, maxseg, s));
-  WN_TRY(dalloc(&sb2, maxseg, s));
-  WN_TRY(dalloc(&se2, maxseg, s));
-  WN_TRY(dalloc(&axis, maxseg, s));
+  wn_status st = dalloc(&key, n, s);
+  if (st == WN_OK) st = dalloc(&skey, n, s);
+  if (st == WN_OK) st = dalloc(&val, n, s);
+  if (st == WN_OK) st = dalloc(&seg, n, s);
+  if (st == WN_OK) st = dalloc(&sb, maxseg, s);
+  if (st == WN_OK) st = dalloc(&se, maxseg, s);
+  if (st == WN_OK) st = dalloc(&sb2, maxseg, s);
+  if (st == WN_OK) st = dalloc(&se2, maxseg, s);
+  if (st == WN_OK) st = dalloc(&axis, maxseg, s);
+  if (st == WN_OK) st = kd_levels(pts, n, levels, order, key, skey, val, seg, sb, se, sb2, se2, axis, s);
+  for (void* p : {(void*)key, (void*)skey, (void*)val, (void*)seg, (void*)sb, (void*)se, (void*)sb2, (void*)se2,
+                  (void*)axis})
+    if (p) cudaFreeAsync(p, s);
+  return st;
+}
+
+wn_status kd_levels(const float4* pts, int64_t n, int levels, int32_t* order, uint64_t* key, uint64_t* skey,
+                    int32_t* val, int32_t* seg, int32_t* sb, int32_t* se, int32_t* sb2, int32_t* se2, uint8_t* axis,
+                    cudaStream_t s) {
   const unsigned g = (unsigned)((n + 255) / 256);
   {
     ProfScope ps(WN_PROF_TREE, s, 0);
@@ -857,9 +871,6 @@ wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t
     count_launches(2);
     WN_CUDA(cudaGetLastError());
   }
-  for (void* p : {(void*)key, (void*)skey, (void*)val, (void*)seg, (void*)sb, (void*)se, (void*)sb2, (void*)se2,
-                  (void*)axis})
-    cudaFreeAsync(p, s);
   return WN_OK;
 }
 
