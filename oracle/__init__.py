@@ -64,6 +64,7 @@ def lib():
         L.wo_solve.argtypes = [P, P, D, D, I32, I32, I32, D, I32, I32, I32, I32, P]
         L.wo_solve.restype = I32
         L.wo_num_threads.restype = I32
+        L.wo_rescale.argtypes = [I64, P, P, P]
         _lib = L
     return _lib
 
@@ -205,6 +206,15 @@ class Tree:
                        float(theta), 0 if backend == "tree" else 1, 0 if mode == "gather" else 1,
                        1 if wnnc else 0, int(order), _p(stats))
         return mu, stats
+
+
+def rescale(mu_prev, mu_hat):
+    """WNNC rescale (Alg. 3): μ̂_i |μ'_i| / |μ̂_i|, μ'_i kept where |μ̂_i| = 0."""
+    mp = _f64(mu_prev).reshape(-1, 3)
+    mh = _f64(mu_hat).reshape(-1, 3)
+    out = np.empty_like(mp)
+    lib().wo_rescale(mp.shape[0], _p(mp), _p(mh), _p(out))
+    return out
 
 
 def width_schedule(k: int, n: int, w1: float, w2: float) -> float:

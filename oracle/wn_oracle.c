@@ -617,6 +617,16 @@ static void apply(const wo_tree* t, int backend, int op, const double* nu, int d
   else wo_tree_op(t, op, nu, dim, NULL, NULL, t->n, w, theta, out, NULL);
 }
 
+/* WNNC update's rescale (Alg. 3): μ_i = μ̂_i |μ'_i| / |μ̂_i| — the new direction μ̂_i with
+   the length of the grad-step result μ'_i; |μ̂_i| = 0 keeps μ'_i (reading R-rescale). */
+void wo_rescale(int64_t n, const double* mp, const double* mh, double* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    double a = sqrt(mp[3 * i] * mp[3 * i] + mp[3 * i + 1] * mp[3 * i + 1] + mp[3 * i + 2] * mp[3 * i + 2]);
+    double h = sqrt(mh[3 * i] * mh[3 * i] + mh[3 * i + 1] * mh[3 * i + 1] + mh[3 * i + 2] * mh[3 * i + 2]);
+    for (int c = 0; c < 3; ++c) out[3 * i + c] = h > 0 ? mh[3 * i + c] * (a / h) : mp[3 * i + c];
+  }
+}
+
 int wo_solve(const wo_tree* t, double* mu, double w1, double w2, int iters, int first_iter, int total_iters,
              double theta, int backend, int mode, int wnnc, int order, double* stats) {
   const int o1 = (order == 1 && backend == 0) ? WO_ORDER1 : 0;
@@ -649,11 +659,7 @@ int wo_solve(const wo_tree* t, double* mu, double w1, double w2, int iters, int 
     /* WNNC update + rescale */
     if (wnnc) {
       apply(t, backend, WO_OP_G | o1, mp, 3, w, theta, mh);
-      for (int64_t i = 0; i < n; ++i) {
-        double a = sqrt(mp[3 * i] * mp[3 * i] + mp[3 * i + 1] * mp[3 * i + 1] + mp[3 * i + 2] * mp[3 * i + 2]);
-        double h = sqrt(mh[3 * i] * mh[3 * i] + mh[3 * i + 1] * mh[3 * i + 1] + mh[3 * i + 2] * mh[3 * i + 2]);
-        for (int c = 0; c < 3; ++c) mu[3 * i + c] = h > 0 ? mh[3 * i + c] * (a / h) : mp[3 * i + c];
-      }
+      wo_rescale(n, mp, mh, mu);
     } else {
       memcpy(mu, mp, (size_t)n * 3 * sizeof(double));
     }

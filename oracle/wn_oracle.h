@@ -60,6 +60,9 @@ void wo_tree_A_frozen(const wo_tree* t, const double* mu_geom, const double* nu,
 void wo_tree_AT_transpose(const wo_tree* t, const double* mu_geom, const double* s, double w, double theta,
                           double* out);
 
+/* WNNC rescale (Alg. 3): out_i = mh_i |mp_i| / |mh_i|, mp_i kept where |mh_i| = 0 (n×3). */
+void wo_rescale(int64_t n, const double* mp, const double* mh, double* out);
+
 /* Alg. 3 + Alg. 2 solver in the normalized frame.  mu: n×3 in/out (caller order).
    backend: 0 treecode, 1 dense.  mode: 0 gather Aᵀ (paper text), 1 transpose (frozen geometry).
    wnnc: 1 normal, 0 ablation (skip the WNNC update + rescale).

@@ -71,6 +71,22 @@ int64_t* work_counters(int cls) {
   return g_work + 4 * cls;
 }
 
+void invalidate_graph(wn_tree_s* t) {
+  if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
+  t->graph_exec = nullptr;
+  t->graph_key.clear();
+}
+
+// marks the end of a call on a tree: free_tree waits for this point of the caller's stream
+struct TreeUse {
+  wn_tree_s* t;
+  cudaStream_t s;
+  TreeUse(wn_tree_s* tree, void* stream) : t(tree), s((cudaStream_t)stream) {}
+  ~TreeUse() {
+    if (t && t->done_ev) cudaEventRecord(t->done_ev, s);
+  }
+};
+
 static wn_status check_device() {
   int dev = 0, n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -92,12 +108,6 @@ static wn_status check_device() {
   return WN_OK;
 }
 
-#define WN_TRY(x)                 \
-  do {                            \
-    wn_status st_ = (x);          \
-    if (st_ != WN_OK) return st_; \
-  } while (0)
-
 static wn_status ensure_scratch(wn_tree_s* t, cudaStream_t s) {
   IterScratch& it = t->it;
   if (it.mu) return WN_OK;
@@ -115,6 +125,33 @@ static wn_status ensure_scratch(wn_tree_s* t, cudaStream_t s) {
 }
 
 static int stack_depth(const wn_tree_s* t) { return 8 * (t->depth_used + 2); }
+
+// per-iteration stats buffer (E, α, Σr², Σ(Ar)², w per iteration) of at least `iters` rows; growing it
+// frees the old block, which a cached CUDA graph may still reference: the graph is dropped with it
+static wn_status ensure_dstats(wn_tree_s* t, int iters, cudaStream_t s) {
+  IterScratch& it = t->it;
+  if (it.stats_cap >= iters) return WN_OK;
+  invalidate_graph(t);
+  if (it.dstats) cudaFreeAsync(it.dstats, s);
+  if (it.dcounts) cudaFreeAsync(it.dcounts, s);
+  it.dstats = nullptr;
+  it.dcounts = nullptr;
+  it.stats_cap = 0;
+  WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)iters, s));
+  WN_CUDA(cudaMallocAsync((void**)&it.dcounts, 12 * sizeof(int64_t) * (size_t)(iters + 1), s));
+  while ((int)it.ev.size() < iters + 1) {
+    cudaEvent_t e;
+    WN_CUDA(cudaEventCreate(&e));
+    it.ev.push_back(e);
+  }
+  it.stats_cap = iters;
+  return WN_OK;
+}
+
+// per-iteration work counts (only while counting is on): snapshot of the class totals
+static void snap_counts(wn_tree_s* t, int row, cudaStream_t s) {
+  if (g_count_on && g_work) cudaMemcpyAsync(t->it.dcounts + 12 * row, g_work, 12 * sizeof(int64_t), cudaMemcpyDeviceToDevice, s);
+}
 
 // several warps per query group below this many queries (too few query warps to fill the GPU otherwise);
 // decided on the whole cloud, so every rank of a sharded run picks the same kernel
@@ -414,6 +451,8 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     for (int v = 0; v < nviews; ++v) comm_peer_wait(*views[v], s);
     return WN_OK;
   };
+  cudaEventRecord(it.ev[0], s);
+  snap_counts(t, 0, s);
   for (int i = 0; i < p.iters; ++i) {
     const int k = p.first_iter + i;
     const float w = width_at(k, total, (double)p.w_min, (double)p.w_max);
@@ -514,6 +553,8 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a4.order1 = t->far_order;
     WN_TRY(run_traversal(a4, 0, NONE, cur ? MU0 : MU1));
     if (nccl) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, &t->shard, s));
+    cudaEventRecord(it.ev[i + 1], s);
+    snap_counts(t, i + 1, s);
   }
   return WN_OK;
 }
@@ -581,10 +622,12 @@ wn_status wn_build_tree(const float* pts, int64_t n, int32_t max_depth, void* st
   wn_tree_s* t = new (std::nothrow) wn_tree_s();
   if (!t) return set_error(WN_ERR_OOM, "host allocation failed");
   cudaGetDevice(&t->device);
-  wn_status st = build_tree(pts, n, max_depth, (cudaStream_t)stream, t);
+  const cudaError_t ee = cudaEventCreateWithFlags(&t->done_ev, cudaEventDisableTiming);
+  wn_status st = ee == cudaSuccess ? build_tree(pts, n, max_depth, (cudaStream_t)stream, t)
+                                   : cuda_status(ee, "cudaEventCreate");
   if (st == WN_OK) st = choose_schedule(t, (cudaStream_t)stream);
+  if (t->done_ev) cudaEventRecord(t->done_ev, (cudaStream_t)stream);
   if (st != WN_OK) {
-    cudaStreamSynchronize((cudaStream_t)stream);
     free_tree(t);
     delete t;
     return st;
@@ -601,6 +644,7 @@ wn_status wn_tree_destroy(wn_tree t) {
 }
 
 wn_status wn_tree_set_far_order(wn_tree t, int32_t order, void* stream) {
+  TreeUse use_(t, stream);
   if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
   if (order != 0 && order != 1) return set_error(WN_ERR_ARG, "far-field order must be 0 or 1");
   if (order == 1) WN_TRY(enable_order1(t, (cudaStream_t)stream));
@@ -620,6 +664,7 @@ wn_status wn_tree_info(wn_tree t, int64_t* num_points, int64_t* num_nodes, int32
 
 wn_status wn_tree_export(wn_tree t, uint64_t* keys, int32_t* perm, float* xn, int32_t* depth, int32_t* pb,
                          int32_t* pe, int32_t* child_begin, int32_t* child_count, void* stream) {
+  TreeUse use_(t, stream);
   if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t N = t->n, NN = t->nn;
@@ -636,6 +681,7 @@ wn_status wn_tree_export(wn_tree t, uint64_t* keys, int32_t* perm, float* xn, in
 
 wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, float* rep, float* attr, double* W,
                      void* stream) {
+  TreeUse use_(t, stream);
   if (!t || !nu) return set_error(WN_ERR_ARG, "tree or nu is NULL");
   if (dim != 1 && dim != 3) return set_error(WN_ERR_ARG, "dim must be 1 or 3");
   cudaStream_t s = (cudaStream_t)stream;
@@ -669,6 +715,7 @@ wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, fl
 
 static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a, const float* q, int64_t m,
                              float width, float theta, float* out, void* stream, int32_t* qcounts = nullptr) {
+  TreeUse use_(t, stream);
   if (!t || !mu || (!out && !qcounts)) return set_error(WN_ERR_ARG, "tree, mu or output is NULL");
   if (bad_width(width)) return set_error(WN_ERR_ARG, "width must be > 0");
   if (bad_theta(theta)) return set_error(WN_ERR_ARG, "theta must be > 0");
@@ -700,6 +747,9 @@ static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a,
     if (t->qcap < m) {
       if (t->qbuf) cudaFreeAsync(t->qbuf, s);
       if (t->qbuf_order) cudaFreeAsync(t->qbuf_order, s);
+      t->qbuf = nullptr;
+      t->qbuf_order = nullptr;
+      t->qcap = 0;
       WN_CUDA(cudaMallocAsync((void**)&t->qbuf, m * sizeof(float4), s));
       WN_CUDA(cudaMallocAsync((void**)&t->qbuf_order, m * sizeof(int32_t), s));
       t->qcap = m;
@@ -742,6 +792,7 @@ wn_status wn_query_work(wn_tree t, int32_t op, const float* attr, const float* q
 
 wn_status wn_eval_adjoint(wn_tree t, const float* sv, float width, float theta, int32_t mode, const float* mu_geom,
                           float* out, void* stream) {
+  TreeUse use_(t, stream);
   if (!t || !sv || !out) return set_error(WN_ERR_ARG, "tree, s or output is NULL");
   if (bad_width(width)) return set_error(WN_ERR_ARG, "width must be > 0");
   if (bad_theta(theta)) return set_error(WN_ERR_ARG, "theta must be > 0");
@@ -801,6 +852,7 @@ static wn_status check_params(const wnnc_params* p) {
 
 wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int32_t world, float* replicas,
                                 void* stream) {
+  TreeUse use_(t, stream);
   if (!t || !mu) return set_error(WN_ERR_ARG, "tree or mu is NULL");
   WN_TRY(check_params(p));
   if (world < 1 || world > kMaxPeers) return set_error(WN_ERR_ARG, "world must be 1..8");
@@ -808,11 +860,7 @@ wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int3
   cudaStream_t s = (cudaStream_t)stream;
   WN_TRY(ensure_scratch(t, s));
   IterScratch& it = t->it;
-  if (it.stats_cap < p->iters) {
-    if (it.dstats) cudaFreeAsync(it.dstats, s);
-    WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)p->iters, s));
-    it.stats_cap = p->iters;
-  }
+  WN_TRY(ensure_dstats(t, p->iters, s));
   WN_TRY(plan_shards(t, world, nullptr, s));
   PeerArena arenas[kMaxPeers];
   void* blocks[kMaxPeers] = {};
@@ -843,6 +891,7 @@ wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int3
 
 wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm, wnnc_iter_stats* stats,
                        void* stream) {
+  TreeUse use_(t, stream);
   if (!t || !mu) return set_error(WN_ERR_ARG, "tree or mu is NULL");
   WN_TRY(check_params(p));
   if (comm && p->adjoint_mode == WN_ADJ_TRANSPOSE)
@@ -852,22 +901,20 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
   cudaStream_t s = (cudaStream_t)stream;
   WN_TRY(ensure_scratch(t, s));
   IterScratch& it = t->it;
-  if (it.stats_cap < p->iters) {
-    if (it.dstats) cudaFreeAsync(it.dstats, s);
-    WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)p->iters, s));
-    it.stats_cap = p->iters;
-  }
+  WN_TRY(ensure_dstats(t, p->iters, s));
   const double sc2 = t->xf[3] * t->xf[3];
   // multi-GPU exchange: peer-memory stores fused into the traversal epilogues (default), or NCCL
   const PeerArena* P = nullptr;
   if (comm && !(p->flags & WN_FLAG_COMM_NCCL)) WN_TRY(comm_peer_arena(comm, t->n, s, &P));
   if (comm) WN_TRY(plan_shards(t, comm_world(comm), comm, s));
+  if (p->adjoint_mode == WN_ADJ_TRANSPOSE) WN_TRY(ensure_transpose_scratch(t, s));  // before any capture
   float4* mu0 = P ? P->mu[0][P->rank] : t->it.mu;
   gather_vec(t->n, t->perm, mu, sc2, mu0, s);             // μ_norm = scale²·μ
   if (p->flags & WN_FLAG_GRAPH) {
     // the whole iteration loop as one CUDA graph: captured on a private stream, cached per parameters
     const void* arena = P ? P->own : nullptr;
-    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm) + sizeof(int) + sizeof(arena) + sizeof(ShardPlan));
+    std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm) + sizeof(int) + sizeof(arena) + sizeof(ShardPlan) + 1);
+    key.back() = g_count_on ? 1 : 0;  // counting traversal variants are baked into the captured kernels
     uint8_t* kp = key.data();
     memcpy(kp, p, sizeof(wnnc_params));
     kp += sizeof(wnnc_params);
@@ -918,10 +965,31 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
   scatter_vec(t->n, t->perm, mu_end, 1.0 / sc2, mu, s);  // back to the input frame
   if (stats) {
     std::vector<double> h(5 * (size_t)p->iters);
+    std::vector<int64_t> c(12 * (size_t)(p->iters + 1), 0);
     WN_CUDA(cudaMemcpyAsync(h.data(), t->it.dstats, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (g_count_on) WN_CUDA(cudaMemcpyAsync(c.data(), t->it.dcounts, c.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     WN_CUDA(cudaStreamSynchronize(s));
-    for (int i = 0; i < p->iters; ++i)
-      stats[i] = {h[5 * i], h[5 * i + 1], h[5 * i + 2], h[5 * i + 3], h[5 * i + 4]};
+    for (int i = 0; i < p->iters; ++i) {
+      wnnc_iter_stats& o = stats[i];
+      o.E = h[5 * i];
+      o.alpha = h[5 * i + 1];
+      o.rr = h[5 * i + 2];
+      o.qq = h[5 * i + 3];
+      o.width = h[5 * i + 4];
+      float ms = -1.f;
+      o.ms = cudaEventElapsedTime(&ms, t->it.ev[i], t->it.ev[i + 1]) == cudaSuccess ? ms : -1.0;
+      int64_t w[4] = {-1, -1, -1, -1};
+      if (g_count_on)
+        for (int k = 0; k < 4; ++k) {
+          w[k] = 0;
+          for (int cls = 0; cls < 3; ++cls) w[k] += c[12 * (i + 1) + 4 * cls + k] - c[12 * i + 4 * cls + k];
+        }
+      o.tests = w[0];
+      o.far_terms = w[1];
+      o.near_terms = w[2];
+      o.live_terms = w[3];
+    }
+    cudaGetLastError();  // (an unavailable event time is reported as −1, not as an error)
   }
   WN_CUDA(cudaGetLastError());
   return WN_OK;
@@ -962,6 +1030,7 @@ wn_status wnnc_solve_host(const float* pts_host, int64_t n, int32_t max_depth, c
 }
 
 wn_status wn_tree_schedule(wn_tree t, int32_t* qorder, void* stream) {
+  TreeUse use_(t, stream);
   if (!t || !qorder) return set_error(WN_ERR_ARG, "tree or output is NULL");
   WN_CUDA(cudaMemcpyAsync(qorder, t->qorder, t->n * sizeof(int32_t), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return WN_OK;
@@ -976,6 +1045,7 @@ wn_status wn_tree_schedule_stats(wn_tree t, int32_t* kind, int64_t stats[4]) {
 }
 
 wn_status wn_shard_plan(wn_tree t, int32_t world, int64_t* bounds, void* stream) {
+  TreeUse use_(t, stream);
   if (!t || !bounds || world < 1 || world > kMaxShardRanks) return set_error(WN_ERR_ARG, "bad shard-plan arguments");
   cudaStream_t s = (cudaStream_t)stream;
   WN_TRY(ensure_scratch(t, s));

@@ -726,6 +726,7 @@ wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
 // order-1 far field (row f2): larger prefix entries and tile totals, the node sets' ext arrays
 wn_status enable_order1(wn_tree_s* t, cudaStream_t s) {
   if (t->mom_order1_ready) return WN_OK;
+  invalidate_graph(t);  // a cached order-0 graph references the prefix scratch freed here
   cudaFreeAsync(t->mom_pre, s);
   cudaFreeAsync(t->mom_tile, s);
   t->mom_pre = nullptr;

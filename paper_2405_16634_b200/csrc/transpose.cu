@@ -187,12 +187,17 @@ __global__ void pushdown_kernel(int64_t n, const int32_t* __restrict__ leaf_of, 
 
 }  // namespace
 
+wn_status ensure_transpose_scratch(wn_tree_s* t, cudaStream_t st) {
+  if (t->tvb && t->tu) return WN_OK;
+  WN_CUDA(cudaMallocAsync((void**)&t->tvb, 3 * sizeof(double) * (size_t)t->nn, st));
+  WN_CUDA(cudaMallocAsync((void**)&t->tu, 3 * sizeof(double) * (size_t)t->n, st));
+  return WN_OK;
+}
+
 wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sorted, float w2, float4* r_out,
                             double* partial, cudaStream_t st) {
-  if (!t->tvb) {
-    WN_CUDA(cudaMallocAsync((void**)&t->tvb, 3 * sizeof(double) * (size_t)t->nn, st));
-    WN_CUDA(cudaMallocAsync((void**)&t->tu, 3 * sizeof(double) * (size_t)t->n, st));
-  }
+  // (inside a graph capture the accumulators exist already: wnnc_iterate allocates them before capturing)
+  WN_TRY(ensure_transpose_scratch(t, st));
   WN_CUDA(cudaMemsetAsync(t->tvb, 0, 3 * sizeof(double) * (size_t)t->nn, st));
   WN_CUDA(cudaMemsetAsync(t->tu, 0, 3 * sizeof(double) * (size_t)t->n, st));
   const int stack_depth = 8 * (t->depth_used + 2);

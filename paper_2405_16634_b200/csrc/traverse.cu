@@ -435,104 +435,14 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
       acc.flush();  // (no trailing __syncwarp: every lane writes the same stack words and reads its own)
     }
   }
-  // ---------------- epilogue ----------------
-  double part = 0.0;
-  if (valid) {
-    const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
-    if (OP == OP_A) {
-      const double val = acc.d * 0.0795774715459476679;  // Σ / (4π)
-      if (EPI == EPI_PLAIN && a.out_f) a.out_f[oq] = (float)(val * (double)a.scale_out);
-      if (EPI == EPI_S) {
-        const double sv = 0.5 - val;
-        if (a.world) {  // peer-memory exchange: this row into every rank's replica (NVLink stores)
-          for (int r = 0; r < a.world; ++r) a.peer_f[r][q] = (float)sv;
-        } else {
-          a.out_f[q] = (float)sv;
-        }
-        part = sv * sv;
-      }
-      if (EPI == EPI_SQ) part = val * val;
-    } else {
-      const float vx = acc.x * kInv4Pi, vy = acc.y * kInv4Pi, vz = acc.z * kInv4Pi;
-      if (EPI == EPI_PLAIN && a.out_v3) {
-        a.out_v3[3 * oq + 0] = vx * a.scale_out;
-        a.out_v3[3 * oq + 1] = vy * a.scale_out;
-        a.out_v3[3 * oq + 2] = vz * a.scale_out;
-      }
-      if (EPI == EPI_R) {
-        const float4 o = make_float4(vx, vy, vz, 0.f);
-        if (a.world) {
-          for (int r = 0; r < a.world; ++r) a.peer_v4[r][q] = o;
-        } else {
-          a.out_v4[q] = o;
-        }
-        part = (double)vx * vx + (double)vy * vy + (double)vz * vz;
-      }
-      if (EPI == EPI_RESCALE) {  // μ_i = μ̂_i |μ'_i| / |μ̂_i|, μ'_i kept if |μ̂_i| = 0 (Alg. 3)
-        const float4 m = a.mup[q];
-        const double hm = sqrt((double)vx * vx + (double)vy * vy + (double)vz * vz);
-        const double mm = sqrt((double)m.x * m.x + (double)m.y * m.y + (double)m.z * m.z);
-        float4 o = m;
-        if (hm > 0.0) {
-          const double f = mm / hm;
-          o = make_float4((float)(vx * f), (float)(vy * f), (float)(vz * f), 0.f);
-        }
-        if (a.world) {
-          for (int r = 0; r < a.world; ++r) a.peer_v4[r][q] = o;
-        } else {
-          a.out_v4[q] = o;
-        }
-      }
-    }
-  }
-  if (COUNT) {  // algorithmic work: node tests, representative terms, leaf-point terms, live terms (r ≥ w)
-    if (a.wvisits && active && lane == 0) a.wvisits[kq >> 5] = wvis;  // (lane 0's schedule position / 32)
-    if (a.qcounts && valid) {
-      const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
-      a.qcounts[4 * oq + 0] = ntest;
-      a.qcounts[4 * oq + 1] = nfar;
-      a.qcounts[4 * oq + 2] = nnear;
-      a.qcounts[4 * oq + 3] = nlive;
-    }
-    if (a.work) {
-      unsigned long long c[4] = {(unsigned long long)ntest, (unsigned long long)nfar, (unsigned long long)nnear,
-                                 (unsigned long long)nlive};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) c[k] += __shfl_xor_sync(FULL, c[k], o);
-        if (lane == 0) atomicAdd((unsigned long long*)a.work + k, c[k]);
-      }
-    }
-  }
-  if (EPI == EPI_S || EPI == EPI_SQ || EPI == EPI_R) {
-    part = warp_sum(part);
-    if (lane == 0) red[warp] = part;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = 0.0;
-      for (int k = 0; k < kTravBlock / 32; ++k) b += red[k];
-      const int64_t ib = (a.q_begin / kTravBlock) + blockIdx.x;
-      WN_DCHECK(ib < (a.npts + kTravBlock - 1) / kTravBlock || a.queries != a.pts, "partial slot");
-      if (a.world) {
-        for (int r = 0; r < a.world; ++r) a.peer_part[r][ib] = b;
-      } else {
-        a.partial[ib] = b;
-      }
-    }
-  }
-  if (a.world) {  // signal: every thread's remote stores, then one count per block, the last block tells every rank
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned int prev = atomicAdd(a.done, 1u);
-      if (prev == gridDim.x - 1) {
-        __threadfence_system();
-        *a.done = 0u;  // ready for the next exchange (stream-ordered)
-        for (int r = 0; r < a.world; ++r) atomicAdd_system(a.peer_sig[r], 1ull);
-      }
-    }
-  }
+  // ---------------- epilogue (shared with the split kernel) ----------------
+  if (COUNT && a.wvisits && active && lane == 0) a.wvisits[kq >> 5] = wvis;  // (lane 0's schedule position / 32)
+  Work wk;
+  wk.test = ntest;
+  wk.far = nfar;
+  wk.near = nnear;
+  wk.live = nlive;
+  trav_epilogue<OP, EPI, COUNT, kTravBlock / 32>(a, valid, q, acc, wk, red, (a.q_begin / kTravBlock) + blockIdx.x);
 }
 
 // Small clouds (few query warps for the GPU): kSplit warps share each group of 32 queries.  All of them

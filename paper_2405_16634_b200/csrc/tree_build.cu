@@ -502,6 +502,32 @@ wn_status dalloc(T** p, size_t count, cudaStream_t s) {
   return WN_OK;
 }
 
+// temporaries of one host routine: every block still held is freed (stream-ordered) when the routine
+// returns, on the error paths too; keep() hands a block over to a longer-lived owner
+struct TempSet {
+  cudaStream_t s;
+  std::vector<void*> held;
+  explicit TempSet(cudaStream_t st) : s(st) {}
+  ~TempSet() {
+    for (void* p : held) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  wn_status alloc(T** p, size_t count) {
+    *p = nullptr;
+    WN_TRY(dalloc(p, count, s));
+    held.push_back((void*)*p);
+    return WN_OK;
+  }
+  void keep(void* p) {
+    for (auto& q : held)
+      if (q == p) q = held.back(), held.pop_back();
+  }
+  void release(void* p) {
+    keep(p);
+    cudaFreeAsync(p, s);
+  }
+};
+
 // exclusive scan (in may equal out); total (device) optional
 wn_status scan_excl(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* total, cudaStream_t s) {
   const int nb = (int)((m + kScanBlk - 1) / kScanBlk);
@@ -517,12 +543,6 @@ wn_status scan_excl(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* tota
 
 }  // namespace
 
-#define WN_TRY(x)                       \
-  do {                                  \
-    wn_status st_ = (x);                \
-    if (st_ != WN_OK) return st_;       \
-  } while (0)
-
 // stable LSD radix sort of (key, value) pairs on the low `bits` bits of the keys; ka / va are consumed,
 // the values in key order are copied to out
 static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int32_t* out, cudaStream_t s,
@@ -531,11 +551,10 @@ static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int3
   uint64_t* kb = nullptr;
   int32_t* vb = nullptr;
   uint32_t* hist = nullptr;
-  WN_TRY(dalloc(&kb, n, s));
-  WN_TRY(dalloc(&vb, n, s));
-  WN_TRY(dalloc(&hist, (size_t)256 * ntiles, s));
-  uint64_t* const own_k = kb;  // freed here whatever the parity of the passes
-  int32_t* const own_v = vb;
+  TempSet tmp(s);  // kb, vb, hist: freed here whatever the parity of the passes (and on errors)
+  WN_TRY(tmp.alloc(&kb, n));
+  WN_TRY(tmp.alloc(&vb, n));
+  WN_TRY(tmp.alloc(&hist, (size_t)256 * ntiles));
   const int passes = (bits + 7) / 8;
   for (int p = 0; p < passes; ++p) {
     radix_hist<<<ntiles, kSortThreads, 0, s>>>(ka, n, 8 * p, ntiles, hist);
@@ -546,9 +565,6 @@ static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int3
   }
   WN_CUDA(cudaMemcpyAsync(out, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   if (kout) WN_CUDA(cudaMemcpyAsync(kout, ka, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-  cudaFreeAsync(own_k, s);
-  cudaFreeAsync(own_v, s);
-  cudaFreeAsync(hist, s);
   count_launches(5 * passes);
   WN_CUDA(cudaGetLastError());
   return WN_OK;
@@ -558,8 +574,9 @@ wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStr
   if (n <= 0) return WN_OK;
   uint64_t* ka = nullptr;
   int32_t* va = nullptr;
-  WN_TRY(dalloc(&ka, n, s));
-  WN_TRY(dalloc(&va, n, s));
+  TempSet tmp(s);
+  WN_TRY(tmp.alloc(&ka, n));
+  WN_TRY(tmp.alloc(&va, n));
   const int hbits = 3 * kHilbertBits;
   {
     ProfScope ps(WN_PROF_TREE, s, 0);
@@ -567,8 +584,6 @@ wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStr
     count_launches(1);
     WN_TRY(sort_pairs(ka, va, n, hbits, order, s));
   }
-  cudaFreeAsync(ka, s);
-  cudaFreeAsync(va, s);
   return WN_OK;
 }
 
@@ -888,14 +903,15 @@ __global__ void live_keys(int64_t m, const int32_t* __restrict__ list, const int
 wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree_s* t) {
   t->n = n;
   t->D = D;
+  TempSet tmp(s);  // temporaries: freed on every return path
   // --- bbox + transform (a1) ---
   int nb = (int)std::min<int64_t>((n + 255) / 256, 1184);
   float* part = nullptr;
   int* bad = nullptr;
   BBox* bb = nullptr;
-  WN_TRY(dalloc(&part, 6 * (size_t)nb, s));
-  WN_TRY(dalloc(&bad, 1, s));
-  WN_TRY(dalloc(&bb, 1, s));
+  WN_TRY(tmp.alloc(&part, 6 * (size_t)nb));
+  WN_TRY(tmp.alloc(&bad, 1));
+  WN_TRY(tmp.alloc(&bb, 1));
   WN_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   {
     ProfScope ps(WN_PROF_TREE, s, 2);
@@ -905,28 +921,22 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   BBox hb;
   WN_CUDA(cudaMemcpyAsync(&hb, bb, sizeof(BBox), cudaMemcpyDeviceToHost, s));
   WN_CUDA(cudaStreamSynchronize(s));
-  if (hb.nonfinite) {
-    cudaFreeAsync(part, s); cudaFreeAsync(bad, s); cudaFreeAsync(bb, s);
-    return set_error(WN_ERR_NONFINITE, "non-finite point coordinate");
-  }
-  if (!(hb.xf[3] > 0.0)) {
-    cudaFreeAsync(part, s); cudaFreeAsync(bad, s); cudaFreeAsync(bb, s);
-    return set_error(WN_ERR_DEGENERATE, "all points coincide (zero extent)");
-  }
+  if (hb.nonfinite) return set_error(WN_ERR_NONFINITE, "non-finite point coordinate");
+  if (!(hb.xf[3] > 0.0)) return set_error(WN_ERR_DEGENERATE, "all points coincide (zero extent)");
   for (int a = 0; a < 4; ++a) t->xf[a] = hb.xf[a];
 
   // --- normalize, keys, sort (a1) ---
   float4* xn = nullptr;
   uint64_t *k0 = nullptr, *k1 = nullptr;
   int32_t *v0 = nullptr, *v1 = nullptr;
-  WN_TRY(dalloc(&xn, n, s));
-  WN_TRY(dalloc(&k0, n, s));
-  WN_TRY(dalloc(&k1, n, s));
-  WN_TRY(dalloc(&v0, n, s));
-  WN_TRY(dalloc(&v1, n, s));
+  WN_TRY(tmp.alloc(&xn, n));
+  WN_TRY(tmp.alloc(&k0, n));
+  WN_TRY(tmp.alloc(&k1, n));
+  WN_TRY(tmp.alloc(&v0, n));
+  WN_TRY(tmp.alloc(&v1, n));
   int ntiles = (int)((n + kSortTile - 1) / kSortTile);
   uint32_t* hist = nullptr;
-  WN_TRY(dalloc(&hist, (size_t)256 * ntiles, s));
+  WN_TRY(tmp.alloc(&hist, (size_t)256 * ntiles));
   int passes = (3 * D + 7) / 8;
   {
     ProfScope ps(WN_PROF_TREE, s, 1 + 5 * passes + 1);
@@ -943,27 +953,22 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
     gather_sorted<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(xn, v0, n, t->pts, t->perm);
   }
   t->keys = k0;
+  tmp.keep(k0);  // owned by the tree from here
   // --- query schedule: the sorted points in Hilbert order (warps get spatially compact query sets;
   //     a Z-order jump between diagonal octants no longer splits a warp's 32 queries) ---
   if (!getenv("WN_EXP_NOHILBERT")) {
     WN_TRY(dalloc(&t->qorder, n, s));
     WN_TRY(hilbert_schedule(t->pts, n, t->qorder, s));
   }
-  cudaFreeAsync(k1, s);
-  cudaFreeAsync(v0, s);
-  cudaFreeAsync(v1, s);
-  cudaFreeAsync(xn, s);
-  cudaFreeAsync(hist, s);
-  cudaFreeAsync(part, s);
-  cudaFreeAsync(bad, s);
-  cudaFreeAsync(bb, s);
+  for (void* p : {(void*)k1, (void*)v0, (void*)v1, (void*)xn, (void*)hist, (void*)part, (void*)bad, (void*)bb})
+    tmp.release(p);
 
   // --- node counts per level (a2) ---
   int etiles = (int)((n + kEmitThreads - 1) / kEmitThreads);
   int64_t m = (int64_t)(D + 1) * etiles;
   uint32_t *cnt = nullptr, *offs = nullptr;
-  WN_TRY(dalloc(&cnt, m + 1, s));
-  WN_TRY(dalloc(&offs, m + 1, s));
+  WN_TRY(tmp.alloc(&cnt, m + 1));
+  WN_TRY(tmp.alloc(&offs, m + 1));
   {
     ProfScope ps(WN_PROF_TREE, s, 4);
     level_counts<<<etiles, kEmitThreads, 0, s>>>(t->keys, n, D, etiles, cnt);
@@ -974,8 +979,6 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   WN_CUDA(cudaStreamSynchronize(s));
   t->nn = hoffs[m];
   if (t->nn + 1 > ((int64_t)1 << 26)) {  // the traversal addresses 64-byte records with 32-bit byte offsets
-    cudaFreeAsync(cnt, s);
-    cudaFreeAsync(offs, s);
     return set_error(WN_ERR_ARG, "octree with more than 2^26 - 1 nodes (deep chains of close points)");
   }
   t->level_off.assign(D + 2, t->nn);
@@ -1007,7 +1010,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
     WN_CUDA(cudaMemsetAsync(t->set[k].rec, 0, sizeof(float4) * kRec * (nn + 1), s));
   }
   int64_t* loff = nullptr;
-  WN_TRY(dalloc(&loff, t->level_off.size(), s));
+  WN_TRY(tmp.alloc(&loff, t->level_off.size()));
   WN_CUDA(cudaMemcpyAsync(loff, t->level_off.data(), t->level_off.size() * sizeof(int64_t),
                           cudaMemcpyHostToDevice, s));
   {
@@ -1025,8 +1028,8 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
   }
   {  // the visited nodes, compacted in BFS order (per-iteration moment builds skip the rest)
     uint32_t *vis = nullptr, *pos = nullptr;
-    WN_TRY(dalloc(&vis, nn + 1, s));
-    WN_TRY(dalloc(&pos, nn + 1, s));
+    WN_TRY(tmp.alloc(&vis, nn + 1));
+    WN_TRY(tmp.alloc(&pos, nn + 1));
     WN_CUDA(cudaMemsetAsync(vis, 0, (nn + 1) * sizeof(uint32_t), s));
     const unsigned g = (unsigned)((nn + 255) / 256);
     mark_visited<<<g, 256, 0, s>>>(nn, t->topo, vis);
@@ -1037,28 +1040,28 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
     t->mom_nlive = nlive;
     WN_TRY(dalloc(&t->mom_live, std::max<int64_t>(nlive, 1), s));
     compact_visited<<<g, 256, 0, s>>>(nn, vis, pos, t->mom_live);
-    cudaFreeAsync(vis, s);
-    cudaFreeAsync(pos, s);
+    tmp.release(vis);
+    tmp.release(pos);
     count_launches(5);
 #ifndef WN_EXP_LIVE_BFS
     if (nlive > 1) {  // in point order: neighbouring threads read neighbouring (often shared) prefix entries
       uint64_t* k = nullptr;
       int32_t* v = nullptr;
-      WN_TRY(dalloc(&k, nlive, s));
-      WN_TRY(dalloc(&v, nlive, s));
+      WN_TRY(tmp.alloc(&k, nlive));
+      WN_TRY(tmp.alloc(&v, nlive));
       live_keys<<<(unsigned)((nlive + 255) / 256), 256, 0, s>>>(nlive, t->mom_live, t->pb, k, v);
       count_launches(1);
       int bits = 1;
       while (bits < 62 && ((int64_t)1 << bits) <= n) ++bits;
       WN_TRY(sort_pairs(k, v, nlive, bits, t->mom_live, s));
-      cudaFreeAsync(k, s);
-      cudaFreeAsync(v, s);
+      tmp.release(k);
+      tmp.release(v);
     }
 #endif
   }
-  cudaFreeAsync(loff, s);
-  cudaFreeAsync(cnt, s);
-  cudaFreeAsync(offs, s);
+  tmp.release(loff);
+  tmp.release(cnt);
+  tmp.release(offs);
   WN_CUDA(cudaGetLastError());
 
   // --- fixed node data: unweighted centroids (unit weights) ---
@@ -1077,13 +1080,26 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->qorder, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
                   t->topo, t->smask, t->tdepth, t->mom_live, t->mom_loff, t->mom_pre, t->mom_tile, t->centroid, t->sums, t->set[0].rec, t->set[1].rec, t->set[0].ext,
-                  t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.alpha, t->it.tmp,
+                  t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.dcounts, t->it.alpha, t->it.tmp,
                   t->qbuf, t->qbuf_order, t->tvb, t->tu};
-  // stream-ordered frees on the legacy stream: no device-wide synchronization, memory returns to the pool
+  // the last call's work (on whatever stream it was queued) must finish before the memory returns to
+  // the pool; then stream-ordered frees, no device-wide synchronization
+  if (t->done_ev) {
+    cudaEventSynchronize(t->done_ev);
+    cudaEventDestroy(t->done_ev);
+    t->done_ev = nullptr;
+  }
+  if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
+  t->graph_exec = nullptr;
+  if (t->cap_stream) {
+    cudaStreamSynchronize(t->cap_stream);
+    cudaStreamDestroy(t->cap_stream);
+    t->cap_stream = nullptr;
+  }
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, 0);
-  if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
-  if (t->cap_stream) cudaStreamDestroy(t->cap_stream);
+  for (cudaEvent_t e : t->it.ev) cudaEventDestroy(e);
+  t->it.ev.clear();
 }
 
 }  // namespace wn

@@ -57,7 +57,9 @@ struct IterScratch {
   float* s = nullptr;        // s = ½ − A μ
   double* part = nullptr;    // per-block partials: [3][nblk] (Σs², Σ|r|², Σq²)
   double* dstats = nullptr;  // per-iteration (E, α, rr, qq, w) — device
+  int64_t* dcounts = nullptr;  // (iters + 1) × 12 snapshots of the work counters (counting runs only)
   int64_t stats_cap = 0;
+  std::vector<cudaEvent_t> ev;  // iters + 1 timing events: iteration i runs between ev[i] and ev[i + 1]
   double* alpha = nullptr;   // current α (device)
   float* tmp = nullptr;      // generic N×4 scratch
   int nblk = 0;
@@ -119,6 +121,9 @@ struct wn_tree_s {
   cudaGraphExec_t graph_exec = nullptr;
   uint64_t graph_launches = 0;  // kernel nodes in the graph
   std::vector<uint8_t> graph_key;
+  // recorded on the caller's stream at the end of every call on the tree: destruction waits for it, so
+  // no buffer returns to the pool while queued work (on any stream, blocking or not) may still read it
+  cudaEvent_t done_ev = nullptr;
 };
 
 namespace wn {
@@ -126,6 +131,11 @@ namespace wn {
 // ---- error plumbing (capi.cu) ----
 wn_status set_error(wn_status st, const std::string& msg);
 wn_status cuda_status(cudaError_t e, const char* what);
+#define WN_TRY(x)                 \
+  do {                            \
+    wn_status st_ = (x);          \
+    if (st_ != WN_OK) return st_; \
+  } while (0)
 #define WN_CUDA(call)                                                      \
   do {                                                                     \
     cudaError_t e_ = (call);                                               \
@@ -142,6 +152,9 @@ struct ProfScope {
 };
 void count_launches(int n);
 int64_t* work_counters(int cls);  // device counters of a traversal class, or null when counting is off
+
+// drop the cached CUDA graph of the iteration loop (a buffer it references is about to be freed)
+void invalidate_graph(wn_tree_s* t);
 
 // ---- tree build (tree_build.cu) ----
 wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree_s* t);
@@ -245,6 +258,8 @@ struct PeerArena {
 };
 
 // ---- transpose-mode adjoint (transpose.cu) ----
+// node / point accumulators, allocated once per tree — before any graph capture that uses them
+wn_status ensure_transpose_scratch(wn_tree_s* t, cudaStream_t st);
 wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sorted, float w2,
                             float4* r_out, double* partial, cudaStream_t st);
 

@@ -41,7 +41,8 @@ class wnnc_params(C.Structure):
 
 class wnnc_iter_stats(C.Structure):
     _fields_ = [("E", C.c_double), ("alpha", C.c_double), ("rr", C.c_double), ("qq", C.c_double),
-                ("width", C.c_double)]
+                ("width", C.c_double), ("ms", C.c_double), ("tests", C.c_int64), ("far_terms", C.c_int64),
+                ("near_terms", C.c_int64), ("live_terms", C.c_int64)]
 
 
 P, I32, I64, F32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
@@ -241,6 +242,10 @@ def make_params(w_min=0.002, w_max=0.016, theta=2.0, iters=40, first_iter=1, tot
     return wnnc_params(w_min, w_max, theta, iters, first_iter, total_iters, adjoint_mode, flags)
 
 
+def _stats_dict(s):
+    return {k: getattr(s, k) for k, _ in wnnc_iter_stats._fields_}
+
+
 def wnnc_iterate(tree: Tree, mu: torch.Tensor, comm=None, stats: bool = False, **params):
     """In-place Alg. 3 on mu (N×3, input frame).  Returns per-iteration stats (list of dicts) if asked."""
     _dev_f32(mu, 3)
@@ -248,7 +253,7 @@ def wnnc_iterate(tree: Tree, mu: torch.Tensor, comm=None, stats: bool = False, *
     st = (wnnc_iter_stats * p.iters)() if stats else None
     _check(_L.wnnc_iterate(tree.handle, _ptr(mu), C.byref(p), comm.handle if comm else None, st, _stream()))
     if stats:
-        return [dict(E=s.E, alpha=s.alpha, rr=s.rr, qq=s.qq, width=s.width) for s in st]
+        return [_stats_dict(s) for s in st]
     return None
 
 
@@ -267,7 +272,7 @@ def wnnc_solve_host(pts_host: torch.Tensor, max_depth=15, return_mu=False, stats
     if return_mu:
         out.append(mu)
     if stats:
-        out.append([dict(E=s.E, alpha=s.alpha, rr=s.rr, qq=s.qq, width=s.width) for s in st])
+        out.append([_stats_dict(s) for s in st])
     return out[0] if len(out) == 1 else tuple(out)
 
 

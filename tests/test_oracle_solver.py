@@ -31,6 +31,28 @@ def _E(c, mu, w):
     return float(np.sum((0.5 - c.t.dense(OP_A, mu, w)) ** 2))
 
 
+def test_rescale_spec_example_and_zero_branch():
+    # SPEC.md:L330 golden: μ' = (0,0,2), μ̂ = (3,4,0) → μ̂·|μ'|/|μ̂| = (1.2, 1.6, 0)
+    g = GOLD["rescale"]
+    out = oracle.rescale(np.array([g["mu_prev"]]), np.array([g["mu_hat"]]))
+    np.testing.assert_allclose(out[0], g["out"], rtol=0, atol=1e-15)
+    # |μ̂| = 0 keeps μ' (reading R-rescale); |μ'| = 0 gives 0; direction from μ̂, length from μ'
+    mp = np.array([[1.0, -2.0, 2.0], [0.0, 0.0, 0.0], [0.5, 0.0, 0.0]])
+    mh = np.array([[0.0, 0.0, 0.0], [7.0, 1.0, 0.0], [0.0, -4.0, 3.0]])
+    out = oracle.rescale(mp, mh)
+    np.testing.assert_array_equal(out[0], mp[0])
+    np.testing.assert_array_equal(out[1], 0.0)
+    np.testing.assert_allclose(out[2], [0.0, -0.4, 0.3], atol=1e-15)
+    # inside the solver: a width above the cloud's diameter cuts every term, so A = 0, r = 0, α = 0,
+    # μ̂ = G(μ') = 0 and every point takes the keep branch — μ is returned unchanged
+    p, nr = synth.sphere(300, seed=31)
+    t = oracle.Tree(oracle.normalize(p)[0])
+    mu0 = nr * 0.01
+    mu, st = t.solve(mu0=mu0, w1=4.0, w2=4.0, iters=2)
+    np.testing.assert_array_equal(mu, mu0)
+    assert st[0, 1] == 0.0
+
+
 def test_grad_step_is_exact_line_search():
     # Alg. 2: α = rᵀr / rᵀAᵀAr minimizes E(μ + t r) along r; checked against a
     # brute-force scan of E, and E never increases
