@@ -86,8 +86,9 @@ typedef struct {
   double rr;     /* rᵀr                                                                        */
   double qq;     /* ‖A_w r‖²                                                                   */
   double width;  /* w used in this iteration                                                   */
-  double ms;     /* device time of the iteration (CUDA events on the iteration's stream; inside a
-                    CUDA graph too), −1 if unavailable                                          */
+  double ms;     /* device time of the iteration: the GPU's global timer read by a one-thread kernel
+                    at every iteration boundary (inside the CUDA graph too; only in calls that ask
+                    for stats, which get their own cached graph)                                 */
   /* algorithmic work of the iteration's traversals (summed over A, Aᵀ, G), only while
      wn_work_count_enable(1) is on, else −1: opening tests, representative (far) terms,
      leaf-point (near) terms, terms past the cutoff (r ≥ w)                                      */

@@ -139,13 +139,25 @@ static wn_status ensure_dstats(wn_tree_s* t, int iters, cudaStream_t s) {
   it.stats_cap = 0;
   WN_CUDA(cudaMallocAsync((void**)&it.dstats, 5 * sizeof(double) * (size_t)iters, s));
   WN_CUDA(cudaMallocAsync((void**)&it.dcounts, 12 * sizeof(int64_t) * (size_t)(iters + 1), s));
-  while ((int)it.ev.size() < iters + 1) {
-    cudaEvent_t e;
-    WN_CUDA(cudaEventCreate(&e));
-    it.ev.push_back(e);
-  }
+  if (it.dstamp) cudaFreeAsync(it.dstamp, s);
+  it.dstamp = nullptr;
+  WN_CUDA(cudaMallocAsync((void**)&it.dstamp, sizeof(unsigned long long) * (size_t)(iters + 1), s));
   it.stats_cap = iters;
   return WN_OK;
+}
+
+// per-iteration device time: the global nanosecond timer at each iteration boundary (a one-thread kernel;
+// works inside the captured graph, where event timing is not available); only for calls that ask for stats
+constexpr int kFlagStamps = 1 << 16;  // internal wnnc_params flag (part of the graph key)
+__global__ void k_stamp(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+static void stamp(wn_tree_s* t, const wnnc_params& p, int row, cudaStream_t s) {
+  if (!(p.flags & kFlagStamps)) return;
+  k_stamp<<<1, 1, 0, s>>>(t->it.dstamp + row);
+  count_launches(1);
 }
 
 // per-iteration work counts (only while counting is on): snapshot of the class totals
@@ -451,7 +463,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     for (int v = 0; v < nviews; ++v) comm_peer_wait(*views[v], s);
     return WN_OK;
   };
-  cudaEventRecord(it.ev[0], s);
+  stamp(t, p, 0, s);
   snap_counts(t, 0, s);
   for (int i = 0; i < p.iters; ++i) {
     const int k = p.first_iter + i;
@@ -553,7 +565,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     a4.order1 = t->far_order;
     WN_TRY(run_traversal(a4, 0, NONE, cur ? MU0 : MU1));
     if (nccl) WN_TRY(comm_allgather_f(comm, (float*)it.mu, 4, t->n, qord, stage, &t->shard, s));
-    cudaEventRecord(it.ev[i + 1], s);
+    stamp(t, p, i + 1, s);
     snap_counts(t, i + 1, s);
   }
   return WN_OK;
@@ -889,11 +901,14 @@ wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int3
   return st;
 }
 
-wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm, wnnc_iter_stats* stats,
+wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p_in, wn_comm comm, wnnc_iter_stats* stats,
                        void* stream) {
   TreeUse use_(t, stream);
   if (!t || !mu) return set_error(WN_ERR_ARG, "tree or mu is NULL");
-  WN_TRY(check_params(p));
+  WN_TRY(check_params(p_in));
+  wnnc_params pl = *p_in;
+  pl.flags = (pl.flags & ~kFlagStamps) | (stats ? kFlagStamps : 0);
+  const wnnc_params* p = &pl;
   if (comm && p->adjoint_mode == WN_ADJ_TRANSPOSE)
     return set_error(WN_ERR_ARG, "transpose-mode adjoint is single-GPU only in this build");
   if (t->far_order != 0 && p->adjoint_mode == WN_ADJ_TRANSPOSE)
@@ -967,7 +982,9 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
     std::vector<double> h(5 * (size_t)p->iters);
     std::vector<int64_t> c(12 * (size_t)(p->iters + 1), 0);
     WN_CUDA(cudaMemcpyAsync(h.data(), t->it.dstats, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    std::vector<unsigned long long> ts(p->iters + 1, 0);
     if (g_count_on) WN_CUDA(cudaMemcpyAsync(c.data(), t->it.dcounts, c.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaMemcpyAsync(ts.data(), t->it.dstamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     WN_CUDA(cudaStreamSynchronize(s));
     for (int i = 0; i < p->iters; ++i) {
       wnnc_iter_stats& o = stats[i];
@@ -976,8 +993,7 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
       o.rr = h[5 * i + 2];
       o.qq = h[5 * i + 3];
       o.width = h[5 * i + 4];
-      float ms = -1.f;
-      o.ms = cudaEventElapsedTime(&ms, t->it.ev[i], t->it.ev[i + 1]) == cudaSuccess ? ms : -1.0;
+      o.ms = 1e-6 * (double)(ts[i + 1] - ts[i]);
       int64_t w[4] = {-1, -1, -1, -1};
       if (g_count_on)
         for (int k = 0; k < 4; ++k) {
@@ -989,7 +1005,6 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm,
       o.near_terms = w[2];
       o.live_terms = w[3];
     }
-    cudaGetLastError();  // (an unavailable event time is reported as −1, not as an error)
   }
   WN_CUDA(cudaGetLastError());
   return WN_OK;

@@ -205,59 +205,38 @@ __global__ void __launch_bounds__(kMomThreads, WN_EXP_MOM_LB) moments_range(Tree
   else process_node<KIND, true>(i, level - 1, tv, m, alpha);
 }
 
-// ---------------- prefix-difference builds (per-iteration attributes: ATTR_VEC, ATTR_SCALAR) ----------------
-// Every node B covers a contiguous range [pb, pe) of the Morton-sorted points, so its sums are
-// E[pe] − E[pb] of one exclusive prefix E over the points' (|ν|, |ν|x, ν) — no level-by-level chain:
-// one scan (3 launches) and one fully parallel node launch.  E is double-double (hi + lo, error-free
-// two-sum adds; lo stored in fp32), so a difference keeps ≈ 2^-77·|Σ_all| accuracy — far below the bottom-up fp64
-// rounding — and an exact integer count of the points with |ν| > 0 decides Σ|ν| = 0 (⇒ centroid)
-// exactly.  One-point nodes take their point's own values (exact: rep = the point).  DESIGN.md §Moments.
-// First-order far field (ORD = 1): the prefix also carries sym(Σ ν_j x_jᵀ) (vector ν,
-// 6 terms) or Σ s_j x_j (scalar, 3), and each node stores its first moment about the representative,
-// sym M = sym(Σ ν_j x_jᵀ) − sym(ν_B x_Bᵀ) or D = Σ s_j x_j − s_B x_B, in NodeSet::ext.
-#ifndef WN_EXP_SCANITEMS
-#define WN_EXP_SCANITEMS 8
-#endif
-constexpr int kScanThreads = 256, kScanItems = WN_EXP_SCANITEMS, kScanTile = kScanThreads * kScanItems;
-constexpr int kScanTopThreads = 256;
-#ifndef WN_EXP_FEWTILES
-#define WN_EXP_FEWTILES 512
-#endif
-constexpr int kFewTiles = WN_EXP_FEWTILES;  // up to this many tiles the prefix blocks sum earlier totals themselves
+// ---------------- tile builds (per-iteration attributes: ATTR_VEC, ATTR_SCALAR) ----------------
+// Every octree node B covers a contiguous range [pb, pe) of the Morton-sorted points.  The sorted points
+// are cut into tiles of kMomTile (tree_build.cu:plan_moment_tiles lists, per tile, the nodes whose points
+// lie in it):
+//   mom_tiles  (one block per tile) computes every point's terms (|ν|, |ν|x, ν, …) once into shared memory
+//              (coalesced loads; μ' = μ + α r written here; a one-point node's V = ν_j written here), then
+//              sums each node's range directly — one thread per node below kMomWarpNode points, one warp
+//              per larger node (lane-strided, then a fixed butterfly) — and writes its record; the same
+//              warps form the tile's total and, for the nodes across tiles, the partial sums at their ends;
+//   mom_cross  (one warp per node across tiles) adds  the partial sum at pb + the totals of the tiles in
+//              between (lane-strided, fixed butterfly) + the partial sum at pe.
+// fp64 direct sums in a fixed order: the error of a node's sum is relative to its own terms (as the
+// oracle's direct sums), Σ|ν| = 0 exactly iff every ν_j = 0 (a sum of non-negative terms), and the result
+// is bit-deterministic.  One-point nodes take their point's own values (rep = the point).
+// First-order far field (ORD = 1): the terms also carry sym(ν_j x_jᵀ) (vector ν, 6) or
+// s_j x_j (scalar, 3), and each node stores its first moment about the representative,
+// sym M = sym(Σ ν_j x_jᵀ) − sym(ν_B x_Bᵀ) or D = Σ s_j x_j − s_B x_B, in NodeSet::ext.  DESIGN.md §Moments.
 
-// components per prefix entry; entry j (exclusive: points [0, j)) = hi[EH] fp64 (the NC sums, the count,
-// padding) in E_hi and lo[EL] = the double-double low parts rounded to fp32 in E_lo
+// components of a point's terms: 0: |ν|, 1-3: |ν|x, 4..: ν (3 or 1), then the first-order sums (6 or 3)
 template <int KIND, int ORD>
-struct PreLayout {
-  static constexpr int NC = ORD == 0 ? 7 : (KIND == ATTR_VEC ? 13 : 10);
-  static constexpr int EH = (NC + 2) & ~1;
-  static constexpr int EL = (NC + 3) & ~3;
+struct Lay {
+  static constexpr int NV = KIND == ATTR_VEC ? 3 : 1;
+  static constexpr int NX = ORD == 1 ? (KIND == ATTR_VEC ? 6 : 3) : 0;
+  static constexpr int NC = 4 + NV + NX;
 };
-constexpr int kPreDoublesMax = 14 + 8;  // EH + EL/2 of the largest layout (vector, ORD 1)
+static_assert(Lay<ATTR_VEC, 1>::NC <= kMomNC, "tile totals / endpoint sums sized for the widest layout");
 
-struct DD {
-  double hi, lo;
-};
-
-// two-sum based double-double addition (adds only: nothing for the compiler to contract)
-__device__ __forceinline__ DD dd_add(DD a, DD b) {
-  const double s = __dadd_rn(a.hi, b.hi);
-  const double bb = __dsub_rn(s, a.hi);
-  double e = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(s, bb)), __dsub_rn(b.hi, bb));
-  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
-  const double h = __dadd_rn(s, e);
-  return DD{h, __dsub_rn(e, __dsub_rn(h, s))};
-}
-
-// per-point terms: (|ν|, |ν|x, |ν|y, |ν|z, ν) and, for ORD 1, sym(ν xᵀ) (xx, yy, zz, xy, xz, yz) or s x;
-// v: the attribute (vector: μ, or μ + α r when r is given; scalar: v.x), f: the per-point factor a (or 1)
+// per-point terms of attribute v (vector: ν, scalar: v.x; the a-factor f applied when `scaled`)
 template <int KIND, int ORD>
-__device__ __forceinline__ void point_terms(float4 x, float4 v, const float4* r, float alpha, double f,
-                                            bool scaled, double* o) {
+__device__ __forceinline__ void point_terms(float4 x, float4 v, double f, bool scaled, double* o) {
   double a, v0, v1 = 0.0, v2 = 0.0;
   if (KIND == ATTR_VEC) {
-    if (r)  // μ' = μ + α r (Alg. 2 line 3) — the same fmaf as the record's one-point branch
-      v = make_float4(fmaf(alpha, r->x, v.x), fmaf(alpha, r->y, v.y), fmaf(alpha, r->z, v.z), 0.f);
     v0 = v.x; v1 = v.y; v2 = v.z;
     if (scaled) {
       v0 *= f; v1 *= f; v2 *= f;
@@ -274,350 +253,55 @@ __device__ __forceinline__ void point_terms(float4 x, float4 v, const float4* r,
   o[2] = a * py;
   o[3] = a * pz;
   o[4] = v0;
-  o[5] = v1;
-  o[6] = v2;
-  if (ORD == 1) {
-    if (KIND == ATTR_VEC) {
-      o[7] = v0 * px;
-      o[8] = v1 * py;
-      o[9] = v2 * pz;
-      o[10] = 0.5 * (v0 * py + v1 * px);
-      o[11] = 0.5 * (v0 * pz + v2 * px);
-      o[12] = 0.5 * (v1 * pz + v2 * py);
-    } else {
-      o[7] = v0 * px;
-      o[8] = v0 * py;
-      o[9] = v0 * pz;
-    }
-  }
-}
-
-template <int KIND, int ORD>
-__device__ __forceinline__ void point_vals(int64_t j, const float4* __restrict__ pts, const MomentArgs& m, float alpha,
-                                           double* o) {
-  float4 v;
-  float4 r;
   if (KIND == ATTR_VEC) {
-    v = m.vec[j];
-    if (m.axpy_r) r = m.axpy_r[j];
-  } else {
-    v = make_float4(m.scal[j], 0.f, 0.f, 0.f);
+    o[5] = v1;
+    o[6] = v2;
   }
-  const bool scaled = m.a_sorted != nullptr;
-  point_terms<KIND, ORD>(pts[j], v, KIND == ATTR_VEC && m.axpy_r ? &r : nullptr, alpha,
-                         scaled ? (double)m.a_sorted[j] : 1.0, scaled, o);
-}
-
-// scan element: NC double-double sums + the number of points with |ν| > 0 (an exact integer)
-template <int NC>
-struct Elt {
-  DD v[NC];
-  double cnt;
-};
-
-template <int NC>
-__device__ __forceinline__ void elt_zero(Elt<NC>& e) {
-#pragma unroll
-  for (int c = 0; c < NC; ++c) e.v[c] = DD{0.0, 0.0};
-  e.cnt = 0.0;
-}
-template <int NC>
-__device__ __forceinline__ void elt_add(Elt<NC>& e, const Elt<NC>& f) {
-#pragma unroll
-  for (int c = 0; c < NC; ++c) e.v[c] = dd_add(e.v[c], f.v[c]);
-  e.cnt += f.cnt;
-}
-template <int NC>
-__device__ __forceinline__ void elt_add_point(Elt<NC>& e, const double* o) {
-#pragma unroll
-  for (int c = 0; c < NC; ++c) e.v[c] = dd_add(e.v[c], DD{o[c], 0.0});
-  e.cnt += o[0] > 0.0 ? 1.0 : 0.0;
-}
-template <int NC>
-__device__ __forceinline__ Elt<NC> elt_shfl_up(const Elt<NC>& e, int d) {
-  Elt<NC> r;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    r.v[c].hi = __shfl_up_sync(0xffffffffu, e.v[c].hi, d);
-    r.v[c].lo = __shfl_up_sync(0xffffffffu, e.v[c].lo, d);
-  }
-  r.cnt = __shfl_up_sync(0xffffffffu, e.cnt, d);
-  return r;
-}
-// inclusive warp scan over the first `width` lanes (fixed order)
-template <int NC>
-__device__ __forceinline__ void warp_inscan(Elt<NC>& x, int lane, int width) {
-  for (int o = 1; o < width; o <<= 1) {
-    const Elt<NC> y = elt_shfl_up(x, o);
-    if (lane >= o) {
-      Elt<NC> z = y;
-      elt_add(z, x);
-      x = z;
-    }
-  }
-}
-
-// block-wide exclusive scan (fixed order: deterministic); e becomes the exclusive prefix, tot the total
-template <int NT, int NC>
-__device__ __forceinline__ void block_exscan(Elt<NC>& e, Elt<NC>& tot) {
-  constexpr int NW = NT / 32;
-  __shared__ Elt<NC> ws[NW + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Elt<NC> inc = e;
-  warp_inscan(inc, lane, 32);
-  if (lane == 31) ws[warp] = inc;
-  Elt<NC> prev = elt_shfl_up(inc, 1);
-  if (lane == 0) elt_zero(prev);
-  __syncthreads();
-  if (warp == 0) {  // scan of the warp totals by one warp
-    Elt<NC> x;
-    if (lane < NW) x = ws[lane];
-    else elt_zero(x);
-    warp_inscan(x, lane, NW);
-    Elt<NC> xp = elt_shfl_up(x, 1);
-    if (lane == 0) elt_zero(xp);
-    __syncwarp();
-    if (lane < NW) ws[lane] = xp;
-    if (lane == NW - 1) ws[NW] = x;
-  }
-  __syncthreads();
-  e = ws[warp];
-  elt_add(e, prev);
-  tot = ws[NW];
-  __syncthreads();
-}
-
-template <int KIND, int ORD>
-__global__ void __launch_bounds__(kScanThreads) mom_tile_sum(const float4* __restrict__ pts, MomentArgs m, int64_t n,
-                                                             Elt<PreLayout<KIND, ORD>::NC>* __restrict__ tile_tot) {
-  constexpr int NC = PreLayout<KIND, ORD>::NC;
-  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-  Elt<NC> t, tot;
-  elt_zero(t);
-  // coalesced: item k of thread x is point tile·T + k·256 + x (totals need no ownership order)
-  const int64_t j0 = blockIdx.x * (int64_t)kScanTile + threadIdx.x;
-#pragma unroll 2
-  for (int k = 0; k < kScanItems; ++k) {
-    const int64_t j = j0 + k * kScanThreads;
-    if (j < n) {
-      double o[NC];
-      point_vals<KIND, ORD>(j, pts, m, alpha, o);
-      elt_add_point(t, o);
-    }
-  }
-  block_exscan<kScanThreads>(t, tot);
-  if (threadIdx.x == 0) tile_tot[blockIdx.x] = tot;
-}
-
-template <int NC>
-__global__ void __launch_bounds__(kScanTopThreads) mom_tile_scan(const Elt<NC>* __restrict__ tile_tot, int64_t ntiles,
-                                                                 Elt<NC>* __restrict__ tile_off) {
-  const int64_t per = (ntiles + kScanTopThreads - 1) / kScanTopThreads;
-  const int64_t t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
-  Elt<NC> v, tot;
-  elt_zero(v);
-  for (int64_t t = t0; t < t1; ++t) elt_add(v, tile_tot[t]);
-  block_exscan<kScanTopThreads>(v, tot);
-  for (int64_t t = t0; t < t1; ++t) {
-    tile_off[t] = v;
-    elt_add(v, tile_tot[t]);
-  }
-}
-
-template <int KIND, int ORD>
-__device__ __forceinline__ void store_pre(double* __restrict__ Eh, float* __restrict__ El, int64_t j,
-                                          const Elt<PreLayout<KIND, ORD>::NC>& t) {
-  using Lay = PreLayout<KIND, ORD>;
-  double h[Lay::EH];
-  float l[Lay::EL];
-#pragma unroll
-  for (int c = 0; c < Lay::EH; ++c) h[c] = c < Lay::NC ? t.v[c].hi : (c == Lay::NC ? t.cnt : 0.0);
-#pragma unroll
-  for (int c = 0; c < Lay::EL; ++c) l[c] = c < Lay::NC ? (float)t.v[c].lo : 0.f;
-  double2* hp = reinterpret_cast<double2*>(Eh + Lay::EH * j);
-#pragma unroll
-  for (int c = 0; c < Lay::EH / 2; ++c) hp[c] = make_double2(h[2 * c], h[2 * c + 1]);
-  float4* lp = reinterpret_cast<float4*>(El + Lay::EL * j);
-#pragma unroll
-  for (int c = 0; c < Lay::EL / 4; ++c) lp[c] = make_float4(l[4 * c], l[4 * c + 1], l[4 * c + 2], l[4 * c + 3]);
-}
-
-// the prefix stages its tile's inputs in shared memory with coalesced loads (points, attribute, r) and the
-// threads then read their consecutive items from there: padded one float4 (float) per 8 so that the
-// stride-8 item reads of a warp are free of bank conflicts
-constexpr int kStageN = kScanTile + kScanTile / 8;
-__device__ __forceinline__ int stage_ix(int jl) { return jl + (jl >> 3); }
-template <int KIND>
-constexpr size_t stage_bytes() {  // points, attribute (float4 / float), r (vector only)
-  return KIND == ATTR_VEC ? 3 * kStageN * sizeof(float4) : kStageN * (sizeof(float4) + sizeof(float));
-}
-
-template <int KIND, int ORD>
-__global__ void __launch_bounds__(kScanThreads) mom_tile_prefix(const float4* __restrict__ pts, MomentArgs m,
-                                                                int64_t n,
-                                                                const Elt<PreLayout<KIND, ORD>::NC>* __restrict__ tile_off,
-                                                                const Elt<PreLayout<KIND, ORD>::NC>* __restrict__ tile_tot,
-                                                                double* __restrict__ Eh, float* __restrict__ El) {
-  constexpr int NC = PreLayout<KIND, ORD>::NC;
-  extern __shared__ float4 stage[];
-  float4* sp = stage;
-  float4* sv = stage + kStageN;                                   // vector attribute
-  float4* sr = stage + 2 * kStageN;                               // r (μ' = μ + α r)
-  float* ss = reinterpret_cast<float*>(stage + kStageN);          // scalar attribute
-  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-  const bool axpy = KIND == ATTR_VEC && m.axpy_r;
-  const bool scaled = m.a_sorted != nullptr;
-  const int64_t base = blockIdx.x * (int64_t)kScanTile;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {  // coalesced staging
-    const int jl = threadIdx.x + k * kScanThreads;
-    const int64_t j = base + jl;
-    if (j < n) {
-      const int x = stage_ix(jl);
-      sp[x] = pts[j];
-      if (KIND == ATTR_VEC) {
-        sv[x] = m.vec[j];
-        if (axpy) sr[x] = m.axpy_r[j];
-      } else {
-        ss[x] = m.scal[j];
-      }
-    }
-  }
-  __syncthreads();
-  auto vals = [&](int jl, double* o) {
-    const int x = stage_ix(jl);
-    const float4 v = KIND == ATTR_VEC ? sv[x] : make_float4(ss[x], 0.f, 0.f, 0.f);
-    float4 r;
-    if (axpy) r = sr[x];
-    point_terms<KIND, ORD>(sp[x], v, axpy ? &r : nullptr, alpha, scaled ? (double)m.a_sorted[base + jl] : 1.0,
-                           scaled, o);
-  };
-  Elt<NC> t, tot;
-  elt_zero(t);
-  const int jl0 = threadIdx.x * kScanItems;  // consecutive ownership
-  const int64_t j0 = base + jl0;
-  for (int k = 0; k < kScanItems; ++k)
-    if (j0 + k < n) {
-      double o[NC];
-      vals(jl0 + k, o);
-      elt_add_point(t, o);
-    }
-  block_exscan<kScanThreads>(t, tot);
-  if (tile_off) {  // the tile offsets of mom_tile_scan
-    Elt<NC> z = tile_off[blockIdx.x];
-    elt_add(z, t);
-    t = z;
-  } else if (tile_tot && blockIdx.x > 0) {  // few tiles: this tile's offset = Σ of the earlier totals, here
-    Elt<NC> v, z;
-    elt_zero(v);
-    for (int64_t k = threadIdx.x; k < blockIdx.x; k += kScanThreads) elt_add(v, tile_tot[k]);
-    block_exscan<kScanThreads>(v, z);  // z: the block total, a fixed-order reduction
-    elt_add(z, t);
-    t = z;
-  }  // (neither: a single tile, offset 0)
-  for (int k = 0; k < kScanItems; ++k) {
-    const int64_t j = j0 + k;
-    if (j < n) {
-      store_pre<KIND, ORD>(Eh, El, j, t);
-      double o[NC];
-      vals(jl0 + k, o);
-      elt_add_point(t, o);
-      if (j == n - 1) store_pre<KIND, ORD>(Eh, El, n, t);
-    }
-  }
-  if (axpy) {  // μ' written once here (coalesced), read by the G traversal
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      const int jl = threadIdx.x + k * kScanThreads;
-      if (base + jl < n) {
-        const int x = stage_ix(jl);
-        const float4 v = sv[x], r = sr[x];
-        m.axpy_out[base + jl] = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
-      }
-    }
-  }
-}
-
-template <int KIND, int ORD>
-__global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int64_t nn, const double* __restrict__ Eh,
-                                                 const float* __restrict__ El, const int32_t* __restrict__ list) {
-  using Lay = PreLayout<KIND, ORD>;
-  constexpr int NC = Lay::NC;
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= nn) return;
-  const int64_t i = list ? (int64_t)list[k] : k;  // list: only the nodes a traversal can visit
-  WN_DCHECK(i >= 0 && i < (list ? (int64_t)1 << 31 : nn), "moment node index");
-  const int j0 = tv.pb[i], j1 = tv.pe[i];
-  double d[NC];
-  const float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (j1 - j0 == 1) {  // one-point node: R = (x_j, −1), L and ext (= 0) are fixed per tree — only V = ν_j
-    const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
-    double v0, v1 = 0.0, v2 = 0.0;
+  if (ORD == 1) {
+    constexpr int X = Lay<KIND, ORD>::NC - Lay<KIND, ORD>::NX;
     if (KIND == ATTR_VEC) {
-      float4 v = m.vec[j0];
-      if (m.axpy_r) {
-        const float4 r = m.axpy_r[j0];
-        v = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
-      }
-      v0 = v.x; v1 = v.y; v2 = v.z;
-      if (m.a_sorted) {
-        const double f = m.a_sorted[j0];
-        v0 *= f; v1 *= f; v2 *= f;
-      }
-      if (m.write_W) tv.sums[8 * i] = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+      o[X + 0] = v0 * px;
+      o[X + 1] = v1 * py;
+      o[X + 2] = v2 * pz;
+      o[X + 3] = 0.5 * (v0 * py + v1 * px);
+      o[X + 4] = 0.5 * (v0 * pz + v2 * px);
+      o[X + 5] = 0.5 * (v1 * pz + v2 * py);
     } else {
-      v0 = m.scal[j0];
-      if (m.a_sorted) v0 *= (double)m.a_sorted[j0];
-      if (m.write_W) tv.sums[8 * i] = fabs(v0);
-    }
-    m.out.rec[kRec * i + 1] = make_float4((float)v0, (float)v1, (float)v2, __int_as_float(tv.topo[i]));
-    return;
-  } else {
-    WN_DCHECK(j0 >= 0 && j0 < j1, "moment point range");
-    const double2* a = reinterpret_cast<const double2*>(Eh + Lay::EH * (int64_t)j0);
-    const double2* b = reinterpret_cast<const double2*>(Eh + Lay::EH * (int64_t)j1);
-    double ah[Lay::EH], bh[Lay::EH];
-#pragma unroll
-    for (int c = 0; c < Lay::EH / 2; ++c) {
-      const double2 x = a[c], y = b[c];
-      ah[2 * c] = x.x; ah[2 * c + 1] = x.y;
-      bh[2 * c] = y.x; bh[2 * c + 1] = y.y;
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) d[c] = 0.0;
-    if (bh[NC] != ah[NC]) {  // else no point has |ν| > 0: Σ|ν| = 0 and every ν_j = 0, exactly
-      const float4* al = reinterpret_cast<const float4*>(El + Lay::EL * (int64_t)j0);
-      const float4* bl = reinterpret_cast<const float4*>(El + Lay::EL * (int64_t)j1);
-      float alo[Lay::EL], blo[Lay::EL];
-#pragma unroll
-      for (int c = 0; c < Lay::EL / 4; ++c) {
-        const float4 x = al[c], y = bl[c];
-        alo[4 * c] = x.x; alo[4 * c + 1] = x.y; alo[4 * c + 2] = x.z; alo[4 * c + 3] = x.w;
-        blo[4 * c] = y.x; blo[4 * c + 1] = y.y; blo[4 * c + 2] = y.z; blo[4 * c + 3] = y.w;
-      }
-#pragma unroll
-      for (int c = 0; c < NC; ++c) d[c] = dd_add(DD{bh[c], (double)blo[c]}, DD{-ah[c], -(double)alo[c]}).hi;
+      o[X + 0] = v0 * px;
+      o[X + 1] = v0 * py;
+      o[X + 2] = v0 * pz;
     }
   }
+}
+
+// record of a node with ≥ 2 points from its sums d (Σ|ν| = d[0] = 0 exactly iff every ν_j = 0)
+template <int KIND, int ORD>
+__device__ __forceinline__ void sums_record(int64_t i, int npts, const double* d, const TreeView& tv,
+                                            const MomentArgs& m, int tdepth, int topo, int smask) {
+  using Ly = Lay<KIND, ORD>;
   Sums S;
   S.W = d[0];
   S.P[0] = d[1]; S.P[1] = d[2]; S.P[2] = d[3];
-  S.V[0] = d[4]; S.V[1] = d[5]; S.V[2] = d[6];
+  S.V[0] = d[4];
+  S.V[1] = KIND == ATTR_VEC ? d[5] : 0.0;
+  S.V[2] = KIND == ATTR_VEC ? d[6] : 0.0;
   if (m.write_W) tv.sums[8 * i] = S.W;
-  write_record<KIND>(i, S, j1 - j0, p0, tv.depth[i], tv.topo[i], tv.smask[i], m.theta, tv.centroid, m);
+  write_record<KIND>(i, S, npts, make_float4(0.f, 0.f, 0.f, 0.f), tdepth, topo, smask, m.theta, tv.centroid, m);
   if (ORD == 1) {  // first moment about the fp64 representative (0 for Σ|ν| = 0)
+    constexpr int X = Ly::NC - Ly::NX;
     float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f), e1 = e0;
     if (S.W > 0.0) {
-      const double X = S.P[0] / S.W, Y = S.P[1] / S.W, Z = S.P[2] / S.W;
+      const double Xr = S.P[0] / S.W, Yr = S.P[1] / S.W, Zr = S.P[2] / S.W;
       if (KIND == ATTR_VEC) {
-        const double mxx = d[7] - S.V[0] * X, myy = d[8] - S.V[1] * Y, mzz = d[9] - S.V[2] * Z;
-        const double mxy = d[10] - 0.5 * (S.V[0] * Y + S.V[1] * X);
-        const double mxz = d[11] - 0.5 * (S.V[0] * Z + S.V[2] * X);
-        const double myz = d[12] - 0.5 * (S.V[1] * Z + S.V[2] * Y);
+        const double mxx = d[X] - S.V[0] * Xr, myy = d[X + 1] - S.V[1] * Yr, mzz = d[X + 2] - S.V[2] * Zr;
+        const double mxy = d[X + 3] - 0.5 * (S.V[0] * Yr + S.V[1] * Xr);
+        const double mxz = d[X + 4] - 0.5 * (S.V[0] * Zr + S.V[2] * Xr);
+        const double myz = d[X + 5] - 0.5 * (S.V[1] * Zr + S.V[2] * Yr);
         e0 = make_float4((float)mxx, (float)myy, (float)mzz, (float)(mxx + myy + mzz));
         e1 = make_float4((float)mxy, (float)mxz, (float)myz, 0.f);
       } else {
-        e0 = make_float4((float)(d[7] - S.V[0] * X), (float)(d[8] - S.V[0] * Y), (float)(d[9] - S.V[0] * Z), 0.f);
+        e0 = make_float4((float)(d[X] - S.V[0] * Xr), (float)(d[X + 1] - S.V[0] * Yr), (float)(d[X + 2] - S.V[0] * Zr),
+                         0.f);
       }
     }
     m.out.ext[2 * i] = e0;
@@ -625,35 +309,168 @@ __global__ void __launch_bounds__(256) mom_nodes(TreeView tv, MomentArgs m, int6
   }
 }
 
+struct TilePlanView {
+  const int4 *small, *large;
+  const int32_t *tile_soff, *tile_loff, *cross, *ep_slot, *tile_eoff;
+  const int2* onept;
+  const uint64_t* ep_key;
+  double* epval;  // 2·ncross × kMomNC
+  double* ttot;   // ntiles × kMomNC
+  int64_t ncross;
+};
+
+constexpr int kTileThreads = 256, kTileWarps = kTileThreads / 32;
+
+// warp sum of NC planes over [l0, l1): lanes stride, then a fixed xor butterfly (every lane gets the same bits)
+template <int NC>
+__device__ __forceinline__ void warp_range_sum(const double* __restrict__ sm, int l0, int l1, int lane, double* d) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) d[c] = 0.0;
+  for (int l = l0 + lane; l < l1; l += 32)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) d[c] += sm[c * kMomTile + l];
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) d[c] += __shfl_xor_sync(0xffffffffu, d[c], o);
+}
+
+// d[k] (registers are not indexable at run time: a select chain)
+template <int NC>
+__device__ __forceinline__ double pick(const double* d, int k) {
+  double r = d[0];
+#pragma unroll
+  for (int c = 1; c < NC; ++c)
+    if (k == c) r = d[c];
+  return r;
+}
+
 template <int KIND, int ORD>
-void launch_prefix(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
-  using Lay = PreLayout<KIND, ORD>;
-  TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->tdepth, t->topo, t->smask, t->sums, t->centroid};
-  const int64_t nt = t->mom_ntiles;
-  Elt<Lay::NC>* tot = reinterpret_cast<Elt<Lay::NC>*>(t->mom_tile);
-  Elt<Lay::NC>* off = tot + nt;
-  double* Eh = t->mom_pre;
-  float* El = reinterpret_cast<float*>(t->mom_pre + Lay::EH * (t->n + 1));
-  // a single tile needs no tile totals; up to kFewTiles tiles each prefix block sums the earlier tile
-  // totals itself (no one-block scan launch); more tiles go through mom_tile_scan
-  const bool scan = nt > kFewTiles;
-  if (nt > 1) {
-    mom_tile_sum<KIND, ORD><<<(unsigned)nt, kScanThreads, 0, s>>>(t->pts, m, t->n, tot);
-    if (scan) mom_tile_scan<Lay::NC><<<1, kScanTopThreads, 0, s>>>(tot, nt, off);
+__global__ void __launch_bounds__(kTileThreads) mom_tiles(TreeView tv, MomentArgs m, int64_t n, TilePlanView P) {
+  constexpr int NC = Lay<KIND, ORD>::NC;
+  extern __shared__ double sm[];  // NC planes of kMomTile per-point terms
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
+  const bool axpy = KIND == ATTR_VEC && m.axpy_r;
+  const bool scaled = m.a_sorted != nullptr;
+  const int64_t tile = blockIdx.x, base = tile * (int64_t)kMomTile;
+  const int nv = (int)(n - base < kMomTile ? n - base : kMomTile);
+  for (int jl = threadIdx.x; jl < nv; jl += kTileThreads) {  // coalesced
+    const int64_t j = base + jl;
+    float4 v = KIND == ATTR_VEC ? m.vec[j] : make_float4(m.scal[j], 0.f, 0.f, 0.f);
+    if (axpy) {  // μ' = μ + α r (Alg. 2 line 3), written once here, read by the G traversal
+      const float4 r = m.axpy_r[j];
+      v = make_float4(fmaf(alpha, r.x, v.x), fmaf(alpha, r.y, v.y), fmaf(alpha, r.z, v.z), 0.f);
+      m.axpy_out[j] = v;
+    }
+    const double f = scaled ? (double)m.a_sorted[j] : 1.0;
+    double o[NC];
+    point_terms<KIND, ORD>(tv.pts[j], v, f, scaled, o);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) sm[c * kMomTile + jl] = o[c];
+    const int2 op = P.onept[j];
+    if (op.x >= 0) {  // one-point node: R = (x_j, −1), L, ext (= 0) fixed per tree; V = ν_j, the leaf term's ν
+      if (m.write_W) tv.sums[8 * (int64_t)op.x] = o[0];
+      const float4 V = KIND == ATTR_VEC ? make_float4((float)o[4], (float)o[5], (float)o[6], __int_as_float(op.y))
+                                        : make_float4((float)o[4], 0.f, 0.f, __int_as_float(op.y));
+      m.out.rec[kRec * (int64_t)op.x + 1] = V;
+    }
   }
-  static bool smem_set = false;  // per instantiation: the staging buffer exceeds the 48 KB default
+  __syncthreads();
+  // small nodes: one thread each, points in order
+  for (int x = P.tile_soff[tile] + threadIdx.x; x < P.tile_soff[tile + 1]; x += kTileThreads) {
+    const int4 d4 = P.small[x];
+    const int l0 = d4.y & 0xffff, l1 = d4.y >> 16;
+    WN_DCHECK(l0 + 1 < l1 && l1 <= nv, "moment node range");
+    double d[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) d[c] = sm[c * kMomTile + l0];
+    for (int l = l0 + 1; l < l1; ++l)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) d[c] += sm[c * kMomTile + l];
+    sums_record<KIND, ORD>(d4.x, l1 - l0, d, tv, m, d4.w >> 16, d4.z, d4.w & 0xffff);
+  }
+  // warp items: the large nodes, the endpoint sums, the tile total
+  const int L0 = P.tile_loff[tile], nl = P.tile_loff[tile + 1] - L0;
+  const int E0 = P.tile_eoff[tile], ne = P.tile_eoff[tile + 1] - E0;
+  for (int w = warp; w < nl + ne + 1; w += kTileWarps) {
+    double d[NC];
+    if (w < nl) {
+      const int4 d4 = P.large[L0 + w];
+      const int l0 = d4.y & 0xffff, l1 = d4.y >> 16;
+      WN_DCHECK(l0 < l1 && l1 <= nv, "moment node range");
+      warp_range_sum<NC>(sm, l0, l1, lane, d);
+      if (lane == 0) sums_record<KIND, ORD>(d4.x, l1 - l0, d, tv, m, d4.w >> 16, d4.z, d4.w & 0xffff);
+    } else if (w < nl + ne) {
+      const int e = E0 + w - nl, slot = P.ep_slot[e];
+      const int j = (int)(P.ep_key[e] - (uint64_t)tile * (kMomTile + 1));
+      WN_DCHECK(j >= 0 && j <= nv, "moment endpoint");
+      // slot 2c: the node starts here — its points from j to the tile's end; 2c + 1: it ends here — [0, j)
+      if (slot & 1) warp_range_sum<NC>(sm, 0, j, lane, d);
+      else warp_range_sum<NC>(sm, j, nv, lane, d);
+      if (lane < NC) P.epval[(size_t)kMomNC * slot + lane] = pick<NC>(d, lane);
+    } else {
+      warp_range_sum<NC>(sm, 0, nv, lane, d);
+      if (lane < NC) P.ttot[(size_t)kMomNC * tile + lane] = pick<NC>(d, lane);
+    }
+  }
+}
+
+// one warp per node across tiles: Σ at pb's end + the tile totals in between + Σ at pe's end
+template <int KIND, int ORD>
+__global__ void __launch_bounds__(256) mom_cross(TreeView tv, MomentArgs m, TilePlanView P) {
+  constexpr int NC = Lay<KIND, ORD>::NC;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (c >= P.ncross) return;
+  const int64_t i = P.cross[c];
+  const int j0 = tv.pb[i], j1 = tv.pe[i];
+  const int64_t ta = j0 / kMomTile, tb = (j1 - 1) / kMomTile;
+  double d[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) d[k] = 0.0;
+  // lane-strided over the middle tiles, four tiles' loads in flight per step (added in tile order)
+  constexpr int U = 4;
+  for (int64_t k0 = ta + 1 + lane; k0 < tb; k0 += 32 * U) {
+    double x[U][NC];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + 32 * u;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) x[u][q] = k < tb ? P.ttot[(size_t)kMomNC * k + q] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < NC; ++q) d[q] += x[u][q];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+#pragma unroll
+    for (int q = 0; q < NC; ++q) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+  if (lane != 0) return;
+  const double* ea = P.epval + (size_t)kMomNC * (2 * c);
+  const double* eb = ea + kMomNC;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) d[q] = (ea[q] + d[q]) + eb[q];
+  sums_record<KIND, ORD>(i, j1 - j0, d, tv, m, tv.depth[i], tv.topo[i], tv.smask[i]);
+}
+
+template <int KIND, int ORD>
+void launch_tiles(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
+  constexpr int NC = Lay<KIND, ORD>::NC;
+  TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->tdepth, t->topo, t->smask, t->sums, t->centroid};
+  const MomPlan& Pl = t->mplan[(m.all_nodes || m.write_W || !t->mom_live) ? 1 : 0];
+  TilePlanView P{Pl.small, Pl.large, Pl.tile_soff, Pl.tile_loff, Pl.cross, Pl.ep_slot, Pl.tile_eoff, Pl.onept,
+                 Pl.ep_key, Pl.epval, t->mom_ttot, Pl.ncross};
+  constexpr size_t smem = (size_t)NC * kMomTile * sizeof(double);
+  static bool smem_set = false;  // per instantiation: beyond the 48 KB default
   if (!smem_set) {
-    cudaFuncSetAttribute(mom_tile_prefix<KIND, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)stage_bytes<KIND>());
+    cudaFuncSetAttribute(mom_tiles<KIND, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     smem_set = true;
   }
-  mom_tile_prefix<KIND, ORD><<<(unsigned)nt, kScanThreads, stage_bytes<KIND>(), s>>>(
-      t->pts, m, t->n, scan ? off : nullptr, nt > 1 ? tot : nullptr, Eh, El);
-  // per-iteration builds: only the nodes a traversal can read (chain interiors and the children of
-  // pseudo-leaves are never visited); the diagnostic export (write_W) builds every node
-  const bool all = m.all_nodes || m.write_W || !t->mom_live;
-  const int64_t cnt = all ? t->nn : t->mom_nlive;
-  mom_nodes<KIND, ORD><<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(tv, m, cnt, Eh, El, all ? nullptr : t->mom_live);
+  mom_tiles<KIND, ORD><<<(unsigned)t->mom_ntiles, kTileThreads, smem, s>>>(tv, m, t->n, P);
+  if (Pl.ncross > 0) mom_cross<KIND, ORD><<<(unsigned)((Pl.ncross * 32 + 255) / 256), 256, 0, s>>>(tv, m, P);
 }
 
 template <int KIND>
@@ -691,28 +508,27 @@ wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
   WN_CUDA(cudaMallocAsync((void**)&t->mom_loff, t->level_off.size() * sizeof(int64_t), s));
   WN_CUDA(cudaMemcpyAsync(t->mom_loff, t->level_off.data(), t->level_off.size() * sizeof(int64_t),
                           cudaMemcpyHostToDevice, s));
-  t->mom_ntiles = (t->n + kScanTile - 1) / kScanTile;
-  WN_CUDA(cudaMallocAsync((void**)&t->mom_pre, 12 * (size_t)(t->n + 1) * sizeof(double), s));
-  WN_CUDA(cudaMallocAsync((void**)&t->mom_tile, 2 * (size_t)t->mom_ntiles * sizeof(Elt<7>), s));
+  t->mom_ntiles = (t->n + kMomTile - 1) / kMomTile;
+  WN_TRY(plan_moment_tiles(t, 0, s));
   return WN_OK;
 }
 
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
-#ifndef WN_EXP_OLD_MOM
-  if (m.kind != ATTR_UNIT) {  // per-iteration attributes: prefix differences
-    ProfScope ps(WN_PROF_MOMENTS, s, t->mom_ntiles > 1 ? (t->mom_ntiles > kFewTiles ? 4 : 3) : 2);
+  if (m.kind != ATTR_UNIT) {  // per-iteration attributes: tile builds
+    const int which = (m.all_nodes || m.write_W || !t->mom_live) ? 1 : 0;
+    WN_TRY(plan_moment_tiles(t, which, s));  // (the export plan on first use; never inside a graph capture)
+    ProfScope ps(WN_PROF_MOMENTS, s, t->mplan[which].ncross > 0 ? 2 : 1);  // mom_tiles (+ mom_cross)
     if (m.order1 && !(m.out.ext && t->mom_order1_ready)) return set_error(WN_ERR_ARG, "internal: order-1 scratch");
     if (m.kind == ATTR_VEC) {
-      if (m.order1) launch_prefix<ATTR_VEC, 1>(t, m, s);
-      else launch_prefix<ATTR_VEC, 0>(t, m, s);
+      if (m.order1) launch_tiles<ATTR_VEC, 1>(t, m, s);
+      else launch_tiles<ATTR_VEC, 0>(t, m, s);
     } else {
-      if (m.order1) launch_prefix<ATTR_SCALAR, 1>(t, m, s);
-      else launch_prefix<ATTR_SCALAR, 0>(t, m, s);
+      if (m.order1) launch_tiles<ATTR_SCALAR, 1>(t, m, s);
+      else launch_tiles<ATTR_SCALAR, 0>(t, m, s);
     }
     WN_CUDA(cudaGetLastError());
     return WN_OK;
   }
-#endif
   ProfScope ps(WN_PROF_MOMENTS, s, (t->mom_cut <= t->depth_used ? 1 + (t->depth_used - t->mom_cut + 1) / 2 : 0) + (t->mom_cut > 0));
   switch (m.kind) {
     case ATTR_VEC: launch_all<ATTR_VEC>(t, m, s, t->mom_loff); break;
@@ -726,13 +542,7 @@ wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
 // order-1 far field (row f2): larger prefix entries and tile totals, the node sets' ext arrays
 wn_status enable_order1(wn_tree_s* t, cudaStream_t s) {
   if (t->mom_order1_ready) return WN_OK;
-  invalidate_graph(t);  // a cached order-0 graph references the prefix scratch freed here
-  cudaFreeAsync(t->mom_pre, s);
-  cudaFreeAsync(t->mom_tile, s);
-  t->mom_pre = nullptr;
-  t->mom_tile = nullptr;
-  WN_CUDA(cudaMallocAsync((void**)&t->mom_pre, kPreDoublesMax * (size_t)(t->n + 1) * sizeof(double), s));
-  WN_CUDA(cudaMallocAsync((void**)&t->mom_tile, 2 * (size_t)t->mom_ntiles * sizeof(Elt<13>), s));
+  invalidate_graph(t);  // (no captured buffer changes; a cached graph is keyed on the order anyway)
   WN_CUDA(cudaMallocAsync((void**)&t->set[0].ext, 2 * (size_t)(t->nn + 1) * sizeof(float4), s));
   WN_CUDA(cudaMemsetAsync(t->set[0].ext, 0, 2 * (size_t)(t->nn + 1) * sizeof(float4), s));
   t->mom_order1_ready = true;

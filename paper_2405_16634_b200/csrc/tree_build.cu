@@ -900,6 +900,185 @@ __global__ void live_keys(int64_t m, const int32_t* __restrict__ list, const int
   v[i] = node;
 }
 
+// ---- tile plan of the per-iteration moment builds (moments.cu: mom_tiles / mom_cross) ----
+__global__ void k_node_keys(int64_t m, const int32_t* __restrict__ list, const int32_t* __restrict__ pb,
+                            uint64_t* __restrict__ k, int32_t* __restrict__ v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int32_t node = list ? list[i] : (int32_t)i;
+  k[i] = (uint64_t)pb[node];
+  v[i] = node;
+}
+
+// class of a listed node: 0 one point, 1 small (one tile), 2 large (one tile), 3 across tiles
+__device__ __forceinline__ int node_class(int32_t b, int32_t e) {
+  if (e - b == 1) return 0;
+  if (b / kMomTile != (e - 1) / kMomTile) return 3;
+  return e - b < kMomWarpNode ? 1 : 2;
+}
+
+__global__ void k_class_flag(int64_t m, const int32_t* __restrict__ list, const int32_t* __restrict__ pb,
+                             const int32_t* __restrict__ pe, int cls, uint32_t* __restrict__ flag) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int32_t i = list[k];
+  flag[k] = node_class(pb[i], pe[i]) == cls;
+}
+
+// compaction of one class in list order; one-tile classes as descriptors (local point range, code, one-point
+// child mask, threshold depth: what the tile build needs in one load)
+__global__ void k_class_put(int64_t m, const int32_t* __restrict__ list, const uint32_t* __restrict__ flag,
+                            const uint32_t* __restrict__ pos, const int32_t* __restrict__ pb,
+                            const int32_t* __restrict__ pe, const int32_t* __restrict__ topo,
+                            const int32_t* __restrict__ smask, const int32_t* __restrict__ tdepth,
+                            int4* __restrict__ desc, int32_t* __restrict__ ids) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m || !flag[k]) return;
+  const int32_t i = list[k];
+  if (ids) {
+    ids[pos[k]] = i;
+  } else {
+    const int32_t b0 = (pb[i] / kMomTile) * kMomTile;
+    desc[pos[k]] = make_int4(i, (pb[i] - b0) | ((pe[i] - b0) << 16), topo[i], smask[i] | (tdepth[i] << 16));
+  }
+}
+
+__global__ void k_onept(int64_t m, const int32_t* __restrict__ list, const int32_t* __restrict__ pb,
+                        const int32_t* __restrict__ pe, const int32_t* __restrict__ topo, int2* __restrict__ onept) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int32_t i = list[k];
+  if (pe[i] - pb[i] == 1) onept[pb[i]] = make_int2(i, topo[i]);  // (a point's one-point node is its leaf: unique)
+}
+
+// tile k's descriptors start at the first whose first point is ≥ k·kMomTile (lists sorted by first point)
+__global__ void k_tile_off(int64_t ntiles, const int4* __restrict__ desc, int64_t nd, const int32_t* __restrict__ pb,
+                           int32_t* __restrict__ off) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k > ntiles) return;
+  const int64_t target = k * (int64_t)kMomTile;
+  int64_t lo = 0, hi = nd;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)pb[desc[mid].x] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  off[k] = (int32_t)lo;
+}
+
+// endpoints of the cross-tile nodes: Σ from pb to the end of pb's tile, Σ from the start of (pe − 1)'s tile to pe
+__global__ void k_ep_keys(int64_t nc, const int32_t* __restrict__ cross, const int32_t* __restrict__ pb,
+                          const int32_t* __restrict__ pe, uint64_t* __restrict__ key, int32_t* __restrict__ slot) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const int64_t b = pb[cross[c]], e = pe[cross[c]];
+  const int64_t ta = b / kMomTile, tb = (e - 1) / kMomTile;
+  key[2 * c] = (uint64_t)(ta * (kMomTile + 1) + (b - ta * kMomTile));
+  key[2 * c + 1] = (uint64_t)(tb * (kMomTile + 1) + (e - tb * kMomTile));
+  slot[2 * c] = (int32_t)(2 * c);
+  slot[2 * c + 1] = (int32_t)(2 * c + 1);
+}
+
+__global__ void k_tile_eoff(int64_t ntiles, const uint64_t* __restrict__ key, int64_t ne, int32_t* __restrict__ off) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k > ntiles) return;
+  const uint64_t target = (uint64_t)k * (kMomTile + 1);
+  int64_t lo = 0, hi = ne;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (key[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  off[k] = (int32_t)lo;
+}
+
+static int key_bits(int64_t maxval) {
+  int bits = 1;
+  while (bits < 62 && ((int64_t)1 << bits) <= maxval) ++bits;
+  return bits;
+}
+
+wn_status plan_moment_tiles(wn_tree_s* t, int which, cudaStream_t s) {
+  MomPlan& P = t->mplan[which];
+  if (P.ready) return WN_OK;
+  TempSet tmp(s);
+  const int64_t n = t->n, ntiles = (n + kMomTile - 1) / kMomTile;
+  // the node list in ascending first point: the visitable nodes (already sorted) or all nodes (sorted here)
+  const int32_t* list = t->mom_live;
+  int64_t m = t->mom_nlive;
+  if (which == 1) {
+    m = t->nn;
+    uint64_t* k = nullptr;
+    int32_t *v = nullptr, *sorted = nullptr;
+    WN_TRY(tmp.alloc(&k, m));
+    WN_TRY(tmp.alloc(&v, m));
+    WN_TRY(tmp.alloc(&sorted, m));
+    k_node_keys<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, nullptr, t->pb, k, v);
+    count_launches(1);
+    WN_TRY(sort_pairs(k, v, m, key_bits(n), sorted, s));
+    list = sorted;
+  }
+  uint32_t *flag = nullptr, *pos = nullptr;
+  WN_TRY(tmp.alloc(&flag, m + 1));
+  WN_TRY(tmp.alloc(&pos, m + 1));
+  const unsigned g = (unsigned)((m + 255) / 256);
+  int64_t cnt[4] = {0, 0, 0, 0};
+  for (int cls = 1; cls <= 3; ++cls) {
+    k_class_flag<<<g, 256, 0, s>>>(m, list, t->pb, t->pe, cls, flag);
+    WN_TRY(scan_excl(flag, pos, m, pos + m, s));
+    uint32_t c = 0;
+    WN_CUDA(cudaMemcpyAsync(&c, pos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaStreamSynchronize(s));
+    cnt[cls] = c;
+    int4* desc = nullptr;
+    int32_t* ids = nullptr;
+    if (cls == 1) {
+      WN_TRY(dalloc(&P.small, std::max<int64_t>(c, 1), s));
+      desc = P.small;
+    } else if (cls == 2) {
+      WN_TRY(dalloc(&P.large, std::max<int64_t>(c, 1), s));
+      desc = P.large;
+    } else {
+      WN_TRY(dalloc(&P.cross, std::max<int64_t>(c, 1), s));
+      ids = P.cross;
+    }
+    k_class_put<<<g, 256, 0, s>>>(m, list, flag, pos, t->pb, t->pe, t->topo, t->smask, t->tdepth, desc, ids);
+    count_launches(5);
+  }
+  P.nsmall = cnt[1];
+  P.nlarge = cnt[2];
+  P.ncross = cnt[3];
+  WN_TRY(dalloc(&P.onept, n, s));
+  WN_CUDA(cudaMemsetAsync(P.onept, 0xff, n * sizeof(int2), s));
+  k_onept<<<g, 256, 0, s>>>(m, list, t->pb, t->pe, t->topo, P.onept);
+  WN_TRY(dalloc(&P.tile_soff, ntiles + 1, s));
+  WN_TRY(dalloc(&P.tile_loff, ntiles + 1, s));
+  WN_TRY(dalloc(&P.tile_eoff, ntiles + 1, s));
+  const unsigned gt = (unsigned)((ntiles + 256) / 256);
+  k_tile_off<<<gt, 256, 0, s>>>(ntiles, P.small, P.nsmall, t->pb, P.tile_soff);
+  k_tile_off<<<gt, 256, 0, s>>>(ntiles, P.large, P.nlarge, t->pb, P.tile_loff);
+  count_launches(3);
+  const int64_t ne = 2 * P.ncross;
+  WN_TRY(dalloc(&P.ep_key, std::max<int64_t>(ne, 1), s));
+  WN_TRY(dalloc(&P.ep_slot, std::max<int64_t>(ne, 1), s));
+  WN_TRY(dalloc(&P.epval, (size_t)kMomNC * std::max<int64_t>(ne, 1), s));
+  if (ne > 0) {
+    uint64_t* k = nullptr;
+    int32_t* v = nullptr;
+    WN_TRY(tmp.alloc(&k, ne));
+    WN_TRY(tmp.alloc(&v, ne));
+    k_ep_keys<<<(unsigned)((P.ncross + 255) / 256), 256, 0, s>>>(P.ncross, P.cross, t->pb, t->pe, k, v);
+    count_launches(1);
+    WN_TRY(sort_pairs(k, v, ne, key_bits(ntiles * (int64_t)(kMomTile + 1)), P.ep_slot, s, P.ep_key));
+  }
+  k_tile_eoff<<<gt, 256, 0, s>>>(ntiles, P.ep_key, ne, P.tile_eoff);
+  count_launches(1);
+  if (!t->mom_ttot) WN_TRY(dalloc(&t->mom_ttot, (size_t)kMomNC * ntiles, s));
+  WN_CUDA(cudaGetLastError());
+  P.ready = true;
+  return WN_OK;
+}
+
 wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree_s* t) {
   t->n = n;
   t->D = D;
@@ -1043,8 +1222,7 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
     tmp.release(vis);
     tmp.release(pos);
     count_launches(5);
-#ifndef WN_EXP_LIVE_BFS
-    if (nlive > 1) {  // in point order: neighbouring threads read neighbouring (often shared) prefix entries
+    if (nlive > 1) {  // in first-point order (the moment builds' tile plan relies on it)
       uint64_t* k = nullptr;
       int32_t* v = nullptr;
       WN_TRY(tmp.alloc(&k, nlive));
@@ -1057,7 +1235,6 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
       tmp.release(k);
       tmp.release(v);
     }
-#endif
   }
   tmp.release(loff);
   tmp.release(cnt);
@@ -1079,8 +1256,8 @@ wn_status build_tree(const float* pts, int64_t n, int D, cudaStream_t s, wn_tree
 
 void free_tree(wn_tree_s* t) {
   void* ptrs[] = {t->pts, t->perm, t->keys, t->qorder, t->depth, t->pb, t->pe, t->cb, t->cc, t->parent, t->leaf_of,
-                  t->topo, t->smask, t->tdepth, t->mom_live, t->mom_loff, t->mom_pre, t->mom_tile, t->centroid, t->sums, t->set[0].rec, t->set[1].rec, t->set[0].ext,
-                  t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.dcounts, t->it.alpha, t->it.tmp,
+                  t->topo, t->smask, t->tdepth, t->mom_live, t->mom_loff, t->mom_ttot, t->centroid, t->sums, t->set[0].rec, t->set[1].rec, t->set[0].ext,
+                  t->it.mu, t->it.mup, t->it.r, t->it.s, t->it.part, t->it.dstats, t->it.dcounts, t->it.dstamp, t->it.alpha, t->it.tmp,
                   t->qbuf, t->qbuf_order, t->tvb, t->tu};
   // the last call's work (on whatever stream it was queued) must finish before the memory returns to
   // the pool; then stream-ordered frees, no device-wide synchronization
@@ -1098,8 +1275,11 @@ void free_tree(wn_tree_s* t) {
   }
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, 0);
-  for (cudaEvent_t e : t->it.ev) cudaEventDestroy(e);
-  t->it.ev.clear();
+  for (MomPlan& P : t->mplan)
+    for (void* p : {(void*)P.small, (void*)P.large, (void*)P.tile_soff, (void*)P.tile_loff, (void*)P.onept,
+                    (void*)P.cross, (void*)P.ep_key, (void*)P.ep_slot, (void*)P.tile_eoff, (void*)P.epval})
+      if (p) cudaFreeAsync(p, 0);
+
 }
 
 }  // namespace wn

@@ -59,10 +59,36 @@ struct IterScratch {
   double* dstats = nullptr;  // per-iteration (E, α, rr, qq, w) — device
   int64_t* dcounts = nullptr;  // (iters + 1) × 12 snapshots of the work counters (counting runs only)
   int64_t stats_cap = 0;
-  std::vector<cudaEvent_t> ev;  // iters + 1 timing events: iteration i runs between ev[i] and ev[i + 1]
+  unsigned long long* dstamp = nullptr;  // iters + 1 device timestamps (ns): iteration i runs between [i] and [i + 1]
   double* alpha = nullptr;   // current α (device)
   float* tmp = nullptr;      // generic N×4 scratch
   int nblk = 0;
+};
+// Tile plan of the per-iteration moment builds (moments.cu): the sorted points are cut into tiles of
+// kMomTile; a node whose points lie in one tile is summed from that tile's per-point terms in shared memory
+// (one thread per node below kMomWarpNode points, one warp above), a node across tiles from the partial
+// sums at its two ends (the "endpoints") and the totals of the tiles in between.
+#ifndef WN_EXP_MOMTILE
+#define WN_EXP_MOMTILE 1024
+#endif
+constexpr int kMomTile = WN_EXP_MOMTILE;
+constexpr int kMomWarpNode = 32;  // nodes with this many points or more are summed by a warp
+constexpr int kMomNC = 13;        // sums per node of the widest layout (vector attribute, first order)
+struct MomPlan {
+  bool ready = false;
+  int64_t nsmall = 0, nlarge = 0, ncross = 0;
+  // one-tile nodes with ≥ 2 points, ascending first point (hence grouped by tile), as descriptors
+  // {node, pb − tile start | (pe − tile start) << 16, topo, smask | tdepth << 16}; small: < kMomWarpNode points
+  int4* small = nullptr;
+  int4* large = nullptr;
+  int32_t* tile_soff = nullptr;  // ntiles + 1: tile k's small nodes are small[tile_soff[k], tile_soff[k + 1])
+  int32_t* tile_loff = nullptr;  // likewise for the large ones
+  int2* onept = nullptr;         // per sorted point: {its one-point node, topo} if that node is built, else {−1, ·}
+  int32_t* cross = nullptr;      // nodes over more than one tile
+  uint64_t* ep_key = nullptr;    // 2·ncross, ascending: tile·(kMomTile + 1) + local index
+  int32_t* ep_slot = nullptr;    // its slot: 2c ↔ Σ from pb to its tile's end, 2c + 1 ↔ Σ from pe's tile start to pe
+  int32_t* tile_eoff = nullptr;  // ntiles + 1 offsets into ep_key
+  double* epval = nullptr;       // 2·ncross × kMomNC endpoint sums
 };
 // Query shards of a multi-GPU solve: schedule positions [b[r], b[r+1]) for rank r, multiples of
 // WN_SHARD_ALIGN, split by estimated work (capi.cu:plan_shards); world = 0 ⇒ equal counts (wn_shard_range)
@@ -101,8 +127,8 @@ struct wn_tree_s {
   double* sums = nullptr;       // Nn × 8 fp64 node sums of the running build
   int mom_cut = 0;              // moment builds: levels < mom_cut run in one block
   int64_t* mom_loff = nullptr;  //   level offsets on the device
-  double* mom_pre = nullptr;    // (N+1) × 8 fp64 exclusive prefix of the point sums (moments.cu)
-  double* mom_tile = nullptr;   // 2 × tiles × 8 fp64: per-tile totals, per-tile offsets
+  wn::MomPlan mplan[2];          // per-iteration moment builds: [0] the visitable nodes, [1] every node (export)
+  double* mom_ttot = nullptr;    // per-tile totals of the running build (ntiles × kMomNC)
   wn::ShardPlan shard;           // work-weighted query shards for the last world size used
   int64_t mom_ntiles = 0;
   bool mom_order1_ready = false;  // prefix scratch + set[0].ext sized for the first-order far field
@@ -185,6 +211,8 @@ struct MomentArgs {
 };
 wn_status build_moments(wn_tree_s* t, const MomentArgs& m, cudaStream_t s);
 wn_status plan_moments(wn_tree_s* t, cudaStream_t s);  // once per tree, after the topology
+// tile plan over the visitable nodes (which = 0) or every node (1; wn_moments export) — tree_build.cu
+wn_status plan_moment_tiles(wn_tree_s* t, int which, cudaStream_t s);
 wn_status enable_order1(wn_tree_s* t, cudaStream_t s);  // first wn_tree_set_far_order(t, 1)
 
 // ---- traversal (traverse.cu) ----
