@@ -63,9 +63,13 @@ enum {
   WN_FLAG_GRAPH = 1,      /* wnnc_params.flags: capture the iteration loop in a CUDA graph */
   WN_FLAG_COMM_NCCL = 2,  /* multi-GPU: exchange with NCCL broadcasts instead of the default peer-memory
                              stores fused into the traversal epilogues (see wnnc_iterate) */
-  WN_FLAG_MU_ZERO = 4     /* the caller's mu is all zeros (the paper's initialization) and
+  WN_FLAG_MU_ZERO = 4,    /* the caller's mu is all zeros (the paper's initialization) and
                              first_iter = 1: iteration 1 takes A(0) = 0, i.e. s = ½ exactly, without a
                              moment build and traversal (bit-identical to computing it) */
+  WN_FLAG_HOST_WAIT = 8   /* peer-memory exchange: after each exchanging traversal the HOST waits for every
+                             rank's signal (stream synchronize + polling), instead of a device-side wait
+                             kernel — no kernel ever waits on another process, so ranks may share a GPU
+                             (the multi-process tests); not with WN_FLAG_GRAPH (WN_ERR_ARG) */
 };
 
 typedef struct {
@@ -205,6 +209,15 @@ wn_status wn_comm_unique_id(uint8_t id[128] /*host*/);
 /* Collective over `world` processes, one GPU each (the current device of the calling thread). */
 wn_status wn_comm_init(int32_t rank, int32_t world, const uint8_t id[128] /*host*/, wn_comm* out /*host*/);
 wn_status wn_comm_destroy(wn_comm c);
+/* Communicator without NCCL (bootstrap over the caller's own channel, e.g. torch.distributed gloo): the
+   peer-memory arena is set up by wn_comm_arena_export on every rank (allocates this rank's block for n
+   points, writes its 64-byte CUDA IPC handle to `handle`, host) and wn_comm_arena_import with all ranks'
+   handles in rank order (world × 64 bytes, host; opens the peers' blocks).  Work-weighted shards are then
+   computed by every rank alone (identical: the plan is deterministic).  The NCCL exchange
+   (WN_FLAG_COMM_NCCL) is unavailable on such a communicator (WN_ERR_ARG). */
+wn_status wn_comm_init_local(int32_t rank, int32_t world, wn_comm* out /*host*/);
+wn_status wn_comm_arena_export(wn_comm c, int64_t n, uint8_t handle[64] /*host*/, void* stream);
+wn_status wn_comm_arena_import(wn_comm c, const uint8_t* handles /*host, world × 64*/);
 /* (host) Query shard of `rank`: sorted-point range [*begin, *end) of n points split over `world`
    ranks in contiguous Morton ranges aligned to WN_SHARD_ALIGN queries (so per-block reduction
    partials are identical for every world size).  Pure host arithmetic. */

@@ -228,6 +228,7 @@ static wn_status plan_shards(wn_tree_s* t, int world, wn_comm comm, cudaStream_t
   IterScratch& it = t->it;
   const int64_t n = t->n, nb = (n + WN_SHARD_ALIGN - 1) / WN_SHARD_ALIGN;
   int64_t q0 = 0, q1 = n;
+  if (comm && !comm_has_nccl(comm)) comm = nullptr;  // a local communicator: every rank counts all blocks
   if (comm) wn_shard_range(n, comm_rank(comm), world, &q0, &q1);
   int64_t* bw = nullptr;
   WN_CUDA(cudaMallocAsync((void**)&bw, nb * sizeof(int64_t), s));
@@ -460,7 +461,10 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
                  out == R ? A.r : (out == MU0 || out == MU1) ? A.mu[out == MU1] : nullptr, slot);
       WN_TRY(traverse(tv, s));
     }
-    for (int v = 0; v < nviews; ++v) comm_peer_wait(*views[v], s);
+    for (int v = 0; v < nviews; ++v) {
+      if (p.flags & WN_FLAG_HOST_WAIT) WN_TRY(comm_peer_wait_host(*views[v], s));
+      else comm_peer_wait(*views[v], s);
+    }
     return WN_OK;
   };
   stamp(t, p, 0, s);
@@ -911,6 +915,10 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p_in, wn_comm co
   const wnnc_params* p = &pl;
   if (comm && p->adjoint_mode == WN_ADJ_TRANSPOSE)
     return set_error(WN_ERR_ARG, "transpose-mode adjoint is single-GPU only in this build");
+  if ((p->flags & WN_FLAG_HOST_WAIT) && (p->flags & WN_FLAG_GRAPH))
+    return set_error(WN_ERR_ARG, "WN_FLAG_HOST_WAIT waits on the host: it cannot be captured in a CUDA graph");
+  if (comm && !comm_has_nccl(comm) && (p->flags & WN_FLAG_COMM_NCCL))
+    return set_error(WN_ERR_ARG, "a local communicator has no NCCL exchange");
   if (t->far_order != 0 && p->adjoint_mode == WN_ADJ_TRANSPOSE)
     return set_error(WN_ERR_ARG, "transpose-mode adjoint is defined for the order-0 far field only");
   cudaStream_t s = (cudaStream_t)stream;

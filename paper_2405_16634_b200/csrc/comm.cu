@@ -11,7 +11,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <string>
 
@@ -253,6 +255,8 @@ wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena*
     *out = &A;
     return WN_OK;
   }
+  if (!c->comm)  // a local communicator's arena comes from wn_comm_arena_export / _import
+    return set_error(WN_ERR_ARG, "local communicator: call wn_comm_arena_export/_import for this N first");
   // (re)build, collectively: every rank reaches this point in the same wnnc_iterate call
   arena_release(A);
   const ArenaLayout L(n);
@@ -334,6 +338,26 @@ void comm_peer_wait(const PeerArena& A, cudaStream_t s) {
   count_launches(1);
 }
 
+wn_status comm_peer_wait_host(const PeerArena& A, cudaStream_t s) {
+  WN_CUDA(cudaStreamSynchronize(s));  // this rank's signals and stores are issued and done
+  unsigned long long cur = 0;         // the wait target lives on the device (device-side waits advance it too)
+  WN_CUDA(cudaMemcpy(&cur, A.expected, sizeof(cur), cudaMemcpyDeviceToHost));
+  const unsigned long long target = cur + (unsigned long long)A.world;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    unsigned long long v = 0;
+    WN_CUDA(cudaMemcpy(&v, A.sig[A.rank], sizeof(v), cudaMemcpyDeviceToHost));
+    if (v >= target) break;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+      return set_error(WN_ERR_CUDA, "peer-memory exchange: a rank did not signal within 120 s");
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  WN_CUDA(cudaMemcpy(A.expected, &target, sizeof(target), cudaMemcpyHostToDevice));
+  return WN_OK;
+}
+
+bool comm_has_nccl(wn_comm c) { return c && c->comm; }
+
 }  // namespace wn
 
 using namespace wn;
@@ -369,6 +393,70 @@ wn_status wn_comm_init(int32_t rank, int32_t world, const uint8_t id[128], wn_co
     return st;
   }
   *out = c;
+  return WN_OK;
+}
+
+wn_status wn_comm_init_local(int32_t rank, int32_t world, wn_comm* out) {
+  if (!out || world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return set_error(WN_ERR_ARG, "bad local comm arguments (world 1..8)");
+  wn_comm_s* c = new (std::nothrow) wn_comm_s();
+  if (!c) return set_error(WN_ERR_OOM, "host allocation failed");
+  c->rank = rank;
+  c->world = world;
+  *out = c;
+  return WN_OK;
+}
+
+wn_status wn_comm_arena_export(wn_comm c, int64_t n, uint8_t handle[64], void* stream) {
+  if (!c || !handle || n < 1) return set_error(WN_ERR_ARG, "bad arena export arguments");
+  if (c->comm) return set_error(WN_ERR_ARG, "NCCL communicators set their arena up collectively");
+  arena_release(c->arena);
+  const ArenaLayout L(n);
+  WN_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  void* own = nullptr;
+  WN_CUDA(cudaMalloc(&own, L.bytes));
+  cudaError_t e = cudaMemset(own, 0, L.bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, own);
+  if (e != cudaSuccess) {
+    cudaFree(own);
+    return cuda_status(e, "wn_comm_arena_export");
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  std::copy(reinterpret_cast<const uint8_t*>(&h), reinterpret_cast<const uint8_t*>(&h) + 64, handle);
+  c->arena.own = own;
+  c->arena.cap = 0;  // not usable before the import
+  c->arena.pending_n = n;
+  return WN_OK;
+}
+
+wn_status wn_comm_arena_import(wn_comm c, const uint8_t* handles) {
+  if (!c || !handles || !c->arena.own || c->arena.pending_n < 1)
+    return set_error(WN_ERR_ARG, "wn_comm_arena_import: export this rank's arena first");
+  PeerArena& A = c->arena;
+  void* blocks[kMaxPeers] = {};
+  bool opened[kMaxPeers] = {};
+  cudaError_t e = cudaSuccess;
+  for (int r = 0; r < c->world && e == cudaSuccess; ++r) {
+    if (r == c->rank) {
+      blocks[r] = A.own;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::copy(handles + 64 * r, handles + 64 * (r + 1), reinterpret_cast<uint8_t*>(&h));
+    e = cudaIpcOpenMemHandle(&blocks[r], h, cudaIpcMemLazyEnablePeerAccess);
+    opened[r] = e == cudaSuccess;
+  }
+  if (e != cudaSuccess) {
+    for (int r = 0; r < c->world; ++r)
+      if (opened[r]) cudaIpcCloseMemHandle(blocks[r]);
+    return cuda_status(e, "cudaIpcOpenMemHandle (wn_comm_arena_import)");
+  }
+  void* own = A.own;
+  const int64_t n = A.pending_n;
+  arena_bind(A, blocks, c->world, c->rank, n);
+  A.own = own;
+  for (int r = 0; r < c->world; ++r) A.opened[r] = opened[r];
   return WN_OK;
 }
 

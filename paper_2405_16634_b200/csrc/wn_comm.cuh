@@ -25,6 +25,9 @@ int comm_world(wn_comm c);
 // and the per-exchange device-side wait for every rank's signal.
 wn_status comm_peer_arena(wn_comm c, int64_t n, cudaStream_t s, const PeerArena** out);
 void comm_peer_wait(const PeerArena& A, cudaStream_t s);
+// the same wait on the host: synchronize s, then poll this rank's signal word (WN_FLAG_HOST_WAIT)
+wn_status comm_peer_wait_host(const PeerArena& A, cudaStream_t s);
+bool comm_has_nccl(wn_comm c);  // false for wn_comm_init_local communicators
 // W emulated ranks in one process (diagnostic): plain blocks[W] bound as each other's replicas
 wn_status emulated_arenas(int world, int64_t n, PeerArena* arenas, void** blocks);
 }  // namespace wn

@@ -282,6 +282,7 @@ struct PeerArena {
   double* part[kMaxPeers] = {};        // Σ partials [3][blocks]
   unsigned long long* sig[kMaxPeers] = {};  // signal words (remote atomic adds)
   unsigned long long* expected = nullptr;   // local: next wait target (advanced by the wait kernel)
+  int64_t pending_n = 0;                    // local communicators: exported for this N, not yet imported
   unsigned int* done = nullptr;             // local: finished blocks of the running traversal
 };
 

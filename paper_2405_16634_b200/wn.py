@@ -22,6 +22,7 @@ WN_ADJ_GATHER, WN_ADJ_TRANSPOSE = 0, 1
 WN_FLAG_GRAPH = 1
 WN_FLAG_COMM_NCCL = 2
 WN_FLAG_MU_ZERO = 4
+WN_FLAG_HOST_WAIT = 8
 PROF_CLASSES = ("trav_A", "trav_AT", "trav_G", "moments", "tree", "other")
 STATUS_NAMES = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_EMPTY", 3: "WN_ERR_NONFINITE", 4: "WN_ERR_DEGENERATE",
                 5: "WN_ERR_CUDA", 6: "WN_ERR_OOM", 7: "WN_ERR_NCCL"}
@@ -30,7 +31,7 @@ EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", 
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
             "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work",
             "wn_tree_set_far_order", "wnnc_iterate_emulated", "wn_shard_plan", "wn_tree_schedule",
-            "wn_tree_schedule_stats")
+            "wn_tree_schedule_stats", "wn_comm_init_local", "wn_comm_arena_export", "wn_comm_arena_import")
 
 
 class wnnc_params(C.Structure):
@@ -64,6 +65,9 @@ _sig = {
     "wn_shard_plan": ([P, I32, P, P], I32),
     "wn_tree_schedule": ([P, P, P], I32),
     "wn_tree_schedule_stats": ([P, P, P], I32),
+    "wn_comm_init_local": ([I32, I32, P], I32),
+    "wn_comm_arena_export": ([P, I64, P, P], I32),
+    "wn_comm_arena_import": ([P, P], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -339,6 +343,26 @@ def wn_comm_init(rank: int, world: int, uid: bytes) -> Comm:
     h = C.c_void_p()
     _check(_L.wn_comm_init(int(rank), int(world), buf, C.byref(h)))
     return Comm(h, rank, world)
+
+
+def wn_comm_init_local(rank: int, world: int) -> Comm:
+    """Communicator without NCCL: the caller exchanges the arena handles (wn_comm_arena_export/_import)."""
+    h = C.c_void_p()
+    _check(_L.wn_comm_init_local(int(rank), int(world), C.byref(h)))
+    return Comm(h, rank, world)
+
+
+def wn_comm_arena_export(comm: Comm, n: int) -> bytes:
+    buf = (C.c_uint8 * 64)()
+    _check(_L.wn_comm_arena_export(comm.handle, int(n), buf, _stream()))
+    return bytes(buf)
+
+
+def wn_comm_arena_import(comm: Comm, handles):
+    """handles: every rank's 64-byte handle, in rank order."""
+    blob = b"".join(handles)
+    buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+    _check(_L.wn_comm_arena_import(comm.handle, buf))
 
 
 def wn_comm_destroy(comm: Comm):
