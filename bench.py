@@ -366,10 +366,106 @@ def run_ours(args):
     return 0
 
 
+def run_grid(args):
+    """Row f1: the winding-number field F(q) = Σ_j ∇Φ_w(q − x_j)·μ_j (the WNF
+    reconstruction of §6.1.4) at the R³ points of a grid around the cloud, with μ the solved
+    WNNC normals (one untimed 40-iteration solve).  A step = one wn_eval over the whole grid (queries
+    resident in HBM; normalization, Hilbert query schedule, moment build, traversal)."""
+    import torch
+
+    world, rank, local = _dist()
+    if world > 1 and rank != 0:
+        return 0  # (grid evaluation is a one-GPU line)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2405_16634_b200.wn as wn
+
+    cfg = synth.config(args.config)
+    pts_h = cfg["points"]
+    n = len(pts_h)
+    pts = torch.from_numpy(pts_h).to(dev)
+    tree = wn.wn_build_tree(pts)
+    mu = torch.zeros(n, 3, device=dev)
+    wn.wnnc_iterate(tree, mu, iters=ITERS, theta=args.theta, flags=wn.WN_FLAG_GRAPH | wn.WN_FLAG_MU_ZERO)
+    R = args.grid
+    lo, hi = pts_h.min(0), pts_h.max(0)
+    c, h = (lo + hi) / 2, (hi - lo) / 2 * 1.1
+    axes = [torch.linspace(float(c[k] - h[k]), float(c[k] + h[k]), R, device=dev) for k in range(3)]
+    q = torch.stack(torch.meshgrid(*axes, indexing="ij"), -1).reshape(-1, 3).contiguous()
+    m = q.shape[0]
+    w = float(np.float32(0.002))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        F = wn.wn_eval(tree, mu, w, args.theta, q=q)
+    torch.cuda.synchronize()
+    # algorithmic work (counting variant, same decisions; untimed)
+    wn.wn_work_count_enable(True)
+    wn.wn_eval(tree, mu, w, args.theta, q=q)
+    work = wn.wn_work_count_read()["A"]
+    wn.wn_work_count_enable(False)
+    wn.wn_prof_enable(True)
+    wn.wn_eval(tree, mu, w, args.theta, q=q)
+    prof = wn.wn_prof_read()
+    wn.wn_prof_enable(False)
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    l0 = wn.wn_launch_count()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            F = wn.wn_eval(tree, mu, w, args.theta, q=q)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = wn.wn_launch_count() - l0
+    ms = float(sum(a.elapsed_time(b) for a, b in ev)) / args.steps
+    inside = float((F > 0.5).float().mean().item())
+    # end to end: host grid in (pinned), F back to the host, through the same public call
+    q_pin, F_pin = q.cpu().pin_memory(), torch.empty(m, dtype=torch.float32).pin_memory()
+    q_dev = torch.empty_like(q)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        q_dev.copy_(q_pin, non_blocking=True)
+        F_pin.copy_(wn.wn_eval(tree, mu, w, args.theta, q=q_dev), non_blocking=True)
+    torch.cuda.synchronize()
+    te = (time.perf_counter() - t0) / args.steps
+    trav_ms = prof["trav_A"][0]
+    flops = FLOPS_TEST * work["tests"] + FLOPS_TERM["A"] * work["live"]
+    props = torch.cuda.get_device_properties(dev)
+    fmax = 1965.0
+    try:
+        fmax = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", fmax))
+    except OSError:
+        pass
+    peak = props.multi_processor_count * 128 * 2 * fmax * 1e6 / 1e12
+    achieved = flops / (trav_ms / 1e3) / 1e12
+    line = {"metric": "off-surface winding-number field F(q) queries/s", "value": m / (ms / 1e3),
+            "unit": "queries/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"F on a {R}^3 grid (1.1 x bbox) around {CONFIG_TEXT[args.config]}; "
+                                   f"mu = the solved WNNC normals; w = 0.002, theta = {args.theta}",
+                       "n_points": n, "queries": m, "query_schedule": "hilbert (per call)",
+                       "l2": "flushed between steps (256 MiB write outside the per-step events)",
+                       "step": "wn_eval: normalize + Hilbert schedule of the queries + moment build + traversal",
+                       "inside_fraction": inside},
+            "breakdown_ms_per_step": {k: v[0] for k, v in prof.items() if v[1]},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": f"treecode traversal trav_kernel<A> over {m} queries, {trav_ms:.3f} ms",
+                         "work": work},
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+            "e2e": {"value": m / te, "unit": "queries/s", "h2d_bytes_per_step": int(m * 12),
+                    "d2h_bytes_per_step": int(m * 4), "ms_per_step": 1e3 * te}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default 5; 64 with --grid)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--theta", type=float, default=2.0)
@@ -383,9 +479,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prof-steps", type=int, default=2, help="untimed steps with per-kernel CUDA events")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels one by one (no CUDA graph)")
+    ap.add_argument("--grid", type=int, default=0,
+                    help="row f1: time F(q) on a GRID^3 grid around the cloud (queries/s) instead of the solve")
     args = ap.parse_args()
+    if args.steps is None:  # a grid step takes ~8 ms: enough of them to span the clock sampler's 100 ms period
+        args.steps = 64 if args.grid else 5
     if args.impl == "reference":
         return run_reference(args)
+    if args.grid:
+        return run_grid(args)
     return run_ours(args)
 
 
