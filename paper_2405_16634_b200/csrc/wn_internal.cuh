@@ -72,7 +72,10 @@ struct IterScratch {
 #define WN_EXP_MOMTILE 1024
 #endif
 constexpr int kMomTile = WN_EXP_MOMTILE;
-constexpr int kMomWarpNode = 32;  // nodes with this many points or more are summed by a warp
+#ifndef WN_EXP_MOMWARP
+#define WN_EXP_MOMWARP 32
+#endif
+constexpr int kMomWarpNode = WN_EXP_MOMWARP;  // nodes with this many points or more are summed by a warp
 constexpr int kMomNC = 13;        // sums per node of the widest layout (vector attribute, first order)
 struct MomPlan {
   bool ready = false;

@@ -11,6 +11,8 @@ VARIANTS = {
     "lb5": ["WN_EXP_LBMIN=5"],  # resident 256-thread-equivalents per SM of the one-warp traversal
     "mt512": ["WN_EXP_MOMTILE=512"],  # moment-build tiles of 512 / 2048 points (default 1024)
     "mt2048": ["WN_EXP_MOMTILE=2048"],
+    "mw64": ["WN_EXP_MOMWARP=64"],  # moment build: nodes of >= 64 / 128 points summed by a warp (default 32)
+    "mw128": ["WN_EXP_MOMWARP=128"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
