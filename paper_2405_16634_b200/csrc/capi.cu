@@ -113,7 +113,7 @@ static wn_status ensure_scratch(wn_tree_s* t, cudaStream_t s) {
   if (it.mu) return WN_OK;
   const int64_t n = t->n;
   it.n = n;
-  it.nblk = trav_blocks(n);
+  it.nblk = (int)part_slots(n);
   WN_CUDA(cudaMallocAsync((void**)&it.mu, n * sizeof(float4), s));
   WN_CUDA(cudaMallocAsync((void**)&it.mup, n * sizeof(float4), s));
   WN_CUDA(cudaMallocAsync((void**)&it.r, n * sizeof(float4), s));
@@ -546,7 +546,7 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
     if (nccl) WN_TRY(comm_allgather_partials(comm, part, stride, t->n, &t->shard, s));
     // α = Σr² / Σ(Ar)²  (Alg. 2), fixed-order reduction of the partials
     // (the partial arrays' stride may exceed this cloud's block count: a peer arena sized for a larger N)
-    alpha_step(part, trav_blocks(t->n), stride, (double)w, it.alpha, it.dstats + 5 * i, s);
+    alpha_step(part, (int)part_slots(t->n), stride, (double)w, it.alpha, it.dstats + 5 * i, s);
     // (4) μ' = μ + α r (fused into the moment build), μ̂ = G_w(μ'), μ = μ̂ |μ'|/|μ̂|
     MomentArgs m4;
     m4.kind = ATTR_VEC;
@@ -839,7 +839,7 @@ wn_status wn_eval_adjoint(wn_tree t, const float* sv, float width, float theta, 
     ta.out_map = t->perm;
     ta.out_v3 = out;
     ta.scale_out = (float)sc2;
-    return traverse(ta, s);
+      return traverse(ta, s);
   }
   gather_vec(t->n, t->perm, mu_geom, 1.0, it.mu, s);
   MomentArgs m;

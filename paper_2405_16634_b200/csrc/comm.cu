@@ -145,7 +145,7 @@ wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64
     for (int k = 0; k < c->world && r == ncclSuccess; ++k) {
       int64_t b = 0, e = 0;
       shard_of(plan, n, k, c->world, &b, &e);
-      const int64_t b0 = b / kTravBlock, b1 = (e + kTravBlock - 1) / kTravBlock;  // partials per traversal block
+      const int64_t b0 = b / kPartQ, b1 = (e + kPartQ - 1) / kPartQ;  // partials per 32-query group
       if (b1 > b0) {
         double* p = part + a * stride + b0;
         r = N.Broadcast(p, p, (size_t)(b1 - b0), ncclFloat64, k, c->comm, s);
@@ -215,7 +215,7 @@ struct ArenaLayout {
   size_t o_s, o_r, o_mu0, o_mu1, o_part, o_sig, bytes;
   int64_t nb;
   explicit ArenaLayout(int64_t n) {
-    nb = trav_blocks(n);
+    nb = part_slots(n);
     o_s = 0;
     o_r = align256(o_s + n * sizeof(float));
     o_mu0 = align256(o_r + n * sizeof(float4));

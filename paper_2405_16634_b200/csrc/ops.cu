@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kAlphaThreads) k_alpha(const double* __restric
   }
 }
 
-// s = ½ − A(0) = ½ for every query and the block partials Σ s² = 0.25 · (queries in the block) — exactly the
+// s = ½ − A(0) = ½ for every query and the group partials Σ s² = 0.25 · (queries in the group) — exactly the
 // values the A traversal's EPI_S epilogue produces for μ = 0 (every term 0), without the traversal
 __global__ void k_s_half(int64_t n, float* __restrict__ s, double* __restrict__ part, int block) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -138,7 +138,7 @@ void alpha_step(const double* part, int nblk, int64_t stride, double w, double* 
   k_alpha<<<1, kAlphaThreads, 0, s>>>(part, nblk, stride, w, alpha, stats);
 }
 void s_half(int64_t n, float* s_out, double* part, cudaStream_t s) {
-  k_s_half<<<g256(n), 256, 0, s>>>(n, s_out, part, kTravBlock);
+  k_s_half<<<g256(n), 256, 0, s>>>(n, s_out, part, kPartQ);
   count_launches(1);
 }
 void unit_normals(int64_t n, const float* mu, float* out, cudaStream_t s) {

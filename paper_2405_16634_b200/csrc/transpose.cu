@@ -158,7 +158,6 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
 __global__ void pushdown_kernel(int64_t n, const int32_t* __restrict__ leaf_of, const int32_t* __restrict__ parent,
                                 const double* __restrict__ VB, const double* __restrict__ U, float scale,
                                 float4* __restrict__ r, double* __restrict__ partial) {
-  __shared__ double red[kTravBlock / 32];
   const int64_t j = (int64_t)blockIdx.x * kTravBlock + threadIdx.x;
   double part = 0.0;
   if (j < n) {
@@ -172,16 +171,10 @@ __global__ void pushdown_kernel(int64_t n, const int32_t* __restrict__ leaf_of, 
     r[j] = make_float4(fx, fy, fz, 0.f);
     part = (double)fx * fx + (double)fy * fy + (double)fz * fz;
   }
-  if (partial) {
+  if (partial) {  // one slot per 32 points (kPartQ), as the traversal epilogues
 #pragma unroll
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = 0.0;
-      for (int k = 0; k < kTravBlock / 32; ++k) b += red[k];
-      partial[blockIdx.x] = b;
-    }
+    if ((threadIdx.x & 31) == 0 && j - (threadIdx.x & 31) < n) partial[j >> 5] = part;
   }
 }
 

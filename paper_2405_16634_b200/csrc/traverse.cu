@@ -226,11 +226,11 @@ __device__ __forceinline__ void trav_loop(const TravArgs& a, int2* stk, int sp, 
   }
 }
 
-// outputs of one query (fused solver epilogues), its work counts, and the block's Σ partial (NW warps)
-template <int OP, int EPI, bool COUNT, int NW>
+// outputs of one query (fused solver epilogues), its work counts, and its warp group's Σ partial (slot ib)
+template <int OP, int EPI, bool COUNT>
 __device__ __forceinline__ void trav_epilogue(const TravArgs& a, bool valid, int64_t q, const Acc<OP>& acc,
-                                              const Work& wk, double* red, int64_t ib) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                              const Work& wk, bool has_group, int64_t ib) {
+  const int lane = threadIdx.x & 31;
   double part = 0.0;
   if (valid) {
     const int64_t oq = a.out_map ? (int64_t)a.out_map[q] : q;
@@ -299,18 +299,14 @@ __device__ __forceinline__ void trav_epilogue(const TravArgs& a, bool valid, int
       }
     }
   }
-  if (EPI == EPI_S || EPI == EPI_SQ || EPI == EPI_R) {
+  if (EPI == EPI_S || EPI == EPI_SQ || EPI == EPI_R) {  // this warp's group slot ib (schedule position / 32)
     part = warp_sum(part);
-    if (lane == 0) red[warp] = part;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = 0.0;
-      for (int k = 0; k < NW; ++k) b += red[k];
-      WN_DCHECK(ib < (a.npts + kTravBlock - 1) / kTravBlock || a.queries != a.pts, "partial slot");
+    if (lane == 0 && has_group) {
+      WN_DCHECK(ib < part_slots(a.npts) || a.queries != a.pts, "partial slot");
       if (a.world) {
-        for (int r = 0; r < a.world; ++r) a.peer_part[r][ib] = b;
+        for (int r = 0; r < a.world; ++r) a.peer_part[r][ib] = part;
       } else {
-        a.partial[ib] = b;
+        a.partial[ib] = part;
       }
     }
   }
@@ -328,18 +324,11 @@ __device__ __forceinline__ void trav_epilogue(const TravArgs& a, bool valid, int
   }
 }
 
-// one warp = 32 consecutive queries of the schedule, traversing from the root (the hot kernel: its
-// loop is written out here — the same steps as trav_visit / trav_loop, which the compiler schedules worse)
+// one warp = 32 consecutive queries of the schedule (positions kq of the lanes), traversing from the root (the
+// hot loop: written out here — the same steps as trav_visit / trav_loop, which the compiler schedules worse)
 template <int OP, int EPI, bool COUNT, bool FROZEN, int ORD>
-#ifndef WN_EXP_LBMIN
-#define WN_EXP_LBMIN 6  // 6 resident blocks (48 warps) per SM: ≤ 42 registers, no spills; measured best
-#endif
-__global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 256 / kTravBlock) trav_kernel(const TravArgs a) {
-  extern __shared__ int2 stk_all[];
-  __shared__ double red[kTravBlock / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int2* stk = stk_all + warp * a.stack_depth;
-  const int64_t kq = a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;  // schedule position
+__device__ __forceinline__ void trav_group(const TravArgs& a, int2* stk, const int64_t kq) {
+  const int lane = threadIdx.x & 31;
   const bool valid = kq < a.q_end;
   const int64_t q = (valid && a.qorder) ? (int64_t)a.qorder[kq] : kq;             // query index
   WN_DCHECK(!valid || (q >= 0 && (a.npts == 0 || a.queries != a.pts || q < a.npts)), "query index");
@@ -442,7 +431,17 @@ __global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 25
   wk.far = nfar;
   wk.near = nnear;
   wk.live = nlive;
-  trav_epilogue<OP, EPI, COUNT, kTravBlock / 32>(a, valid, q, acc, wk, red, (a.q_begin / kTravBlock) + blockIdx.x);
+  trav_epilogue<OP, EPI, COUNT>(a, valid, q, acc, wk, active != 0u, kq >> 5);  // (kq: lane's position; q_begin % 32 = 0)
+}
+
+#ifndef WN_EXP_LBMIN
+#define WN_EXP_LBMIN 6  // 6 resident blocks (48 warps) per SM: ≤ 42 registers, no spills; measured best
+#endif
+template <int OP, int EPI, bool COUNT, bool FROZEN, int ORD>
+__global__ void __launch_bounds__(kTravBlock, (ORD == 1 ? 5 : WN_EXP_LBMIN) * 256 / kTravBlock) trav_kernel(const TravArgs a) {
+  extern __shared__ int2 stk_all[];
+  int2* stk = stk_all + (threadIdx.x >> 5) * a.stack_depth;
+  trav_group<OP, EPI, COUNT, FROZEN, ORD>(a, stk, a.q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x);
 }
 
 // Small clouds (few query warps for the GPU): kSplit warps share each group of 32 queries.  All of them
@@ -455,7 +454,6 @@ __global__ void __launch_bounds__(KS * (kTravBlock / 32) * 32) trav_split_kernel
   constexpr int kSplit = KS, kSplitWarps = KS * (kTravBlock / 32);
   constexpr int NG = kTravBlock / 32;  // query groups per block
   extern __shared__ int2 stk_all[];
-  __shared__ double red[kSplitWarps];
   __shared__ uint32_t sm_open[NG][8];
   __shared__ int sm_topo[NG][8];
   __shared__ float sm_v[kSplitWarps][3][32];
@@ -547,8 +545,7 @@ __global__ void __launch_bounds__(KS * (kTravBlock / 32) * 32) trav_split_kernel
   } else {
     wk = Work();
   }
-  trav_epilogue<OP, EPI, COUNT, kSplitWarps>(a, valid && sub == 0, q, acc, wk, red,
-                                             (a.q_begin / kTravBlock) + blockIdx.x);
+  trav_epilogue<OP, EPI, COUNT>(a, valid && sub == 0, q, acc, wk, sub == 0 && active != 0u, kq >> 5);
 }
 
 template <int OP, int EPI, bool C, bool F, int O>

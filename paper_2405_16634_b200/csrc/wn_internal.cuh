@@ -55,7 +55,7 @@ struct IterScratch {
   float4* mup = nullptr;     // μ' = μ + α r
   float4* r = nullptr;       // r = Aᵀ s
   float* s = nullptr;        // s = ½ − A μ
-  double* part = nullptr;    // per-block partials: [3][nblk] (Σs², Σ|r|², Σq²)
+  double* part = nullptr;    // per-group partials: [3][nblk] (Σs², Σ|r|², Σq²), nblk = part_slots(n)
   double* dstats = nullptr;  // per-iteration (E, α, rr, qq, w) — device
   int64_t* dcounts = nullptr;  // (iters + 1) × 12 snapshots of the work counters (counting runs only)
   int64_t stats_cap = 0;
@@ -247,7 +247,7 @@ struct TravArgs {
   float* out_v3 = nullptr;          // N×3 output (caller layout)
   float scale_out = 1.0f;
   const float4* mup = nullptr;      // EPI_RESCALE: μ'
-  double* partial = nullptr;        // per-block partials (indexed by global block of 256 queries)
+  double* partial = nullptr;        // per-group partials (indexed by schedule position / kPartQ)
   float w2 = 0.0f;
   int stack_depth = 128;
   int root_single = 0;              // 1 iff the root is a one-point leaf (n = 1)
@@ -302,5 +302,10 @@ wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sor
 constexpr int kTravBlock = WN_EXP_TRAVBLOCK;  // queries per block (4 warps: the block tail holds an SM slot for less; 256: +0.8 %)
 static_assert(WN_SHARD_ALIGN % kTravBlock == 0, "rank shards must hold whole traversal blocks (Σ partials)");
 inline int trav_blocks(int64_t nq) { return (int)((nq + kTravBlock - 1) / kTravBlock); }
+// Σ partials (s², |r|², (Ar)²) are kept per 32-query warp group of the query schedule: each warp writes its
+// own slot (no block barrier in the epilogues), and α sums the slots in one fixed order
+constexpr int kPartQ = 32;
+static_assert(WN_SHARD_ALIGN % kPartQ == 0, "rank shards must hold whole partial groups");
+inline int64_t part_slots(int64_t nq) { return (nq + kPartQ - 1) / kPartQ; }
 
 }  // namespace wn
