@@ -65,6 +65,7 @@ def lib():
         L.wo_solve.restype = I32
         L.wo_num_threads.restype = I32
         L.wo_rescale.argtypes = [I64, P, P, P]
+        L.wo_fmm_op.argtypes = [P, I32, P, I32, D, I32, D, I32, P, P]
         _lib = L
     return _lib
 
@@ -183,6 +184,17 @@ class Tree:
         lib().wo_tree_op(self._h, op, _p(nu), dim, None if q is None else _p(q),
                          None if qi is None else _p(qi), m, float(w), float(theta), _p(out),
                          None if cnt is None else _p(cnt))
+        out = out[:, 0] if od == 1 else out
+        return (out, cnt) if counters else out
+
+    def fmm(self, op, nu, w, p=4, theta=0.5, leaf=32, counters=False):
+        """FMM: A (op OP_A, ν n×3) / G (OP_G, ν n×3) / Aᵀ (OP_AT, s n) at the sources."""
+        nu = _f64(nu)
+        dim = 1 if nu.ndim == 1 else 3
+        od = 1 if op == OP_A else 3
+        out = np.empty((self.n, od))
+        cnt = np.zeros(2, np.int64)
+        lib().wo_fmm_op(self._h, op, _p(nu), dim, float(w), int(p), float(theta), int(leaf), _p(out), _p(cnt))
         out = out[:, 0] if od == 1 else out
         return (out, cnt) if counters else out
 

@@ -679,3 +679,332 @@ int wo_num_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Fast multipole method (SURVEY §8 row f4 — the paper's future work, §6.3 and  */
+/* L409; not the paper's method).  The same sums as the dense operators (PAPER.md:L222, L266,  */
+/* L316), written as one potential                                                             */
+/*   V(y) = Σ_j [ q_j Φ(y − x_j) + ν_j·∇Φ(y − x_j) ],   Φ(r) = 1/(4π|r|)                          */
+/* so that A(ν) = V (dipoles ν), G(ν) = −∇V (dipoles ν) and Aᵀ(s) = −∇V (charges q = s).         */
+/* Cells = octree nodes (cube centres c, radius = half-diagonal √3·2^−depth); an FMM leaf is a  */
+/* node with no children or at most `leaf` points.  Cartesian Taylor expansions of total degree */
+/* ≤ p, plain textbook steps:                                                                  */
+/*   P2M  M_β = Σ_j [ q_j (−1)^|β| (x_j−c)^β/β! + Σ_k ν_jk (−1)^(|β|−1) (x_j−c)^(β−e_k)/(β−e_k)! ] */
+/*        (Taylor of Φ(y − x) in x about c:  V(y) = Σ_β M_β ∂^βΦ(y − c))                         */
+/*   M2M  M'_β = Σ_{γ≤β} M_γ (c'−c)^(β−γ)/(β−γ)!                     (child c → parent c')       */
+/*   M2L  L_γ += Σ_β M_β ∂^(β+γ)Φ(c_t − c_s)          (local Taylor coefficients L_γ = ∂^γV(c_t)) */
+/*   L2L  L'_δ = Σ_{γ≥δ} L_γ (c'−c)^(γ−δ)/(γ−δ)!                      (parent c → child c')       */
+/*   L2P  V(y) = Σ_γ L_γ (y−c)^γ/γ!,  ∂_k V(y) = Σ_γ L_γ (y−c)^(γ−e_k)/(γ−e_k)!                   */
+/* ∂^δ(1/|R|) = δ! b_δ from the Taylor-coefficient recurrence (b_0 = 1/|R|)                      */
+/*   |δ| |R|² b_δ = −(2|δ|−1) Σ_i R_i b_(δ−e_i) − (|δ|−1) Σ_i b_(δ−2e_i).                         */
+/* Dual traversal from (root, root): a cell pair is well separated — one M2L — iff              */
+/* |c_t − c_s| > (r_t + r_s)/θ_f and |c_t − c_s| − r_t − r_s > w (every pair beyond the smoothing */
+/* cutoff: the expansion is of the unsmoothed kernel, exact there); else two leaves interact   */
+/* directly (P2P: the definition, cutoff r < w decided in fp32 as in wo_dense_op); else the     */
+/* larger cell (the target on ties) is split.  θ_f → 0 makes every pair direct: the dense sums. */
+/* ------------------------------------------------------------------------------------------ */
+typedef struct {
+  int p, P, np, nP;      /* expansion degree p, derivative degree P = 2p; coefficient counts */
+  int* mi;               /* nP × 3 multi-indices, by total degree, then lexicographic (a, b, c) desc */
+  int* lut;              /* (P+1)^3 → index or −1 */
+  double* fact;          /* fact[k] = k! */
+} fmm_idx;
+
+static int fmm_count(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
+
+static void fmm_idx_init(fmm_idx* I, int p) {
+  I->p = p;
+  I->P = 2 * p;
+  I->np = fmm_count(p);
+  I->nP = fmm_count(I->P);
+  int P1 = I->P + 1;
+  I->mi = (int*)malloc((size_t)I->nP * 3 * sizeof(int));
+  I->lut = (int*)malloc((size_t)P1 * P1 * P1 * sizeof(int));
+  for (int k = 0; k < P1 * P1 * P1; ++k) I->lut[k] = -1;
+  int n = 0;
+  for (int deg = 0; deg <= I->P; ++deg)
+    for (int a = deg; a >= 0; --a)
+      for (int b = deg - a; b >= 0; --b) {
+        int c = deg - a - b;
+        I->mi[3 * n] = a; I->mi[3 * n + 1] = b; I->mi[3 * n + 2] = c;
+        I->lut[(a * P1 + b) * P1 + c] = n++;
+      }
+  I->fact = (double*)malloc((size_t)(I->P + 2) * sizeof(double));
+  I->fact[0] = 1.0;
+  for (int k = 1; k <= I->P + 1; ++k) I->fact[k] = I->fact[k - 1] * k;
+}
+
+static void fmm_idx_free(fmm_idx* I) { free(I->mi); free(I->lut); free(I->fact); }
+
+static int fmm_at(const fmm_idx* I, int a, int b, int c) {
+  if (a < 0 || b < 0 || c < 0 || a + b + c > I->P) return -1;
+  int P1 = I->P + 1;
+  return I->lut[(a * P1 + b) * P1 + c];
+}
+
+/* x^α / α! for every |α| ≤ deg (first fmm_count(deg) entries) */
+static void fmm_monomials(const fmm_idx* I, const double x[3], int deg, double* out) {
+  int n = fmm_count(deg);
+  for (int k = 0; k < n; ++k) {
+    const int* a = I->mi + 3 * k;
+    out[k] = pow(x[0], a[0]) * pow(x[1], a[1]) * pow(x[2], a[2]) / (I->fact[a[0]] * I->fact[a[1]] * I->fact[a[2]]);
+  }
+}
+
+/* T_δ = ∂^δ Φ(R), |δ| ≤ P, Φ = 1/(4π|R|) */
+static void fmm_derivs(const fmm_idx* I, const double R[3], double* T) {
+  double r2 = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
+  double* b = (double*)malloc((size_t)I->nP * sizeof(double));
+  b[0] = 1.0 / sqrt(r2);
+  for (int k = 1; k < I->nP; ++k) {
+    const int* d = I->mi + 3 * k;
+    int n = d[0] + d[1] + d[2];
+    double s = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      int e[3] = {d[0], d[1], d[2]};
+      e[i] -= 1;
+      int j = fmm_at(I, e[0], e[1], e[2]);
+      if (j >= 0) s -= (2.0 * n - 1.0) * R[i] * b[j];
+      e[i] -= 1;
+      j = fmm_at(I, e[0], e[1], e[2]);
+      if (j >= 0) s -= (n - 1.0) * b[j];
+    }
+    b[k] = s / (n * r2);
+  }
+  for (int k = 0; k < I->nP; ++k) {
+    const int* d = I->mi + 3 * k;
+    T[k] = b[k] * I->fact[d[0]] * I->fact[d[1]] * I->fact[d[2]] / WO_4PI;
+  }
+  free(b);
+}
+
+typedef struct {
+  const wo_tree* t;
+  fmm_idx I;
+  int leaf, dim;           /* dim 1: charges q (Aᵀ), dim 3: dipoles ν (A, G) */
+  double theta, w;
+  float w2f;
+  double* ctr;             /* nn × 3 cube centres (node id order) */
+  double* rad;             /* nn half-diagonals */
+  double* M;               /* nn × np multipole coefficients */
+  double* L;               /* nn × np local coefficients */
+  const double* nu;        /* caller order */
+  double* pot;             /* n × 4: V, ∂V (caller order), accumulated */
+  int64_t m2l, p2p;        /* counters: M2L cell pairs, P2P point pairs */
+} fmm_ctx;
+
+static int fmm_is_leaf(const fmm_ctx* f, int64_t id) {
+  const wo_node* nd = &f->t->nodes[id];
+  return nd->nchild == 0 || nd->pe - nd->pb <= f->leaf;
+}
+
+static void fmm_up(fmm_ctx* f, int64_t id) {
+  const wo_node* nd = &f->t->nodes[id];
+  const fmm_idx* I = &f->I;
+  double* M = f->M + (size_t)id * I->np;
+  const double* c = f->ctr + 3 * id;
+  if (fmm_is_leaf(f, id)) {  /* P2M */
+    double* mono = (double*)malloc((size_t)I->np * sizeof(double));
+    for (int64_t k = nd->pb; k < nd->pe; ++k) {
+      int64_t j = f->t->order[k];
+      double x[3];
+      for (int a = 0; a < 3; ++a) x[a] = (double)f->t->xn[3 * j + a] - c[a];
+      fmm_monomials(I, x, I->p, mono);
+      const double* v = f->nu + (size_t)f->dim * j;
+      for (int b = 0; b < I->np; ++b) {
+        const int* be = I->mi + 3 * b;
+        int deg = be[0] + be[1] + be[2];
+        if (f->dim == 1) {
+          M[b] += v[0] * ((deg & 1) ? -1.0 : 1.0) * mono[b];
+        } else {
+          for (int kk = 0; kk < 3; ++kk) {
+            int e[3] = {be[0], be[1], be[2]};
+            e[kk] -= 1;
+            int g = fmm_at(I, e[0], e[1], e[2]);
+            if (g >= 0 && g < I->np) M[b] += v[kk] * ((deg - 1) & 1 ? -1.0 : 1.0) * mono[g];
+          }
+        }
+      }
+    }
+    free(mono);
+    return;
+  }
+  double* shift = (double*)malloc((size_t)I->np * sizeof(double));
+  for (int ci = 0; ci < nd->nchild; ++ci) {  /* M2M, children in octant order */
+    int64_t ch = nd->child[ci];
+    fmm_up(f, ch);
+    const double* Mc = f->M + (size_t)ch * I->np;
+    double d[3];
+    for (int a = 0; a < 3; ++a) d[a] = c[a] - f->ctr[3 * ch + a];  /* c' − c (parent − child) */
+    fmm_monomials(I, d, I->p, shift);
+    for (int b = 0; b < I->np; ++b) {
+      const int* be = I->mi + 3 * b;
+      for (int g = 0; g <= b; ++g) {
+        const int* ge = I->mi + 3 * g;
+        int s = fmm_at(I, be[0] - ge[0], be[1] - ge[1], be[2] - ge[2]);
+        if (s >= 0) M[b] += Mc[g] * shift[s];
+      }
+    }
+  }
+  free(shift);
+}
+
+static void fmm_p2p(fmm_ctx* f, int64_t T, int64_t S) {
+  const wo_node* nt = &f->t->nodes[T];
+  const wo_node* ns = &f->t->nodes[S];
+  for (int64_t a = nt->pb; a < nt->pe; ++a) {
+    int64_t i = f->t->order[a];
+    const float* yf = f->t->xn + 3 * i;
+    double* out = f->pot + 4 * i;
+    for (int64_t b = ns->pb; b < ns->pe; ++b) {
+      int64_t j = f->t->order[b];
+      const float* xf = f->t->xn + 3 * j;
+      if (d2_f32(xf, yf) < f->w2f) continue;  /* smoothing cutoff (§4.4), fp32 decision (R-prec) */
+      double d[3] = {(double)yf[0] - xf[0], (double)yf[1] - xf[1], (double)yf[2] - xf[2]};
+      double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2], r = sqrt(r2);
+      double k1 = 1.0 / (WO_4PI * r), k3 = k1 / r2, k5 = 3.0 * k3 / r2;
+      const double* v = f->nu + (size_t)f->dim * j;
+      if (f->dim == 1) {  /* q Φ(d): V += q/(4πr), ∇V += −q d/(4πr³) */
+        out[0] += v[0] * k1;
+        for (int c = 0; c < 3; ++c) out[1 + c] -= v[0] * d[c] * k3;
+      } else {  /* ν·∇Φ(d) = −(d·ν)/(4πr³);  ∇(ν·∇Φ)(d) = HΦ(d)ν = 3(d·ν)d/(4πr⁵) − ν/(4πr³) */
+        double dn = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
+        out[0] -= dn * k3;
+        for (int c = 0; c < 3; ++c) out[1 + c] += dn * d[c] * k5 - v[c] * k3;
+      }
+      f->p2p++;
+    }
+  }
+}
+
+static void fmm_m2l(fmm_ctx* f, int64_t T, int64_t S, double* Tbuf) {
+  const fmm_idx* I = &f->I;
+  double R[3];
+  for (int a = 0; a < 3; ++a) R[a] = f->ctr[3 * T + a] - f->ctr[3 * S + a];
+  fmm_derivs(I, R, Tbuf);
+  const double* M = f->M + (size_t)S * I->np;
+  double* L = f->L + (size_t)T * I->np;
+  for (int g = 0; g < I->np; ++g) {
+    const int* ge = I->mi + 3 * g;
+    double acc = 0.0;
+    for (int b = 0; b < I->np; ++b) {
+      const int* be = I->mi + 3 * b;
+      acc += M[b] * Tbuf[fmm_at(I, be[0] + ge[0], be[1] + ge[1], be[2] + ge[2])];
+    }
+    L[g] += acc;
+  }
+  f->m2l++;
+}
+
+static void fmm_dual(fmm_ctx* f, int64_t T, int64_t S, double* Tbuf) {
+  const double* ct = f->ctr + 3 * T;
+  const double* cs = f->ctr + 3 * S;
+  double d = sqrt((ct[0] - cs[0]) * (ct[0] - cs[0]) + (ct[1] - cs[1]) * (ct[1] - cs[1]) +
+                  (ct[2] - cs[2]) * (ct[2] - cs[2]));
+  double rt = f->rad[T], rs = f->rad[S];
+  if (d * f->theta > rt + rs && d - rt - rs > f->w) {
+    fmm_m2l(f, T, S, Tbuf);
+    return;
+  }
+  int lt = fmm_is_leaf(f, T), ls = fmm_is_leaf(f, S);
+  if (lt && ls) {
+    fmm_p2p(f, T, S);
+    return;
+  }
+  const wo_node* nt = &f->t->nodes[T];
+  const wo_node* ns = &f->t->nodes[S];
+  if (ls || (!lt && rt >= rs)) {
+    for (int c = 0; c < nt->nchild; ++c) fmm_dual(f, nt->child[c], S, Tbuf);
+  } else {
+    for (int c = 0; c < ns->nchild; ++c) fmm_dual(f, T, ns->child[c], Tbuf);
+  }
+}
+
+static void fmm_down(fmm_ctx* f, int64_t id) {
+  const wo_node* nd = &f->t->nodes[id];
+  const fmm_idx* I = &f->I;
+  const double* L = f->L + (size_t)id * I->np;
+  const double* c = f->ctr + 3 * id;
+  double* mono = (double*)malloc((size_t)I->np * sizeof(double));
+  if (fmm_is_leaf(f, id)) {  /* L2P */
+    for (int64_t k = nd->pb; k < nd->pe; ++k) {
+      int64_t i = f->t->order[k];
+      double y[3];
+      for (int a = 0; a < 3; ++a) y[a] = (double)f->t->xn[3 * i + a] - c[a];
+      fmm_monomials(I, y, I->p, mono);
+      double* out = f->pot + 4 * i;
+      for (int g = 0; g < I->np; ++g) {
+        const int* ge = I->mi + 3 * g;
+        out[0] += L[g] * mono[g];
+        for (int kk = 0; kk < 3; ++kk) {
+          int e[3] = {ge[0], ge[1], ge[2]};
+          e[kk] -= 1;
+          int h = fmm_at(I, e[0], e[1], e[2]);
+          if (h >= 0) out[1 + kk] += L[g] * mono[h];
+        }
+      }
+    }
+    free(mono);
+    return;
+  }
+  for (int ci = 0; ci < nd->nchild; ++ci) {  /* L2L */
+    int64_t ch = nd->child[ci];
+    double* Lc = f->L + (size_t)ch * I->np;
+    double d[3];
+    for (int a = 0; a < 3; ++a) d[a] = f->ctr[3 * ch + a] - c[a];  /* c' − c (child − parent) */
+    fmm_monomials(I, d, I->p, mono);
+    for (int dl = 0; dl < I->np; ++dl) {
+      const int* de = I->mi + 3 * dl;
+      for (int g = 0; g < I->np; ++g) {
+        const int* ge = I->mi + 3 * g;
+        int s = fmm_at(I, ge[0] - de[0], ge[1] - de[1], ge[2] - de[2]);
+        if (s >= 0 && s < I->np) Lc[dl] += L[g] * mono[s];
+      }
+    }
+    fmm_down(f, ch);
+  }
+  free(mono);
+}
+
+void wo_fmm_op(const wo_tree* t, int op, const double* nu, int dim, double w, int p, double theta, int leaf,
+               double* out, int64_t* counts) {
+  fmm_ctx f;
+  memset(&f, 0, sizeof(f));
+  f.t = t;
+  fmm_idx_init(&f.I, p);
+  f.leaf = leaf;
+  f.dim = dim;
+  f.theta = theta;
+  f.w = w;
+  float wf = (float)w;
+  f.w2f = wf * wf;
+  f.nu = nu;
+  f.ctr = (double*)malloc((size_t)t->nn * 3 * sizeof(double));
+  f.rad = (double*)malloc((size_t)t->nn * sizeof(double));
+  for (int64_t id = 0; id < t->nn; ++id) {  /* cube of the node: its first point's cell at its depth */
+    const wo_node* nd = &t->nodes[id];
+    const uint32_t* q = t->q + 3 * t->order[nd->pb];
+    double edge = ldexp(1.0, 1 - nd->depth);
+    for (int a = 0; a < 3; ++a) {
+      uint32_t cell = nd->depth == 0 ? 0u : q[a] >> (t->D - nd->depth);
+      f.ctr[3 * id + a] = -1.0 + ((double)cell + 0.5) * edge;
+    }
+    f.rad[id] = sqrt(3.0) * 0.5 * edge;
+  }
+  f.M = (double*)calloc((size_t)t->nn * f.I.np, sizeof(double));
+  f.L = (double*)calloc((size_t)t->nn * f.I.np, sizeof(double));
+  f.pot = (double*)calloc((size_t)t->n * 4, sizeof(double));
+  double* Tbuf = (double*)malloc((size_t)f.I.nP * sizeof(double));
+  int64_t root = t->bfs[0];
+  fmm_up(&f, root);
+  fmm_dual(&f, root, root, Tbuf);
+  fmm_down(&f, root);
+  for (int64_t i = 0; i < t->n; ++i) {
+    const double* v = f.pot + 4 * i;
+    if (op == WO_OP_A) out[i] = v[0];
+    else for (int c = 0; c < 3; ++c) out[3 * i + c] = -v[1 + c];  /* G = −∇V (dipoles), Aᵀ = −∇V (charges) */
+  }
+  if (counts) { counts[0] = f.m2l; counts[1] = f.p2p; }
+  free(Tbuf); free(f.pot); free(f.L); free(f.M); free(f.rad); free(f.ctr);
+  fmm_idx_free(&f.I);
+}

@@ -60,6 +60,13 @@ void wo_tree_A_frozen(const wo_tree* t, const double* mu_geom, const double* nu,
 void wo_tree_AT_transpose(const wo_tree* t, const double* mu_geom, const double* s, double w, double theta,
                           double* out);
 
+/* FMM (not the paper's method; see wn_oracle.c): op WO_OP_A (nu dim 3: A(ν), n out),
+   WO_OP_G (dim 3: G(ν), n×3) or WO_OP_AT (dim 1: Aᵀ(s), n×3) at the n sources, caller order, normalized
+   frame; expansion degree p, separation θ_f, at most `leaf` points per FMM leaf; counts (2 or NULL):
+   M2L cell pairs, P2P point pairs. */
+void wo_fmm_op(const wo_tree* t, int op, const double* nu, int dim, double w, int p, double theta, int leaf,
+               double* out, int64_t* counts);
+
 /* WNNC rescale (Alg. 3): out_i = mh_i |mp_i| / |mh_i|, mp_i kept where |mh_i| = 0 (n×3). */
 void wo_rescale(int64_t n, const double* mp, const double* mh, double* out);
 
