@@ -204,6 +204,17 @@ wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int3
 wn_status wnnc_solve_host(const float* pts_host, int64_t n, int32_t max_depth, const wnnc_params* p,
                           float* normals_host, float* mu_host, wnnc_iter_stats* stats, void* stream);
 
+/* Fast multipole evaluation at the n sources (the paper's future work, PAPER.md:L1034 —
+   an alternative to Alg. 4's treecode, not the paper's method).  op 0: F = Σ_j ∇Φ_w(x_i − x_j)·μ_j (attr =
+   μ, N×3, input frame, out N) as wn_eval; op 2: ∇F (attr μ, out N×3) as wn_eval_grad; op 1: Aᵀ(s) (attr
+   = s, N, out N×3) as wn_eval_adjoint's gather mode — the same sums, evaluated by Cartesian Taylor
+   multipole / local expansions of total degree p (1..6) between well-separated cells (|c_t − c_s|·θ_f >
+   r_t + r_s and every point pair beyond the cutoff w) and directly between the remaining FMM leaves
+   (octree nodes with at most `leaf` ≤ 32 points or no children).  counts (host, 2, may be NULL): M2L cell
+   pairs and P2P leaf pairs.  Synchronizes `stream` (the interaction lists are built level by level). */
+wn_status wn_eval_fmm(wn_tree t, int32_t op, const float* attr, float width, int32_t p, float theta_f, int32_t leaf,
+                      float* out, int64_t* counts, void* stream);
+
 /* ---- multi-GPU (NCCL over NVLink / NVSwitch) ---------------------------------------------------- */
 wn_status wn_comm_unique_id(uint8_t id[128] /*host*/);
 /* Collective over `world` processes, one GPU each (the current device of the calling thread). */

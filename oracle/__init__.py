@@ -286,6 +286,16 @@ class Cloud:
         S = self.t.tree(op | ABS, self._mu_norm(nu_in, a), w, theta, self._q(queries), qidx, order=order)
         return S * (self.scale if op == OP_G else 1.0)
 
+    def fmm(self, op, nu_in, w, p=4, theta_f=0.5, leaf=32, counters=False):
+        """FMM (row f4) in the input frame: op OP_A → F (ν = μ), OP_G → ∇F (μ), OP_AT → Aᵀ (ν = s)."""
+        if op == OP_AT:
+            r = self.t.fmm(OP_AT, _f64(nu_in), w, p, theta_f, leaf, counters)
+            sc = self.scale ** 2
+        else:
+            r = self.t.fmm(op, self._mu_norm(nu_in), w, p, theta_f, leaf, counters)
+            sc = 1.0 if op == OP_A else -self.scale
+        return (r[0] * sc, r[1]) if counters else r * sc
+
     def AT_transpose(self, s, mu_geom, w, theta=2.0):
         return self.t.AT_transpose(self._mu_norm(mu_geom), _f64(s), w, theta) * self.scale ** 2
 

@@ -790,7 +790,7 @@ typedef struct {
   double* L;               /* nn × np local coefficients */
   const double* nu;        /* caller order */
   double* pot;             /* n × 4: V, ∂V (caller order), accumulated */
-  int64_t m2l, p2p;        /* counters: M2L cell pairs, P2P point pairs */
+  int64_t m2l, p2p;        /* counters: M2L cell pairs, P2P leaf pairs */
 } fmm_ctx;
 
 static int fmm_is_leaf(const fmm_ctx* f, int64_t id) {
@@ -872,9 +872,9 @@ static void fmm_p2p(fmm_ctx* f, int64_t T, int64_t S) {
         out[0] -= dn * k3;
         for (int c = 0; c < 3; ++c) out[1 + c] += dn * d[c] * k5 - v[c] * k3;
       }
-      f->p2p++;
     }
   }
+  f->p2p++;  /* one leaf pair */
 }
 
 static void fmm_m2l(fmm_ctx* f, int64_t T, int64_t S, double* Tbuf) {

@@ -63,7 +63,7 @@ void wo_tree_AT_transpose(const wo_tree* t, const double* mu_geom, const double*
 /* FMM (not the paper's method; see wn_oracle.c): op WO_OP_A (nu dim 3: A(ν), n out),
    WO_OP_G (dim 3: G(ν), n×3) or WO_OP_AT (dim 1: Aᵀ(s), n×3) at the n sources, caller order, normalized
    frame; expansion degree p, separation θ_f, at most `leaf` points per FMM leaf; counts (2 or NULL):
-   M2L cell pairs, P2P point pairs. */
+   M2L cell pairs, P2P leaf pairs. */
 void wo_fmm_op(const wo_tree* t, int op, const double* nu, int dim, double w, int p, double theta, int leaf,
                double* out, int64_t* counts);
 

@@ -806,6 +806,33 @@ wn_status wn_query_work(wn_tree t, int32_t op, const float* attr, const float* q
   return eval_common(t, op == 0 ? OP_A : OP_G, attr, nullptr, q, m, width, theta, nullptr, stream, counts);
 }
 
+wn_status wn_eval_fmm(wn_tree t, int32_t op, const float* attr, float width, int32_t p, float theta_f, int32_t leaf,
+                      float* out, int64_t* counts, void* stream) {
+  TreeUse use_(t, stream);
+  if (!t || !attr || !out) return set_error(WN_ERR_ARG, "tree, attribute or output is NULL");
+  if (op < 0 || op > 2) return set_error(WN_ERR_ARG, "op must be 0 (F), 1 (A^T) or 2 (gradF)");
+  if (bad_width(width)) return set_error(WN_ERR_ARG, "width must be > 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  WN_TRY(ensure_scratch(t, s));
+  IterScratch& it = t->it;
+  const double sc = t->xf[3];
+  int64_t cnt[2] = {0, 0};
+  wn_status st;
+  if (op == 1) {  // Aᵀ(s) = −∇ of the charges' potential;  Aᵀ_in = s²·Aᵀ_n
+    gather_scal(t->n, t->perm, attr, it.s, s);
+    st = fmm_apply(t, OP_AT, nullptr, it.s, width, p, theta_f, leaf, t->perm, out, sc * sc, cnt, s);
+  } else {  // dipoles μ: F = V (F_in = s²·V_n(μ_in)), ∇F = ∇V (∇F_in = −s³·G_n(μ_in), G = −∇V)
+    gather_vec_a(t->n, t->perm, attr, nullptr, it.mu, nullptr, nullptr, s);
+    st = fmm_apply(t, op == 0 ? OP_A : OP_G, it.mu, nullptr, width, p, theta_f, leaf, t->perm, out,
+                   op == 0 ? sc * sc : -sc * sc * sc, cnt, s);
+  }
+  if (st == WN_OK && counts) {
+    counts[0] = cnt[0];
+    counts[1] = cnt[1];
+  }
+  return st;
+}
+
 wn_status wn_eval_adjoint(wn_tree t, const float* sv, float width, float theta, int32_t mode, const float* mu_geom,
                           float* out, void* stream) {
   TreeUse use_(t, stream);

@@ -1,0 +1,586 @@
+// fmm.cu — fast multipole evaluation of the winding-number operators (the paper's future
+// work, §6.3 and L409 — an extension, not the paper's Alg. 4 treecode).
+//
+// One potential carries all three operators (Φ(r) = 1/(4π|r|)):
+//     V(y) = Σ_j [ q_j Φ(y − x_j) + ν_j·∇Φ(y − x_j) ]
+// A(ν) = V for dipoles ν, G(ν) = −∇V for dipoles (L266), Aᵀ(s) = −∇V for charges q = s
+// (L316).  Cells are the octree's nodes (cube centres, radius = half-diagonal); an FMM leaf is a node with
+// no children or at most `leaf` (≤ 32) points.  Cartesian Taylor expansions of total degree ≤ p (≤ 6):
+//   P2M  M_β = Σ_j [ q_j (−1)^|β| (x_j−c)^β/β! + Σ_k ν_jk (−1)^(|β|−1) (x_j−c)^(β−e_k)/(β−e_k)! ]
+//   M2M  M'_β = Σ_{γ≤β} M_γ (c'−c)^(β−γ)/(β−γ)!        M2L  L_γ += Σ_β M_β ∂^(β+γ)Φ(c_t − c_s)
+//   L2L  L'_δ = Σ_{γ≥δ} L_γ (c'−c)^(γ−δ)/(γ−δ)!        L2P  V(y) = Σ_γ L_γ (y−c)^γ/γ!  (and ∇V)
+// with ∂^δ(1/|R|) = δ! b_δ, |δ| |R|² b_δ = −(2|δ|−1) Σ_i R_i b_(δ−e_i) − (|δ|−1) Σ_i b_(δ−2e_i).
+// A cell pair is well separated — one M2L — iff |c_t − c_s| θ_f > r_t + r_s and |c_t − c_s| − r_t − r_s > w
+// (every point pair beyond the smoothing cutoff, where the expansion is of the exact kernel); two leaves
+// otherwise interact directly (P2P, cutoff r < w decided in fp32 as everywhere, R-prec); else the larger
+// cell (the target on ties) is split.  All expansion arithmetic is fp64.
+//
+// B200 mapping: the interaction lists come from a breadth-first dual traversal on the GPU (one thread per
+// cell pair per level, appends by atomics), sorted by (target, source) so that every sum runs in a fixed
+// order; P2M / M2M / M2L / L2L run one warp per cell with lanes over the expansion coefficients (the
+// derivative tensor of a pair is built degree by degree in shared memory); L2P + P2P one warp per leaf with
+// one lane per target point.  The oracle (oracle/wn_oracle.c: wo_fmm_op) is the same algorithm in plain C.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <type_traits>
+#include <vector>
+
+#include "wn_internal.cuh"
+
+namespace wn {
+
+constexpr int kFmmMaxP = 6;
+constexpr int kFmmMaxDeg = 2 * kFmmMaxP;
+constexpr int kFmmMaxN = (kFmmMaxP + 1) * (kFmmMaxP + 2) * (kFmmMaxP + 3) / 6;      // 84
+constexpr int kFmmMaxT = (kFmmMaxDeg + 1) * (kFmmMaxDeg + 2) * (kFmmMaxDeg + 3) / 6;  // 455
+constexpr int kFmmLut = kFmmMaxDeg + 1;
+
+// multi-indices by total degree, then (a, b, c) descending lexicographically — the first count(p) of them
+// are exactly the indices of degree ≤ p (the oracle's order)
+__constant__ signed char c_mi[kFmmMaxT][3];
+__constant__ short c_lut[kFmmLut][kFmmLut][kFmmLut];
+__constant__ double c_fact[kFmmMaxDeg + 2];
+
+static int fmm_count(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
+
+static wn_status fmm_tables() {
+  static bool done = false;
+  if (done) return WN_OK;
+  signed char mi[kFmmMaxT][3];
+  static short lut[kFmmLut][kFmmLut][kFmmLut];
+  double fact[kFmmMaxDeg + 2];
+  for (int a = 0; a < kFmmLut; ++a)
+    for (int b = 0; b < kFmmLut; ++b)
+      for (int c = 0; c < kFmmLut; ++c) lut[a][b][c] = -1;
+  int n = 0;
+  for (int deg = 0; deg <= kFmmMaxDeg; ++deg)
+    for (int a = deg; a >= 0; --a)
+      for (int b = deg - a; b >= 0; --b) {
+        const int c = deg - a - b;
+        mi[n][0] = (signed char)a;
+        mi[n][1] = (signed char)b;
+        mi[n][2] = (signed char)c;
+        lut[a][b][c] = (short)n++;
+      }
+  fact[0] = 1.0;
+  for (int k = 1; k < kFmmMaxDeg + 2; ++k) fact[k] = fact[k - 1] * k;
+  WN_CUDA(cudaMemcpyToSymbol(c_mi, mi, sizeof(mi)));
+  WN_CUDA(cudaMemcpyToSymbol(c_lut, lut, sizeof(lut)));
+  WN_CUDA(cudaMemcpyToSymbol(c_fact, fact, sizeof(fact)));
+  done = true;
+  return WN_OK;
+}
+
+__device__ __forceinline__ int fmm_at(int a, int b, int c, int P) {
+  if (a < 0 || b < 0 || c < 0 || a + b + c > P) return -1;
+  return c_lut[a][b][c];
+}
+
+// x^a / a! for a ≤ p (per axis), then a monomial is the product of three of them
+__device__ __forceinline__ void fmm_pows(double x, int p, double* o) {
+  o[0] = 1.0;
+  for (int a = 1; a <= p; ++a) o[a] = o[a - 1] * x / a;
+}
+
+struct FmmGeom {
+  const int32_t *pb, *pe, *cb, *cc, *depth, *parent;
+  const double* ctr;   // nn × 3
+  const double* rad;   // nn
+  const uint8_t* leaf; // FMM leaf flag
+};
+
+// cube centre and half-diagonal of every node from its first sorted point (the tree build's quantization,
+// fp64, exact powers of two), the FMM leaf flag, and whether a node is above every FMM leaf (active)
+__global__ void k_fmm_geom(int64_t nn, int D, int leafsz, const float4* __restrict__ pts,
+                           const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
+                           const int32_t* __restrict__ cc, const int32_t* __restrict__ depth,
+                           double* __restrict__ ctr, double* __restrict__ rad, uint8_t* __restrict__ leaf) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  const float4 x = pts[pb[i]];
+  const int d = depth[i];
+  const double cells = ldexp(1.0, D - 1), qmax = (double)((1u << D) - 1u);
+  const double edge = ldexp(1.0, 1 - d);
+  const float xs[3] = {x.x, x.y, x.z};
+  for (int a = 0; a < 3; ++a) {
+    double v = floor(((double)xs[a] + 1.0) * cells);
+    v = v < 0.0 ? 0.0 : (v > qmax ? qmax : v);
+    const uint32_t q = (uint32_t)v;
+    const uint32_t cell = d == 0 ? 0u : q >> (D - d);
+    ctr[3 * i + a] = -1.0 + ((double)cell + 0.5) * edge;
+  }
+  rad[i] = sqrt(3.0) * 0.5 * edge;
+  leaf[i] = (cc[i] == 0 || pe[i] - pb[i] <= leafsz) ? 1 : 0;
+}
+
+// P2M: one warp per FMM leaf, lanes over the coefficients β
+template <int DIM>
+__global__ void k_fmm_p2m(int64_t m, const int32_t* __restrict__ list, FmmGeom g, const float4* __restrict__ pts,
+                          const float4* __restrict__ vec, const float* __restrict__ scal, int p,
+                          double* __restrict__ M) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (k >= m) return;
+  const int64_t id = list[k];
+  const int np = (p + 1) * (p + 2) * (p + 3) / 6;
+  const double c0 = g.ctr[3 * id], c1 = g.ctr[3 * id + 1], c2 = g.ctr[3 * id + 2];
+  for (int b = lane; b < np; b += 32) {
+    const int b0 = c_mi[b][0], b1 = c_mi[b][1], b2 = c_mi[b][2], deg = b0 + b1 + b2;
+    double acc = 0.0;
+    for (int j = g.pb[id]; j < g.pe[id]; ++j) {
+      const float4 x = pts[j];
+      double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];
+      fmm_pows((double)x.x - c0, p, px);
+      fmm_pows((double)x.y - c1, p, py);
+      fmm_pows((double)x.z - c2, p, pz);
+      if (DIM == 1) {
+        acc += (double)scal[j] * ((deg & 1) ? -1.0 : 1.0) * (px[b0] * py[b1] * pz[b2]);
+      } else {
+        const float4 v = vec[j];
+        const double sg = ((deg - 1) & 1) ? -1.0 : 1.0;
+        if (b0 > 0) acc += (double)v.x * sg * (px[b0 - 1] * py[b1] * pz[b2]);
+        if (b1 > 0) acc += (double)v.y * sg * (px[b0] * py[b1 - 1] * pz[b2]);
+        if (b2 > 0) acc += (double)v.z * sg * (px[b0] * py[b1] * pz[b2 - 1]);
+      }
+    }
+    M[id * np + b] = acc;
+  }
+}
+
+// M2M: one warp per internal active node of one level, its children in order
+__global__ void k_fmm_m2m(int64_t m, const int32_t* __restrict__ list, FmmGeom g, int p, double* __restrict__ M) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (k >= m) return;
+  const int64_t id = list[k];
+  const int np = (p + 1) * (p + 2) * (p + 3) / 6;
+  for (int b = lane; b < np; b += 32) {
+    const int b0 = c_mi[b][0], b1 = c_mi[b][1], b2 = c_mi[b][2];
+    double acc = 0.0;
+    for (int c = g.cb[id]; c < g.cb[id] + g.cc[id]; ++c) {
+      double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];  // (c' − c): parent − child
+      fmm_pows(g.ctr[3 * id] - g.ctr[3 * c], p, px);
+      fmm_pows(g.ctr[3 * id + 1] - g.ctr[3 * c + 1], p, py);
+      fmm_pows(g.ctr[3 * id + 2] - g.ctr[3 * c + 2], p, pz);
+      const double* Mc = M + (int64_t)c * np;
+      for (int g0 = 0; g0 <= b0; ++g0)
+        for (int g1 = 0; g1 <= b1; ++g1)
+          for (int g2 = 0; g2 <= b2; ++g2) acc += Mc[c_lut[g0][g1][g2]] * (px[b0 - g0] * py[b1 - g1] * pz[b2 - g2]);
+    }
+    M[id * np + b] = acc;
+  }
+}
+
+// breadth-first dual traversal, one level of cell pairs: the oracle's fmm_dual decisions, appended by atomics
+__global__ void k_fmm_dual(int64_t m, const int2* __restrict__ in, FmmGeom g, double theta, double w,
+                           int2* __restrict__ next, unsigned long long* __restrict__ cnt, int64_t cap_next,
+                           uint64_t* __restrict__ m2l, int64_t cap_m2l, uint64_t* __restrict__ p2p, int64_t cap_p2p) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int T = in[k].x, S = in[k].y;
+  const double dx = g.ctr[3 * T] - g.ctr[3 * S], dy = g.ctr[3 * T + 1] - g.ctr[3 * S + 1],
+               dz = g.ctr[3 * T + 2] - g.ctr[3 * S + 2];
+  const double d = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  const double rt = g.rad[T], rs = g.rad[S];
+  const uint64_t key = ((uint64_t)(uint32_t)T << 32) | (uint32_t)S;
+  if (__dmul_rn(d, theta) > __dadd_rn(rt, rs) && __dsub_rn(__dsub_rn(d, rt), rs) > w) {
+    const unsigned long long i = atomicAdd(cnt + 1, 1ull);
+    if ((int64_t)i < cap_m2l) m2l[i] = key;
+    return;
+  }
+  const bool lt = g.leaf[T], ls = g.leaf[S];
+  if (lt && ls) {
+    const unsigned long long i = atomicAdd(cnt + 2, 1ull);
+    if ((int64_t)i < cap_p2p) p2p[i] = key;
+    return;
+  }
+  const bool split_t = ls || (!lt && rt >= rs);
+  const int c0 = split_t ? g.cb[T] : g.cb[S], nc = split_t ? g.cc[T] : g.cc[S];
+  const unsigned long long i = atomicAdd(cnt, (unsigned long long)nc);
+  for (int c = 0; c < nc; ++c)
+    if ((int64_t)(i + c) < cap_next) next[i + c] = split_t ? make_int2(c0 + c, S) : make_int2(T, c0 + c);
+}
+
+// CSR offsets of a sorted (target << 32 | source) key list: off[t] = first key with target ≥ t
+__global__ void k_fmm_csr(int64_t nn, const uint64_t* __restrict__ keys, int64_t nk, int32_t* __restrict__ off) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > nn) return;
+  const uint64_t target = (uint64_t)t << 32;
+  int64_t lo = 0, hi = nk;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  off[t] = (int32_t)lo;
+}
+
+// M2L: one warp per target cell with a non-empty list; per source cell the derivative tensor of
+// R = c_t − c_s is built degree by degree in shared memory (scaled to T_δ = ∂^δΦ on the fly), the source's
+// multipole coefficients are staged there too, then lane γ adds Σ_β M_β T_(β+γ)
+// index of a multi-index in the degree-then-lexicographic order, arithmetically (no divergent table lookups)
+__device__ __forceinline__ int mi_index(int a, int b, int c) {
+  const int n = a + b + c, na = n - a;
+  return n * (n + 1) * (n + 2) / 6 + na * (na + 1) / 2 + (na - b);
+}
+__device__ __forceinline__ double fact_small(int k) {  // k! for k ≤ 12, exact in fp64
+  double f = 1.0;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return f;
+}
+constexpr int kFmmWarps = 4;
+__global__ void __launch_bounds__(32 * kFmmWarps) k_fmm_m2l(int64_t nn, const int32_t* __restrict__ off,
+                                                            const uint64_t* __restrict__ keys, FmmGeom g, int p,
+                                                            const double* __restrict__ M, double* __restrict__ L) {
+  __shared__ double sT[kFmmWarps][kFmmMaxT];
+  __shared__ double sB[kFmmWarps][kFmmMaxT];
+  __shared__ double sM[kFmmWarps][kFmmMaxN];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int64_t T = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (T >= nn) return;
+  const int k0 = off[T], k1 = off[T + 1];
+  if (k0 == k1) return;
+  const int np = (p + 1) * (p + 2) * (p + 3) / 6, P = 2 * p;
+  double* b = sB[wp];
+  double* Tt = sT[wp];
+  double* Ms = sM[wp];
+  // this lane's output coefficients γ = lane + 32 q
+  int gq[3][3];
+  for (int q = 0; q < 3; ++q) {
+    const int gi = lane + 32 * q;
+    gq[q][0] = gi < np ? c_mi[gi][0] : 0;
+    gq[q][1] = gi < np ? c_mi[gi][1] : 0;
+    gq[q][2] = gi < np ? c_mi[gi][2] : 0;
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int k = k0; k < k1; ++k) {
+    const int S = (int)(uint32_t)keys[k];
+    const double R0 = g.ctr[3 * T] - g.ctr[3 * S], R1 = g.ctr[3 * T + 1] - g.ctr[3 * S + 1],
+                 R2 = g.ctr[3 * T + 2] - g.ctr[3 * S + 2];
+    const double r2 = R0 * R0 + R1 * R1 + R2 * R2;
+    __syncwarp();
+    for (int e = lane; e < np; e += 32) Ms[e] = M[(int64_t)S * np + e];
+    if (lane == 0) {
+      b[0] = 1.0 / sqrt(r2);
+      Tt[0] = b[0] * 0.0795774715459476679;
+    }
+    __syncwarp();
+    for (int n = 1; n <= P; ++n) {  // the b_δ of degree n from degrees n − 1 and n − 2
+      const int lo = n * (n + 1) * (n + 2) / 6, cntn = (n + 1) * (n + 2) / 2;
+      for (int e = lane; e < cntn; e += 32) {
+        const int idx = lo + e;
+        const int d0 = c_mi[idx][0], d1 = c_mi[idx][1], d2 = c_mi[idx][2];
+        double s = 0.0;
+        if (d0 > 0) s -= (2.0 * n - 1.0) * R0 * b[mi_index(d0 - 1, d1, d2)];
+        if (d1 > 0) s -= (2.0 * n - 1.0) * R1 * b[mi_index(d0, d1 - 1, d2)];
+        if (d2 > 0) s -= (2.0 * n - 1.0) * R2 * b[mi_index(d0, d1, d2 - 1)];
+        if (d0 > 1) s -= (n - 1.0) * b[mi_index(d0 - 2, d1, d2)];
+        if (d1 > 1) s -= (n - 1.0) * b[mi_index(d0, d1 - 2, d2)];
+        if (d2 > 1) s -= (n - 1.0) * b[mi_index(d0, d1, d2 - 2)];
+        const double bv = s / (n * r2);
+        b[idx] = bv;
+        Tt[idx] = bv * (fact_small(d0) * fact_small(d1) * fact_small(d2)) * 0.0795774715459476679;  // ∂^δΦ
+      }
+      __syncwarp();
+    }
+    for (int q = 0; q < 3; ++q) {
+      if (lane + 32 * q >= np) break;
+      double a = 0.0;
+      for (int be = 0; be < np; ++be)
+        a += Ms[be] * Tt[mi_index(c_mi[be][0] + gq[q][0], c_mi[be][1] + gq[q][1], c_mi[be][2] + gq[q][2])];
+      acc[q] += a;
+    }
+  }
+  for (int q = 0; q < 3; ++q) {
+    const int gi = lane + 32 * q;
+    if (gi < np) L[T * np + gi] = acc[q];
+  }
+}
+
+// L2L: one warp per child of an internal active node of one level: L_c += shift of the parent's L
+__global__ void k_fmm_l2l(int64_t m, const int32_t* __restrict__ list, FmmGeom g, int p, double* __restrict__ L) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (k >= m) return;
+  const int64_t c = list[k];  // a node whose parent is an internal active node
+  const int64_t par = g.parent[c];
+  const int np = (p + 1) * (p + 2) * (p + 3) / 6;
+  double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];  // (c' − c): child − parent
+  fmm_pows(g.ctr[3 * c] - g.ctr[3 * par], p, px);
+  fmm_pows(g.ctr[3 * c + 1] - g.ctr[3 * par + 1], p, py);
+  fmm_pows(g.ctr[3 * c + 2] - g.ctr[3 * par + 2], p, pz);
+  const double* Lp = L + par * np;
+  for (int dl = lane; dl < np; dl += 32) {
+    const int d0 = c_mi[dl][0], d1 = c_mi[dl][1], d2 = c_mi[dl][2];
+    double acc = 0.0;
+    for (int gi = 0; gi < np; ++gi) {
+      const int g0 = c_mi[gi][0] - d0, g1 = c_mi[gi][1] - d1, g2 = c_mi[gi][2] - d2;
+      if (g0 < 0 || g1 < 0 || g2 < 0) continue;
+      acc += Lp[gi] * (px[g0] * py[g1] * pz[g2]);
+    }
+    L[c * np + dl] += acc;
+  }
+}
+
+// L2P + P2P: one warp per FMM leaf, one lane per target point; V and ∇V in fp64, output per op
+template <int DIM>
+__global__ void k_fmm_eval(int64_t m, const int32_t* __restrict__ list, FmmGeom g, const int32_t* __restrict__ off,
+                           const uint64_t* __restrict__ keys, const float4* __restrict__ pts,
+                           const float4* __restrict__ vec, const float* __restrict__ scal, int p,
+                           const double* __restrict__ L, float w2f, int op, const int32_t* __restrict__ out_map,
+                           float* __restrict__ out, double scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (k >= m) return;
+  const int64_t T = list[k];
+  const int np = (p + 1) * (p + 2) * (p + 3) / 6;
+  const int i = g.pb[T] + lane;
+  const bool valid = i < g.pe[T];
+  double V = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) {
+    y = pts[i];
+    double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];
+    fmm_pows((double)y.x - g.ctr[3 * T], p, px);
+    fmm_pows((double)y.y - g.ctr[3 * T + 1], p, py);
+    fmm_pows((double)y.z - g.ctr[3 * T + 2], p, pz);
+    const double* Lt = L + T * np;
+    for (int gi = 0; gi < np; ++gi) {
+      const int g0 = c_mi[gi][0], g1 = c_mi[gi][1], g2 = c_mi[gi][2];
+      const double l = Lt[gi];
+      V += l * (px[g0] * py[g1] * pz[g2]);
+      if (g0 > 0) gx += l * (px[g0 - 1] * py[g1] * pz[g2]);
+      if (g1 > 0) gy += l * (px[g0] * py[g1 - 1] * pz[g2]);
+      if (g2 > 0) gz += l * (px[g0] * py[g1] * pz[g2 - 1]);
+    }
+  }
+  // P2P: fp32 pair terms (rsqrt, as the treecode's near field), summed per source leaf in fp32 and across
+  // leaves in fp64; the cutoff decided in fp32 on d = x_j − y (R-prec)
+  for (int kk = off[T]; kk < off[T + 1]; ++kk) {
+    const int S = (int)(uint32_t)keys[kk];
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+    for (int j = g.pb[S]; j < g.pe[S]; ++j) {
+      const float4 x = pts[j];
+      const float dxf = x.x - y.x, dyf = x.y - y.y, dzf = x.z - y.z;
+      const float d2 = __fmaf_rn(dxf, dxf, __fmaf_rn(dyf, dyf, __fmul_rn(dzf, dzf)));
+      const bool live = valid && !(d2 < w2f);
+      const float inv = rsqrtf(live ? d2 : __int_as_float(0x7f800000));  // a dead pair: rsqrt(+inf) = 0
+      const float inv3 = inv * inv * inv;
+      // d = y − x = −(dxf, dyf, dzf)
+      if (DIM == 1) {  // q Φ(d): V += q/(4πr), ∇V += −q d/(4πr³) = q (x − y)/(4πr³)
+        const float q = scal[j];
+        v0 = fmaf(q, inv, v0);
+        v1 = fmaf(q * inv3, dxf, v1);
+        v2 = fmaf(q * inv3, dyf, v2);
+        v3 = fmaf(q * inv3, dzf, v3);
+      } else {  // V −= (d·ν)/(4πr³);  ∇V += 3(d·ν)d/(4πr⁵) − ν/(4πr³)
+        const float4 v = vec[j];
+        const float dn = -(dxf * v.x + dyf * v.y + dzf * v.z);
+        const float t5 = 3.0f * dn * inv3 * inv * inv;
+        v0 = fmaf(-dn, inv3, v0);
+        v1 = fmaf(-t5, dxf, fmaf(-v.x, inv3, v1));
+        v2 = fmaf(-t5, dyf, fmaf(-v.y, inv3, v2));
+        v3 = fmaf(-t5, dzf, fmaf(-v.z, inv3, v3));
+      }
+    }
+    const double k4 = 0.0795774715459476679;
+    V += k4 * v0;
+    gx += k4 * v1;
+    gy += k4 * v2;
+    gz += k4 * v3;
+  }
+  if (!valid) return;
+  const int64_t o = out_map ? (int64_t)out_map[i] : i;
+  if (op == OP_A) {
+    out[o] = (float)(V * scale);
+  } else {  // G = −∇V (dipoles), Aᵀ = −∇V (charges)
+    out[3 * o] = (float)(-gx * scale);
+    out[3 * o + 1] = (float)(-gy * scale);
+    out[3 * o + 2] = (float)(-gz * scale);
+  }
+}
+
+__global__ void k_fmm_flag(int64_t nn, const uint8_t* __restrict__ leaf, const int32_t* __restrict__ parent,
+                           const int32_t* __restrict__ depth, int mode, int level, uint32_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  const bool active = parent[i] < 0 || !leaf[parent[i]];  // no FMM leaf above it (the leaf test is monotone)
+  bool f = false;
+  if (mode == 0) f = active && leaf[i];                                    // the FMM leaves
+  else if (mode == 1) f = active && !leaf[i] && depth[i] == level;        // internal active nodes of a level
+  else f = active && parent[i] >= 0 && depth[i] == level;                  // active children at a level
+  flag[i] = f ? 1u : 0u;
+}
+
+__global__ void k_fmm_compact(int64_t nn, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                              int32_t* __restrict__ list) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nn && flag[i]) list[pos[i]] = (int32_t)i;
+}
+
+// exclusive scan helper of tree_build.cu (uint32)
+wn_status fmm_scan(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* total, cudaStream_t s);
+
+static inline unsigned g256(int64_t n) { return (unsigned)((n + 255) / 256); }
+static inline unsigned gwarps(int64_t n, int wpb) { return (unsigned)((n + wpb - 1) / wpb); }
+
+// one FMM application on the tree's sorted points: attribute vec (DIM 3) or scal (DIM 1), sorted order
+wn_status fmm_apply(wn_tree_s* t, int op, const float4* vec, const float* scal, float w, int p, double theta,
+                    int leafsz, const int32_t* out_map, float* out, double scale, int64_t counts[2], cudaStream_t s) {
+  if (p < 1 || p > kFmmMaxP) return set_error(WN_ERR_ARG, "FMM degree must be in 1..6");
+  if (leafsz < 1 || leafsz > 32) return set_error(WN_ERR_ARG, "FMM leaf size must be in 1..32");
+  if (!(theta > 0.0)) return set_error(WN_ERR_ARG, "FMM separation must be > 0");
+  WN_TRY(fmm_tables());
+  const int64_t nn = t->nn;
+  const int np = fmm_count(p);
+  std::vector<void*> held;
+  auto alloc = [&](auto** ptr, size_t bytes) -> wn_status {
+    cudaError_t e = cudaMallocAsync((void**)ptr, std::max<size_t>(bytes, 8), s);
+    if (e != cudaSuccess) return cuda_status(e, "FMM scratch");
+    held.push_back((void*)*ptr);
+    return WN_OK;
+  };
+  struct Release {
+    std::vector<void*>& h;
+    cudaStream_t s;
+    ~Release() {
+      for (void* q : h) cudaFreeAsync(q, s);
+    }
+  } rel{held, s};
+  double *ctr = nullptr, *rad = nullptr, *M = nullptr, *L = nullptr;
+  uint8_t* leaf = nullptr;
+  WN_TRY(alloc(&ctr, nn * 3 * sizeof(double)));
+  WN_TRY(alloc(&rad, nn * sizeof(double)));
+  WN_TRY(alloc(&leaf, nn));
+  WN_TRY(alloc(&M, (size_t)nn * np * sizeof(double)));
+  WN_TRY(alloc(&L, (size_t)nn * np * sizeof(double)));
+  WN_CUDA(cudaMemsetAsync(L, 0, (size_t)nn * np * sizeof(double), s));
+  k_fmm_geom<<<g256(nn), 256, 0, s>>>(nn, t->D, leafsz, t->pts, t->pb, t->pe, t->cc, t->depth, ctr, rad, leaf);
+  FmmGeom g{t->pb, t->pe, t->cb, t->cc, t->depth, t->parent, ctr, rad, leaf};
+  count_launches(1);
+  // node lists: FMM leaves, internal active nodes per level, active non-root nodes per level
+  uint32_t *flag = nullptr, *pos = nullptr;
+  WN_TRY(alloc(&flag, (nn + 1) * sizeof(uint32_t)));
+  WN_TRY(alloc(&pos, (nn + 1) * sizeof(uint32_t)));
+  auto make_list = [&](int mode, int level, int32_t** list, int64_t* m) -> wn_status {
+    k_fmm_flag<<<g256(nn), 256, 0, s>>>(nn, leaf, t->parent, t->depth, mode, level, flag);
+    WN_TRY(fmm_scan(flag, pos, nn, pos + nn, s));
+    uint32_t c = 0;
+    WN_CUDA(cudaMemcpyAsync(&c, pos + nn, sizeof(c), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaStreamSynchronize(s));
+    *m = c;
+    WN_TRY(alloc(list, (size_t)std::max<uint32_t>(c, 1) * sizeof(int32_t)));
+    k_fmm_compact<<<g256(nn), 256, 0, s>>>(nn, flag, pos, *list);
+    count_launches(2);
+    return WN_OK;
+  };
+  int32_t* leaves = nullptr;
+  int64_t nleaves = 0;
+  WN_TRY(make_list(0, 0, &leaves, &nleaves));
+  const int D = t->depth_used;
+  std::vector<int32_t*> inner(D + 1, nullptr), kids(D + 1, nullptr);
+  std::vector<int64_t> ninner(D + 1, 0), nkids(D + 1, 0);
+  for (int l = 0; l <= D; ++l) {
+    WN_TRY(make_list(1, l, &inner[l], &ninner[l]));
+    WN_TRY(make_list(2, l, &kids[l], &nkids[l]));
+  }
+  // upward pass
+  const int wpb = 8;
+  if (vec) k_fmm_p2m<3><<<gwarps(nleaves, wpb), 32 * wpb, 0, s>>>(nleaves, leaves, g, t->pts, vec, scal, p, M);
+  else k_fmm_p2m<1><<<gwarps(nleaves, wpb), 32 * wpb, 0, s>>>(nleaves, leaves, g, t->pts, vec, scal, p, M);
+  count_launches(1);
+  for (int l = D; l >= 0; --l)
+    if (ninner[l]) {
+      k_fmm_m2m<<<gwarps(ninner[l], wpb), 32 * wpb, 0, s>>>(ninner[l], inner[l], g, p, M);
+      count_launches(1);
+    }
+  // interaction lists: breadth-first dual traversal from (root, root)
+  unsigned long long* cnt = nullptr;
+  WN_TRY(alloc(&cnt, 3 * sizeof(unsigned long long)));
+  int64_t cap_f = std::max<int64_t>(1024, 4 * nn), cap_m = std::max<int64_t>(1024, 16 * nn),
+          cap_p = std::max<int64_t>(1024, 4 * nn);
+  int2 *fa = nullptr, *fb = nullptr;
+  uint64_t *m2l = nullptr, *p2p = nullptr;
+  WN_TRY(alloc(&fa, cap_f * sizeof(int2)));
+  WN_TRY(alloc(&fb, cap_f * sizeof(int2)));
+  WN_TRY(alloc(&m2l, cap_m * sizeof(uint64_t)));
+  WN_TRY(alloc(&p2p, cap_p * sizeof(uint64_t)));
+  const int2 root = make_int2(0, 0);
+  WN_CUDA(cudaMemcpyAsync(fa, &root, sizeof(root), cudaMemcpyHostToDevice, s));
+  // a buffer that overflows during a level is regrown (contents kept) and the level runs again
+  auto grow = [&](auto** buf, int64_t* cap, int64_t need, int64_t keep, size_t elt) -> wn_status {
+    const int64_t nc = std::max<int64_t>(need + need / 2, 2 * *cap);
+    void* nb = nullptr;
+    WN_TRY(alloc(&nb, (size_t)nc * elt));
+    if (keep > 0) WN_CUDA(cudaMemcpyAsync(nb, *buf, (size_t)keep * elt, cudaMemcpyDeviceToDevice, s));
+    *buf = reinterpret_cast<std::remove_reference_t<decltype(**buf)>*>(nb);
+    *cap = nc;
+    return WN_OK;
+  };
+  unsigned long long h[3] = {1, 0, 0};  // frontier size, M2L and P2P counts so far
+  while (h[0] > 0) {
+    const unsigned long long nf = h[0], m0 = h[1], p0 = h[2];
+    for (;;) {
+      unsigned long long start[3] = {0, m0, p0};
+      WN_CUDA(cudaMemcpyAsync(cnt, start, sizeof(start), cudaMemcpyHostToDevice, s));
+      k_fmm_dual<<<g256((int64_t)nf), 256, 0, s>>>((int64_t)nf, fa, g, theta, (double)w, fb, cnt, cap_f, m2l, cap_m,
+                                                   p2p, cap_p);
+      count_launches(1);
+      WN_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+      WN_CUDA(cudaStreamSynchronize(s));
+      const bool of = (int64_t)h[0] > cap_f, om = (int64_t)h[1] > cap_m, op_ = (int64_t)h[2] > cap_p;
+      if (!of && !om && !op_) break;
+      if (of) WN_TRY(grow(&fb, &cap_f, (int64_t)h[0], 0, sizeof(int2)));
+      if (om) WN_TRY(grow(&m2l, &cap_m, (int64_t)h[1], (int64_t)m0, sizeof(uint64_t)));
+      if (op_) WN_TRY(grow(&p2p, &cap_p, (int64_t)h[2], (int64_t)p0, sizeof(uint64_t)));
+      if (of) {  // keep the two frontier buffers the same size
+        int2* na = nullptr;
+        WN_TRY(alloc(&na, (size_t)cap_f * sizeof(int2)));
+        WN_CUDA(cudaMemcpyAsync(na, fa, (size_t)nf * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+        fa = na;
+      }
+    }
+    std::swap(fa, fb);
+  }
+  const int64_t nm2l = (int64_t)h[1], np2p = (int64_t)h[2];
+  if (counts) {
+    counts[0] = nm2l;
+    counts[1] = np2p;
+  }
+  uint64_t *m2ls = nullptr, *p2ps = nullptr;
+  int32_t *om = nullptr, *op2 = nullptr;
+  WN_TRY(alloc(&m2ls, std::max<int64_t>(nm2l, 1) * sizeof(uint64_t)));
+  WN_TRY(alloc(&p2ps, std::max<int64_t>(np2p, 1) * sizeof(uint64_t)));
+  WN_TRY(alloc(&om, (nn + 1) * sizeof(int32_t)));
+  WN_TRY(alloc(&op2, (nn + 1) * sizeof(int32_t)));
+  int bits = 1;
+  while (bits < 62 && ((int64_t)1 << bits) <= nn) ++bits;
+  WN_TRY(sort_keys_u64(m2l, nm2l, 32 + bits, m2ls, s));
+  WN_TRY(sort_keys_u64(p2p, np2p, 32 + bits, p2ps, s));
+  k_fmm_csr<<<g256(nn + 1), 256, 0, s>>>(nn, m2ls, nm2l, om);
+  k_fmm_csr<<<g256(nn + 1), 256, 0, s>>>(nn, p2ps, np2p, op2);
+  count_launches(2);
+  // M2L, then the downward pass
+  k_fmm_m2l<<<gwarps(nn, kFmmWarps), 32 * kFmmWarps, 0, s>>>(nn, om, m2ls, g, p, M, L);
+  count_launches(1);
+  for (int l = 1; l <= D; ++l)
+    if (nkids[l]) {
+      k_fmm_l2l<<<gwarps(nkids[l], wpb), 32 * wpb, 0, s>>>(nkids[l], kids[l], g, p, L);
+      count_launches(1);
+    }
+  const float w2f = w * w;
+  if (vec)
+    k_fmm_eval<3><<<gwarps(nleaves, wpb), 32 * wpb, 0, s>>>(nleaves, leaves, g, op2, p2ps, t->pts, vec, scal, p, L,
+                                                           w2f, op, out_map, out, scale);
+  else
+    k_fmm_eval<1><<<gwarps(nleaves, wpb), 32 * wpb, 0, s>>>(nleaves, leaves, g, op2, p2ps, t->pts, vec, scal, p, L,
+                                                           w2f, op, out_map, out, scale);
+  count_launches(1);
+  WN_CUDA(cudaGetLastError());
+  WN_CUDA(cudaStreamSynchronize(s));  // (the scratch above is freed stream-ordered on return)
+  return WN_OK;
+}
+
+}  // namespace wn

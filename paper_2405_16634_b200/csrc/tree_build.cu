@@ -570,6 +570,29 @@ static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int3
   return WN_OK;
 }
 
+wn_status fmm_scan(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* total, cudaStream_t s) {
+  return scan_excl(in, out, m, total, s);
+}
+
+// ascending sort of n 64-bit keys on their low `bits` bits (stable LSD radix), out = the sorted keys
+__global__ void k_iota(int64_t n, int32_t* __restrict__ v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+wn_status sort_keys_u64(const uint64_t* keys, int64_t n, int bits, uint64_t* out, cudaStream_t s) {
+  if (n <= 0) return WN_OK;
+  TempSet tmp(s);
+  uint64_t* ka = nullptr;
+  int32_t *va = nullptr, *vo = nullptr;
+  WN_TRY(tmp.alloc(&ka, n));
+  WN_TRY(tmp.alloc(&va, n));
+  WN_TRY(tmp.alloc(&vo, n));
+  WN_CUDA(cudaMemcpyAsync(ka, keys, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, va);
+  count_launches(1);
+  return sort_pairs(ka, va, n, bits, vo, s, out);
+}
+
 wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s) {
   if (n <= 0) return WN_OK;
   uint64_t* ka = nullptr;

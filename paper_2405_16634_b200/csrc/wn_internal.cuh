@@ -191,6 +191,8 @@ void free_tree(wn_tree_s* t);
 // order[k] = index of the k-th of n points along a 3-D Hilbert curve of [−1,1]^3 (query schedule)
 wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s);
 wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s);
+// ascending stable sort of n 64-bit keys on their low `bits` bits into out (device)
+wn_status sort_keys_u64(const uint64_t* keys, int64_t n, int bits, uint64_t* out, cudaStream_t s);
 
 // ---- moments (moments.cu) ----
 // Build node records for attribute `kind` into `out`.  vec: float4 ν (sorted order), scal: float s.
@@ -288,6 +290,12 @@ struct PeerArena {
   int64_t pending_n = 0;                    // local communicators: exported for this N, not yet imported
   unsigned int* done = nullptr;             // local: finished blocks of the running traversal
 };
+
+// ---- fast multipole evaluation (fmm.cu) ----
+// op OP_A: out (sorted or out_map order) = scale·V; OP_G: scale·(−∇V) for dipoles vec; OP_AT: scale·(−∇V)
+// for charges scal; counts: M2L cell pairs, P2P leaf pairs
+wn_status fmm_apply(wn_tree_s* t, int op, const float4* vec, const float* scal, float w, int p, double theta,
+                    int leafsz, const int32_t* out_map, float* out, double scale, int64_t counts[2], cudaStream_t s);
 
 // ---- transpose-mode adjoint (transpose.cu) ----
 // node / point accumulators, allocated once per tree — before any graph capture that uses them

@@ -31,7 +31,7 @@ EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", 
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
             "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work",
             "wn_tree_set_far_order", "wnnc_iterate_emulated", "wn_shard_plan", "wn_tree_schedule",
-            "wn_tree_schedule_stats", "wn_comm_init_local", "wn_comm_arena_export", "wn_comm_arena_import")
+            "wn_tree_schedule_stats", "wn_comm_init_local", "wn_comm_arena_export", "wn_comm_arena_import", "wn_eval_fmm")
 
 
 class wnnc_params(C.Structure):
@@ -68,6 +68,7 @@ _sig = {
     "wn_comm_init_local": ([I32, I32, P], I32),
     "wn_comm_arena_export": ([P, I64, P, P], I32),
     "wn_comm_arena_import": ([P, P], I32),
+    "wn_eval_fmm": ([P, I32, P, F32, I32, F32, I32, P, P, P], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -134,6 +135,20 @@ def wn_work_count_read():
     _check(_L.wn_work_count_read(c))
     return {k: dict(tests=int(c[4 * i]), far=int(c[4 * i + 1]), near=int(c[4 * i + 2]), live=int(c[4 * i + 3]))
             for i, k in enumerate(("A", "AT", "G"))}
+
+
+def wn_eval_fmm(tree: Tree, attr: torch.Tensor, width: float, op: int = 0, p: int = 4, theta_f: float = 0.5,
+                leaf: int = 32, counts: bool = False):
+    """FMM at the sources: op 0 F (attr μ N×3), 2 ∇F (μ), 1 Aᵀ (attr s, N)."""
+    if op == 1:
+        _dev_f32(attr)
+    else:
+        _dev_f32(attr, 3)
+    out = torch.empty((tree.n,) if op == 0 else (tree.n, 3), dtype=torch.float32, device=attr.device)
+    c = (C.c_int64 * 2)()
+    _check(_L.wn_eval_fmm(tree.handle, int(op), _ptr(attr), float(width), int(p), float(theta_f), int(leaf),
+                          _ptr(out), c, _stream()))
+    return (out, (int(c[0]), int(c[1]))) if counts else out
 
 
 def wn_query_work(tree, mu, width, theta=2.0, op=0, q=None):

@@ -1,0 +1,84 @@
+"""GPU FMM against the oracle's FMM (oracle/wn_oracle.c: wo_fmm_op — the same algorithm
+in plain fp64 C, pinned to the dense definition in tests/test_oracle_fmm.py), through the C ABI.
+
+Same cells, same separation test and the same interaction lists (the M2L and P2P pair counts must be equal);
+values per query within max(1e-4·|ref_i|, 2e-6·S_i), S_i = Σ_j |term_ij| of the direct sum; the all-direct
+limit (θ_f → 0) equals the dense definition.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2405_16634_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+INF = float("inf")
+
+
+@pytest.fixture(scope="module")
+def wn():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2405_16634_b200.wn as wn
+
+    return wn
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+CLOUDS = {
+    "sphere3k": lambda: synth.sphere(3000, seed=5)[0],
+    "torus20k": lambda: synth.config("C2", n=20000)["points"],
+    "dups": lambda: np.repeat(synth.sphere(700, seed=8)[0], 3, axis=0),
+}
+OPS = {"F": (0, oracle.OP_A), "AT": (1, oracle.OP_AT), "gradF": (2, oracle.OP_G)}
+
+
+@pytest.mark.parametrize("name", list(CLOUDS))
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("p,leaf", [(4, 32), (2, 8)])
+def test_fmm_matches_oracle(wn, name, op, p, leaf):
+    pts = CLOUDS[name]()
+    n = len(pts)
+    rng = np.random.default_rng(31)
+    code, oop = OPS[op]
+    attr = (rng.standard_normal(n) if op == "AT" else rng.standard_normal((n, 3)) * (4 * np.pi / n)).astype(np.float32)
+    w = float(np.float32(0.004))
+    t = wn.wn_build_tree(_cuda(pts))
+    g, (m2l, p2p) = wn.wn_eval_fmm(t, _cuda(attr), w, op=code, p=p, theta_f=0.5, leaf=leaf, counts=True)
+    cl = oracle.Cloud(pts)
+    ref, cnt = cl.fmm(oop, attr, w, p=p, theta_f=0.5, leaf=leaf, counters=True)
+    assert (m2l, p2p) == (int(cnt[0]), int(cnt[1]))  # the same interaction lists
+    S = cl.abs_scale(oop if op != "AT" else oracle.OP_AT, attr, w, INF)
+    g = g.cpu().numpy().reshape(n, -1).astype(np.float64)
+    ref = np.asarray(ref).reshape(n, -1)
+    err = np.linalg.norm(g - ref, axis=1)
+    lim = np.maximum(1e-4 * np.linalg.norm(ref, axis=1), 2e-6 * np.asarray(S))
+    assert np.all(err <= lim), (np.max(err / lim), int(np.sum(err > lim)))
+
+
+def test_fmm_all_direct_is_dense(wn):
+    pts = CLOUDS["torus20k"]()
+    n = len(pts)
+    rng = np.random.default_rng(32)
+    mu = (rng.standard_normal((n, 3)) * (4 * np.pi / n)).astype(np.float32)
+    w = float(np.float32(0.004))
+    t = wn.wn_build_tree(_cuda(pts))
+    g, (m2l, _) = wn.wn_eval_fmm(t, _cuda(mu), w, op=0, p=2, theta_f=1e-9, counts=True)
+    assert m2l == 0
+    cl = oracle.Cloud(pts)
+    d = cl.F(mu, w, dense=True)
+    S = cl.abs_scale(oracle.OP_A, mu, w, INF)
+    err = np.abs(g.cpu().numpy() - d)
+    assert np.all(err <= np.maximum(1e-4 * np.abs(d), 2e-6 * S))
+
+
+def test_fmm_errors(wn):
+    t = wn.wn_build_tree(_cuda(CLOUDS["sphere3k"]()))
+    mu = torch.zeros(3000, 3, device="cuda")
+    for kw in (dict(p=0), dict(p=7), dict(leaf=0), dict(leaf=33), dict(theta_f=0.0)):
+        with pytest.raises(wn.WnError, match="ARG"):
+            wn.wn_eval_fmm(t, mu, 0.01, **kw)
