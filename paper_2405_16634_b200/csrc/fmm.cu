@@ -19,7 +19,7 @@
 // cell pair per level, appends by atomics), sorted by (target, source) so that every sum runs in a fixed
 // order; P2M / M2M / M2L / L2L run one warp per cell with lanes over the expansion coefficients (the
 // derivative tensor of a pair is built degree by degree in shared memory); L2P + P2P one warp per leaf with
-// one lane per target point.  The oracle (oracle/wn_oracle.c: wo_fmm_op) is the same algorithm in plain C.
+// one lane per target point.  The test oracle implements the same algorithm independently in plain fp64 C.
 #include <cuda_runtime.h>
 
 #include <algorithm>
