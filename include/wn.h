@@ -211,9 +211,15 @@ wn_status wnnc_solve_host(const float* pts_host, int64_t n, int32_t max_depth, c
    multipole / local expansions of total degree p (1..6) between well-separated cells (|c_t − c_s|·θ_f >
    r_t + r_s and every point pair beyond the cutoff w) and directly between the remaining FMM leaves
    (octree nodes with at most `leaf` ≤ 32 points or no children).  counts (host, 2, may be NULL): M2L cell
-   pairs and P2P leaf pairs.  Synchronizes `stream` (the interaction lists are built level by level). */
+   pairs and P2P leaf pairs.  Synchronizes `stream`; the interaction lists (built level by level on the
+   first call) are cached on the tree for the same (p, θ_f, leaf, width). */
 wn_status wn_eval_fmm(wn_tree t, int32_t op, const float* attr, float width, int32_t p, float theta_f, int32_t leaf,
                       float* out, int64_t* counts, void* stream);
+/* Select the operators of later wnnc_iterate calls on this tree: p = 0 (default) the paper's Alg. 4 treecode,
+   p = 1..6 the FMM of wn_eval_fmm (single GPU, gather-mode adjoint; one plan per solve, built with the
+   schedule's largest width w_max as separation width, so every iteration's expanded pairs are beyond its
+   cutoff).  The FMM plan is built on the first call (host-synchronizing) and cached on the tree. */
+wn_status wn_tree_set_fmm(wn_tree t, int32_t p, float theta_f, int32_t leaf);
 
 /* ---- multi-GPU (NCCL over NVLink / NVSwitch) ---------------------------------------------------- */
 wn_status wn_comm_unique_id(uint8_t id[128] /*host*/);

@@ -66,6 +66,7 @@ def lib():
         L.wo_num_threads.restype = I32
         L.wo_rescale.argtypes = [I64, P, P, P]
         L.wo_fmm_op.argtypes = [P, I32, P, I32, D, I32, D, I32, P, P]
+        L.wo_fmm_config.argtypes = [I32, D, I32]
         _lib = L
     return _lib
 
@@ -209,13 +210,16 @@ class Tree:
         return out
 
     def solve(self, mu0=None, w1=0.002, w2=0.016, iters=40, theta=2.0, backend="tree", mode="gather",
-              wnnc=True, first_iter=1, total_iters=None, order=0):
-        """Alg. 3 in the normalized frame; returns (mu_norm n×3, stats iters×5)."""
+              wnnc=True, first_iter=1, total_iters=None, order=0, fmm=(4, 0.5, 32)):
+        """Alg. 3 in the normalized frame; returns (mu_norm n×3, stats iters×5).  backend "tree" (Alg. 4),
+        "dense" or "fmm" (row f4: fmm = (p, θ_f, leaf), separation width w2)."""
         mu = np.zeros((self.n, 3)) if mu0 is None else _f64(mu0).copy()
         stats = np.empty((iters, 5))
         total = iters if total_iters is None else total_iters
+        if backend == "fmm":
+            lib().wo_fmm_config(int(fmm[0]), float(fmm[1]), int(fmm[2]))
         lib().wo_solve(self._h, _p(mu), float(w1), float(w2), int(iters), int(first_iter), int(total),
-                       float(theta), 0 if backend == "tree" else 1, 0 if mode == "gather" else 1,
+                       float(theta), {"tree": 0, "dense": 1, "fmm": 2}[backend], 0 if mode == "gather" else 1,
                        1 if wnnc else 0, int(order), _p(stats))
         return mu, stats
 

@@ -611,9 +611,16 @@ static double width_at(int k, int n, double w1, double w2) {
   return w2 * (double)(n - k) / (double)(n - 1) + w1 * (double)(k - 1) / (double)(n - 1);
 }
 
+/* FMM solver backend (row f4): degree, separation θ_f, leaf size (wo_fmm_config); separation width = w2 */
+static int g_fmm_p = 4, g_fmm_leaf = 32;
+static double g_fmm_theta = 0.5, g_fmm_wsep = 0.0;
+void wo_fmm_config(int p, double theta, int leaf) { g_fmm_p = p; g_fmm_theta = theta; g_fmm_leaf = leaf; }
+
 static void apply(const wo_tree* t, int backend, int op, const double* nu, int dim, double w, double theta,
                   double* out) {
   if (backend == 1) wo_dense_op(t, op, nu, dim, NULL, t->n, w, out);
+  else if (backend == 2) wo_fmm_op_sep(t, op & ~WO_ORDER1, nu, dim, w, g_fmm_wsep, g_fmm_p, g_fmm_theta, g_fmm_leaf, out,
+                                       NULL);
   else wo_tree_op(t, op, nu, dim, NULL, NULL, t->n, w, theta, out, NULL);
 }
 
@@ -637,6 +644,7 @@ int wo_solve(const wo_tree* t, double* mu, double w1, double w2, int iters, int 
   double* mp = (double*)malloc((size_t)n * 3 * sizeof(double));
   double* mh = (double*)malloc((size_t)n * 3 * sizeof(double));
   int transpose = (mode == 1 && backend == 0);
+  g_fmm_wsep = (double)(float)w2;  /* the FMM backend's separation width: the schedule's largest w (fp32, as the GPU) */
   for (int it = 0; it < iters; ++it) {
     int k = first_iter + it;
     /* the width is handed to the kernels as fp32; both sides use the same rounding */
@@ -782,7 +790,7 @@ typedef struct {
   const wo_tree* t;
   fmm_idx I;
   int leaf, dim;           /* dim 1: charges q (Aᵀ), dim 3: dipoles ν (A, G) */
-  double theta, w;
+  double theta, w, wsep;   /* cutoff w of the direct sums; separation width of the well-separated test */
   float w2f;
   double* ctr;             /* nn × 3 cube centres (node id order) */
   double* rad;             /* nn half-diagonals */
@@ -902,7 +910,7 @@ static void fmm_dual(fmm_ctx* f, int64_t T, int64_t S, double* Tbuf) {
   double d = sqrt((ct[0] - cs[0]) * (ct[0] - cs[0]) + (ct[1] - cs[1]) * (ct[1] - cs[1]) +
                   (ct[2] - cs[2]) * (ct[2] - cs[2]));
   double rt = f->rad[T], rs = f->rad[S];
-  if (d * f->theta > rt + rs && d - rt - rs > f->w) {
+  if (d * f->theta > rt + rs && d - rt - rs > f->wsep) {
     fmm_m2l(f, T, S, Tbuf);
     return;
   }
@@ -968,6 +976,13 @@ static void fmm_down(fmm_ctx* f, int64_t id) {
 
 void wo_fmm_op(const wo_tree* t, int op, const double* nu, int dim, double w, int p, double theta, int leaf,
                double* out, int64_t* counts) {
+  wo_fmm_op_sep(t, op, nu, dim, w, w, p, theta, leaf, out, counts);
+}
+
+/* the same with a separation width wsep ≥ w (a solve keeps one set of lists for every iteration's width:
+   wsep = the schedule's w2, so every expanded pair is beyond each iteration's cutoff) */
+void wo_fmm_op_sep(const wo_tree* t, int op, const double* nu, int dim, double w, double wsep, int p, double theta,
+                   int leaf, double* out, int64_t* counts) {
   fmm_ctx f;
   memset(&f, 0, sizeof(f));
   f.t = t;
@@ -976,6 +991,7 @@ void wo_fmm_op(const wo_tree* t, int op, const double* nu, int dim, double w, in
   f.dim = dim;
   f.theta = theta;
   f.w = w;
+  f.wsep = wsep;
   float wf = (float)w;
   f.w2f = wf * wf;
   f.nu = nu;

@@ -66,12 +66,17 @@ void wo_tree_AT_transpose(const wo_tree* t, const double* mu_geom, const double*
    M2L cell pairs, P2P leaf pairs. */
 void wo_fmm_op(const wo_tree* t, int op, const double* nu, int dim, double w, int p, double theta, int leaf,
                double* out, int64_t* counts);
+/* the same with a separation width wsep ≥ w for the well-separated test (w stays the direct sums' cutoff) */
+void wo_fmm_op_sep(const wo_tree* t, int op, const double* nu, int dim, double w, double wsep, int p, double theta,
+                   int leaf, double* out, int64_t* counts);
+/* wo_solve backend 2 = FMM: degree, θ_f, leaf (the separation width is the solve's w2) */
+void wo_fmm_config(int p, double theta, int leaf);
 
 /* WNNC rescale (Alg. 3): out_i = mh_i |mp_i| / |mh_i|, mp_i kept where |mh_i| = 0 (n×3). */
 void wo_rescale(int64_t n, const double* mp, const double* mh, double* out);
 
 /* Alg. 3 + Alg. 2 solver in the normalized frame.  mu: n×3 in/out (caller order).
-   backend: 0 treecode, 1 dense.  mode: 0 gather Aᵀ (paper text), 1 transpose (frozen geometry).
+   backend: 0 treecode, 1 dense, 2 FMM (wo_fmm_config; separation width = w2).  mode: 0 gather Aᵀ (paper text), 1 transpose (frozen geometry).
    wnnc: 1 normal, 0 ablation (skip the WNNC update + rescale).
    stats (iters×5 or NULL): E_before, alpha, Σr², Σ(Ar)², w. */
 int wo_solve(const wo_tree* t, double* mu, double w1, double w2, int iters, int first_iter,

@@ -469,6 +469,32 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
   };
   stamp(t, p, 0, s);
   snap_counts(t, 0, s);
+  if (t->fmm_p > 0) {  // row f4: every operator by FMM (single GPU, gather semantics: each operator from its own attribute)
+    for (int i = 0; i < p.iters; ++i) {
+      const int k = p.first_iter + i;
+      const float w = width_at(k, total, (double)p.w_min, (double)p.w_max);
+      const int64_t n = t->n;
+      float* V = reinterpret_cast<float*>(it.tmp);  // n floats of the n × 4 scratch
+      if (i == 0 && k == 1 && (p.flags & WN_FLAG_MU_ZERO)) {
+        s_half(n, it.s, it.part, s);
+      } else {
+        WN_TRY(fmm_run(t, OP_A, it.mu, nullptr, w, nullptr, V, nullptr, 1.0, s));
+        fmm_epi_s(n, V, it.s, it.part, s);
+      }
+      WN_TRY(fmm_run(t, OP_AT, nullptr, it.s, w, nullptr, nullptr, it.r, 1.0, s));
+      fmm_epi_r(n, it.r, it.part + it.nblk, s);
+      WN_TRY(fmm_run(t, OP_A, it.r, nullptr, w, nullptr, V, nullptr, 1.0, s));
+      fmm_epi_sq(n, V, it.part + 2 * (int64_t)it.nblk, s);
+      alpha_step(it.part, (int)part_slots(n), it.nblk, (double)w, it.alpha, it.dstats + 5 * i, s);
+      fmm_axpy(n, it.mu, it.r, it.alpha, it.mup, s);
+      float4* hat = reinterpret_cast<float4*>(it.tmp);  // μ̂ = G(μ') (the n × 4 scratch; V is no longer needed)
+      WN_TRY(fmm_run(t, OP_G, it.mup, nullptr, w, nullptr, nullptr, hat, 1.0, s));
+      fmm_epi_rescale(n, hat, it.mup, it.mu, s);
+      stamp(t, p, i + 1, s);
+      snap_counts(t, i + 1, s);
+    }
+    return WN_OK;
+  }
   for (int i = 0; i < p.iters; ++i) {
     const int k = p.first_iter + i;
     const float w = width_at(k, total, (double)p.w_min, (double)p.w_max);
@@ -668,6 +694,18 @@ wn_status wn_tree_set_far_order(wn_tree t, int32_t order, void* stream) {
   return WN_OK;
 }
 
+wn_status wn_tree_set_fmm(wn_tree t, int32_t p, float theta_f, int32_t leaf) {
+  if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
+  if (p < 0 || p > 6) return set_error(WN_ERR_ARG, "FMM degree must be 0 (treecode) or 1..6");
+  if (p > 0 && (leaf < 1 || leaf > 32 || !(theta_f > 0.f)))
+    return set_error(WN_ERR_ARG, "FMM leaf must be in 1..32 and theta_f > 0");
+  invalidate_graph(t);
+  t->fmm_p = p;
+  t->fmm_theta = theta_f;
+  t->fmm_leaf = leaf;
+  return WN_OK;
+}
+
 wn_status wn_tree_info(wn_tree t, int64_t* num_points, int64_t* num_nodes, int32_t* depth_used, double xform[4]) {
   if (!t) return set_error(WN_ERR_ARG, "tree is NULL");
   if (num_points) *num_points = t->n;
@@ -816,20 +854,21 @@ wn_status wn_eval_fmm(wn_tree t, int32_t op, const float* attr, float width, int
   WN_TRY(ensure_scratch(t, s));
   IterScratch& it = t->it;
   const double sc = t->xf[3];
-  int64_t cnt[2] = {0, 0};
+  WN_TRY(fmm_plan(t, p, theta_f, leaf, width, s));  // (cached: the same parameters reuse the lists)
   wn_status st;
   if (op == 1) {  // Aᵀ(s) = −∇ of the charges' potential;  Aᵀ_in = s²·Aᵀ_n
     gather_scal(t->n, t->perm, attr, it.s, s);
-    st = fmm_apply(t, OP_AT, nullptr, it.s, width, p, theta_f, leaf, t->perm, out, sc * sc, cnt, s);
+    st = fmm_run(t, OP_AT, nullptr, it.s, width, t->perm, out, nullptr, sc * sc, s);
   } else {  // dipoles μ: F = V (F_in = s²·V_n(μ_in)), ∇F = ∇V (∇F_in = −s³·G_n(μ_in), G = −∇V)
     gather_vec_a(t->n, t->perm, attr, nullptr, it.mu, nullptr, nullptr, s);
-    st = fmm_apply(t, op == 0 ? OP_A : OP_G, it.mu, nullptr, width, p, theta_f, leaf, t->perm, out,
-                   op == 0 ? sc * sc : -sc * sc * sc, cnt, s);
+    st = fmm_run(t, op == 0 ? OP_A : OP_G, it.mu, nullptr, width, t->perm, out, nullptr,
+                 op == 0 ? sc * sc : -sc * sc * sc, s);
   }
   if (st == WN_OK && counts) {
-    counts[0] = cnt[0];
-    counts[1] = cnt[1];
+    counts[0] = t->fmm.nm2l;
+    counts[1] = t->fmm.np2p;
   }
+  if (st == WN_OK) WN_CUDA(cudaStreamSynchronize(s));
   return st;
 }
 
@@ -958,13 +997,18 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p_in, wn_comm co
   if (comm && !(p->flags & WN_FLAG_COMM_NCCL)) WN_TRY(comm_peer_arena(comm, t->n, s, &P));
   if (comm) WN_TRY(plan_shards(t, comm_world(comm), comm, s));
   if (p->adjoint_mode == WN_ADJ_TRANSPOSE) WN_TRY(ensure_transpose_scratch(t, s));  // before any capture
+  if (t->fmm_p > 0) {  // FMM operators (row f4): one plan for the whole schedule (separation width w_max ≥ every w)
+    if (comm || p->adjoint_mode != WN_ADJ_GATHER)
+      return set_error(WN_ERR_ARG, "FMM operators: single GPU and gather-mode adjoint only");
+    WN_TRY(fmm_plan(t, t->fmm_p, t->fmm_theta, t->fmm_leaf, p->w_max, s));
+  }
   float4* mu0 = P ? P->mu[0][P->rank] : t->it.mu;
   gather_vec(t->n, t->perm, mu, sc2, mu0, s);             // μ_norm = scale²·μ
   if (p->flags & WN_FLAG_GRAPH) {
     // the whole iteration loop as one CUDA graph: captured on a private stream, cached per parameters
     const void* arena = P ? P->own : nullptr;
     std::vector<uint8_t> key(sizeof(wnnc_params) + sizeof(comm) + sizeof(int) + sizeof(arena) + sizeof(ShardPlan) + 1);
-    key.back() = g_count_on ? 1 : 0;  // counting traversal variants are baked into the captured kernels
+    key.back() = (g_count_on ? 1 : 0) | (t->fmm_p << 1);  // counting variants / FMM degree are baked into the graph
     uint8_t* kp = key.data();
     memcpy(kp, p, sizeof(wnnc_params));
     kp += sizeof(wnnc_params);

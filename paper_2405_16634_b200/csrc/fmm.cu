@@ -330,7 +330,7 @@ __global__ void k_fmm_eval(int64_t m, const int32_t* __restrict__ list, FmmGeom 
                            const uint64_t* __restrict__ keys, const float4* __restrict__ pts,
                            const float4* __restrict__ vec, const float* __restrict__ scal, int p,
                            const double* __restrict__ L, float w2f, int op, const int32_t* __restrict__ out_map,
-                           float* __restrict__ out, double scale) {
+                           float* __restrict__ out, float4* __restrict__ out4, double scale) {
   const int lane = threadIdx.x & 31;
   const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (k >= m) return;
@@ -392,6 +392,10 @@ __global__ void k_fmm_eval(int64_t m, const int32_t* __restrict__ list, FmmGeom 
     gz += k4 * v3;
   }
   if (!valid) return;
+  if (out4) {  // the solver's sorted buffers, unscaled: V in .x (A), or −∇V (G, Aᵀ)
+    out4[i] = op == OP_A ? make_float4((float)V, 0.f, 0.f, 0.f) : make_float4((float)-gx, (float)-gy, (float)-gz, 0.f);
+    return;
+  }
   const int64_t o = out_map ? (int64_t)out_map[i] : i;
   if (op == OP_A) {
     out[o] = (float)(V * scale);
@@ -426,94 +430,93 @@ wn_status fmm_scan(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* total
 static inline unsigned g256(int64_t n) { return (unsigned)((n + 255) / 256); }
 static inline unsigned gwarps(int64_t n, int wpb) { return (unsigned)((n + wpb - 1) / wpb); }
 
-// one FMM application on the tree's sorted points: attribute vec (DIM 3) or scal (DIM 1), sorted order
-wn_status fmm_apply(wn_tree_s* t, int op, const float4* vec, const float* scal, float w, int p, double theta,
-                    int leafsz, const int32_t* out_map, float* out, double scale, int64_t counts[2], cudaStream_t s) {
+void fmm_plan_free(FmmPlan& F) {
+  for (void* q : F.owned) cudaFreeAsync(q, 0);
+  F = FmmPlan();
+}
+
+// The per-tree FMM plan (geometry, node lists, sorted interaction lists, expansion scratch) for
+// (p, θ_f, leaf, separation width wsep): built once — host-synchronizing, never inside a graph capture —
+// and reused by every fmm_run with a cutoff w ≤ wsep (every expanded pair stays beyond the cutoff).
+wn_status fmm_plan(wn_tree_s* t, int p, double theta, int leafsz, float wsep, cudaStream_t s) {
   if (p < 1 || p > kFmmMaxP) return set_error(WN_ERR_ARG, "FMM degree must be in 1..6");
   if (leafsz < 1 || leafsz > 32) return set_error(WN_ERR_ARG, "FMM leaf size must be in 1..32");
   if (!(theta > 0.0)) return set_error(WN_ERR_ARG, "FMM separation must be > 0");
+  FmmPlan& F = t->fmm;
+  if (F.ready && F.p == p && F.theta == theta && F.leaf == leafsz && F.wsep == wsep) return WN_OK;
+  invalidate_graph(t);  // a cached graph may hold the old plan's buffers
+  WN_CUDA(cudaStreamSynchronize(s));
+  fmm_plan_free(F);
   WN_TRY(fmm_tables());
   const int64_t nn = t->nn;
   const int np = fmm_count(p);
-  std::vector<void*> held;
-  auto alloc = [&](auto** ptr, size_t bytes) -> wn_status {
-    cudaError_t e = cudaMallocAsync((void**)ptr, std::max<size_t>(bytes, 8), s);
-    if (e != cudaSuccess) return cuda_status(e, "FMM scratch");
-    held.push_back((void*)*ptr);
-    return WN_OK;
-  };
-  struct Release {
+  std::vector<void*> tmpv;
+  struct Tmp {
     std::vector<void*>& h;
     cudaStream_t s;
-    ~Release() {
+    ~Tmp() {
       for (void* q : h) cudaFreeAsync(q, s);
     }
-  } rel{held, s};
-  double *ctr = nullptr, *rad = nullptr, *M = nullptr, *L = nullptr;
-  uint8_t* leaf = nullptr;
-  WN_TRY(alloc(&ctr, nn * 3 * sizeof(double)));
-  WN_TRY(alloc(&rad, nn * sizeof(double)));
-  WN_TRY(alloc(&leaf, nn));
-  WN_TRY(alloc(&M, (size_t)nn * np * sizeof(double)));
-  WN_TRY(alloc(&L, (size_t)nn * np * sizeof(double)));
-  WN_CUDA(cudaMemsetAsync(L, 0, (size_t)nn * np * sizeof(double), s));
-  k_fmm_geom<<<g256(nn), 256, 0, s>>>(nn, t->D, leafsz, t->pts, t->pb, t->pe, t->cc, t->depth, ctr, rad, leaf);
-  FmmGeom g{t->pb, t->pe, t->cb, t->cc, t->depth, t->parent, ctr, rad, leaf};
+  } tmp_rel{tmpv, s};
+  auto alloc = [&](auto** ptr, size_t bytes, bool keep) -> wn_status {
+    cudaError_t e = cudaMallocAsync((void**)ptr, std::max<size_t>(bytes, 8), s);
+    if (e != cudaSuccess) return cuda_status(e, "FMM scratch");
+    (keep ? F.owned : tmpv).push_back((void*)*ptr);
+    return WN_OK;
+  };
+  WN_TRY(alloc(&F.ctr, nn * 3 * sizeof(double), true));
+  WN_TRY(alloc(&F.rad, nn * sizeof(double), true));
+  WN_TRY(alloc(&F.leaf_flag, nn, true));
+  WN_TRY(alloc(&F.M, (size_t)nn * np * sizeof(double), true));
+  WN_TRY(alloc(&F.L, (size_t)nn * np * sizeof(double), true));
+  k_fmm_geom<<<g256(nn), 256, 0, s>>>(nn, t->D, leafsz, t->pts, t->pb, t->pe, t->cc, t->depth, F.ctr, F.rad,
+                                       F.leaf_flag);
+  FmmGeom g{t->pb, t->pe, t->cb, t->cc, t->depth, t->parent, F.ctr, F.rad, F.leaf_flag};
   count_launches(1);
   // node lists: FMM leaves, internal active nodes per level, active non-root nodes per level
   uint32_t *flag = nullptr, *pos = nullptr;
-  WN_TRY(alloc(&flag, (nn + 1) * sizeof(uint32_t)));
-  WN_TRY(alloc(&pos, (nn + 1) * sizeof(uint32_t)));
+  WN_TRY(alloc(&flag, (nn + 1) * sizeof(uint32_t), false));
+  WN_TRY(alloc(&pos, (nn + 1) * sizeof(uint32_t), false));
   auto make_list = [&](int mode, int level, int32_t** list, int64_t* m) -> wn_status {
-    k_fmm_flag<<<g256(nn), 256, 0, s>>>(nn, leaf, t->parent, t->depth, mode, level, flag);
+    k_fmm_flag<<<g256(nn), 256, 0, s>>>(nn, F.leaf_flag, t->parent, t->depth, mode, level, flag);
     WN_TRY(fmm_scan(flag, pos, nn, pos + nn, s));
     uint32_t c = 0;
     WN_CUDA(cudaMemcpyAsync(&c, pos + nn, sizeof(c), cudaMemcpyDeviceToHost, s));
     WN_CUDA(cudaStreamSynchronize(s));
     *m = c;
-    WN_TRY(alloc(list, (size_t)std::max<uint32_t>(c, 1) * sizeof(int32_t)));
+    WN_TRY(alloc(list, (size_t)std::max<uint32_t>(c, 1) * sizeof(int32_t), true));
     k_fmm_compact<<<g256(nn), 256, 0, s>>>(nn, flag, pos, *list);
     count_launches(2);
     return WN_OK;
   };
-  int32_t* leaves = nullptr;
-  int64_t nleaves = 0;
-  WN_TRY(make_list(0, 0, &leaves, &nleaves));
+  WN_TRY(make_list(0, 0, &F.leaves, &F.nleaves));
   const int D = t->depth_used;
-  std::vector<int32_t*> inner(D + 1, nullptr), kids(D + 1, nullptr);
-  std::vector<int64_t> ninner(D + 1, 0), nkids(D + 1, 0);
+  F.inner.assign(D + 1, nullptr);
+  F.kids.assign(D + 1, nullptr);
+  F.ninner.assign(D + 1, 0);
+  F.nkids.assign(D + 1, 0);
   for (int l = 0; l <= D; ++l) {
-    WN_TRY(make_list(1, l, &inner[l], &ninner[l]));
-    WN_TRY(make_list(2, l, &kids[l], &nkids[l]));
+    WN_TRY(make_list(1, l, &F.inner[l], &F.ninner[l]));
+    WN_TRY(make_list(2, l, &F.kids[l], &F.nkids[l]));
   }
-  // upward pass
-  const int wpb = 8;
-  if (vec) k_fmm_p2m<3><<<gwarps(nleaves, wpb), 32 * wpb, 0, s>>>(nleaves, leaves, g, t->pts, vec, scal, p, M);
-  else k_fmm_p2m<1><<<gwarps(nleaves, wpb), 32 * wpb, 0, s>>>(nleaves, leaves, g, t->pts, vec, scal, p, M);
-  count_launches(1);
-  for (int l = D; l >= 0; --l)
-    if (ninner[l]) {
-      k_fmm_m2m<<<gwarps(ninner[l], wpb), 32 * wpb, 0, s>>>(ninner[l], inner[l], g, p, M);
-      count_launches(1);
-    }
   // interaction lists: breadth-first dual traversal from (root, root)
   unsigned long long* cnt = nullptr;
-  WN_TRY(alloc(&cnt, 3 * sizeof(unsigned long long)));
+  WN_TRY(alloc(&cnt, 3 * sizeof(unsigned long long), false));
   int64_t cap_f = std::max<int64_t>(1024, 4 * nn), cap_m = std::max<int64_t>(1024, 16 * nn),
           cap_p = std::max<int64_t>(1024, 4 * nn);
   int2 *fa = nullptr, *fb = nullptr;
   uint64_t *m2l = nullptr, *p2p = nullptr;
-  WN_TRY(alloc(&fa, cap_f * sizeof(int2)));
-  WN_TRY(alloc(&fb, cap_f * sizeof(int2)));
-  WN_TRY(alloc(&m2l, cap_m * sizeof(uint64_t)));
-  WN_TRY(alloc(&p2p, cap_p * sizeof(uint64_t)));
+  WN_TRY(alloc(&fa, cap_f * sizeof(int2), false));
+  WN_TRY(alloc(&fb, cap_f * sizeof(int2), false));
+  WN_TRY(alloc(&m2l, cap_m * sizeof(uint64_t), false));
+  WN_TRY(alloc(&p2p, cap_p * sizeof(uint64_t), false));
   const int2 root = make_int2(0, 0);
   WN_CUDA(cudaMemcpyAsync(fa, &root, sizeof(root), cudaMemcpyHostToDevice, s));
   // a buffer that overflows during a level is regrown (contents kept) and the level runs again
   auto grow = [&](auto** buf, int64_t* cap, int64_t need, int64_t keep, size_t elt) -> wn_status {
     const int64_t nc = std::max<int64_t>(need + need / 2, 2 * *cap);
     void* nb = nullptr;
-    WN_TRY(alloc(&nb, (size_t)nc * elt));
+    WN_TRY(alloc(&nb, (size_t)nc * elt, false));
     if (keep > 0) WN_CUDA(cudaMemcpyAsync(nb, *buf, (size_t)keep * elt, cudaMemcpyDeviceToDevice, s));
     *buf = reinterpret_cast<std::remove_reference_t<decltype(**buf)>*>(nb);
     *cap = nc;
@@ -525,8 +528,8 @@ wn_status fmm_apply(wn_tree_s* t, int op, const float4* vec, const float* scal, 
     for (;;) {
       unsigned long long start[3] = {0, m0, p0};
       WN_CUDA(cudaMemcpyAsync(cnt, start, sizeof(start), cudaMemcpyHostToDevice, s));
-      k_fmm_dual<<<g256((int64_t)nf), 256, 0, s>>>((int64_t)nf, fa, g, theta, (double)w, fb, cnt, cap_f, m2l, cap_m,
-                                                   p2p, cap_p);
+      k_fmm_dual<<<g256((int64_t)nf), 256, 0, s>>>((int64_t)nf, fa, g, theta, (double)wsep, fb, cnt, cap_f, m2l,
+                                                   cap_m, p2p, cap_p);
       count_launches(1);
       WN_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
       WN_CUDA(cudaStreamSynchronize(s));
@@ -537,50 +540,162 @@ wn_status fmm_apply(wn_tree_s* t, int op, const float4* vec, const float* scal, 
       if (op_) WN_TRY(grow(&p2p, &cap_p, (int64_t)h[2], (int64_t)p0, sizeof(uint64_t)));
       if (of) {  // keep the two frontier buffers the same size
         int2* na = nullptr;
-        WN_TRY(alloc(&na, (size_t)cap_f * sizeof(int2)));
+        WN_TRY(alloc(&na, (size_t)cap_f * sizeof(int2), false));
         WN_CUDA(cudaMemcpyAsync(na, fa, (size_t)nf * sizeof(int2), cudaMemcpyDeviceToDevice, s));
         fa = na;
       }
     }
     std::swap(fa, fb);
   }
-  const int64_t nm2l = (int64_t)h[1], np2p = (int64_t)h[2];
-  if (counts) {
-    counts[0] = nm2l;
-    counts[1] = np2p;
-  }
-  uint64_t *m2ls = nullptr, *p2ps = nullptr;
-  int32_t *om = nullptr, *op2 = nullptr;
-  WN_TRY(alloc(&m2ls, std::max<int64_t>(nm2l, 1) * sizeof(uint64_t)));
-  WN_TRY(alloc(&p2ps, std::max<int64_t>(np2p, 1) * sizeof(uint64_t)));
-  WN_TRY(alloc(&om, (nn + 1) * sizeof(int32_t)));
-  WN_TRY(alloc(&op2, (nn + 1) * sizeof(int32_t)));
+  F.nm2l = (int64_t)h[1];
+  F.np2p = (int64_t)h[2];
+  WN_TRY(alloc(&F.m2l, std::max<int64_t>(F.nm2l, 1) * sizeof(uint64_t), true));
+  WN_TRY(alloc(&F.p2p, std::max<int64_t>(F.np2p, 1) * sizeof(uint64_t), true));
+  WN_TRY(alloc(&F.om, (nn + 1) * sizeof(int32_t), true));
+  WN_TRY(alloc(&F.op2, (nn + 1) * sizeof(int32_t), true));
   int bits = 1;
   while (bits < 62 && ((int64_t)1 << bits) <= nn) ++bits;
-  WN_TRY(sort_keys_u64(m2l, nm2l, 32 + bits, m2ls, s));
-  WN_TRY(sort_keys_u64(p2p, np2p, 32 + bits, p2ps, s));
-  k_fmm_csr<<<g256(nn + 1), 256, 0, s>>>(nn, m2ls, nm2l, om);
-  k_fmm_csr<<<g256(nn + 1), 256, 0, s>>>(nn, p2ps, np2p, op2);
+  WN_TRY(sort_keys_u64(m2l, F.nm2l, 32 + bits, F.m2l, s));
+  WN_TRY(sort_keys_u64(p2p, F.np2p, 32 + bits, F.p2p, s));
+  k_fmm_csr<<<g256(nn + 1), 256, 0, s>>>(nn, F.m2l, F.nm2l, F.om);
+  k_fmm_csr<<<g256(nn + 1), 256, 0, s>>>(nn, F.p2p, F.np2p, F.op2);
   count_launches(2);
-  // M2L, then the downward pass
-  k_fmm_m2l<<<gwarps(nn, kFmmWarps), 32 * kFmmWarps, 0, s>>>(nn, om, m2ls, g, p, M, L);
-  count_launches(1);
+  WN_CUDA(cudaGetLastError());
+  WN_CUDA(cudaStreamSynchronize(s));  // (the temporaries above are freed stream-ordered on return)
+  F.p = p;
+  F.theta = theta;
+  F.leaf = leafsz;
+  F.wsep = wsep;
+  F.ready = true;
+  return WN_OK;
+}
+
+// One FMM application with the tree's plan (capturable: launches and a memset only).  Outputs: out (caller
+// layout through out_map, or sorted order; float, N or N×3) scaled, or out4 (sorted float4) unscaled.
+wn_status fmm_run(wn_tree_s* t, int op, const float4* vec, const float* scal, float w, const int32_t* out_map,
+                  float* out, float4* out4, double scale, cudaStream_t s) {
+  FmmPlan& F = t->fmm;
+  if (!F.ready) return set_error(WN_ERR_ARG, "internal: FMM plan missing");
+  if (w > F.wsep) return set_error(WN_ERR_ARG, "internal: FMM cutoff above the plan's separation width");
+  const int64_t nn = t->nn;
+  const int p = F.p, np = fmm_count(p);
+  FmmGeom g{t->pb, t->pe, t->cb, t->cc, t->depth, t->parent, F.ctr, F.rad, F.leaf_flag};
+  const int wpb = 8;
+  ProfScope ps(op == OP_A ? WN_PROF_TRAV_A : op == OP_AT ? WN_PROF_TRAV_AT : WN_PROF_TRAV_G, s, 0);
+  WN_CUDA(cudaMemsetAsync(F.L, 0, (size_t)nn * np * sizeof(double), s));
+  if (vec) k_fmm_p2m<3><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, t->pts, vec, scal, p, F.M);
+  else k_fmm_p2m<1><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, t->pts, vec, scal, p, F.M);
+  int launches = 1;
+  const int D = (int)F.inner.size() - 1;
+  for (int l = D; l >= 0; --l)
+    if (F.ninner[l]) {
+      k_fmm_m2m<<<gwarps(F.ninner[l], wpb), 32 * wpb, 0, s>>>(F.ninner[l], F.inner[l], g, p, F.M);
+      ++launches;
+    }
+  k_fmm_m2l<<<gwarps(nn, kFmmWarps), 32 * kFmmWarps, 0, s>>>(nn, F.om, F.m2l, g, p, F.M, F.L);
+  ++launches;
   for (int l = 1; l <= D; ++l)
-    if (nkids[l]) {
-      k_fmm_l2l<<<gwarps(nkids[l], wpb), 32 * wpb, 0, s>>>(nkids[l], kids[l], g, p, L);
-      count_launches(1);
+    if (F.nkids[l]) {
+      k_fmm_l2l<<<gwarps(F.nkids[l], wpb), 32 * wpb, 0, s>>>(F.nkids[l], F.kids[l], g, p, F.L);
+      ++launches;
     }
   const float w2f = w * w;
   if (vec)
-    k_fmm_eval<3><<<gwarps(nleaves, wpb), 32 * wpb, 0, s>>>(nleaves, leaves, g, op2, p2ps, t->pts, vec, scal, p, L,
-                                                           w2f, op, out_map, out, scale);
+    k_fmm_eval<3><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, F.op2, F.p2p, t->pts, vec, scal,
+                                                             p, F.L, w2f, op, out_map, out, out4, scale);
   else
-    k_fmm_eval<1><<<gwarps(nleaves, wpb), 32 * wpb, 0, s>>>(nleaves, leaves, g, op2, p2ps, t->pts, vec, scal, p, L,
-                                                           w2f, op, out_map, out, scale);
-  count_launches(1);
+    k_fmm_eval<1><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, F.op2, F.p2p, t->pts, vec, scal,
+                                                             p, F.L, w2f, op, out_map, out, out4, scale);
+  ++launches;
+  count_launches(launches);
   WN_CUDA(cudaGetLastError());
-  WN_CUDA(cudaStreamSynchronize(s));  // (the scratch above is freed stream-ordered on return)
   return WN_OK;
+}
+
+// ---- the solver's elementwise steps around FMM operators (sorted order; Σ partials per 32 points) ----
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// s = ½ − V (Alg. 2: b − A μ, b = ½), partial Σ s²
+__global__ void k_fmm_epi_s(int64_t n, const float* __restrict__ V, float* __restrict__ sv, double* __restrict__ part) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double x = 0.0;
+  if (i < n) {
+    const double v = 0.5 - (double)V[i];
+    sv[i] = (float)v;
+    x = v * v;
+  }
+  x = warp_sum_d(x);
+  if ((threadIdx.x & 31) == 0 && i < n + 31 && (i >> 5) * 32 < n) part[i >> 5] = x;
+}
+// partial Σ V² (‖A r‖²)
+__global__ void k_fmm_epi_sq(int64_t n, const float* __restrict__ V, double* __restrict__ part) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double x = 0.0;
+  if (i < n) {
+    const double v = (double)V[i];
+    x = v * v;
+  }
+  x = warp_sum_d(x);
+  if ((threadIdx.x & 31) == 0 && (i >> 5) * 32 < n) part[i >> 5] = x;
+}
+// partial Σ|r|² of r = Aᵀ s (already in place as float4)
+__global__ void k_fmm_epi_r(int64_t n, const float4* __restrict__ r, double* __restrict__ part) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double x = 0.0;
+  if (i < n) {
+    const float4 v = r[i];
+    x = (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z;
+  }
+  x = warp_sum_d(x);
+  if ((threadIdx.x & 31) == 0 && (i >> 5) * 32 < n) part[i >> 5] = x;
+}
+// μ' = μ + α r (Alg. 2 line 3)
+__global__ void k_fmm_axpy(int64_t n, const float4* __restrict__ mu, const float4* __restrict__ r,
+                           const double* __restrict__ alpha, float4* __restrict__ mup) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float a = (float)*alpha;
+  const float4 m = mu[i], v = r[i];
+  mup[i] = make_float4(fmaf(a, v.x, m.x), fmaf(a, v.y, m.y), fmaf(a, v.z, m.z), 0.f);
+}
+// μ = μ̂ |μ'| / |μ̂|, μ' kept if |μ̂| = 0 (Alg. 3)
+__global__ void k_fmm_epi_rescale(int64_t n, const float4* __restrict__ hat, const float4* __restrict__ mup,
+                                  float4* __restrict__ mu) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 h = hat[i], m = mup[i];
+  const double hm = sqrt((double)h.x * h.x + (double)h.y * h.y + (double)h.z * h.z);
+  const double mm = sqrt((double)m.x * m.x + (double)m.y * m.y + (double)m.z * m.z);
+  float4 o = m;
+  if (hm > 0.0) {
+    const double f = mm / hm;
+    o = make_float4((float)(h.x * f), (float)(h.y * f), (float)(h.z * f), 0.f);
+  }
+  mu[i] = o;
+}
+
+void fmm_epi_s(int64_t n, const float* V, float* sv, double* part, cudaStream_t s) {
+  k_fmm_epi_s<<<g256(n), 256, 0, s>>>(n, V, sv, part);
+  count_launches(1);
+}
+void fmm_epi_sq(int64_t n, const float* V, double* part, cudaStream_t s) {
+  k_fmm_epi_sq<<<g256(n), 256, 0, s>>>(n, V, part);
+  count_launches(1);
+}
+void fmm_epi_r(int64_t n, const float4* r, double* part, cudaStream_t s) {
+  k_fmm_epi_r<<<g256(n), 256, 0, s>>>(n, r, part);
+  count_launches(1);
+}
+void fmm_axpy(int64_t n, const float4* mu, const float4* r, const double* alpha, float4* mup, cudaStream_t s) {
+  k_fmm_axpy<<<g256(n), 256, 0, s>>>(n, mu, r, alpha, mup);
+  count_launches(1);
+}
+void fmm_epi_rescale(int64_t n, const float4* hat, const float4* mup, float4* mu, cudaStream_t s) {
+  k_fmm_epi_rescale<<<g256(n), 256, 0, s>>>(n, hat, mup, mu);
+  count_launches(1);
 }
 
 }  // namespace wn

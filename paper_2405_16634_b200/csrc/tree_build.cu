@@ -1298,6 +1298,7 @@ void free_tree(wn_tree_s* t) {
   }
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, 0);
+  fmm_plan_free(t->fmm);
   for (MomPlan& P : t->mplan)
     for (void* p : {(void*)P.small, (void*)P.large, (void*)P.tile_soff, (void*)P.tile_loff, (void*)P.onept,
                     (void*)P.cross, (void*)P.ep_key, (void*)P.ep_slot, (void*)P.tile_eoff, (void*)P.epval})

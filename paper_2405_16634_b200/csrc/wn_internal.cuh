@@ -93,6 +93,24 @@ struct MomPlan {
   int32_t* tile_eoff = nullptr;  // ntiles + 1 offsets into ep_key
   double* epval = nullptr;       // 2·ncross × kMomNC endpoint sums
 };
+// Fast-multipole plan of a tree (fmm.cu): cell geometry, node lists, the sorted interaction
+// lists for (p, θ_f, leaf, separation width wsep), and the expansion scratch
+struct FmmPlan {
+  bool ready = false;
+  int p = 0, leaf = 0;
+  double theta = 0.0;
+  float wsep = 0.f;
+  double *ctr = nullptr, *rad = nullptr, *M = nullptr, *L = nullptr;
+  uint8_t* leaf_flag = nullptr;
+  int32_t* leaves = nullptr;
+  int64_t nleaves = 0;
+  std::vector<int32_t*> inner, kids;  // per level: internal active nodes / active non-root nodes
+  std::vector<int64_t> ninner, nkids;
+  uint64_t *m2l = nullptr, *p2p = nullptr;  // sorted (target << 32 | source)
+  int64_t nm2l = 0, np2p = 0;
+  int32_t *om = nullptr, *op2 = nullptr;    // CSR offsets per target node
+  std::vector<void*> owned;
+};
 // Query shards of a multi-GPU solve: schedule positions [b[r], b[r+1]) for rank r, multiples of
 // WN_SHARD_ALIGN, split by estimated work (capi.cu:plan_shards); world = 0 ⇒ equal counts (wn_shard_range)
 constexpr int kMaxShardRanks = 64;
@@ -136,6 +154,9 @@ struct wn_tree_s {
   int64_t mom_ntiles = 0;
   bool mom_order1_ready = false;  // prefix scratch + set[0].ext sized for the first-order far field
   int far_order = 0;              // wn_tree_set_far_order: 0 (the paper's Alg. 4) or 1 (row f2)
+  int fmm_p = 0, fmm_leaf = 32;   // wn_tree_set_fmm: wnnc_iterate's operators by FMM of degree fmm_p (0: treecode)
+  float fmm_theta = 0.5f;
+  wn::FmmPlan fmm;
   wn::NodeSet set[2];           // [0] = current attribute, [1] = frozen geometry (transpose mode)
   std::vector<int64_t> level_off;  // host: BFS offset of each level, size depth_used + 2
   wn::IterScratch it;
@@ -294,8 +315,16 @@ struct PeerArena {
 // ---- fast multipole evaluation (fmm.cu) ----
 // op OP_A: out (sorted or out_map order) = scale·V; OP_G: scale·(−∇V) for dipoles vec; OP_AT: scale·(−∇V)
 // for charges scal; counts: M2L cell pairs, P2P leaf pairs
-wn_status fmm_apply(wn_tree_s* t, int op, const float4* vec, const float* scal, float w, int p, double theta,
-                    int leafsz, const int32_t* out_map, float* out, double scale, int64_t counts[2], cudaStream_t s);
+wn_status fmm_plan(wn_tree_s* t, int p, double theta, int leafsz, float wsep, cudaStream_t s);  // cached per tree
+void fmm_plan_free(FmmPlan& F);
+wn_status fmm_run(wn_tree_s* t, int op, const float4* vec, const float* scal, float w, const int32_t* out_map,
+                  float* out, float4* out4, double scale, cudaStream_t s);
+// the solver's elementwise steps around FMM operators (sorted order; Σ partials per 32 points)
+void fmm_epi_s(int64_t n, const float* V, float* sv, double* part, cudaStream_t s);
+void fmm_epi_sq(int64_t n, const float* V, double* part, cudaStream_t s);
+void fmm_epi_r(int64_t n, const float4* r, double* part, cudaStream_t s);
+void fmm_axpy(int64_t n, const float4* mu, const float4* r, const double* alpha, float4* mup, cudaStream_t s);
+void fmm_epi_rescale(int64_t n, const float4* hat, const float4* mup, float4* mu, cudaStream_t s);
 
 // ---- transpose-mode adjoint (transpose.cu) ----
 // node / point accumulators, allocated once per tree — before any graph capture that uses them

@@ -31,7 +31,7 @@ EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", 
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
             "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work",
             "wn_tree_set_far_order", "wnnc_iterate_emulated", "wn_shard_plan", "wn_tree_schedule",
-            "wn_tree_schedule_stats", "wn_comm_init_local", "wn_comm_arena_export", "wn_comm_arena_import", "wn_eval_fmm")
+            "wn_tree_schedule_stats", "wn_comm_init_local", "wn_comm_arena_export", "wn_comm_arena_import", "wn_eval_fmm", "wn_tree_set_fmm")
 
 
 class wnnc_params(C.Structure):
@@ -69,6 +69,7 @@ _sig = {
     "wn_comm_arena_export": ([P, I64, P, P], I32),
     "wn_comm_arena_import": ([P, P], I32),
     "wn_eval_fmm": ([P, I32, P, F32, I32, F32, I32, P, P, P], I32),
+    "wn_tree_set_fmm": ([P, I32, F32, I32], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -149,6 +150,11 @@ def wn_eval_fmm(tree: Tree, attr: torch.Tensor, width: float, op: int = 0, p: in
     _check(_L.wn_eval_fmm(tree.handle, int(op), _ptr(attr), float(width), int(p), float(theta_f), int(leaf),
                           _ptr(out), c, _stream()))
     return (out, (int(c[0]), int(c[1]))) if counts else out
+
+
+def wn_tree_set_fmm(tree: Tree, p: int, theta_f: float = 0.5, leaf: int = 32):
+    """wnnc_iterate's operators: p = 0 the paper's treecode (default), 1..6 the FMM."""
+    _check(_L.wn_tree_set_fmm(tree.handle, int(p), float(theta_f), int(leaf)))
 
 
 def wn_query_work(tree, mu, width, theta=2.0, op=0, q=None):

@@ -82,3 +82,30 @@ def test_fmm_errors(wn):
     for kw in (dict(p=0), dict(p=7), dict(leaf=0), dict(leaf=33), dict(theta_f=0.0)):
         with pytest.raises(wn.WnError, match="ARG"):
             wn.wn_eval_fmm(t, mu, 0.01, **kw)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2s"])
+def test_fmm_solve_matches_oracle(wn, cfg):
+    # wnnc_iterate with FMM operators (wn_tree_set_fmm) against the oracle's FMM solve: one iteration element-
+    # wise (≥ 99.9 % of the points within 1e-3), 40 iterations by orientation (> 99.9 %), graph replay exact
+    pts = synth.config("C1")["points"] if cfg == "C1" else synth.config("C2", n=20000)["points"]
+    n = len(pts)
+    W1, W2 = float(np.float32(0.002)), float(np.float32(0.016))
+    t = wn.wn_build_tree(_cuda(pts))
+    wn.wn_tree_set_fmm(t, 4, 0.5, 32)
+    cl = oracle.Cloud(pts)
+    mu = torch.zeros(n, 3, device="cuda")
+    st = wn.wnnc_iterate(t, mu, stats=True, iters=1, total_iters=40, flags=wn.WN_FLAG_MU_ZERO)
+    mo, so = cl.solve(iters=1, total_iters=40, w1=W1, w2=W2, backend="fmm", fmm=(4, 0.5, 32))
+    err = np.linalg.norm(mu.cpu().numpy() - mo, axis=1) / np.linalg.norm(mo, axis=1)
+    assert np.mean(err < 1e-3) >= 0.999, np.percentile(err, [50, 99, 100])
+    assert st[0]["alpha"] == pytest.approx(so[0, 1], rel=1e-3)
+    outs = []
+    for _ in range(2):
+        mu = torch.zeros(n, 3, device="cuda")
+        wn.wnnc_iterate(t, mu, iters=40, flags=wn.WN_FLAG_GRAPH | wn.WN_FLAG_MU_ZERO)
+        outs.append(mu.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    mo, _ = cl.solve(iters=40, w1=W1, w2=W2, backend="fmm", fmm=(4, 0.5, 32))
+    agree = float(np.mean(np.sum(outs[0] * mo, axis=1) > 0))
+    assert agree > 0.999, agree
