@@ -179,6 +179,8 @@ def run_ours(args):
         tree = wn.wn_build_tree(pts)
         if args.order:
             wn.wn_tree_set_far_order(tree, args.order)
+        if args.fmm:
+            wn.wn_tree_set_fmm(tree, args.fmm, args.fmm_theta, args.fmm_leaf)
         mu = torch.zeros(n, 3, dtype=torch.float32, device=dev)
         wn.wnnc_iterate(tree, mu, comm=comm, **{**params, **over})
         return tree, mu
@@ -315,6 +317,35 @@ def run_ours(args):
     except (OSError, ValueError, KeyError):
         pass
     interactions = sum(work[c]["live"] for c in ("A", "AT", "G"))
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "treecode traversals (trav_kernel A/AT/G), %.0f launches/step, %.3f ms/step"
+                          % (trav_launches, trav_ms),
+                "peak_note": f"FP32 FMA pipe: {sm_count} SMs x 128 lanes x 2 flop x {fmax:.0f} MHz "
+                             "(sm_max_mhz of MEASURED_PEAKS.json; derived, DESIGN.md §Roofline)",
+                "bound_note": "the traversals are instruction-issue bound, not FP32-throughput bound: "
+                              "ncu shows 72-81 % issue-slot utilization with ~37 instructions per "
+                              "warp-level node visit, of which 13 flops are the algorithmic node test "
+                              "(profiles/r01_ncu_trav_v9.txt, DESIGN.md §6)",
+                "work": work}
+    if args.fmm:  # FMM operators: the M2L contraction (fp64) of every application over the FMM runs' time
+        tree = wn.wn_build_tree(pts)
+        mu1 = torch.zeros(n, 3, dtype=torch.float32, device=dev)
+        _, (nm2l, np2p) = wn.wn_eval_fmm(tree, mu1, float(np.float32(0.016)), op=0, p=args.fmm,
+                                         theta_f=args.fmm_theta, leaf=args.fmm_leaf, counts=True)
+        del tree
+        ncoef = (args.fmm + 1) * (args.fmm + 2) * (args.fmm + 3) // 6
+        apps = 4 * ITERS - 1  # (iteration 1's A(0) is skipped)
+        flops = apps * nm2l * 2.0 * ncoef * ncoef
+        achieved = flops / (trav_ms / 1e3) / 1e12
+        peak64 = sm_count * 64 * 2 * fmax * 1e6 / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s (fp64)",
+                    "frac": achieved / peak64, "traffic": None,
+                    "kernel": f"FMM runs (P2M/M2M/M2L/L2L/L2P+P2P), {apps} per step, {trav_ms:.1f} ms/step; "
+                              f"{nm2l} M2L cell pairs and {np2p} P2P leaf pairs per application",
+                    "peak_note": f"FP64: {sm_count} SMs x 64 lanes x 2 flop x {fmax:.0f} MHz (derived)",
+                    "bound_note": "achieved counts only the M2L contractions (2 np^2 fp64 flops per cell pair): "
+                                  "a lower bound on the FMM's arithmetic rate"}
     line = {
         "metric": "WNNC iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -322,6 +353,8 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": CONFIG_TEXT[args.config], "n_points": n, "iters_per_step": ITERS,
                    "theta": args.theta, "far_order": args.order, "max_depth": 15, "depth_used": depth_used,
+                   "operators": (f"FMM p={args.fmm} theta_f={args.fmm_theta} leaf={args.fmm_leaf} (row f4)"
+                                 if args.fmm else "treecode (Alg. 4)"),
                    "num_nodes": num_nodes, "query_schedule": sched_kind,
                    "adjoint": "transpose" if args.transpose else "gather",
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
@@ -336,17 +369,7 @@ def run_ours(args):
                                        "effective_dense = 4 N^2 per iteration (the O(N^2) sums replaced)"},
         "breakdown_ms_per_step": {k: v[0] / args.prof_steps for k, v in prof.items()},
         **({"exchange_check": exchange_check} if exchange_check else {}),
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "treecode traversals (trav_kernel A/AT/G), %.0f launches/step, %.3f ms/step"
-                               % (trav_launches, trav_ms),
-                     "peak_note": f"FP32 FMA pipe: {sm_count} SMs x 128 lanes x 2 flop x {fmax:.0f} MHz "
-                                  "(sm_max_mhz of MEASURED_PEAKS.json; derived, DESIGN.md §Roofline)",
-                     "bound_note": "the traversals are instruction-issue bound, not FP32-throughput bound: "
-                                   "ncu shows 72-81 % issue-slot utilization with ~37 instructions per "
-                                   "warp-level node visit, of which 13 flops are the algorithmic node test "
-                                   "(profiles/r01_ncu_trav_v9.txt, DESIGN.md §6)",
-                     "work": work},
+        "roofline": roofline,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks,
@@ -479,6 +502,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prof-steps", type=int, default=2, help="untimed steps with per-kernel CUDA events")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels one by one (no CUDA graph)")
+    ap.add_argument("--fmm", type=int, default=0,
+                    help="row f4: run the solve's operators by FMM of this degree (1..6) instead of the treecode")
+    ap.add_argument("--fmm-theta", type=float, default=0.7, help="FMM separation parameter theta_f")
+    ap.add_argument("--fmm-leaf", type=int, default=32, help="FMM leaf size (<= 32 points)")
     ap.add_argument("--grid", type=int, default=0,
                     help="row f1: time F(q) on a GRID^3 grid around the cloud (queries/s) instead of the solve")
     args = ap.parse_args()

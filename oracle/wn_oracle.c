@@ -759,10 +759,9 @@ static void fmm_monomials(const fmm_idx* I, const double x[3], int deg, double* 
   }
 }
 
-/* T_δ = ∂^δ Φ(R), |δ| ≤ P, Φ = 1/(4π|R|) */
-static void fmm_derivs(const fmm_idx* I, const double R[3], double* T) {
+/* T_δ = ∂^δ Φ(R), |δ| ≤ P, Φ = 1/(4π|R|); b: nP scratch */
+static void fmm_derivs(const fmm_idx* I, const double R[3], double* T, double* b) {
   double r2 = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
-  double* b = (double*)malloc((size_t)I->nP * sizeof(double));
   b[0] = 1.0 / sqrt(r2);
   for (int k = 1; k < I->nP; ++k) {
     const int* d = I->mi + 3 * k;
@@ -783,7 +782,6 @@ static void fmm_derivs(const fmm_idx* I, const double R[3], double* T) {
     const int* d = I->mi + 3 * k;
     T[k] = b[k] * I->fact[d[0]] * I->fact[d[1]] * I->fact[d[2]] / WO_4PI;
   }
-  free(b);
 }
 
 typedef struct {
@@ -889,7 +887,7 @@ static void fmm_m2l(fmm_ctx* f, int64_t T, int64_t S, double* Tbuf) {
   const fmm_idx* I = &f->I;
   double R[3];
   for (int a = 0; a < 3; ++a) R[a] = f->ctr[3 * T + a] - f->ctr[3 * S + a];
-  fmm_derivs(I, R, Tbuf);
+  fmm_derivs(I, R, Tbuf, Tbuf + I->nP);
   const double* M = f->M + (size_t)S * I->np;
   double* L = f->L + (size_t)T * I->np;
   for (int g = 0; g < I->np; ++g) {
@@ -1010,7 +1008,7 @@ void wo_fmm_op_sep(const wo_tree* t, int op, const double* nu, int dim, double w
   f.M = (double*)calloc((size_t)t->nn * f.I.np, sizeof(double));
   f.L = (double*)calloc((size_t)t->nn * f.I.np, sizeof(double));
   f.pot = (double*)calloc((size_t)t->n * 4, sizeof(double));
-  double* Tbuf = (double*)malloc((size_t)f.I.nP * sizeof(double));
+  double* Tbuf = (double*)malloc((size_t)2 * f.I.nP * sizeof(double));  /* T and the recurrence's b */
   int64_t root = t->bfs[0];
   fmm_up(&f, root);
   fmm_dual(&f, root, root, Tbuf);
