@@ -230,72 +230,88 @@ __device__ __forceinline__ double fact_small(int k) {  // k! for k ≤ 12, exact
   for (int i = 2; i <= k; ++i) f *= i;
   return f;
 }
-constexpr int kFmmWarps = 4;
+constexpr int kFmmWarps = 2;  // (the per-block index tables share the 48 KB of static shared memory)
+// M2L: warps stride over the target cells (a resident grid: the index tables below are built once per block);
+// per source cell of a target's list the derivative tensor of R = c_t − c_s is built degree by degree in
+// shared memory (each entry from its ≤ 6 lower-degree dependencies, looked up in a table), scaled to
+// T_δ = ∂^δΦ, the source's coefficients staged beside it, then lane γ adds Σ_β M_β T_(β+γ) through a
+// (β, γ) → β + γ index table
 __global__ void __launch_bounds__(32 * kFmmWarps) k_fmm_m2l(int64_t nn, const int32_t* __restrict__ off,
                                                             const uint64_t* __restrict__ keys, FmmGeom g, int p,
                                                             const double* __restrict__ M, double* __restrict__ L) {
   __shared__ double sT[kFmmWarps][kFmmMaxT];
   __shared__ double sB[kFmmWarps][kFmmMaxT];
   __shared__ double sM[kFmmWarps][kFmmMaxN];
+  __shared__ double sFac[kFmmMaxT];          // δ!/(4π)
+  __shared__ short sDep[kFmmMaxT][6];        // δ − e_i (i = 0..2), δ − 2e_i (i = 0..2), or −1
+  __shared__ short sSum[kFmmMaxN][kFmmMaxN]; // index of β + γ
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int64_t T = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (T >= nn) return;
-  const int k0 = off[T], k1 = off[T + 1];
-  if (k0 == k1) return;
-  const int np = (p + 1) * (p + 2) * (p + 3) / 6, P = 2 * p;
+  const int np = (p + 1) * (p + 2) * (p + 3) / 6, P = 2 * p, nP = (P + 1) * (P + 2) * (P + 3) / 6;
+  for (int e = threadIdx.x; e < nP; e += blockDim.x) {
+    const int d0 = c_mi[e][0], d1 = c_mi[e][1], d2 = c_mi[e][2];
+    sFac[e] = c_fact[d0] * c_fact[d1] * c_fact[d2] * 0.0795774715459476679;
+    sDep[e][0] = d0 > 0 ? (short)mi_index(d0 - 1, d1, d2) : (short)-1;
+    sDep[e][1] = d1 > 0 ? (short)mi_index(d0, d1 - 1, d2) : (short)-1;
+    sDep[e][2] = d2 > 0 ? (short)mi_index(d0, d1, d2 - 1) : (short)-1;
+    sDep[e][3] = d0 > 1 ? (short)mi_index(d0 - 2, d1, d2) : (short)-1;
+    sDep[e][4] = d1 > 1 ? (short)mi_index(d0, d1 - 2, d2) : (short)-1;
+    sDep[e][5] = d2 > 1 ? (short)mi_index(d0, d1, d2 - 2) : (short)-1;
+  }
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int be = e / np, ga = e % np;
+    sSum[be][ga] = (short)mi_index(c_mi[be][0] + c_mi[ga][0], c_mi[be][1] + c_mi[ga][1], c_mi[be][2] + c_mi[ga][2]);
+  }
+  __syncthreads();
   double* b = sB[wp];
   double* Tt = sT[wp];
   double* Ms = sM[wp];
-  // this lane's output coefficients γ = lane + 32 q
-  int gq[3][3];
-  for (int q = 0; q < 3; ++q) {
-    const int gi = lane + 32 * q;
-    gq[q][0] = gi < np ? c_mi[gi][0] : 0;
-    gq[q][1] = gi < np ? c_mi[gi][1] : 0;
-    gq[q][2] = gi < np ? c_mi[gi][2] : 0;
-  }
-  double acc[3] = {0.0, 0.0, 0.0};
-  for (int k = k0; k < k1; ++k) {
-    const int S = (int)(uint32_t)keys[k];
-    const double R0 = g.ctr[3 * T] - g.ctr[3 * S], R1 = g.ctr[3 * T + 1] - g.ctr[3 * S + 1],
-                 R2 = g.ctr[3 * T + 2] - g.ctr[3 * S + 2];
-    const double r2 = R0 * R0 + R1 * R1 + R2 * R2;
-    __syncwarp();
-    for (int e = lane; e < np; e += 32) Ms[e] = M[(int64_t)S * np + e];
-    if (lane == 0) {
-      b[0] = 1.0 / sqrt(r2);
-      Tt[0] = b[0] * 0.0795774715459476679;
-    }
-    __syncwarp();
-    for (int n = 1; n <= P; ++n) {  // the b_δ of degree n from degrees n − 1 and n − 2
-      const int lo = n * (n + 1) * (n + 2) / 6, cntn = (n + 1) * (n + 2) / 2;
-      for (int e = lane; e < cntn; e += 32) {
-        const int idx = lo + e;
-        const int d0 = c_mi[idx][0], d1 = c_mi[idx][1], d2 = c_mi[idx][2];
-        double s = 0.0;
-        if (d0 > 0) s -= (2.0 * n - 1.0) * R0 * b[mi_index(d0 - 1, d1, d2)];
-        if (d1 > 0) s -= (2.0 * n - 1.0) * R1 * b[mi_index(d0, d1 - 1, d2)];
-        if (d2 > 0) s -= (2.0 * n - 1.0) * R2 * b[mi_index(d0, d1, d2 - 1)];
-        if (d0 > 1) s -= (n - 1.0) * b[mi_index(d0 - 2, d1, d2)];
-        if (d1 > 1) s -= (n - 1.0) * b[mi_index(d0, d1 - 2, d2)];
-        if (d2 > 1) s -= (n - 1.0) * b[mi_index(d0, d1, d2 - 2)];
-        const double bv = s / (n * r2);
-        b[idx] = bv;
-        Tt[idx] = bv * (fact_small(d0) * fact_small(d1) * fact_small(d2)) * 0.0795774715459476679;  // ∂^δΦ
+  const int64_t nw = (int64_t)gridDim.x * kFmmWarps;
+  for (int64_t T = (int64_t)blockIdx.x * kFmmWarps + wp; T < nn; T += nw) {
+    const int k0 = off[T], k1 = off[T + 1];
+    if (k0 == k1) continue;
+    double acc[3] = {0.0, 0.0, 0.0};  // γ = lane, lane + 32, lane + 64
+    for (int k = k0; k < k1; ++k) {
+      const int S = (int)(uint32_t)keys[k];
+      const double R[3] = {g.ctr[3 * T] - g.ctr[3 * S], g.ctr[3 * T + 1] - g.ctr[3 * S + 1],
+                           g.ctr[3 * T + 2] - g.ctr[3 * S + 2]};
+      const double r2 = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
+      __syncwarp();
+      for (int e = lane; e < np; e += 32) Ms[e] = M[(int64_t)S * np + e];
+      if (lane == 0) {
+        b[0] = 1.0 / sqrt(r2);
+        Tt[0] = b[0] * sFac[0];
       }
       __syncwarp();
+      for (int n = 1; n <= P; ++n) {  // the b_δ of degree n from degrees n − 1 and n − 2
+        const int lo = n * (n + 1) * (n + 2) / 6, cntn = (n + 1) * (n + 2) / 2;
+        const double c1 = 2.0 * n - 1.0, c2 = n - 1.0, inv = 1.0 / (n * r2);
+        for (int e = lane; e < cntn; e += 32) {
+          const int idx = lo + e;
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const int j1 = sDep[idx][i], j2 = sDep[idx][3 + i];
+            if (j1 >= 0) s -= c1 * R[i] * b[j1];
+            if (j2 >= 0) s -= c2 * b[j2];
+          }
+          const double bv = s * inv;
+          b[idx] = bv;
+          Tt[idx] = bv * sFac[idx];  // ∂^δΦ
+        }
+        __syncwarp();
+      }
+      for (int q = 0; q < 3; ++q) {
+        const int gi = lane + 32 * q;
+        if (gi >= np) break;
+        double a = 0.0;
+        for (int be = 0; be < np; ++be) a += Ms[be] * Tt[sSum[be][gi]];
+        acc[q] += a;
+      }
     }
     for (int q = 0; q < 3; ++q) {
-      if (lane + 32 * q >= np) break;
-      double a = 0.0;
-      for (int be = 0; be < np; ++be)
-        a += Ms[be] * Tt[mi_index(c_mi[be][0] + gq[q][0], c_mi[be][1] + gq[q][1], c_mi[be][2] + gq[q][2])];
-      acc[q] += a;
+      const int gi = lane + 32 * q;
+      if (gi < np) L[T * np + gi] = acc[q];
     }
-  }
-  for (int q = 0; q < 3; ++q) {
-    const int gi = lane + 32 * q;
-    if (gi < np) L[T * np + gi] = acc[q];
   }
 }
 
@@ -592,7 +608,16 @@ wn_status fmm_run(wn_tree_s* t, int op, const float4* vec, const float* scal, fl
       k_fmm_m2m<<<gwarps(F.ninner[l], wpb), 32 * wpb, 0, s>>>(F.ninner[l], F.inner[l], g, p, F.M);
       ++launches;
     }
-  k_fmm_m2l<<<gwarps(nn, kFmmWarps), 32 * kFmmWarps, 0, s>>>(nn, F.om, F.m2l, g, p, F.M, F.L);
+  static int m2l_blocks = 0;  // a resident grid (the blocks build their index tables once)
+  if (!m2l_blocks) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fmm_m2l, 32 * kFmmWarps, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    m2l_blocks = std::max(1, per_sm * sms);
+  }
+  k_fmm_m2l<<<(unsigned)std::min<int64_t>(m2l_blocks, gwarps(nn, kFmmWarps)), 32 * kFmmWarps, 0, s>>>(nn, F.om, F.m2l,
+                                                                                                   g, p, F.M, F.L);
   ++launches;
   for (int l = 1; l <= D; ++l)
     if (F.nkids[l]) {
