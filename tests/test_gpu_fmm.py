@@ -112,3 +112,17 @@ def test_fmm_solve_matches_oracle(wn, cfg):
     mo, _ = cl.solve(iters=40, w1=W1, w2=W2, backend="fmm", fmm=(4, 0.5, 32))
     agree = float(np.mean(np.sum(outs[0] * mo, axis=1) > 0))
     assert agree > 0.999, agree
+
+
+@pytest.mark.parametrize("n", [2, 7, 40])
+def test_fmm_tiny_clouds(wn, n):
+    # degenerate trees (a root leaf, one level) — every pair direct: the dense definition
+    pts = synth.sphere(n, seed=40 + n)[0]
+    rng = np.random.default_rng(n)
+    mu = rng.standard_normal((n, 3)).astype(np.float32)
+    t = wn.wn_build_tree(_cuda(pts))
+    w = float(np.float32(0.01))
+    g = wn.wn_eval_fmm(t, _cuda(mu), w, op=0, p=3, theta_f=0.5, leaf=32).cpu().numpy()
+    cl = oracle.Cloud(pts)
+    d = cl.F(mu, w, dense=True)
+    np.testing.assert_allclose(g, d, rtol=1e-5, atol=1e-6 * np.abs(d).max())
