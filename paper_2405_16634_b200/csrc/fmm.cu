@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(32 * kFmmWarps) k_fmm_m2l(int64_t nn, const in
   __shared__ short sSum[kFmmMaxN][kFmmMaxN]; // index of β + γ
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int np = (p + 1) * (p + 2) * (p + 3) / 6, P = 2 * p, nP = (P + 1) * (P + 2) * (P + 3) / 6;
+  WN_DCHECK(p >= 1 && p <= kFmmMaxP, "M2L degree");
   for (int e = threadIdx.x; e < nP; e += blockDim.x) {
     const int d0 = c_mi[e][0], d1 = c_mi[e][1], d2 = c_mi[e][2];
     sFac[e] = c_fact[d0] * c_fact[d1] * c_fact[d2] * 0.0795774715459476679;
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(32 * kFmmWarps) k_fmm_m2l(int64_t nn, const in
     double acc[3] = {0.0, 0.0, 0.0};  // γ = lane, lane + 32, lane + 64
     for (int k = k0; k < k1; ++k) {
       const int S = (int)(uint32_t)keys[k];
+      WN_DCHECK(S >= 0 && S < nn && (int64_t)(keys[k] >> 32) == T, "M2L list entry");
       const double R[3] = {g.ctr[3 * T] - g.ctr[3 * S], g.ctr[3 * T + 1] - g.ctr[3 * S + 1],
                            g.ctr[3 * T + 2] - g.ctr[3 * S + 2]};
       const double r2 = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
@@ -352,73 +354,76 @@ __global__ void k_fmm_eval(int64_t m, const int32_t* __restrict__ list, FmmGeom 
   if (k >= m) return;
   const int64_t T = list[k];
   const int np = (p + 1) * (p + 2) * (p + 3) / 6;
-  const int i = g.pb[T] + lane;
-  const bool valid = i < g.pe[T];
-  double V = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
-  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (valid) {
-    y = pts[i];
-    double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];
-    fmm_pows((double)y.x - g.ctr[3 * T], p, px);
-    fmm_pows((double)y.y - g.ctr[3 * T + 1], p, py);
-    fmm_pows((double)y.z - g.ctr[3 * T + 2], p, pz);
-    const double* Lt = L + T * np;
-    for (int gi = 0; gi < np; ++gi) {
-      const int g0 = c_mi[gi][0], g1 = c_mi[gi][1], g2 = c_mi[gi][2];
-      const double l = Lt[gi];
-      V += l * (px[g0] * py[g1] * pz[g2]);
-      if (g0 > 0) gx += l * (px[g0 - 1] * py[g1] * pz[g2]);
-      if (g1 > 0) gy += l * (px[g0] * py[g1 - 1] * pz[g2]);
-      if (g2 > 0) gz += l * (px[g0] * py[g1] * pz[g2 - 1]);
-    }
-  }
-  // P2P: fp32 pair terms (rsqrt, as the treecode's near field), summed per source leaf in fp32 and across
-  // leaves in fp64; the cutoff decided in fp32 on d = x_j − y (R-prec)
-  for (int kk = off[T]; kk < off[T + 1]; ++kk) {
-    const int S = (int)(uint32_t)keys[kk];
-    float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
-    for (int j = g.pb[S]; j < g.pe[S]; ++j) {
-      const float4 x = pts[j];
-      const float dxf = x.x - y.x, dyf = x.y - y.y, dzf = x.z - y.z;
-      const float d2 = __fmaf_rn(dxf, dxf, __fmaf_rn(dyf, dyf, __fmul_rn(dzf, dzf)));
-      const bool live = valid && !(d2 < w2f);
-      const float inv = rsqrtf(live ? d2 : __int_as_float(0x7f800000));  // a dead pair: rsqrt(+inf) = 0
-      const float inv3 = inv * inv * inv;
-      // d = y − x = −(dxf, dyf, dzf)
-      if (DIM == 1) {  // q Φ(d): V += q/(4πr), ∇V += −q d/(4πr³) = q (x − y)/(4πr³)
-        const float q = scal[j];
-        v0 = fmaf(q, inv, v0);
-        v1 = fmaf(q * inv3, dxf, v1);
-        v2 = fmaf(q * inv3, dyf, v2);
-        v3 = fmaf(q * inv3, dzf, v3);
-      } else {  // V −= (d·ν)/(4πr³);  ∇V += 3(d·ν)d/(4πr⁵) − ν/(4πr³)
-        const float4 v = vec[j];
-        const float dn = -(dxf * v.x + dyf * v.y + dzf * v.z);
-        const float t5 = 3.0f * dn * inv3 * inv * inv;
-        v0 = fmaf(-dn, inv3, v0);
-        v1 = fmaf(-t5, dxf, fmaf(-v.x, inv3, v1));
-        v2 = fmaf(-t5, dyf, fmaf(-v.y, inv3, v2));
-        v3 = fmaf(-t5, dzf, fmaf(-v.z, inv3, v3));
+  // a leaf holds ≤ `leaf` ≤ 32 points unless it is a depth-D cell of duplicates: chunks of 32 targets
+  for (int i0 = g.pb[T]; i0 < g.pe[T]; i0 += 32) {
+    const int i = i0 + lane;
+    const bool valid = i < g.pe[T];
+    double V = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+      y = pts[i];
+      double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];
+      fmm_pows((double)y.x - g.ctr[3 * T], p, px);
+      fmm_pows((double)y.y - g.ctr[3 * T + 1], p, py);
+      fmm_pows((double)y.z - g.ctr[3 * T + 2], p, pz);
+      const double* Lt = L + T * np;
+      for (int gi = 0; gi < np; ++gi) {
+        const int g0 = c_mi[gi][0], g1 = c_mi[gi][1], g2 = c_mi[gi][2];
+        const double l = Lt[gi];
+        V += l * (px[g0] * py[g1] * pz[g2]);
+        if (g0 > 0) gx += l * (px[g0 - 1] * py[g1] * pz[g2]);
+        if (g1 > 0) gy += l * (px[g0] * py[g1 - 1] * pz[g2]);
+        if (g2 > 0) gz += l * (px[g0] * py[g1] * pz[g2 - 1]);
       }
     }
-    const double k4 = 0.0795774715459476679;
-    V += k4 * v0;
-    gx += k4 * v1;
-    gy += k4 * v2;
-    gz += k4 * v3;
-  }
-  if (!valid) return;
-  if (out4) {  // the solver's sorted buffers, unscaled: V in .x (A), or −∇V (G, Aᵀ)
-    out4[i] = op == OP_A ? make_float4((float)V, 0.f, 0.f, 0.f) : make_float4((float)-gx, (float)-gy, (float)-gz, 0.f);
-    return;
-  }
-  const int64_t o = out_map ? (int64_t)out_map[i] : i;
-  if (op == OP_A) {
-    out[o] = (float)(V * scale);
-  } else {  // G = −∇V (dipoles), Aᵀ = −∇V (charges)
-    out[3 * o] = (float)(-gx * scale);
-    out[3 * o + 1] = (float)(-gy * scale);
-    out[3 * o + 2] = (float)(-gz * scale);
+    // P2P: fp32 pair terms (rsqrt, as the treecode's near field), summed per source leaf in fp32 and across
+    // leaves in fp64; the cutoff decided in fp32 on d = x_j − y (R-prec)
+    for (int kk = off[T]; kk < off[T + 1]; ++kk) {
+      const int S = (int)(uint32_t)keys[kk];
+      float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+      for (int j = g.pb[S]; j < g.pe[S]; ++j) {
+        const float4 x = pts[j];
+        const float dxf = x.x - y.x, dyf = x.y - y.y, dzf = x.z - y.z;
+        const float d2 = __fmaf_rn(dxf, dxf, __fmaf_rn(dyf, dyf, __fmul_rn(dzf, dzf)));
+        const bool live = valid && !(d2 < w2f);
+        const float inv = rsqrtf(live ? d2 : __int_as_float(0x7f800000));  // a dead pair: rsqrt(+inf) = 0
+        const float inv3 = inv * inv * inv;
+        // d = y − x = −(dxf, dyf, dzf)
+        if (DIM == 1) {  // q Φ(d): V += q/(4πr), ∇V += −q d/(4πr³) = q (x − y)/(4πr³)
+          const float q = scal[j];
+          v0 = fmaf(q, inv, v0);
+          v1 = fmaf(q * inv3, dxf, v1);
+          v2 = fmaf(q * inv3, dyf, v2);
+          v3 = fmaf(q * inv3, dzf, v3);
+        } else {  // V −= (d·ν)/(4πr³);  ∇V += 3(d·ν)d/(4πr⁵) − ν/(4πr³)
+          const float4 v = vec[j];
+          const float dn = -(dxf * v.x + dyf * v.y + dzf * v.z);
+          const float t5 = 3.0f * dn * inv3 * inv * inv;
+          v0 = fmaf(-dn, inv3, v0);
+          v1 = fmaf(-t5, dxf, fmaf(-v.x, inv3, v1));
+          v2 = fmaf(-t5, dyf, fmaf(-v.y, inv3, v2));
+          v3 = fmaf(-t5, dzf, fmaf(-v.z, inv3, v3));
+        }
+      }
+      const double k4 = 0.0795774715459476679;
+      V += k4 * v0;
+      gx += k4 * v1;
+      gy += k4 * v2;
+      gz += k4 * v3;
+    }
+    if (!valid) continue;
+    if (out4) {  // the solver's sorted buffers, unscaled: V in .x (A), or −∇V (G, Aᵀ)
+      out4[i] = op == OP_A ? make_float4((float)V, 0.f, 0.f, 0.f) : make_float4((float)-gx, (float)-gy, (float)-gz, 0.f);
+      continue;
+    }
+    const int64_t o = out_map ? (int64_t)out_map[i] : i;
+    if (op == OP_A) {
+      out[o] = (float)(V * scale);
+    } else {  // G = −∇V (dipoles), Aᵀ = −∇V (charges)
+      out[3 * o] = (float)(-gx * scale);
+      out[3 * o + 1] = (float)(-gy * scale);
+      out[3 * o + 2] = (float)(-gz * scale);
+    }
   }
 }
 

@@ -343,6 +343,6 @@ inline int trav_blocks(int64_t nq) { return (int)((nq + kTravBlock - 1) / kTravB
 // own slot (no block barrier in the epilogues), and α sums the slots in one fixed order
 constexpr int kPartQ = 32;
 static_assert(WN_SHARD_ALIGN % kPartQ == 0, "rank shards must hold whole partial groups");
-inline int64_t part_slots(int64_t nq) { return (nq + kPartQ - 1) / kPartQ; }
+__host__ __device__ inline int64_t part_slots(int64_t nq) { return (nq + kPartQ - 1) / kPartQ; }
 
 }  // namespace wn

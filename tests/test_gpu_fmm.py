@@ -33,6 +33,9 @@ CLOUDS = {
     "sphere3k": lambda: synth.sphere(3000, seed=5)[0],
     "torus20k": lambda: synth.config("C2", n=20000)["points"],
     "dups": lambda: np.repeat(synth.sphere(700, seed=8)[0], 3, axis=0),
+    # 60 clusters of ~50 points 1e-6 apart: depth-D leaves of more than 32 points (L2P + P2P in chunks)
+    "clustered": lambda: (np.random.default_rng(5).uniform(-1, 1, (60, 3))[np.random.default_rng(6).integers(0, 60, 3001)]
+                          + 1e-6 * np.random.default_rng(7).standard_normal((3001, 3))).astype(np.float32),
 }
 OPS = {"F": (0, oracle.OP_A), "AT": (1, oracle.OP_AT), "gradF": (2, oracle.OP_G)}
 
