@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "wn_internal.cuh"
@@ -217,103 +218,180 @@ __global__ void k_fmm_csr(int64_t nn, const uint64_t* __restrict__ keys, int64_t
   off[t] = (int32_t)lo;
 }
 
-// M2L: one warp per target cell with a non-empty list; per source cell the derivative tensor of
-// R = c_t − c_s is built degree by degree in shared memory (scaled to T_δ = ∂^δΦ on the fly), the source's
-// multipole coefficients are staged there too, then lane γ adds Σ_β M_β T_(β+γ)
-// index of a multi-index in the degree-then-lexicographic order, arithmetically (no divergent table lookups)
-__device__ __forceinline__ int mi_index(int a, int b, int c) {
-  const int n = a + b + c, na = n - a;
-  return n * (n + 1) * (n + 2) / 6 + na * (na + 1) / 2 + (na - b);
+// M2L, grouped by translation vector.  Octree cell centres are dyadic: c = −1 + (2k + 1)·2^−d, so
+// R = c_t − c_s is an integer vector o in units of 2^−m, m = max(d_t, d_s), and pairs with equal (m, o)
+// share one derivative tensor ∂^δΦ(R).  The plan sorts the pairs by that key; each block takes a chunk
+// of ≤ kChunk pairs of one group, builds the tensor once in shared memory — in a (2p+1)³ box layout, so
+// that the entry of β + γ sits at box(β) + box(γ), box(a, b, c) = (a·E + b)·E + c, E = 2p + 1 — and then
+// every thread contracts one pair, L_γ = Σ_β M_β T_(β+γ), its γ loop unrolled at compile time (box(γ) is
+// an immediate offset; all lanes read the same T entry: a shared-memory broadcast per FMA).  The per-pair
+// results go to Lp (group order); k_fmm_m2l_reduce adds each target's pairs in the (target, source) order
+// of the sorted list — the same fixed order for every run.
+constexpr int kM2lKeyOff = 18;  // |o_i| < 2^18: 19 bits per component; else the pair is a group of its own
+
+__host__ __device__ constexpr int fmm_np(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
+// box offset of the j-th multi-index in the degree-then-(a, b) descending order (the c_mi order)
+constexpr int fmm_box_of(int j, int E) {
+  int n = 0;
+  for (int deg = 0; deg < 64; ++deg)
+    for (int a = deg; a >= 0; --a)
+      for (int b = deg - a; b >= 0; --b) {
+        if (n == j) return (a * E + b) * E + (deg - a - b);
+        ++n;
+      }
+  return -1;
 }
-__device__ __forceinline__ double fact_small(int k) {  // k! for k ≤ 12, exact in fp64
-  double f = 1.0;
-  for (int i = 2; i <= k; ++i) f *= i;
-  return f;
+// component `comp` of the j-th multi-index in the c_mi order
+constexpr int fmm_mi_of(int j, int comp) {
+  int n = 0;
+  for (int deg = 0; deg < 64; ++deg)
+    for (int a = deg; a >= 0; --a)
+      for (int b = deg - a; b >= 0; --b) {
+        if (n == j) return comp == 0 ? a : comp == 1 ? b : deg - a - b;
+        ++n;
+      }
+  return -1;
 }
-constexpr int kFmmWarps = 2;  // (the per-block index tables share the 48 KB of static shared memory)
-// M2L: warps stride over the target cells (a resident grid: the index tables below are built once per block);
-// per source cell of a target's list the derivative tensor of R = c_t − c_s is built degree by degree in
-// shared memory (each entry from its ≤ 6 lower-degree dependencies, looked up in a table), scaled to
-// T_δ = ∂^δΦ, the source's coefficients staged beside it, then lane γ adds Σ_β M_β T_(β+γ) through a
-// (β, γ) → β + γ index table
-__global__ void __launch_bounds__(32 * kFmmWarps) k_fmm_m2l(int64_t nn, const int32_t* __restrict__ off,
-                                                            const uint64_t* __restrict__ keys, FmmGeom g, int p,
-                                                            const double* __restrict__ M, double* __restrict__ L) {
-  __shared__ double sT[kFmmWarps][kFmmMaxT];
-  __shared__ double sB[kFmmWarps][kFmmMaxT];
-  __shared__ double sM[kFmmWarps][kFmmMaxN];
-  __shared__ double sFac[kFmmMaxT];          // δ!/(4π)
-  __shared__ short sDep[kFmmMaxT][6];        // δ − e_i (i = 0..2), δ − 2e_i (i = 0..2), or −1
-  __shared__ short sSum[kFmmMaxN][kFmmMaxN]; // index of β + γ
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int np = (p + 1) * (p + 2) * (p + 3) / 6, P = 2 * p, nP = (P + 1) * (P + 2) * (P + 3) / 6;
-  WN_DCHECK(p >= 1 && p <= kFmmMaxP, "M2L degree");
-  for (int e = threadIdx.x; e < nP; e += blockDim.x) {
-    const int d0 = c_mi[e][0], d1 = c_mi[e][1], d2 = c_mi[e][2];
-    sFac[e] = c_fact[d0] * c_fact[d1] * c_fact[d2] * 0.0795774715459476679;
-    sDep[e][0] = d0 > 0 ? (short)mi_index(d0 - 1, d1, d2) : (short)-1;
-    sDep[e][1] = d1 > 0 ? (short)mi_index(d0, d1 - 1, d2) : (short)-1;
-    sDep[e][2] = d2 > 0 ? (short)mi_index(d0, d1, d2 - 1) : (short)-1;
-    sDep[e][3] = d0 > 1 ? (short)mi_index(d0 - 2, d1, d2) : (short)-1;
-    sDep[e][4] = d1 > 1 ? (short)mi_index(d0, d1 - 2, d2) : (short)-1;
-    sDep[e][5] = d2 > 1 ? (short)mi_index(d0, d1, d2 - 2) : (short)-1;
+template <int P>
+struct M2lCfg {
+  static constexpr int NP = fmm_np(P), E = 2 * P + 1, NT3 = E * E * E;
+  static constexpr int NSPLIT = NP <= 35 ? 1 : (NP + 27) / 28;  // γ parts per pair (≤ 28 accumulators each)
+  static constexpr int GCH = (NP + NSPLIT - 1) / NSPLIT;
+  static constexpr int CHP = NSPLIT == 1 ? 128 : 64;              // pairs per block
+  static constexpr int THREADS = CHP * NSPLIT;
+};
+inline int m2l_chunk(int p) { return fmm_np(p) <= 35 ? 128 : 64; }
+
+__global__ void k_fmm_m2l_gkey(int64_t m, const uint64_t* __restrict__ m2l, FmmGeom g, uint64_t* __restrict__ key) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int T = (int)(m2l[i] >> 32), S = (int)(uint32_t)m2l[i];
+  const int mx = max(g.depth[T], g.depth[S]);
+  uint64_t k = (uint64_t)mx << 57;
+  bool ok = mx < 32;
+  for (int a = 0; a < 3; ++a) {
+    const double o = ldexp(g.ctr[3 * T + a] - g.ctr[3 * S + a], mx);  // exact (dyadic centres)
+    ok = ok && o == rint(o) && fabs(o) < (double)(1 << kM2lKeyOff);
+    const uint64_t f = ok ? (uint64_t)((int64_t)o + (1 << kM2lKeyOff)) : 0;
+    k |= f << (19 * (2 - a));
   }
-  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
-    const int be = e / np, ga = e % np;
-    sSum[be][ga] = (short)mi_index(c_mi[be][0] + c_mi[ga][0], c_mi[be][1] + c_mi[ga][1], c_mi[be][2] + c_mi[ga][2]);
+  key[i] = ok ? k : ((1ull << 62) | (uint64_t)i);
+}
+
+// chunk starts (group boundaries and every kChunk-th position) and the inverse permutation
+__global__ void k_fmm_m2l_ginfo(int64_t m, const uint64_t* __restrict__ skey, const int32_t* __restrict__ gidx,
+                                int chunk, uint32_t* __restrict__ flag, uint32_t* __restrict__ gflag,
+                                int32_t* __restrict__ ginv) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const bool gs = i == 0 || skey[i] != skey[i - 1];
+  flag[i] = (gs || i % chunk == 0) ? 1u : 0u;
+  gflag[i] = gs ? 1u : 0u;
+  ginv[gidx[i]] = (int32_t)i;
+}
+__global__ void k_fmm_chunks(int64_t m, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                             int32_t* __restrict__ chunks) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m && flag[i]) chunks[pos[i]] = (int32_t)i;
+  if (i == m) chunks[pos[m]] = (int32_t)m;
+}
+
+template <int P, int G0, int... J>
+__device__ __forceinline__ void m2l_row(double mb, const double* __restrict__ tb, double* acc,
+                                        std::integer_sequence<int, J...>) {
+  using C = M2lCfg<P>;
+  ((G0 + J < C::NP ? (void)(acc[J] = fma(mb, tb[std::integral_constant<int, fmm_box_of(G0 + J, C::E)>::value],
+                                         acc[J]))
+                   : (void)0),
+   ...);
+}
+template <int P, int PART>
+__device__ __forceinline__ void m2l_contract(const double* __restrict__ Ms, const double* T3, double* __restrict__ out) {
+  using C = M2lCfg<P>;
+  constexpr int G0 = PART * C::GCH;
+  double acc[C::GCH];
+#pragma unroll
+  for (int j = 0; j < C::GCH; ++j) acc[j] = 0.0;
+#pragma unroll 1
+  for (int be = 0; be < C::NP; ++be) {
+    const int base = (c_mi[be][0] * C::E + c_mi[be][1]) * C::E + c_mi[be][2];  // warp-uniform
+    m2l_row<P, G0>(__ldg(Ms + be), T3 + base, acc, std::make_integer_sequence<int, C::GCH>{});
+  }
+#pragma unroll
+  for (int j = 0; j < C::GCH; ++j)
+    if (G0 + j < C::NP) out[G0 + j] = acc[j];
+}
+
+template <int P>
+__global__ void __launch_bounds__(M2lCfg<P>::THREADS) k_fmm_m2l_grp(const int32_t* __restrict__ chunks,
+                                                                     const int32_t* __restrict__ gidx,
+                                                                     const uint64_t* __restrict__ m2l, FmmGeom g,
+                                                                     const double* __restrict__ M,
+                                                                     double* __restrict__ Lp) {
+  using C = M2lCfg<P>;
+  __shared__ double T3[C::NT3];
+  const int tid = threadIdx.x;
+  const int i0 = chunks[blockIdx.x], i1 = chunks[blockIdx.x + 1];
+  const uint64_t k0 = m2l[gidx[i0]];
+  const int Tn = (int)(k0 >> 32), Sn = (int)(uint32_t)k0;
+  const double R0 = g.ctr[3 * Tn] - g.ctr[3 * Sn], R1 = g.ctr[3 * Tn + 1] - g.ctr[3 * Sn + 1],
+               R2 = g.ctr[3 * Tn + 2] - g.ctr[3 * Sn + 2];
+  const double r2 = R0 * R0 + R1 * R1 + R2 * R2;
+  constexpr int E = C::E, E2 = E * E;
+  // b_δ by degree: |δ||R|² b_δ = −(2|δ|−1) Σ_i R_i b_(δ−e_i) − (|δ|−1) Σ_i b_(δ−2e_i)   (1/|R| = b_0)
+  if (tid == 0) T3[0] = 1.0 / sqrt(r2);
+  __syncthreads();
+  for (int n = 1; n <= 2 * P; ++n) {
+    const int cnt = (n + 1) * (n + 2) / 2;
+    const double c1 = 2.0 * n - 1.0, c2 = n - 1.0, inv = 1.0 / (n * r2);
+    for (int e = tid; e < cnt; e += C::THREADS) {
+      int a = n, rem = e;  // e-th (a, b) with a descending, then b descending
+      while (rem > n - a) {
+        rem -= n - a + 1;
+        --a;
+      }
+      const int b = n - a - rem, c = n - a - b;
+      const int idx = (a * E + b) * E + c;
+      double sacc = 0.0;
+      if (a > 0) sacc -= c1 * R0 * T3[idx - E2];
+      if (b > 0) sacc -= c1 * R1 * T3[idx - E];
+      if (c > 0) sacc -= c1 * R2 * T3[idx - 1];
+      if (a > 1) sacc -= c2 * T3[idx - 2 * E2];
+      if (b > 1) sacc -= c2 * T3[idx - 2 * E];
+      if (c > 1) sacc -= c2 * T3[idx - 2];
+      T3[idx] = sacc * inv;
+    }
+    __syncthreads();
+  }
+  // T_δ = ∂^δΦ(R) = δ! b_δ / (4π)
+  for (int e = tid; e < C::NT3; e += C::THREADS) {
+    const int a = e / E2, b = (e / E) % E, c = e % E;
+    if (a + b + c <= 2 * P) T3[e] *= c_fact[a] * c_fact[b] * c_fact[c] * 0.0795774715459476679;
   }
   __syncthreads();
-  double* b = sB[wp];
-  double* Tt = sT[wp];
-  double* Ms = sM[wp];
-  const int64_t nw = (int64_t)gridDim.x * kFmmWarps;
-  for (int64_t T = (int64_t)blockIdx.x * kFmmWarps + wp; T < nn; T += nw) {
-    const int k0 = off[T], k1 = off[T + 1];
-    if (k0 == k1) continue;
-    double acc[3] = {0.0, 0.0, 0.0};  // γ = lane, lane + 32, lane + 64
-    for (int k = k0; k < k1; ++k) {
-      const int S = (int)(uint32_t)keys[k];
-      WN_DCHECK(S >= 0 && S < nn && (int64_t)(keys[k] >> 32) == T, "M2L list entry");
-      const double R[3] = {g.ctr[3 * T] - g.ctr[3 * S], g.ctr[3 * T + 1] - g.ctr[3 * S + 1],
-                           g.ctr[3 * T + 2] - g.ctr[3 * S + 2]};
-      const double r2 = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
-      __syncwarp();
-      for (int e = lane; e < np; e += 32) Ms[e] = M[(int64_t)S * np + e];
-      if (lane == 0) {
-        b[0] = 1.0 / sqrt(r2);
-        Tt[0] = b[0] * sFac[0];
-      }
-      __syncwarp();
-      for (int n = 1; n <= P; ++n) {  // the b_δ of degree n from degrees n − 1 and n − 2
-        const int lo = n * (n + 1) * (n + 2) / 6, cntn = (n + 1) * (n + 2) / 2;
-        const double c1 = 2.0 * n - 1.0, c2 = n - 1.0, inv = 1.0 / (n * r2);
-        for (int e = lane; e < cntn; e += 32) {
-          const int idx = lo + e;
-          double s = 0.0;
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            const int j1 = sDep[idx][i], j2 = sDep[idx][3 + i];
-            if (j1 >= 0) s -= c1 * R[i] * b[j1];
-            if (j2 >= 0) s -= c2 * b[j2];
-          }
-          const double bv = s * inv;
-          b[idx] = bv;
-          Tt[idx] = bv * sFac[idx];  // ∂^δΦ
-        }
-        __syncwarp();
-      }
-      for (int q = 0; q < 3; ++q) {
-        const int gi = lane + 32 * q;
-        if (gi >= np) break;
-        double a = 0.0;
-        for (int be = 0; be < np; ++be) a += Ms[be] * Tt[sSum[be][gi]];
-        acc[q] += a;
-      }
-    }
-    for (int q = 0; q < 3; ++q) {
-      const int gi = lane + 32 * q;
-      if (gi < np) L[T * np + gi] = acc[q];
-    }
+  const int part = tid / C::CHP, i = i0 + tid % C::CHP;
+  if (i >= i1) return;
+  const int S = (int)(uint32_t)m2l[gidx[i]];
+  WN_DCHECK(S >= 0 && (int)(m2l[gidx[i]] >> 32) >= 0, "M2L pair");
+  const double* Ms = M + (int64_t)S * C::NP;
+  double* out = Lp + (int64_t)i * C::NP;
+  if (part == 0) m2l_contract<P, 0>(Ms, T3, out);
+  if (C::NSPLIT > 1 && part == 1) m2l_contract<P, (C::NSPLIT > 1 ? 1 : 0)>(Ms, T3, out);
+  if (C::NSPLIT > 2 && part == 2) m2l_contract<P, (C::NSPLIT > 2 ? 2 : 0)>(Ms, T3, out);
+}
+
+// L_T = Σ of its pairs' local expansions in list order: one warp per target, lanes over γ
+__global__ void k_fmm_m2l_reduce(int64_t nn, const int32_t* __restrict__ off, const int32_t* __restrict__ ginv,
+                                 int np, const double* __restrict__ Lp, double* __restrict__ L) {
+  const int lane = threadIdx.x & 31;
+  const int64_t T = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (T >= nn) return;
+  const int k0 = off[T], k1 = off[T + 1];
+  if (k0 == k1) return;
+  for (int gi = lane; gi < np; gi += 32) {
+    double acc = 0.0;
+    for (int k = k0; k < k1; ++k) acc += Lp[(int64_t)ginv[k] * np + gi];
+    L[T * np + gi] = acc;
   }
 }
 
@@ -342,46 +420,176 @@ __global__ void k_fmm_l2l(int64_t m, const int32_t* __restrict__ list, FmmGeom g
   }
 }
 
-// L2P + P2P: one warp per FMM leaf, one lane per target point; V and ∇V in fp64, output per op
-template <int DIM>
-__global__ void k_fmm_eval(int64_t m, const int32_t* __restrict__ list, FmmGeom g, const int32_t* __restrict__ off,
-                           const uint64_t* __restrict__ keys, const float4* __restrict__ pts,
-                           const float4* __restrict__ vec, const float* __restrict__ scal, int p,
-                           const double* __restrict__ L, float w2f, int op, const int32_t* __restrict__ out_map,
-                           float* __restrict__ out, float4* __restrict__ out4, double scale) {
+// L2P + P2P: one warp per FMM leaf; V and ∇V in fp64, output per op.  A leaf of n ≤ 16 targets splits the
+// warp into 32 / gs lane groups (gs = the power of two ≥ n): lane (grp, t) takes target t and every
+// (32/gs)-th point of each source leaf, the groups' sums are added by shuffles at the end (a fixed order).
+// Pair terms in fp32 (rsqrt, as the treecode's near field), summed per source leaf in fp32 and across
+// leaves in fp64; the cutoff decided in fp32 on d = x_j − y (R-prec).
+template <int P>
+__device__ __forceinline__ void fmm_pows_t(double x, double* o) {
+  o[0] = 1.0;
+#pragma unroll
+  for (int a = 1; a <= P; ++a) o[a] = o[a - 1] * x / a;
+}
+// L2P of one target: V += Σ_γ L_γ (y−c)^γ/γ!, ∇V likewise (exponents constant after unrolling)
+template <int P, int... J>
+__device__ __forceinline__ void l2p_terms(const double* __restrict__ Lt, const double* px, const double* py,
+                                          const double* pz, double& V, double& gx, double& gy, double& gz,
+                                          std::integer_sequence<int, J...>) {
+  (
+      [&] {
+        constexpr int a = fmm_mi_of(J, 0), b = fmm_mi_of(J, 1), c = fmm_mi_of(J, 2);
+        const double l = __ldg(Lt + J);
+        V += l * (px[a] * py[b] * pz[c]);
+        if constexpr (a > 0) gx += l * (px[a > 0 ? a - 1 : 0] * py[b] * pz[c]);
+        if constexpr (b > 0) gy += l * (px[a] * py[b > 0 ? b - 1 : 0] * pz[c]);
+        if constexpr (c > 0) gz += l * (px[a] * py[b] * pz[c > 0 ? c - 1 : 0]);
+      }(),
+      ...);
+}
+// L2P: one warp per FMM leaf, one lane per target point: (V, ∇V) of the far field into VG (sorted order)
+template <int P>
+__global__ void k_fmm_l2p(int64_t m, const int32_t* __restrict__ list, FmmGeom g, const float4* __restrict__ pts,
+                          const double* __restrict__ L, double4* __restrict__ VG) {
   const int lane = threadIdx.x & 31;
   const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (k >= m) return;
   const int64_t T = list[k];
-  const int np = (p + 1) * (p + 2) * (p + 3) / 6;
-  // a leaf holds ≤ `leaf` ≤ 32 points unless it is a depth-D cell of duplicates: chunks of 32 targets
-  for (int i0 = g.pb[T]; i0 < g.pe[T]; i0 += 32) {
-    const int i = i0 + lane;
-    const bool valid = i < g.pe[T];
+  const double c0 = g.ctr[3 * T], c1 = g.ctr[3 * T + 1], c2 = g.ctr[3 * T + 2];
+  for (int i = g.pb[T] + lane; i < g.pe[T]; i += 32) {
+    const float4 y = pts[i];
+    double px[P + 1], py[P + 1], pz[P + 1];
+    fmm_pows_t<P>((double)y.x - c0, px);
+    fmm_pows_t<P>((double)y.y - c1, py);
+    fmm_pows_t<P>((double)y.z - c2, pz);
     double V = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
-    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (valid) {
-      y = pts[i];
-      double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];
-      fmm_pows((double)y.x - g.ctr[3 * T], p, px);
-      fmm_pows((double)y.y - g.ctr[3 * T + 1], p, py);
-      fmm_pows((double)y.z - g.ctr[3 * T + 2], p, pz);
-      const double* Lt = L + T * np;
-      for (int gi = 0; gi < np; ++gi) {
-        const int g0 = c_mi[gi][0], g1 = c_mi[gi][1], g2 = c_mi[gi][2];
-        const double l = Lt[gi];
-        V += l * (px[g0] * py[g1] * pz[g2]);
-        if (g0 > 0) gx += l * (px[g0 - 1] * py[g1] * pz[g2]);
-        if (g1 > 0) gy += l * (px[g0] * py[g1 - 1] * pz[g2]);
-        if (g2 > 0) gz += l * (px[g0] * py[g1] * pz[g2 - 1]);
-      }
+    l2p_terms<P>(L + T * fmm_np(P), px, py, pz, V, gx, gy, gz, std::make_integer_sequence<int, fmm_np(P)>{});
+    VG[i] = make_double4(V, gx, gy, gz);
+  }
+}
+
+// one target's output from its (V, ∇V): the solver's sorted buffers unscaled (V in .x for A, −∇V for G and
+// Aᵀ), or the caller's layout through out_map, scaled (G = −∇V for dipoles, Aᵀ = −∇V for charges)
+struct FmmOut {
+  int op;
+  const int32_t* out_map;
+  float* out;
+  float4* out4;
+  double scale;
+  __device__ __forceinline__ void put(int i, double V, double gx, double gy, double gz) const {
+    if (out4) {
+      out4[i] = op == OP_A ? make_float4((float)V, 0.f, 0.f, 0.f) : make_float4((float)-gx, (float)-gy, (float)-gz, 0.f);
+      return;
     }
-    // P2P: fp32 pair terms (rsqrt, as the treecode's near field), summed per source leaf in fp32 and across
-    // leaves in fp64; the cutoff decided in fp32 on d = x_j − y (R-prec)
-    for (int kk = off[T]; kk < off[T + 1]; ++kk) {
-      const int S = (int)(uint32_t)keys[kk];
+    const int64_t o = out_map ? (int64_t)out_map[i] : i;
+    if (op == OP_A) {
+      out[o] = (float)(V * scale);
+    } else {
+      out[3 * o] = (float)(-gx * scale);
+      out[3 * o + 1] = (float)(-gy * scale);
+      out[3 * o + 2] = (float)(-gz * scale);
+    }
+  }
+};
+
+// P2P work items: the direct list of a target leaf is cut into items of about kFmmItemWork source points
+// (× target chunks of 32), so that the leaves of sparse regions — a depth-3 leaf of C3 sums 55k source
+// points, the average 870 — spread over many warps instead of one warp ending the launch alone.
+// item = {leaf index li, k0, k1, j (item of its leaf)};  linfo[li] = {T, items of the leaf, partial base, 0}
+constexpr int kFmmItemWork = 2048;
+__global__ void k_fmm_items(int64_t m, const int32_t* __restrict__ leaves, FmmGeom g,
+                            const int32_t* __restrict__ off, const uint64_t* __restrict__ keys,
+                            const uint32_t* __restrict__ ibase, int4* __restrict__ items, uint32_t* __restrict__ nit) {
+  const int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (li >= m) return;
+  const int T = leaves[li];
+  const int chunks = (g.pe[T] - g.pb[T] + 31) / 32;
+  const int k0 = off[T], k1 = off[T + 1];
+  int n = 0, start = k0;
+  int64_t acc = 0;
+  for (int k = k0; k < k1; ++k) {
+    const int S = (int)(uint32_t)keys[k];
+    acc += (int64_t)(g.pe[S] - g.pb[S]) * chunks;
+    if (acc >= kFmmItemWork && k + 1 < k1) {
+      if (items) items[ibase[li] + n] = make_int4((int)li, start, k + 1, n);
+      ++n;
+      start = k + 1;
+      acc = 0;
+    }
+  }
+  if (items) items[ibase[li] + n] = make_int4((int)li, start, k1, n);
+  ++n;
+  if (nit) nit[li] = (uint32_t)n;
+}
+__global__ void k_fmm_linfo(int64_t m, const int32_t* __restrict__ leaves, FmmGeom g, const uint32_t* __restrict__ nit,
+                            uint32_t* __restrict__ psize) {
+  const int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (li >= m) return;
+  const int T = leaves[li];
+  psize[li] = nit[li] > 1 ? nit[li] * (uint32_t)(g.pe[T] - g.pb[T]) : 0u;
+}
+__global__ void k_fmm_linfo2(int64_t m, const int32_t* __restrict__ leaves, const uint32_t* __restrict__ nit,
+                             const uint32_t* __restrict__ pbase, int4* __restrict__ linfo, uint32_t* __restrict__ mflag) {
+  const int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (li >= m) return;
+  linfo[li] = make_int4(leaves[li], (int)nit[li], (int)pbase[li], 0);
+  mflag[li] = nit[li] > 1 ? 1u : 0u;
+}
+
+// P2P of one work item: one warp, a leaf of n ≤ 16 targets split into 32 / gs lane groups (gs = the power
+// of two ≥ n): lane (grp, t) takes target t and every (32/gs)-th point of each source leaf, the groups'
+// sums added by shuffles (a fixed order).  Pair terms in fp32 (rsqrt, as the treecode's near field),
+// summed per source leaf in fp32 and across leaves in fp64; the cutoff decided in fp32 on d = x_j − y
+// (R-prec).  A leaf of one item starts from its far field VG and writes the outputs; the items of a
+// longer list write partial sums, added to VG by k_fmm_combine in item order.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_fmm_eval(int64_t m, const int4* __restrict__ items,
+                                                  const int4* __restrict__ linfo, FmmGeom g,
+                                                  const uint64_t* __restrict__ keys, const float4* __restrict__ pts,
+                                                  const float4* __restrict__ vec, const float* __restrict__ scal,
+                                                  const double4* __restrict__ VG, double4* __restrict__ part,
+                                                  float w2f, FmmOut fo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (k >= m) return;
+  const int4 it = items[k];
+  const int4 li = linfo[it.x];
+  const int T = li.x;
+  const bool single = li.y == 1;
+  const int tb = g.pb[T], te = g.pe[T];
+  int gs = 32;  // lanes per group
+  while (gs > 1 && te - tb <= gs / 2) gs >>= 1;
+  const int grp = lane / gs, ng = 32 / gs, tl = lane % gs;
+  const int kb = it.y, ke = it.z;
+  // a leaf holds ≤ `leaf` ≤ 32 points unless it is a depth-D cell of duplicates: chunks of 32 targets
+  for (int i0 = tb; i0 < te; i0 += 32) {
+    const int i = i0 + tl;
+    const bool valid = i < te;
+    double V = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    const float4 y = valid ? pts[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (single && valid && grp == 0) {  // the far field (k_fmm_l2p)
+      const double4 f = VG[i];
+      V = f.x;
+      gx = f.y;
+      gy = f.z;
+      gz = f.w;
+    }
+    // the next source leaf's range is loaded while the current one is summed (a dependent-load chain)
+    int nb = 0, ne = 0;
+    if (kb < ke) {
+      const int S0 = (int)(uint32_t)keys[kb];
+      nb = g.pb[S0];
+      ne = g.pe[S0];
+    }
+    for (int kk = kb; kk < ke; ++kk) {
+      const int jb = nb, je = ne;
+      if (kk + 1 < ke) {
+        const int S1 = (int)(uint32_t)keys[kk + 1];
+        nb = g.pb[S1];
+        ne = g.pe[S1];
+      }
       float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
-      for (int j = g.pb[S]; j < g.pe[S]; ++j) {
+      for (int j = jb + grp; j < je; j += ng) {
         const float4 x = pts[j];
         const float dxf = x.x - y.x, dyf = x.y - y.y, dzf = x.z - y.z;
         const float d2 = __fmaf_rn(dxf, dxf, __fmaf_rn(dyf, dyf, __fmul_rn(dzf, dzf)));
@@ -411,19 +619,36 @@ __global__ void k_fmm_eval(int64_t m, const int32_t* __restrict__ list, FmmGeom 
       gy += k4 * v2;
       gz += k4 * v3;
     }
-    if (!valid) continue;
-    if (out4) {  // the solver's sorted buffers, unscaled: V in .x (A), or −∇V (G, Aᵀ)
-      out4[i] = op == OP_A ? make_float4((float)V, 0.f, 0.f, 0.f) : make_float4((float)-gx, (float)-gy, (float)-gz, 0.f);
-      continue;
+    for (int o = gs; o < 32; o <<= 1) {  // the groups' sums, lane (0, t) ends with all of target t's
+      V += __shfl_xor_sync(0xffffffffu, V, o);
+      gx += __shfl_xor_sync(0xffffffffu, gx, o);
+      gy += __shfl_xor_sync(0xffffffffu, gy, o);
+      gz += __shfl_xor_sync(0xffffffffu, gz, o);
     }
-    const int64_t o = out_map ? (int64_t)out_map[i] : i;
-    if (op == OP_A) {
-      out[o] = (float)(V * scale);
-    } else {  // G = −∇V (dipoles), Aᵀ = −∇V (charges)
-      out[3 * o] = (float)(-gx * scale);
-      out[3 * o + 1] = (float)(-gy * scale);
-      out[3 * o + 2] = (float)(-gz * scale);
+    if (!valid || grp != 0) continue;
+    if (single) fo.put(i, V, gx, gy, gz);
+    else part[li.z + it.w * (te - tb) + (i - tb)] = make_double4(V, gx, gy, gz);
+  }
+}
+
+// leaves of several items: VG + the items' partial sums in item order, one warp per leaf
+__global__ void k_fmm_combine(int64_t m, const int32_t* __restrict__ mleaves, const int4* __restrict__ linfo,
+                              FmmGeom g, const double4* __restrict__ VG, const double4* __restrict__ part, FmmOut fo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (k >= m) return;
+  const int4 li = linfo[mleaves[k]];
+  const int tb = g.pb[li.x], te = g.pe[li.x];
+  for (int i = tb + lane; i < te; i += 32) {
+    double4 a = VG[i];
+    for (int j = 0; j < li.y; ++j) {
+      const double4 q = part[li.z + j * (te - tb) + (i - tb)];
+      a.x += q.x;
+      a.y += q.y;
+      a.z += q.z;
+      a.w += q.w;
     }
+    fo.put(i, a.x, a.y, a.z, a.w);
   }
 }
 
@@ -490,6 +715,7 @@ wn_status fmm_plan(wn_tree_s* t, int p, double theta, int leafsz, float wsep, cu
   WN_TRY(alloc(&F.leaf_flag, nn, true));
   WN_TRY(alloc(&F.M, (size_t)nn * np * sizeof(double), true));
   WN_TRY(alloc(&F.L, (size_t)nn * np * sizeof(double), true));
+  WN_TRY(alloc(&F.VG, (size_t)std::max<int64_t>(t->n, 1) * sizeof(double4), true));
   k_fmm_geom<<<g256(nn), 256, 0, s>>>(nn, t->D, leafsz, t->pts, t->pb, t->pe, t->cc, t->depth, F.ctr, F.rad,
                                        F.leaf_flag);
   FmmGeom g{t->pb, t->pe, t->cb, t->cc, t->depth, t->parent, F.ctr, F.rad, F.leaf_flag};
@@ -581,6 +807,67 @@ wn_status fmm_plan(wn_tree_s* t, int p, double theta, int leafsz, float wsep, cu
   k_fmm_csr<<<g256(nn + 1), 256, 0, s>>>(nn, F.m2l, F.nm2l, F.om);
   k_fmm_csr<<<g256(nn + 1), 256, 0, s>>>(nn, F.p2p, F.np2p, F.op2);
   count_launches(2);
+  // M2L groups (pairs with one translation vector) and their chunks
+  if (F.nm2l > 0) {
+    const int64_t m = F.nm2l;
+    uint64_t *gk = nullptr, *sk = nullptr;
+    uint32_t *cflag = nullptr, *cpos = nullptr, *gflag = nullptr, *gpos = nullptr;
+    WN_TRY(alloc(&gk, m * sizeof(uint64_t), false));
+    WN_TRY(alloc(&sk, m * sizeof(uint64_t), false));
+    WN_TRY(alloc(&cflag, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&cpos, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&gflag, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&gpos, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&F.gidx, m * sizeof(int32_t), true));
+    WN_TRY(alloc(&F.ginv, m * sizeof(int32_t), true));
+    k_fmm_m2l_gkey<<<g256(m), 256, 0, s>>>(m, F.m2l, g, gk);
+    count_launches(1);
+    WN_TRY(sort_keys_u64_perm(gk, m, 63, sk, F.gidx, s));
+    k_fmm_m2l_ginfo<<<g256(m), 256, 0, s>>>(m, sk, F.gidx, m2l_chunk(p), cflag, gflag, F.ginv);
+    uint32_t tot[2] = {0, 0};
+    WN_TRY(fmm_scan(cflag, cpos, m, cpos + m, s));
+    WN_TRY(fmm_scan(gflag, gpos, m, gpos + m, s));
+    WN_CUDA(cudaMemcpyAsync(&tot[0], cpos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaMemcpyAsync(&tot[1], gpos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaStreamSynchronize(s));
+    F.nchunk = tot[0];
+    F.ngroups = tot[1];
+    WN_TRY(alloc(&F.chunks, (F.nchunk + 1) * sizeof(int32_t), true));
+    k_fmm_chunks<<<g256(m + 1), 256, 0, s>>>(m, cflag, cpos, F.chunks);
+    WN_TRY(alloc(&F.Lp, (size_t)m * np * sizeof(double), true));
+    count_launches(2);
+  }
+  // P2P work items of the target leaves (k_fmm_items), the partial-sum slots of the leaves of several
+  {
+    const int64_t m = F.nleaves;
+    uint32_t *nit = nullptr, *ibase = nullptr, *psize = nullptr, *pbase = nullptr, *mflag = nullptr, *mpos = nullptr;
+    WN_TRY(alloc(&nit, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&ibase, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&psize, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&pbase, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&mflag, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&mpos, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&F.linfo, std::max<int64_t>(m, 1) * sizeof(int4), true));
+    k_fmm_items<<<g256(m), 256, 0, s>>>(m, F.leaves, g, F.op2, F.p2p, nullptr, nullptr, nit);
+    k_fmm_linfo<<<g256(m), 256, 0, s>>>(m, F.leaves, g, nit, psize);
+    WN_TRY(fmm_scan(nit, ibase, m, ibase + m, s));
+    WN_TRY(fmm_scan(psize, pbase, m, pbase + m, s));
+    k_fmm_linfo2<<<g256(m), 256, 0, s>>>(m, F.leaves, nit, pbase, F.linfo, mflag);
+    WN_TRY(fmm_scan(mflag, mpos, m, mpos + m, s));
+    uint32_t tot[3] = {0, 0, 0};
+    WN_CUDA(cudaMemcpyAsync(&tot[0], ibase + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaMemcpyAsync(&tot[1], pbase + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaMemcpyAsync(&tot[2], mpos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaStreamSynchronize(s));
+    F.nitems = tot[0];
+    F.nmleaves = tot[2];
+    WN_TRY(alloc(&F.items, std::max<int64_t>(F.nitems, 1) * sizeof(int4), true));
+    WN_TRY(alloc(&F.part, std::max<uint32_t>(tot[1], 1) * sizeof(double4), true));
+    WN_TRY(alloc(&F.mleaves, std::max<int64_t>(F.nmleaves, 1) * sizeof(int32_t), true));
+    k_fmm_items<<<g256(m), 256, 0, s>>>(m, F.leaves, g, F.op2, F.p2p, ibase, F.items, nullptr);
+    k_fmm_compact<<<g256(m), 256, 0, s>>>(m, mflag, mpos, F.mleaves);
+    count_launches(5);
+  }
   WN_CUDA(cudaGetLastError());
   WN_CUDA(cudaStreamSynchronize(s));  // (the temporaries above are freed stream-ordered on return)
   F.p = p;
@@ -613,29 +900,48 @@ wn_status fmm_run(wn_tree_s* t, int op, const float4* vec, const float* scal, fl
       k_fmm_m2m<<<gwarps(F.ninner[l], wpb), 32 * wpb, 0, s>>>(F.ninner[l], F.inner[l], g, p, F.M);
       ++launches;
     }
-  static int m2l_blocks = 0;  // a resident grid (the blocks build their index tables once)
-  if (!m2l_blocks) {
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fmm_m2l, 32 * kFmmWarps, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    m2l_blocks = std::max(1, per_sm * sms);
+  if (F.nchunk > 0) {
+    switch (p) {
+#define WN_M2L_CASE(PP)                                                                                    \
+  case PP:                                                                                                 \
+    k_fmm_m2l_grp<PP><<<(unsigned)F.nchunk, M2lCfg<PP>::THREADS, 0, s>>>(F.chunks, F.gidx, F.m2l, g, F.M, F.Lp); \
+    break;
+      WN_M2L_CASE(1)
+      WN_M2L_CASE(2)
+      WN_M2L_CASE(3)
+      WN_M2L_CASE(4)
+      WN_M2L_CASE(5)
+      WN_M2L_CASE(6)
+#undef WN_M2L_CASE
+    }
+    k_fmm_m2l_reduce<<<gwarps(nn, wpb), 32 * wpb, 0, s>>>(nn, F.om, F.ginv, np, F.Lp, F.L);
+    launches += 2;
   }
-  k_fmm_m2l<<<(unsigned)std::min<int64_t>(m2l_blocks, gwarps(nn, kFmmWarps)), 32 * kFmmWarps, 0, s>>>(nn, F.om, F.m2l,
-                                                                                                   g, p, F.M, F.L);
-  ++launches;
   for (int l = 1; l <= D; ++l)
     if (F.nkids[l]) {
       k_fmm_l2l<<<gwarps(F.nkids[l], wpb), 32 * wpb, 0, s>>>(F.nkids[l], F.kids[l], g, p, F.L);
       ++launches;
     }
   const float w2f = w * w;
+  switch (p) {
+#define WN_L2P_CASE(PP)                                                                                       \
+  case PP:                                                                                                    \
+    k_fmm_l2p<PP><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, t->pts, F.L, F.VG);     \
+    break;
+    WN_L2P_CASE(1) WN_L2P_CASE(2) WN_L2P_CASE(3) WN_L2P_CASE(4) WN_L2P_CASE(5) WN_L2P_CASE(6)
+#undef WN_L2P_CASE
+  }
+  const FmmOut fo{op, out_map, out, out4, scale};
   if (vec)
-    k_fmm_eval<3><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, F.op2, F.p2p, t->pts, vec, scal,
-                                                             p, F.L, w2f, op, out_map, out, out4, scale);
+    k_fmm_eval<3><<<gwarps(F.nitems, wpb), 32 * wpb, 0, s>>>(F.nitems, F.items, F.linfo, g, F.p2p, t->pts, vec, scal,
+                                                            F.VG, F.part, w2f, fo);
   else
-    k_fmm_eval<1><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, F.op2, F.p2p, t->pts, vec, scal,
-                                                             p, F.L, w2f, op, out_map, out, out4, scale);
+    k_fmm_eval<1><<<gwarps(F.nitems, wpb), 32 * wpb, 0, s>>>(F.nitems, F.items, F.linfo, g, F.p2p, t->pts, vec, scal,
+                                                            F.VG, F.part, w2f, fo);
+  if (F.nmleaves) {
+    k_fmm_combine<<<gwarps(F.nmleaves, wpb), 32 * wpb, 0, s>>>(F.nmleaves, F.mleaves, F.linfo, g, F.VG, F.part, fo);
+    ++launches;
+  }
   ++launches;
   count_launches(launches);
   WN_CUDA(cudaGetLastError());

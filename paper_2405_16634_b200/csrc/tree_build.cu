@@ -592,6 +592,20 @@ wn_status sort_keys_u64(const uint64_t* keys, int64_t n, int bits, uint64_t* out
   count_launches(1);
   return sort_pairs(ka, va, n, bits, vo, s, out);
 }
+// the same, also returning the permutation: perm[k] = the input position of the k-th sorted key
+wn_status sort_keys_u64_perm(const uint64_t* keys, int64_t n, int bits, uint64_t* out, int32_t* perm,
+                             cudaStream_t s) {
+  if (n <= 0) return WN_OK;
+  TempSet tmp(s);
+  uint64_t* ka = nullptr;
+  int32_t* va = nullptr;
+  WN_TRY(tmp.alloc(&ka, n));
+  WN_TRY(tmp.alloc(&va, n));
+  WN_CUDA(cudaMemcpyAsync(ka, keys, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, va);
+  count_launches(1);
+  return sort_pairs(ka, va, n, bits, perm, s, out);
+}
 
 wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s) {
   if (n <= 0) return WN_OK;

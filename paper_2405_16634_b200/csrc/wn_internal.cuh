@@ -109,6 +109,19 @@ struct FmmPlan {
   uint64_t *m2l = nullptr, *p2p = nullptr;  // sorted (target << 32 | source)
   int64_t nm2l = 0, np2p = 0;
   int32_t *om = nullptr, *op2 = nullptr;    // CSR offsets per target node
+  // M2L pairs grouped by their translation vector c_t − c_s (equal vectors ⇒ one derivative tensor):
+  // gidx = the m2l positions in group order, ginv its inverse, chunks = [start) of ≤ kChunk pairs of one
+  // group (nchunk + 1 entries), Lp = the per-pair local expansions in group order (nm2l × np)
+  int32_t *gidx = nullptr, *ginv = nullptr, *chunks = nullptr;
+  int64_t nchunk = 0, ngroups = 0;
+  double* Lp = nullptr;
+  double4* VG = nullptr;  // per sorted point: the far field (V, ∇V) from L2P
+  // P2P work items {leaf index, list range, item of its leaf}, per leaf {T, items, partial base}, the
+  // leaves of several items (combined from partial sums)
+  int4 *items = nullptr, *linfo = nullptr;
+  int64_t nitems = 0, nmleaves = 0;
+  int32_t* mleaves = nullptr;
+  double4* part = nullptr;
   std::vector<void*> owned;
 };
 // Query shards of a multi-GPU solve: schedule positions [b[r], b[r+1]) for rank r, multiples of
@@ -214,6 +227,8 @@ wn_status hilbert_schedule(const float4* pts, int64_t n, int32_t* order, cudaStr
 wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t s);
 // ascending stable sort of n 64-bit keys on their low `bits` bits into out (device)
 wn_status sort_keys_u64(const uint64_t* keys, int64_t n, int bits, uint64_t* out, cudaStream_t s);
+wn_status sort_keys_u64_perm(const uint64_t* keys, int64_t n, int bits, uint64_t* out, int32_t* perm,
+                             cudaStream_t s);
 
 // ---- moments (moments.cu) ----
 // Build node records for attribute `kind` into `out`.  vec: float4 ν (sorted order), scal: float s.
