@@ -116,64 +116,6 @@ __global__ void k_fmm_geom(int64_t nn, int D, int leafsz, const float4* __restri
   leaf[i] = (cc[i] == 0 || pe[i] - pb[i] <= leafsz) ? 1 : 0;
 }
 
-// P2M: one warp per FMM leaf, lanes over the coefficients β
-template <int DIM>
-__global__ void k_fmm_p2m(int64_t m, const int32_t* __restrict__ list, FmmGeom g, const float4* __restrict__ pts,
-                          const float4* __restrict__ vec, const float* __restrict__ scal, int p,
-                          double* __restrict__ M) {
-  const int lane = threadIdx.x & 31;
-  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (k >= m) return;
-  const int64_t id = list[k];
-  const int np = (p + 1) * (p + 2) * (p + 3) / 6;
-  const double c0 = g.ctr[3 * id], c1 = g.ctr[3 * id + 1], c2 = g.ctr[3 * id + 2];
-  for (int b = lane; b < np; b += 32) {
-    const int b0 = c_mi[b][0], b1 = c_mi[b][1], b2 = c_mi[b][2], deg = b0 + b1 + b2;
-    double acc = 0.0;
-    for (int j = g.pb[id]; j < g.pe[id]; ++j) {
-      const float4 x = pts[j];
-      double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];
-      fmm_pows((double)x.x - c0, p, px);
-      fmm_pows((double)x.y - c1, p, py);
-      fmm_pows((double)x.z - c2, p, pz);
-      if (DIM == 1) {
-        acc += (double)scal[j] * ((deg & 1) ? -1.0 : 1.0) * (px[b0] * py[b1] * pz[b2]);
-      } else {
-        const float4 v = vec[j];
-        const double sg = ((deg - 1) & 1) ? -1.0 : 1.0;
-        if (b0 > 0) acc += (double)v.x * sg * (px[b0 - 1] * py[b1] * pz[b2]);
-        if (b1 > 0) acc += (double)v.y * sg * (px[b0] * py[b1 - 1] * pz[b2]);
-        if (b2 > 0) acc += (double)v.z * sg * (px[b0] * py[b1] * pz[b2 - 1]);
-      }
-    }
-    M[id * np + b] = acc;
-  }
-}
-
-// M2M: one warp per internal active node of one level, its children in order
-__global__ void k_fmm_m2m(int64_t m, const int32_t* __restrict__ list, FmmGeom g, int p, double* __restrict__ M) {
-  const int lane = threadIdx.x & 31;
-  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (k >= m) return;
-  const int64_t id = list[k];
-  const int np = (p + 1) * (p + 2) * (p + 3) / 6;
-  for (int b = lane; b < np; b += 32) {
-    const int b0 = c_mi[b][0], b1 = c_mi[b][1], b2 = c_mi[b][2];
-    double acc = 0.0;
-    for (int c = g.cb[id]; c < g.cb[id] + g.cc[id]; ++c) {
-      double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];  // (c' − c): parent − child
-      fmm_pows(g.ctr[3 * id] - g.ctr[3 * c], p, px);
-      fmm_pows(g.ctr[3 * id + 1] - g.ctr[3 * c + 1], p, py);
-      fmm_pows(g.ctr[3 * id + 2] - g.ctr[3 * c + 2], p, pz);
-      const double* Mc = M + (int64_t)c * np;
-      for (int g0 = 0; g0 <= b0; ++g0)
-        for (int g1 = 0; g1 <= b1; ++g1)
-          for (int g2 = 0; g2 <= b2; ++g2) acc += Mc[c_lut[g0][g1][g2]] * (px[b0 - g0] * py[b1 - g1] * pz[b2 - g2]);
-    }
-    M[id * np + b] = acc;
-  }
-}
-
 // breadth-first dual traversal, one level of cell pairs: the oracle's fmm_dual decisions, appended by atomics
 __global__ void k_fmm_dual(int64_t m, const int2* __restrict__ in, FmmGeom g, double theta, double w,
                            int2* __restrict__ next, unsigned long long* __restrict__ cnt, int64_t cap_next,
@@ -255,10 +197,11 @@ constexpr int fmm_mi_of(int j, int comp) {
 template <int P>
 struct M2lCfg {
   static constexpr int NP = fmm_np(P), E = 2 * P + 1, NT3 = E * E * E;
-  static constexpr int NSPLIT = NP <= 35 ? 1 : (NP + 27) / 28;  // γ parts per pair (≤ 28 accumulators each)
+  static constexpr int NSPLIT = (NP + 19) / 20;  // γ parts (≤ 20 accumulators per pair each)
   static constexpr int GCH = (NP + NSPLIT - 1) / NSPLIT;
-  static constexpr int CHP = NSPLIT == 1 ? 128 : 64;              // pairs per block
-  static constexpr int THREADS = CHP * NSPLIT;
+  static constexpr int CHP = NP <= 35 ? 128 : 64;  // pairs per block, two per thread (one T load, two FMAs)
+  static constexpr int HALF = CHP / 2;
+  static constexpr int THREADS = HALF * NSPLIT;
 };
 inline int m2l_chunk(int p) { return fmm_np(p) <= 35 ? 128 : 64; }
 
@@ -290,61 +233,97 @@ __global__ void k_fmm_m2l_ginfo(int64_t m, const uint64_t* __restrict__ skey, co
   ginv[gidx[i]] = (int32_t)i;
 }
 __global__ void k_fmm_chunks(int64_t m, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
-                             int32_t* __restrict__ chunks) {
+                             const uint32_t* __restrict__ gflag, const uint32_t* __restrict__ gpos,
+                             int32_t* __restrict__ chunks, int32_t* __restrict__ cgroup, int32_t* __restrict__ gstart) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < m && flag[i]) chunks[pos[i]] = (int32_t)i;
+  if (i < m && flag[i]) {
+    chunks[pos[i]] = (int32_t)i;
+    cgroup[pos[i]] = (int32_t)(gpos[i] + gflag[i]) - 1;  // the group of pair i
+  }
+  if (i < m && gflag[i]) gstart[gpos[i]] = (int32_t)i;
   if (i == m) chunks[pos[m]] = (int32_t)m;
 }
 
 template <int P, int G0, int... J>
-__device__ __forceinline__ void m2l_row(double mb, const double* __restrict__ tb, double* acc,
-                                        std::integer_sequence<int, J...>) {
+__device__ __forceinline__ void m2l_row(double ma, double mb, const double* __restrict__ tb, double* acc_a,
+                                        double* acc_b, std::integer_sequence<int, J...>) {
   using C = M2lCfg<P>;
-  ((G0 + J < C::NP ? (void)(acc[J] = fma(mb, tb[std::integral_constant<int, fmm_box_of(G0 + J, C::E)>::value],
-                                         acc[J]))
-                   : (void)0),
-   ...);
+  (
+      [&] {
+        if constexpr (G0 + J < C::NP) {
+          const double tv = tb[std::integral_constant<int, fmm_box_of(G0 + J, C::E)>::value];
+          acc_a[J] = fma(ma, tv, acc_a[J]);
+          acc_b[J] = fma(mb, tv, acc_b[J]);
+        }
+      }(),
+      ...);
 }
+// two pairs (sources Ma, Mb) of one group, the γ of part PART: out_x[γ] = Σ_β M_x,β T_(β+γ)
 template <int P, int PART>
-__device__ __forceinline__ void m2l_contract(const double* __restrict__ Ms, const double* T3, double* __restrict__ out) {
+__device__ __forceinline__ void m2l_contract(const double* Ma, const double* Mb, const double* T3, double* oa,
+                                             double* ob) {
   using C = M2lCfg<P>;
   constexpr int G0 = PART * C::GCH;
-  double acc[C::GCH];
+  double acc_a[C::GCH], acc_b[C::GCH];
 #pragma unroll
-  for (int j = 0; j < C::GCH; ++j) acc[j] = 0.0;
+  for (int j = 0; j < C::GCH; ++j) acc_a[j] = acc_b[j] = 0.0;
 #pragma unroll 1
   for (int be = 0; be < C::NP; ++be) {
     const int base = (c_mi[be][0] * C::E + c_mi[be][1]) * C::E + c_mi[be][2];  // warp-uniform
-    m2l_row<P, G0>(__ldg(Ms + be), T3 + base, acc, std::make_integer_sequence<int, C::GCH>{});
+    m2l_row<P, G0>(Ma[be * C::CHP], Mb[be * C::CHP], T3 + base, acc_a, acc_b,
+                   std::make_integer_sequence<int, C::GCH>{});
   }
 #pragma unroll
-  for (int j = 0; j < C::GCH; ++j)
-    if (G0 + j < C::NP) out[G0 + j] = acc[j];
+  for (int j = 0; j < C::GCH; ++j) {
+    oa[j] = acc_a[j];
+    ob[j] = acc_b[j];
+  }
+}
+template <int P, int PART>
+__device__ __forceinline__ void m2l_part(int part, const double* Ma, const double* Mb, const double* T3, double* oa,
+                                         double* ob) {
+  if constexpr (PART < M2lCfg<P>::NSPLIT) {
+    if (part == PART) m2l_contract<P, PART>(Ma, Mb, T3, oa, ob);
+    else m2l_part<P, PART + 1>(part, Ma, Mb, T3, oa, ob);
+  }
 }
 
+// the j-th multi-index (c_mi order) of degree ≤ 12, arithmetically (no divergent constant-memory lookups)
+__device__ __forceinline__ void fmm_mi_dev(int j, int& a, int& b, int& c) {
+  int n = 0;
+  while (j >= (n + 1) * (n + 2) * (n + 3) / 6) ++n;
+  int rem = j - n * (n + 1) * (n + 2) / 6;
+  a = n;
+  while (rem > n - a) {
+    rem -= n - a + 1;
+    --a;
+  }
+  b = n - a - rem;
+  c = n - a - b;
+}
+// the derivative tensor T_δ = ∂^δΦ(R), |δ| ≤ 2P, of every M2L group (plan time: T depends on the geometry
+// only), one block per group, graded order.  b_δ by degree:
+//   |δ||R|² b_δ = −(2|δ|−1) Σ_i R_i b_(δ−e_i) − (|δ|−1) Σ_i b_(δ−2e_i),  b_0 = 1/|R|,  T_δ = δ! b_δ / (4π)
 template <int P>
-__global__ void __launch_bounds__(M2lCfg<P>::THREADS) k_fmm_m2l_grp(const int32_t* __restrict__ chunks,
-                                                                     const int32_t* __restrict__ gidx,
-                                                                     const uint64_t* __restrict__ m2l, FmmGeom g,
-                                                                     const double* __restrict__ M,
-                                                                     double* __restrict__ Lp) {
+__global__ void __launch_bounds__(128) k_fmm_m2l_tensor(const int32_t* __restrict__ gstart,
+                                                        const int32_t* __restrict__ gidx,
+                                                        const uint64_t* __restrict__ m2l, FmmGeom g,
+                                                        double* __restrict__ Tg) {
   using C = M2lCfg<P>;
+  constexpr int E = C::E, E2 = E * E, NPT = fmm_np(2 * P);
   __shared__ double T3[C::NT3];
   const int tid = threadIdx.x;
-  const int i0 = chunks[blockIdx.x], i1 = chunks[blockIdx.x + 1];
-  const uint64_t k0 = m2l[gidx[i0]];
+  const uint64_t k0 = m2l[gidx[gstart[blockIdx.x]]];
   const int Tn = (int)(k0 >> 32), Sn = (int)(uint32_t)k0;
   const double R0 = g.ctr[3 * Tn] - g.ctr[3 * Sn], R1 = g.ctr[3 * Tn + 1] - g.ctr[3 * Sn + 1],
                R2 = g.ctr[3 * Tn + 2] - g.ctr[3 * Sn + 2];
   const double r2 = R0 * R0 + R1 * R1 + R2 * R2;
-  constexpr int E = C::E, E2 = E * E;
-  // b_δ by degree: |δ||R|² b_δ = −(2|δ|−1) Σ_i R_i b_(δ−e_i) − (|δ|−1) Σ_i b_(δ−2e_i)   (1/|R| = b_0)
   if (tid == 0) T3[0] = 1.0 / sqrt(r2);
   __syncthreads();
   for (int n = 1; n <= 2 * P; ++n) {
     const int cnt = (n + 1) * (n + 2) / 2;
     const double c1 = 2.0 * n - 1.0, c2 = n - 1.0, inv = 1.0 / (n * r2);
-    for (int e = tid; e < cnt; e += C::THREADS) {
+    for (int e = tid; e < cnt; e += 128) {
       int a = n, rem = e;  // e-th (a, b) with a descending, then b descending
       while (rem > n - a) {
         rem -= n - a + 1;
@@ -363,68 +342,91 @@ __global__ void __launch_bounds__(M2lCfg<P>::THREADS) k_fmm_m2l_grp(const int32_
     }
     __syncthreads();
   }
-  // T_δ = ∂^δΦ(R) = δ! b_δ / (4π)
-  for (int e = tid; e < C::NT3; e += C::THREADS) {
-    const int a = e / E2, b = (e / E) % E, c = e % E;
-    if (a + b + c <= 2 * P) T3[e] *= c_fact[a] * c_fact[b] * c_fact[c] * 0.0795774715459476679;
+  for (int j = tid; j < NPT; j += 128) {
+    int a, b, c;
+    fmm_mi_dev(j, a, b, c);
+    Tg[(int64_t)blockIdx.x * NPT + j] = T3[(a * E + b) * E + c] * (c_fact[a] * c_fact[b] * c_fact[c] * 0.0795774715459476679);
+  }
+}
+
+template <int P>
+constexpr size_t m2l_smem() {
+  return (size_t)(M2lCfg<P>::NT3 + M2lCfg<P>::CHP * M2lCfg<P>::NP) * sizeof(double) + M2lCfg<P>::CHP * sizeof(int);
+}
+// one chunk of ≤ CHP pairs of one group: the group's tensor into a (2P+1)³ box in shared memory, the
+// sources' coefficients staged [β][pair], two pairs per thread, the outputs written back as one run
+template <int P>
+__global__ void __launch_bounds__(M2lCfg<P>::THREADS) k_fmm_m2l_grp(const int32_t* __restrict__ chunks,
+                                                                     const int32_t* __restrict__ cgroup,
+                                                                     const int32_t* __restrict__ gidx,
+                                                                     const uint64_t* __restrict__ m2l,
+                                                                     const double* __restrict__ Tg,
+                                                                     const double* __restrict__ M,
+                                                                     double* __restrict__ Lp) {
+  using C = M2lCfg<P>;
+  constexpr int E = C::E, NPT = fmm_np(2 * P);
+  extern __shared__ double smem[];
+  double* T3 = smem;                      // the group's derivative tensor, box layout
+  double* sMO = smem + C::NT3;            // the chunk's multipole coefficients [β][pair], then outputs [pair][γ]
+  int* sS = reinterpret_cast<int*>(sMO + C::CHP * C::NP);
+  const int tid = threadIdx.x;
+  const int i0 = chunks[blockIdx.x], i1 = chunks[blockIdx.x + 1], npair = i1 - i0;
+  const double* Tgr = Tg + (int64_t)cgroup[blockIdx.x] * NPT;
+  for (int j = tid; j < NPT; j += C::THREADS) {
+    int a, b, c;
+    fmm_mi_dev(j, a, b, c);
+    T3[(a * E + b) * E + c] = __ldg(Tgr + j);
+  }
+  for (int e = tid; e < npair; e += C::THREADS) sS[e] = (int)(uint32_t)m2l[gidx[i0 + e]];
+  __syncthreads();
+  // the sources' coefficients, staged (each pair's np values contiguous in M: coalesced runs)
+  for (int e = tid; e < npair * C::NP; e += C::THREADS) {
+    const int pr = e / C::NP, be = e - pr * C::NP;
+    sMO[be * C::CHP + pr] = __ldg(M + (int64_t)sS[pr] * C::NP + be);
   }
   __syncthreads();
-  const int part = tid / C::CHP, i = i0 + tid % C::CHP;
-  if (i >= i1) return;
-  const int S = (int)(uint32_t)m2l[gidx[i]];
-  WN_DCHECK(S >= 0 && (int)(m2l[gidx[i]] >> 32) >= 0, "M2L pair");
-  const double* Ms = M + (int64_t)S * C::NP;
-  double* out = Lp + (int64_t)i * C::NP;
-  if (part == 0) m2l_contract<P, 0>(Ms, T3, out);
-  if (C::NSPLIT > 1 && part == 1) m2l_contract<P, (C::NSPLIT > 1 ? 1 : 0)>(Ms, T3, out);
-  if (C::NSPLIT > 2 && part == 2) m2l_contract<P, (C::NSPLIT > 2 ? 2 : 0)>(Ms, T3, out);
-}
-
-// L_T = Σ of its pairs' local expansions in list order: one warp per target, lanes over γ
-__global__ void k_fmm_m2l_reduce(int64_t nn, const int32_t* __restrict__ off, const int32_t* __restrict__ ginv,
-                                 int np, const double* __restrict__ Lp, double* __restrict__ L) {
-  const int lane = threadIdx.x & 31;
-  const int64_t T = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (T >= nn) return;
-  const int k0 = off[T], k1 = off[T + 1];
-  if (k0 == k1) return;
-  for (int gi = lane; gi < np; gi += 32) {
-    double acc = 0.0;
-    for (int k = k0; k < k1; ++k) acc += Lp[(int64_t)ginv[k] * np + gi];
-    L[T * np + gi] = acc;
-  }
-}
-
-// L2L: one warp per child of an internal active node of one level: L_c += shift of the parent's L
-__global__ void k_fmm_l2l(int64_t m, const int32_t* __restrict__ list, FmmGeom g, int p, double* __restrict__ L) {
-  const int lane = threadIdx.x & 31;
-  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (k >= m) return;
-  const int64_t c = list[k];  // a node whose parent is an internal active node
-  const int64_t par = g.parent[c];
-  const int np = (p + 1) * (p + 2) * (p + 3) / 6;
-  double px[kFmmMaxP + 1], py[kFmmMaxP + 1], pz[kFmmMaxP + 1];  // (c' − c): child − parent
-  fmm_pows(g.ctr[3 * c] - g.ctr[3 * par], p, px);
-  fmm_pows(g.ctr[3 * c + 1] - g.ctr[3 * par + 1], p, py);
-  fmm_pows(g.ctr[3 * c + 2] - g.ctr[3 * par + 2], p, pz);
-  const double* Lp = L + par * np;
-  for (int dl = lane; dl < np; dl += 32) {
-    const int d0 = c_mi[dl][0], d1 = c_mi[dl][1], d2 = c_mi[dl][2];
-    double acc = 0.0;
-    for (int gi = 0; gi < np; ++gi) {
-      const int g0 = c_mi[gi][0] - d0, g1 = c_mi[gi][1] - d1, g2 = c_mi[gi][2] - d2;
-      if (g0 < 0 || g1 < 0 || g2 < 0) continue;
-      acc += Lp[gi] * (px[g0] * py[g1] * pz[g2]);
+  const int part = tid / C::HALF, pa = tid % C::HALF, pb = pa + C::HALF;
+  double outa[C::GCH], outb[C::GCH];
+  const bool va = pa < npair, vb = pb < npair;
+  if (va) m2l_part<P, 0>(part, sMO + pa, sMO + (vb ? pb : pa), T3, outa, outb);
+  __syncthreads();  // every thread has read the staged coefficients
+  if (va) {
+#pragma unroll
+    for (int j = 0; j < C::GCH; ++j) {
+      const int gi = part * C::GCH + j;
+      if (gi < C::NP) {
+        sMO[pa * C::NP + gi] = outa[j];
+        if (vb) sMO[pb * C::NP + gi] = outb[j];
+      }
     }
-    L[c * np + dl] += acc;
   }
+  __syncthreads();
+  double* dst = Lp + (int64_t)i0 * C::NP;  // the chunk's pairs are consecutive in group order: one coalesced run
+  for (int e = tid; e < npair * C::NP; e += C::THREADS) dst[e] = sMO[e];
 }
 
-// L2P + P2P: one warp per FMM leaf; V and ∇V in fp64, output per op.  A leaf of n ≤ 16 targets splits the
-// warp into 32 / gs lane groups (gs = the power of two ≥ n): lane (grp, t) takes target t and every
-// (32/gs)-th point of each source leaf, the groups' sums are added by shuffles at the end (a fixed order).
-// Pair terms in fp32 (rsqrt, as the treecode's near field), summed per source leaf in fp32 and across
-// leaves in fp64; the cutoff decided in fp32 on d = x_j − y (R-prec).
+// L_T = Σ of its pairs' local expansions in list order: one thread per (target with a list, γ)
+__global__ void k_fmm_m2l_reduce(int64_t m, const int32_t* __restrict__ targets, const int32_t* __restrict__ off,
+                                 const int32_t* __restrict__ ginv, int np, const double* __restrict__ Lp,
+                                 double* __restrict__ L) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= m * np) return;
+  const int64_t T = targets[t / np];
+  const int gi = (int)(t % np);
+  const int k0 = off[T], k1 = off[T + 1];
+  double acc = 0.0;
+  for (int k = k0; k < k1; ++k) acc += Lp[(int64_t)ginv[k] * np + gi];
+  L[T * np + gi] = acc;
+}
+// targets with a non-empty M2L list
+__global__ void k_fmm_has_list(int64_t nn, const int32_t* __restrict__ off, uint32_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nn) flag[i] = off[i + 1] > off[i] ? 1u : 0u;
+}
+
+// ---- P2M, M2M, L2L: one thread per cell, the degree P a template parameter, so that every multi-index
+// (and every β − γ of a shift) is a compile-time constant and the coefficients stay in registers; the
+// β of a cell are done in parts of ≤ kFmmPart accumulators (one part for p ≤ 4) ----
 template <int P>
 __device__ __forceinline__ void fmm_pows_t(double x, double* o) {
   o[0] = 1.0;
@@ -447,6 +449,162 @@ __device__ __forceinline__ void l2p_terms(const double* __restrict__ Lt, const d
       }(),
       ...);
 }
+constexpr int kFmmPart = 35;
+template <int P>
+struct ShiftCfg {
+  static constexpr int NP = fmm_np(P), NPART = (NP + kFmmPart - 1) / kFmmPart,
+                       NB = (NP + NPART - 1) / NPART;
+};
+template <int J>
+struct Mi {
+  static constexpr int a = fmm_mi_of(J, 0), b = fmm_mi_of(J, 1), c = fmm_mi_of(J, 2), deg = a + b + c;
+};
+// the shift of one source coefficient v = src_G into the part's accumulators:
+//   UP (M2M): acc_β += v·d^(β−G)/(β−G)!  for β ≥ G;   down (L2L): acc_δ += v·d^(G−δ)/(G−δ)!  for δ ≤ G
+template <int P, int B0, bool UP, int G, int... J>
+__device__ __forceinline__ void shift_terms(double v, const double* px, const double* py, const double* pz,
+                                            double* acc, std::integer_sequence<int, J...>) {
+  (
+      [&] {
+        constexpr int B = B0 + J;
+        if constexpr (B < ShiftCfg<P>::NP) {
+          constexpr int e0 = UP ? Mi<B>::a - Mi<G>::a : Mi<G>::a - Mi<B>::a;
+          constexpr int e1 = UP ? Mi<B>::b - Mi<G>::b : Mi<G>::b - Mi<B>::b;
+          constexpr int e2 = UP ? Mi<B>::c - Mi<G>::c : Mi<G>::c - Mi<B>::c;
+          if constexpr (e0 >= 0 && e1 >= 0 && e2 >= 0) acc[J] = fma(v, px[e0] * py[e1] * pz[e2], acc[J]);
+        }
+      }(),
+      ...);
+}
+template <int P, int B0, bool UP, int... G>
+__device__ __forceinline__ void shift_all(const double* __restrict__ src, const double* px, const double* py,
+                                          const double* pz, double* acc, std::integer_sequence<int, G...>) {
+  ((shift_terms<P, B0, UP, G>(__ldg(src + G), px, py, pz, acc, std::make_integer_sequence<int, ShiftCfg<P>::NB>{})),
+   ...);
+}
+
+// P2M  M_β = Σ_j [ q_j (−1)^|β| (x_j−c)^β/β! + Σ_k ν_jk (−1)^(|β|−1) (x_j−c)^(β−e_k)/(β−e_k)! ], one thread per leaf
+template <int DIM, int P, int B0, int... J>
+__device__ __forceinline__ void p2m_terms(double q, double vx, double vy, double vz, const double* px,
+                                          const double* py, const double* pz, double* acc,
+                                          std::integer_sequence<int, J...>) {
+  (
+      [&] {
+        constexpr int B = B0 + J;
+        if constexpr (B < ShiftCfg<P>::NP) {
+          constexpr int a = Mi<B>::a, b = Mi<B>::b, c = Mi<B>::c;
+          if constexpr (DIM == 1) {
+            constexpr double sg = (Mi<B>::deg & 1) ? -1.0 : 1.0;
+            acc[J] = fma(sg * q, px[a] * py[b] * pz[c], acc[J]);
+          } else {
+            constexpr double sg = ((Mi<B>::deg + 1) & 1) ? -1.0 : 1.0;  // (−1)^(|β|−1)
+            double t = 0.0;
+            if constexpr (a > 0) t = fma(vx, px[a > 0 ? a - 1 : 0] * py[b] * pz[c], t);
+            if constexpr (b > 0) t = fma(vy, px[a] * py[b > 0 ? b - 1 : 0] * pz[c], t);
+            if constexpr (c > 0) t = fma(vz, px[a] * py[b] * pz[c > 0 ? c - 1 : 0], t);
+            acc[J] = fma(sg, t, acc[J]);
+          }
+        }
+      }(),
+      ...);
+}
+template <int DIM, int P, int PART>
+__device__ __forceinline__ void p2m_part(int64_t id, FmmGeom g, const float4* __restrict__ pts,
+                                         const float4* __restrict__ vec, const float* __restrict__ scal,
+                                         double* __restrict__ M) {
+  using C = ShiftCfg<P>;
+  if constexpr (PART < C::NPART) {
+    constexpr int B0 = PART * C::NB;
+    double acc[C::NB];
+#pragma unroll
+    for (int j = 0; j < C::NB; ++j) acc[j] = 0.0;
+    const double c0 = g.ctr[3 * id], c1 = g.ctr[3 * id + 1], c2 = g.ctr[3 * id + 2];
+    for (int j = g.pb[id]; j < g.pe[id]; ++j) {
+      const float4 x = pts[j];
+      double px[P + 1], py[P + 1], pz[P + 1];
+      fmm_pows_t<P>((double)x.x - c0, px);
+      fmm_pows_t<P>((double)x.y - c1, py);
+      fmm_pows_t<P>((double)x.z - c2, pz);
+      double q = 0.0, vx = 0.0, vy = 0.0, vz = 0.0;
+      if (DIM == 1) {
+        q = (double)scal[j];
+      } else {
+        const float4 v = vec[j];
+        vx = v.x;
+        vy = v.y;
+        vz = v.z;
+      }
+      p2m_terms<DIM, P, B0>(q, vx, vy, vz, px, py, pz, acc, std::make_integer_sequence<int, C::NB>{});
+    }
+#pragma unroll
+    for (int j = 0; j < C::NB; ++j)
+      if (B0 + j < C::NP) M[id * C::NP + B0 + j] = acc[j];
+    p2m_part<DIM, P, PART + 1>(id, g, pts, vec, scal, M);
+  }
+}
+template <int DIM, int P>
+__global__ void k_fmm_p2m(int64_t m, const int32_t* __restrict__ list, FmmGeom g, const float4* __restrict__ pts,
+                          const float4* __restrict__ vec, const float* __restrict__ scal, double* __restrict__ M) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < m) p2m_part<DIM, P, 0>(list[k], g, pts, vec, scal, M);
+}
+
+// M2M: one thread per internal active node of one level, M_β = Σ_children Σ_(γ≤β) M_c,γ (c_c' − c_c)^(β−γ)/(β−γ)!
+// (children in order)
+template <int P, int PART>
+__device__ __forceinline__ void m2m_part(int64_t id, FmmGeom g, double* __restrict__ M) {
+  using C = ShiftCfg<P>;
+  if constexpr (PART < C::NPART) {
+    constexpr int B0 = PART * C::NB;
+    double acc[C::NB];
+#pragma unroll
+    for (int j = 0; j < C::NB; ++j) acc[j] = 0.0;
+    for (int c = g.cb[id]; c < g.cb[id] + g.cc[id]; ++c) {
+      double px[P + 1], py[P + 1], pz[P + 1];  // parent − child
+      fmm_pows_t<P>(g.ctr[3 * id] - g.ctr[3 * c], px);
+      fmm_pows_t<P>(g.ctr[3 * id + 1] - g.ctr[3 * c + 1], py);
+      fmm_pows_t<P>(g.ctr[3 * id + 2] - g.ctr[3 * c + 2], pz);
+      shift_all<P, B0, true>(M + (int64_t)c * C::NP, px, py, pz, acc, std::make_integer_sequence<int, C::NP>{});
+    }
+#pragma unroll
+    for (int j = 0; j < C::NB; ++j)
+      if (B0 + j < C::NP) M[id * C::NP + B0 + j] = acc[j];
+    m2m_part<P, PART + 1>(id, g, M);
+  }
+}
+template <int P>
+__global__ void k_fmm_m2m(int64_t m, const int32_t* __restrict__ list, FmmGeom g, double* __restrict__ M) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < m) m2m_part<P, 0>(list[k], g, M);
+}
+
+// L2L: one thread per child of an internal active node of one level, L_c,δ += Σ_(γ≥δ) L_γ (c_c − c)^(γ−δ)/(γ−δ)!
+template <int P, int PART>
+__device__ __forceinline__ void l2l_part(int64_t c, FmmGeom g, double* __restrict__ L) {
+  using C = ShiftCfg<P>;
+  if constexpr (PART < C::NPART) {
+    constexpr int B0 = PART * C::NB;
+    const int64_t par = g.parent[c];
+    double acc[C::NB];
+#pragma unroll
+    for (int j = 0; j < C::NB; ++j) acc[j] = 0.0;
+    double px[P + 1], py[P + 1], pz[P + 1];  // child − parent
+    fmm_pows_t<P>(g.ctr[3 * c] - g.ctr[3 * par], px);
+    fmm_pows_t<P>(g.ctr[3 * c + 1] - g.ctr[3 * par + 1], py);
+    fmm_pows_t<P>(g.ctr[3 * c + 2] - g.ctr[3 * par + 2], pz);
+    shift_all<P, B0, false>(L + par * C::NP, px, py, pz, acc, std::make_integer_sequence<int, C::NP>{});
+#pragma unroll
+    for (int j = 0; j < C::NB; ++j)
+      if (B0 + j < C::NP) L[c * C::NP + B0 + j] += acc[j];
+    l2l_part<P, PART + 1>(c, g, L);
+  }
+}
+template <int P>
+__global__ void k_fmm_l2l(int64_t m, const int32_t* __restrict__ list, FmmGeom g, double* __restrict__ L) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < m) l2l_part<P, 0>(list[k], g, L);
+}
+
 // L2P: one warp per FMM leaf, one lane per target point: (V, ∇V) of the far field into VG (sorted order)
 template <int P>
 __global__ void k_fmm_l2p(int64_t m, const int32_t* __restrict__ list, FmmGeom g, const float4* __restrict__ pts,
@@ -833,9 +991,30 @@ wn_status fmm_plan(wn_tree_s* t, int p, double theta, int leafsz, float wsep, cu
     F.nchunk = tot[0];
     F.ngroups = tot[1];
     WN_TRY(alloc(&F.chunks, (F.nchunk + 1) * sizeof(int32_t), true));
-    k_fmm_chunks<<<g256(m + 1), 256, 0, s>>>(m, cflag, cpos, F.chunks);
+    WN_TRY(alloc(&F.cgroup, std::max<int64_t>(F.nchunk, 1) * sizeof(int32_t), true));
+    int32_t* gstart = nullptr;
+    WN_TRY(alloc(&gstart, std::max<int64_t>(F.ngroups, 1) * sizeof(int32_t), false));
+    k_fmm_chunks<<<g256(m + 1), 256, 0, s>>>(m, cflag, cpos, gflag, gpos, F.chunks, F.cgroup, gstart);
+    WN_TRY(alloc(&F.Tg, (size_t)std::max<int64_t>(F.ngroups, 1) * fmm_np(2 * p) * sizeof(double), true));
+    switch (p) {
+      case 1: k_fmm_m2l_tensor<1><<<(unsigned)F.ngroups, 128, 0, s>>>(gstart, F.gidx, F.m2l, g, F.Tg); break;
+      case 2: k_fmm_m2l_tensor<2><<<(unsigned)F.ngroups, 128, 0, s>>>(gstart, F.gidx, F.m2l, g, F.Tg); break;
+      case 3: k_fmm_m2l_tensor<3><<<(unsigned)F.ngroups, 128, 0, s>>>(gstart, F.gidx, F.m2l, g, F.Tg); break;
+      case 4: k_fmm_m2l_tensor<4><<<(unsigned)F.ngroups, 128, 0, s>>>(gstart, F.gidx, F.m2l, g, F.Tg); break;
+      case 5: k_fmm_m2l_tensor<5><<<(unsigned)F.ngroups, 128, 0, s>>>(gstart, F.gidx, F.m2l, g, F.Tg); break;
+      default: k_fmm_m2l_tensor<6><<<(unsigned)F.ngroups, 128, 0, s>>>(gstart, F.gidx, F.m2l, g, F.Tg); break;
+    }
+    count_launches(1);
     WN_TRY(alloc(&F.Lp, (size_t)m * np * sizeof(double), true));
-    count_launches(2);
+    k_fmm_has_list<<<g256(nn), 256, 0, s>>>(nn, F.om, flag);
+    WN_TRY(fmm_scan(flag, pos, nn, pos + nn, s));
+    uint32_t nt = 0;
+    WN_CUDA(cudaMemcpyAsync(&nt, pos + nn, sizeof(nt), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaStreamSynchronize(s));
+    F.nm2lt = nt;
+    WN_TRY(alloc(&F.m2lt, std::max<uint32_t>(nt, 1) * sizeof(int32_t), true));
+    k_fmm_compact<<<g256(nn), 256, 0, s>>>(nn, flag, pos, F.m2lt);
+    count_launches(4);
   }
   // P2P work items of the target leaves (k_fmm_items), the partial-sum slots of the leaves of several
   {
@@ -878,6 +1057,43 @@ wn_status fmm_plan(wn_tree_s* t, int p, double theta, int leafsz, float wsep, cu
   return WN_OK;
 }
 
+// the expansions of one application, degree P: P2M, M2M (deepest level first), M2L (grouped, then the
+// per-target sums), L2L (top down), L2P into F.VG; returns the number of launches
+template <int P>
+static int fmm_expansions(wn_tree_s* t, const FmmGeom& g, const float4* vec, const float* scal, cudaStream_t s) {
+  FmmPlan& F = t->fmm;
+  constexpr int np = fmm_np(P);
+  const int wpb = 8;
+  int launches = 0;
+  if (vec) k_fmm_p2m<3, P><<<g256(F.nleaves), 256, 0, s>>>(F.nleaves, F.leaves, g, t->pts, vec, scal, F.M);
+  else k_fmm_p2m<1, P><<<g256(F.nleaves), 256, 0, s>>>(F.nleaves, F.leaves, g, t->pts, vec, scal, F.M);
+  ++launches;
+  const int D = (int)F.inner.size() - 1;
+  for (int l = D; l >= 0; --l)
+    if (F.ninner[l]) {
+      k_fmm_m2m<P><<<g256(F.ninner[l]), 256, 0, s>>>(F.ninner[l], F.inner[l], g, F.M);
+      ++launches;
+    }
+  if (F.nchunk > 0) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_fmm_m2l_grp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m2l_smem<P>());
+      attr_set = true;
+    }
+    k_fmm_m2l_grp<P><<<(unsigned)F.nchunk, M2lCfg<P>::THREADS, m2l_smem<P>(), s>>>(F.chunks, F.cgroup, F.gidx, F.m2l,
+                                                                                  F.Tg, F.M, F.Lp);
+    k_fmm_m2l_reduce<<<g256(F.nm2lt * np), 256, 0, s>>>(F.nm2lt, F.m2lt, F.om, F.ginv, np, F.Lp, F.L);
+    launches += 2;
+  }
+  for (int l = 1; l <= D; ++l)
+    if (F.nkids[l]) {
+      k_fmm_l2l<P><<<g256(F.nkids[l]), 256, 0, s>>>(F.nkids[l], F.kids[l], g, F.L);
+      ++launches;
+    }
+  k_fmm_l2p<P><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, t->pts, F.L, F.VG);
+  return launches + 1;
+}
+
 // One FMM application with the tree's plan (capturable: launches and a memset only).  Outputs: out (caller
 // layout through out_map, or sorted order; float, N or N×3) scaled, or out4 (sorted float4) unscaled.
 wn_status fmm_run(wn_tree_s* t, int op, const float4* vec, const float* scal, float w, const int32_t* out_map,
@@ -891,46 +1107,16 @@ wn_status fmm_run(wn_tree_s* t, int op, const float4* vec, const float* scal, fl
   const int wpb = 8;
   ProfScope ps(op == OP_A ? WN_PROF_TRAV_A : op == OP_AT ? WN_PROF_TRAV_AT : WN_PROF_TRAV_G, s, 0);
   WN_CUDA(cudaMemsetAsync(F.L, 0, (size_t)nn * np * sizeof(double), s));
-  if (vec) k_fmm_p2m<3><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, t->pts, vec, scal, p, F.M);
-  else k_fmm_p2m<1><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, t->pts, vec, scal, p, F.M);
-  int launches = 1;
-  const int D = (int)F.inner.size() - 1;
-  for (int l = D; l >= 0; --l)
-    if (F.ninner[l]) {
-      k_fmm_m2m<<<gwarps(F.ninner[l], wpb), 32 * wpb, 0, s>>>(F.ninner[l], F.inner[l], g, p, F.M);
-      ++launches;
-    }
-  if (F.nchunk > 0) {
-    switch (p) {
-#define WN_M2L_CASE(PP)                                                                                    \
-  case PP:                                                                                                 \
-    k_fmm_m2l_grp<PP><<<(unsigned)F.nchunk, M2lCfg<PP>::THREADS, 0, s>>>(F.chunks, F.gidx, F.m2l, g, F.M, F.Lp); \
-    break;
-      WN_M2L_CASE(1)
-      WN_M2L_CASE(2)
-      WN_M2L_CASE(3)
-      WN_M2L_CASE(4)
-      WN_M2L_CASE(5)
-      WN_M2L_CASE(6)
-#undef WN_M2L_CASE
-    }
-    k_fmm_m2l_reduce<<<gwarps(nn, wpb), 32 * wpb, 0, s>>>(nn, F.om, F.ginv, np, F.Lp, F.L);
-    launches += 2;
-  }
-  for (int l = 1; l <= D; ++l)
-    if (F.nkids[l]) {
-      k_fmm_l2l<<<gwarps(F.nkids[l], wpb), 32 * wpb, 0, s>>>(F.nkids[l], F.kids[l], g, p, F.L);
-      ++launches;
-    }
-  const float w2f = w * w;
+  int launches = 0;
   switch (p) {
-#define WN_L2P_CASE(PP)                                                                                       \
-  case PP:                                                                                                    \
-    k_fmm_l2p<PP><<<gwarps(F.nleaves, wpb), 32 * wpb, 0, s>>>(F.nleaves, F.leaves, g, t->pts, F.L, F.VG);     \
-    break;
-    WN_L2P_CASE(1) WN_L2P_CASE(2) WN_L2P_CASE(3) WN_L2P_CASE(4) WN_L2P_CASE(5) WN_L2P_CASE(6)
-#undef WN_L2P_CASE
+    case 1: launches = fmm_expansions<1>(t, g, vec, scal, s); break;
+    case 2: launches = fmm_expansions<2>(t, g, vec, scal, s); break;
+    case 3: launches = fmm_expansions<3>(t, g, vec, scal, s); break;
+    case 4: launches = fmm_expansions<4>(t, g, vec, scal, s); break;
+    case 5: launches = fmm_expansions<5>(t, g, vec, scal, s); break;
+    default: launches = fmm_expansions<6>(t, g, vec, scal, s); break;
   }
+  const float w2f = w * w;
   const FmmOut fo{op, out_map, out, out4, scale};
   if (vec)
     k_fmm_eval<3><<<gwarps(F.nitems, wpb), 32 * wpb, 0, s>>>(F.nitems, F.items, F.linfo, g, F.p2p, t->pts, vec, scal,

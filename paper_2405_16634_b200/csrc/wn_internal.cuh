@@ -112,9 +112,12 @@ struct FmmPlan {
   // M2L pairs grouped by their translation vector c_t − c_s (equal vectors ⇒ one derivative tensor):
   // gidx = the m2l positions in group order, ginv its inverse, chunks = [start) of ≤ kChunk pairs of one
   // group (nchunk + 1 entries), Lp = the per-pair local expansions in group order (nm2l × np)
-  int32_t *gidx = nullptr, *ginv = nullptr, *chunks = nullptr;
+  int32_t *gidx = nullptr, *ginv = nullptr, *chunks = nullptr, *cgroup = nullptr;
+  double* Tg = nullptr;  // per group: the derivative tensor T_δ, |δ| ≤ 2p (graded order)
   int64_t nchunk = 0, ngroups = 0;
   double* Lp = nullptr;
+  int32_t* m2lt = nullptr;  // the target cells with a non-empty M2L list
+  int64_t nm2lt = 0;
   double4* VG = nullptr;  // per sorted point: the far field (V, ∇V) from L2P
   // P2P work items {leaf index, list range, item of its leaf}, per leaf {T, items, partial base}, the
   // leaves of several items (combined from partial sums)
