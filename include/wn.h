@@ -184,17 +184,24 @@ wn_status wn_eval_adjoint(wn_tree t, const float* s, float width, float theta, i
    traversal's epilogue stores its owned rows and Σ partials straight into every rank's replica through
    CUDA IPC peer mappings (NVLink / NVSwitch), the last block of the launch signals every rank and a
    device-side wait orders the next step — no separate collective; the first call per communicator (and
-   any call with a larger N) sets up the per-rank arena collectively (≈ 52 B per point, synchronizes
-   `stream`).  WN_FLAG_COMM_NCCL selects grouped ncclBroadcasts instead.  Both give the single-GPU
-   trajectory bit for bit.  At most 8 ranks in peer mode (WN_ERR_ARG beyond).  stats (host, p->iters records) may be
-   NULL; when given the call synchronizes `stream` before returning. */
+   any call with a larger N) sets up the per-rank arena collectively (≈ 150 B per point: the exchanged
+   rows, partials and the transpose-mode accumulators; synchronizes `stream`).  WN_FLAG_COMM_NCCL selects
+   grouped ncclBroadcasts instead.  Both give the single-GPU trajectory bit for bit.  Transpose-mode
+   adjoint (WN_ADJ_TRANSPOSE) across ranks — the north star's "scatters into node moments and is then pushed
+   down the tree": every rank scatters its shard into its own node / point accumulators; peer mode: a
+   signal and wait, then every rank adds all ranks' accumulators in rank order (IPC reads) and pushes down
+   for all points; NCCL mode: an all-reduce of the accumulators, then the same push-down.  The replicas
+   stay identical bit for bit; against one GPU the result differs by the rounding of the scatter's fp64
+   atomics (as two single-GPU transpose runs do).  Trees with more than 3 nodes per point are refused
+   across ranks (WN_ERR_ARG).  At most 8 ranks in peer mode (WN_ERR_ARG beyond).  stats (host, p->iters
+   records) may be NULL; when given the call synchronizes `stream` before returning. */
 wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p, wn_comm comm, wnnc_iter_stats* stats,
                        void* stream);
 /* Diagnostic: the peer-memory exchange of `world` (1..8) ranks emulated on this one GPU, serialized on
    `stream` — every rank's traversal over its shard reads its own replica and stores into all replicas,
    every wait is issued after all signals (none ever spins).  mu as in wnnc_iterate (rank 0's result);
    replicas (device, world×N×3, may be NULL) receives every rank's final μ.  No CUDA graph; synchronizes
-   `stream`; gather-mode adjoint only. */
+   `stream`; both adjoint modes. */
 wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int32_t world, float* replicas,
                                 void* stream);
 /* End-to-end convenience for HOST buffers: copies pts_host (N×3) to the device, builds the tree,

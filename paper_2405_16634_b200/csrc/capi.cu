@@ -529,8 +529,35 @@ static wn_status run_iterations(wn_tree_s* t, const wnnc_params& p, wn_comm comm
       if (nccl) WN_TRY(comm_allgather_f(comm, sb, 1, t->n, qord, stage, &t->shard, s));
     }
     // (2) r = A_wᵀ s  (+ Σ|r|² partials)
-    if (transpose) {
+    if (transpose && !comm && !P) {
       WN_TRY(adjoint_transpose(t, t->set[1], sb, w2, rb, part + stride, s));
+    } else if (transpose && P) {
+      // multi-GPU transpose form: every view scatters its shard into its own replica's accumulators and
+      // signals; after all signals each view adds every rank's accumulators (rank order) and pushes down
+      // for all points into its own replica — r and the Σ|r|² partials are whole on every rank
+      for (int v = 0; v < nviews; ++v) {
+        const PeerArena& A = *views[v];
+        int64_t b = 0, e = 0;
+        shard_of(&t->shard, t->n, A.rank, A.world, &b, &e);
+        WN_TRY(adjoint_scatter_shard(t, t->set[1], A.s[A.rank], w2, b, e, A.vb[A.rank], A.u[A.rank], s));
+        comm_peer_signal(A, s);
+      }
+      for (int v = 0; v < nviews; ++v) {
+        if (p.flags & WN_FLAG_HOST_WAIT) WN_TRY(comm_peer_wait_host(*views[v], s));
+        else comm_peer_wait(*views[v], s);
+      }
+      for (int v = 0; v < nviews; ++v) {
+        const PeerArena& A = *views[v];
+        WN_TRY(adjoint_reduce_pushdown(t, A.vb, A.u, A.world, A.r[A.rank], A.part[A.rank] + stride, s));
+      }
+    } else if (transpose) {  // NCCL: all-reduce of the accumulators, then the same replicated push-down
+      WN_TRY(ensure_transpose_scratch(t, s));
+      WN_TRY(adjoint_scatter_shard(t, t->set[1], sb, w2, q0, q1, t->tvb, t->tu, s));
+      WN_TRY(comm_allreduce_f64(comm, t->tvb, 3 * t->nn, s));
+      WN_TRY(comm_allreduce_f64(comm, t->tu, 3 * t->n, s));
+      const double* vb1[1] = {t->tvb};
+      const double* u1[1] = {t->tu};
+      WN_TRY(adjoint_reduce_pushdown(t, vb1, u1, 1, rb, part + stride, s));
     } else {
       MomentArgs m2;
       m2.kind = ATTR_SCALAR;
@@ -938,7 +965,10 @@ wn_status wnnc_iterate_emulated(wn_tree t, float* mu, const wnnc_params* p, int3
   if (!t || !mu) return set_error(WN_ERR_ARG, "tree or mu is NULL");
   WN_TRY(check_params(p));
   if (world < 1 || world > kMaxPeers) return set_error(WN_ERR_ARG, "world must be 1..8");
-  if (p->adjoint_mode == WN_ADJ_TRANSPOSE) return set_error(WN_ERR_ARG, "transpose-mode adjoint is single-GPU only");
+  if (p->adjoint_mode == WN_ADJ_TRANSPOSE && t->far_order != 0)
+    return set_error(WN_ERR_ARG, "transpose-mode adjoint is defined for the order-0 far field only");
+  if (p->adjoint_mode == WN_ADJ_TRANSPOSE && t->nn > kArenaNodesPerPoint * t->n)
+    return set_error(WN_ERR_ARG, "transpose-mode adjoint across ranks: the tree has more than 3 nodes per point");
   cudaStream_t s = (cudaStream_t)stream;
   WN_TRY(ensure_scratch(t, s));
   IterScratch& it = t->it;
@@ -979,8 +1009,6 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p_in, wn_comm co
   wnnc_params pl = *p_in;
   pl.flags = (pl.flags & ~kFlagStamps) | (stats ? kFlagStamps : 0);
   const wnnc_params* p = &pl;
-  if (comm && p->adjoint_mode == WN_ADJ_TRANSPOSE)
-    return set_error(WN_ERR_ARG, "transpose-mode adjoint is single-GPU only in this build");
   if ((p->flags & WN_FLAG_HOST_WAIT) && (p->flags & WN_FLAG_GRAPH))
     return set_error(WN_ERR_ARG, "WN_FLAG_HOST_WAIT waits on the host: it cannot be captured in a CUDA graph");
   if (comm && !comm_has_nccl(comm) && (p->flags & WN_FLAG_COMM_NCCL))
@@ -995,6 +1023,8 @@ wn_status wnnc_iterate(wn_tree t, float* mu, const wnnc_params* p_in, wn_comm co
   // multi-GPU exchange: peer-memory stores fused into the traversal epilogues (default), or NCCL
   const PeerArena* P = nullptr;
   if (comm && !(p->flags & WN_FLAG_COMM_NCCL)) WN_TRY(comm_peer_arena(comm, t->n, s, &P));
+  if (P && p->adjoint_mode == WN_ADJ_TRANSPOSE && t->nn > P->node_cap)
+    return set_error(WN_ERR_ARG, "transpose-mode adjoint across ranks: the tree has more than 3 nodes per point");
   if (comm) WN_TRY(plan_shards(t, comm_world(comm), comm, s));
   if (p->adjoint_mode == WN_ADJ_TRANSPOSE) WN_TRY(ensure_transpose_scratch(t, s));  // before any capture
   if (t->fmm_p > 0) {  // FMM operators (row f4): one plan for the whole schedule (separation width w_max ≥ every w)

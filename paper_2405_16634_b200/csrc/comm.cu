@@ -161,6 +161,11 @@ wn_status comm_allreduce_i64(wn_comm c, int64_t* buf, int64_t count, cudaStream_
   return nccl_status(nccl().AllReduce(buf, buf, (size_t)count, ncclInt64, ncclSum, c->comm, s), "ncclAllReduce (work)");
 }
 
+wn_status comm_allreduce_f64(wn_comm c, double* buf, int64_t count, cudaStream_t s) {
+  return nccl_status(nccl().AllReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, c->comm, s),
+                     "ncclAllReduce (adjoint accumulators)");
+}
+
 int comm_rank(wn_comm c) { return c->rank; }
 int comm_world(wn_comm c) { return c->world; }
 
@@ -212,16 +217,19 @@ static void arena_release(PeerArena& A) {
 
 // the arena's layout inside one block of `arena_bytes(n)` bytes
 struct ArenaLayout {
-  size_t o_s, o_r, o_mu0, o_mu1, o_part, o_sig, bytes;
-  int64_t nb;
+  size_t o_s, o_r, o_mu0, o_mu1, o_part, o_vb, o_u, o_sig, bytes;
+  int64_t nb, node_cap;
   explicit ArenaLayout(int64_t n) {
     nb = part_slots(n);
+    node_cap = kArenaNodesPerPoint * n;
     o_s = 0;
     o_r = align256(o_s + n * sizeof(float));
     o_mu0 = align256(o_r + n * sizeof(float4));
     o_mu1 = align256(o_mu0 + n * sizeof(float4));
     o_part = align256(o_mu1 + n * sizeof(float4));
-    o_sig = align256(o_part + 3 * nb * sizeof(double));
+    o_vb = align256(o_part + 3 * nb * sizeof(double));
+    o_u = align256(o_vb + 3 * node_cap * sizeof(double));
+    o_sig = align256(o_u + 3 * n * sizeof(double));
     bytes = align256(o_sig + 4 * sizeof(uint64_t));
   }
 };
@@ -233,6 +241,7 @@ static void arena_bind(PeerArena& A, void* const* blocks, int world, int rank, i
   A.rank = rank;
   A.cap = n;
   A.part_stride = L.nb;
+  A.node_cap = L.node_cap;
   for (int r = 0; r < world; ++r) {
     char* b = static_cast<char*>(blocks[r]);
     A.base[r] = blocks[r];
@@ -241,6 +250,8 @@ static void arena_bind(PeerArena& A, void* const* blocks, int world, int rank, i
     A.mu[0][r] = reinterpret_cast<float4*>(b + L.o_mu0);
     A.mu[1][r] = reinterpret_cast<float4*>(b + L.o_mu1);
     A.part[r] = reinterpret_cast<double*>(b + L.o_part);
+    A.vb[r] = reinterpret_cast<double*>(b + L.o_vb);
+    A.u[r] = reinterpret_cast<double*>(b + L.o_u);
     A.sig[r] = reinterpret_cast<unsigned long long*>(b + L.o_sig);
   }
   char* own = static_cast<char*>(blocks[rank]);
@@ -335,6 +346,18 @@ wn_status emulated_arenas(int world, int64_t n, PeerArena* arenas, void** blocks
 
 void comm_peer_wait(const PeerArena& A, cudaStream_t s) {
   k_peer_wait<<<1, 1, 0, s>>>(A.sig[A.rank], A.expected, A.world);
+  count_launches(1);
+}
+
+namespace {
+__global__ void k_peer_signal_all(PeerArena A) {
+  __threadfence_system();
+  for (int r = 0; r < A.world; ++r) atomicAdd_system(A.sig[r], 1ull);
+}
+}  // namespace
+
+void comm_peer_signal(const PeerArena& A, cudaStream_t s) {
+  k_peer_signal_all<<<1, 1, 0, s>>>(A);
   count_launches(1);
 }
 

@@ -68,13 +68,13 @@ __device__ __forceinline__ float reduce_scatter16(const float (&v)[16], int lane
 __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
     const float4* __restrict__ G, const float4* __restrict__ pts,
     const int32_t* __restrict__ npb, const int32_t* __restrict__ npe, const float* __restrict__ s_sorted,
-    int64_t n, float w2, int stack_depth, double* __restrict__ VB, double* __restrict__ U,
+    int64_t q_begin, int64_t q_end, float w2, int stack_depth, double* __restrict__ VB, double* __restrict__ U,
     const int32_t* __restrict__ qorder) {
   extern __shared__ int2 stk_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int2* stk = stk_all + warp * stack_depth;
-  const int64_t kq = (int64_t)blockIdx.x * kTravBlock + threadIdx.x;  // schedule position (Hilbert order)
-  const bool valid = kq < n;
+  const int64_t kq = q_begin + (int64_t)blockIdx.x * kTravBlock + threadIdx.x;  // schedule position
+  const bool valid = kq < q_end;
   const int64_t q = (valid && qorder) ? (int64_t)qorder[kq] : kq;
   const float4 xq = valid ? pts[q] : make_float4(0.f, 0.f, 0.f, 0.f);
   const float sq = valid ? s_sorted[q] * kInv4Pi : 0.f;
@@ -155,6 +155,18 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
   }
 }
 
+// the ranks' accumulators added in rank order (every rank computes the same sums)
+struct RankPtrs {
+  const double* p[kMaxPeers];
+};
+__global__ void sum_ranks_kernel(int64_t m, RankPtrs src, int world, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double acc = src.p[0][i];
+  for (int r = 1; r < world; ++r) acc += src.p[r][i];
+  out[i] = acc;
+}
+
 __global__ void pushdown_kernel(int64_t n, const int32_t* __restrict__ leaf_of, const int32_t* __restrict__ parent,
                                 const double* __restrict__ VB, const double* __restrict__ U, float scale,
                                 float4* __restrict__ r, double* __restrict__ partial) {
@@ -198,9 +210,44 @@ wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sor
   {
     ProfScope ps(WN_PROF_TRAV_AT, st, 2);
     scatter_kernel<<<grid, kTravBlock, (size_t)(kTravBlock / 32) * stack_depth * sizeof(int2), st>>>(
-        geo.rec, t->pts, t->pb, t->pe, s_sorted, t->n, w2, stack_depth, t->tvb, t->tu, t->qorder);
+        geo.rec, t->pts, t->pb, t->pe, s_sorted, 0, t->n, w2, stack_depth, t->tvb, t->tu, t->qorder);
     pushdown_kernel<<<grid, kTravBlock, 0, st>>>(t->n, t->leaf_of, t->parent, t->tvb, t->tu, 1.0f, r_out, partial);
   }
+  count_launches(2);
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
+wn_status adjoint_scatter_shard(wn_tree_s* t, const NodeSet& geo, const float* s_sorted, float w2, int64_t q0,
+                                int64_t q1, double* vb, double* u, cudaStream_t st) {
+  WN_CUDA(cudaMemsetAsync(vb, 0, 3 * sizeof(double) * (size_t)t->nn, st));
+  WN_CUDA(cudaMemsetAsync(u, 0, 3 * sizeof(double) * (size_t)t->n, st));
+  if (q1 <= q0) return WN_OK;
+  const int stack_depth = 8 * (t->depth_used + 2);
+  ProfScope ps(WN_PROF_TRAV_AT, st, 1);
+  scatter_kernel<<<(unsigned)trav_blocks(q1 - q0), kTravBlock, (size_t)(kTravBlock / 32) * stack_depth * sizeof(int2),
+                   st>>>(geo.rec, t->pts, t->pb, t->pe, s_sorted, q0, q1, w2, stack_depth, vb, u, t->qorder);
+  count_launches(1);
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
+
+wn_status adjoint_reduce_pushdown(wn_tree_s* t, const double* const* vbs, const double* const* us, int world,
+                                  float4* r_out, double* partial, cudaStream_t st) {
+  WN_TRY(ensure_transpose_scratch(t, st));
+  if (world < 1 || world > kMaxPeers) return set_error(WN_ERR_ARG, "internal: adjoint world size");
+  RankPtrs pv{}, pu{};
+  for (int r = 0; r < world; ++r) {
+    pv.p[r] = vbs[r];
+    pu.p[r] = us[r];
+  }
+  ProfScope ps(WN_PROF_TRAV_AT, st, 3);
+  const int64_t mv = 3 * t->nn, mu = 3 * t->n;
+  sum_ranks_kernel<<<(unsigned)((mv + 255) / 256), 256, 0, st>>>(mv, pv, world, t->tvb);
+  sum_ranks_kernel<<<(unsigned)((mu + 255) / 256), 256, 0, st>>>(mu, pu, world, t->tu);
+  pushdown_kernel<<<(unsigned)trav_blocks(t->n), kTravBlock, 0, st>>>(t->n, t->leaf_of, t->parent, t->tvb, t->tu,
+                                                                       1.0f, r_out, partial);
+  count_launches(3);
   WN_CUDA(cudaGetLastError());
   return WN_OK;
 }

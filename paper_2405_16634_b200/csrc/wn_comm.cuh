@@ -19,6 +19,9 @@ wn_status comm_allgather_partials(wn_comm c, double* part, int64_t stride, int64
 // rank r's query range [*b, *e): the plan's when it is for this world size, else equal counts
 void shard_of(const ShardPlan* plan, int64_t n, int rank, int world, int64_t* b, int64_t* e);
 wn_status comm_allreduce_i64(wn_comm c, int64_t* buf, int64_t count, cudaStream_t s);
+wn_status comm_allreduce_f64(wn_comm c, double* buf, int64_t count, cudaStream_t s);
+// this rank's signal to every rank (after a step that is not a traversal, e.g. the adjoint scatter)
+void comm_peer_signal(const PeerArena& A, cudaStream_t s);
 int comm_rank(wn_comm c);
 int comm_world(wn_comm c);
 // Peer-memory exchange: the communicator's arena (collective on first use or growth; synchronizes s),

@@ -324,6 +324,9 @@ struct PeerArena {
   float4* r[kMaxPeers] = {};           // r = Aᵀ s              (N)
   float4* mu[2][kMaxPeers] = {};       // μ, ping-pong by iteration parity (N each)
   double* part[kMaxPeers] = {};        // Σ partials [3][blocks]
+  double* vb[kMaxPeers] = {};          // transpose-mode adjoint: node accumulators V_B (node_cap × 3)
+  double* u[kMaxPeers] = {};           //   and the near-field accumulators U_j (N × 3) of each rank's shard
+  int64_t node_cap = 0;                // nodes the vb block holds (kArenaNodesPerPoint · N)
   unsigned long long* sig[kMaxPeers] = {};  // signal words (remote atomic adds)
   unsigned long long* expected = nullptr;   // local: next wait target (advanced by the wait kernel)
   int64_t pending_n = 0;                    // local communicators: exported for this N, not yet imported
@@ -349,6 +352,15 @@ void fmm_epi_rescale(int64_t n, const float4* hat, const float4* mup, float4* mu
 wn_status ensure_transpose_scratch(wn_tree_s* t, cudaStream_t st);
 wn_status adjoint_transpose(wn_tree_s* t, const NodeSet& geo, const float* s_sorted, float w2,
                             float4* r_out, double* partial, cudaStream_t st);
+// multi-GPU form: (1) each rank scatters its shard [q0, q1) of the schedule into its own accumulators
+// vb (nodes × 3) and u (N × 3); (2) after every rank has scattered, each rank adds all ranks' accumulators
+// in rank order (identical sums on every rank) and pushes them down for every point, so r and its Σ|r|²
+// partials are whole on every rank without a further exchange
+wn_status adjoint_scatter_shard(wn_tree_s* t, const NodeSet& geo, const float* s_sorted, float w2, int64_t q0,
+                                int64_t q1, double* vb, double* u, cudaStream_t st);
+wn_status adjoint_reduce_pushdown(wn_tree_s* t, const double* const* vbs, const double* const* us, int world,
+                                  float4* r_out, double* partial, cudaStream_t st);
+constexpr int kArenaNodesPerPoint = 3;  // node capacity of a peer arena's transpose accumulators, per point
 
 // ---- small utility kernels (iterate.cu) ----
 #ifndef WN_EXP_TRAVBLOCK

@@ -36,10 +36,49 @@ def test_world1_comm_matches_single_gpu(wn):
     for m, a in outs[1:]:
         np.testing.assert_array_equal(m, outs[0][0])
         assert a == outs[0][1]
-    with pytest.raises(wn.WnError, match="ARG"):
-        t = wn.wn_build_tree(p)
-        wn.wnnc_iterate(t, torch.zeros(len(p), 3, device="cuda"), comm=comm, adjoint_mode=wn.WN_ADJ_TRANSPOSE)
     comm.close()
+
+
+def _close(a, b):
+    # two transpose-mode trajectories: the scatter's fp64 atomics add in a run-dependent order, so equal up to
+    # rounding (after 5 iterations: 1e-4 of the largest |μ| per entry) and every orientation the same
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-4 * np.abs(b).max())
+    assert np.all(np.sum(a * b, axis=1) > 0)
+
+
+def test_world1_comm_transpose(wn):
+    # the multi-GPU form of the transpose-mode adjoint on a world-1 communicator: peer path (scatter into the
+    # arena's accumulators, signal, wait, rank-order sum, replicated push-down; stream and graph) and NCCL
+    # (all-reduce of the accumulators) — the single-GPU transpose trajectory up to the atomics' rounding
+    comm = wn.wn_comm_init(0, 1, wn.wn_comm_unique_id())
+    p = torch.from_numpy(synth.config("C2")["points"]).cuda()
+    T, G, NC = wn.WN_ADJ_TRANSPOSE, wn.WN_FLAG_GRAPH, wn.WN_FLAG_COMM_NCCL
+    outs = []
+    for c, flags in ((None, 0), (comm, 0), (comm, G), (comm, NC)):
+        t = wn.wn_build_tree(p)
+        mu = torch.zeros(len(p), 3, device="cuda")
+        wn.wnnc_iterate(t, mu, comm=c, iters=5, total_iters=40, flags=flags, adjoint_mode=T)
+        outs.append(mu.cpu().numpy())
+    for m in outs[1:]:
+        _close(m, outs[0])
+    comm.close()
+
+
+@pytest.mark.parametrize("world,n", [(2, 30011), (3, 70001), (8, 30011)])
+def test_emulated_ranks_transpose(wn, world, n):
+    # W emulated ranks, transpose-mode adjoint (SURVEY §8(e) + row a7): each rank scatters its shard into its
+    # own accumulators, every rank adds all ranks' in rank order and pushes down for all points — every
+    # replica is the same bit for bit, and the trajectory is the single-GPU transpose one up to rounding
+    p = torch.from_numpy(synth.config("C2" if n <= 50000 else "C3")["points"][:n]).cuda()
+    t = wn.wn_build_tree(p)
+    T = wn.WN_ADJ_TRANSPOSE
+    ref = torch.zeros(len(p), 3, device="cuda")
+    wn.wnnc_iterate(t, ref, iters=5, total_iters=40, adjoint_mode=T)
+    mu = torch.zeros(len(p), 3, device="cuda")
+    reps = wn.wnnc_iterate_emulated(t, mu, world, iters=5, total_iters=40, adjoint_mode=T).cpu().numpy()
+    for r in range(1, world):
+        np.testing.assert_array_equal(reps[r], reps[0])
+    _close(reps[0], ref.cpu().numpy())
 
 
 def test_peer_arena_grows_with_n(wn):

@@ -35,7 +35,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, out_dir):
+def _rank_main(rank, world, port, out_dir, adjoint_mode=0):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -55,7 +55,7 @@ def _rank_main(rank, world, port, out_dir):
         dist.barrier()  # every rank mapped every replica before anyone stores into a peer
         mu = torch.zeros(tree.n, 3, device="cuda")
         st = wn.wnnc_iterate(tree, mu, comm=comm, stats=True, iters=ITERS, total_iters=40,
-                             flags=wn.WN_FLAG_HOST_WAIT | wn.WN_FLAG_MU_ZERO)
+                             flags=wn.WN_FLAG_HOST_WAIT | wn.WN_FLAG_MU_ZERO, adjoint_mode=adjoint_mode)
         np.save(os.path.join(out_dir, f"mu{rank}.npy"), mu.cpu().numpy())
         np.save(os.path.join(out_dir, f"alpha{rank}.npy"), np.array([s["alpha"] for s in st]))
         bounds = wn.wn_shard_plan(tree, world)
@@ -94,3 +94,29 @@ def test_processes_exchange_over_ipc_bit_identical(single_gpu, world):
             assert len(np.unique(bounds[0])) == world + 1  # nobody's shard is empty here
             np.testing.assert_array_equal(np.load(os.path.join(d, f"alpha{r}.npy")), ref_alpha)
             np.testing.assert_array_equal(np.load(os.path.join(d, f"mu{r}.npy")), ref_mu)
+
+
+def test_processes_transpose_adjoint():
+    # the transpose-mode adjoint across 2 processes: each scatters its shard into the accumulators of its own
+    # arena, signals; after both signals each adds both ranks' accumulators (IPC reads of the peer's block) in
+    # rank order and pushes down — both ranks end with the same μ bit for bit, the single-GPU transpose
+    # trajectory up to the scatter atomics' rounding
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2405_16634_b200.wn as wn
+
+    p = synth.config("C3", n=N_PTS)["points"]
+    t = wn.wn_build_tree(torch.from_numpy(p).cuda())
+    ref = torch.zeros(t.n, 3, device="cuda")
+    wn.wnnc_iterate(t, ref, iters=ITERS, total_iters=40, flags=wn.WN_FLAG_MU_ZERO, adjoint_mode=wn.WN_ADJ_TRANSPOSE)
+    ref = ref.cpu().numpy()
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_rank_main, args=(2, _free_port(), d, wn.WN_ADJ_TRANSPOSE), nprocs=2, join=True,
+                           start_method="spawn")
+        mus = [np.load(os.path.join(d, f"mu{r}.npy")) for r in range(2)]
+        np.testing.assert_array_equal(mus[1], mus[0])
+        np.testing.assert_array_equal(np.load(os.path.join(d, "alpha1.npy")), np.load(os.path.join(d, "alpha0.npy")))
+        np.testing.assert_allclose(mus[0], ref, rtol=0, atol=1e-4 * np.abs(ref).max())
+        assert np.all(np.sum(mus[0] * ref, axis=1) > 0)
