@@ -168,6 +168,20 @@ wn_status wn_eval_grad(wn_tree t, const float* mu, const float* a, const float* 
    far + leaf-point terms equals Alg. 4's far + near count.  Diagnostic / parity entry point. */
 wn_status wn_query_work(wn_tree t, int32_t op, const float* mu, const float* q, int64_t m, float width, float theta,
                         int32_t* counts, void* stream);
+/* Adaptive octree sampling of F around its iso level (the WNF reconstruction hand-off,
+   PAPER.md:L1005-L1008).  box = {lo_x, lo_y, lo_z, hi_x, hi_y, hi_z} (input frame) is cut into 2^base_level
+   cells per axis (base_level 0..7); per level F is evaluated once at every distinct corner of the active
+   cells (wn_eval's Alg. 4 traversal, width, theta), a cell stays active while min ≤ iso + band and
+   max ≥ iso − band over its corners (band ≥ 0) and is split in eight, down to max_level (≤ 20).  Output:
+   the max_level cells the level set crosses (min < iso ≤ max): cells[k×3] (int32 lattice coordinates
+   i, j, k of the cell's low corner; its extent is (hi − lo)/2^max_level), values[k×8] (corner F, corner
+   b at (i + (b&1), j + (b>>1&1), k + (b>>2&1))), at most `capacity` of them (device buffers; may be NULL
+   when capacity = 0); *count (host) = the number of crossed cells (may exceed capacity: call again with
+   more room); *evals (host, may be NULL) = F evaluations over all levels.  Synchronizes `stream`.
+   WN_ERR_ARG for bad levels, band, box or buffers, or more than 2^26 active cells in a level. */
+wn_status wn_iso_cells(wn_tree t, const float* mu, float width, float theta, const float box[6], int32_t base_level,
+                       int32_t max_level, float iso, float band, int64_t capacity, int32_t* cells, float* values,
+                       int64_t* count, int64_t* evals, void* stream);
 /* out[N×3] = (Aᵀ s)_j = Σ_i s_i ∇Φ_w(x_i − x_j)  (input frame), s[N] caller order.
    mode WN_ADJ_GATHER: own traversal with |s|-weighted representatives.
    mode WN_ADJ_TRANSPOSE: exact transpose of wn_eval's treecode at the geometry of mu_geom[N×3]

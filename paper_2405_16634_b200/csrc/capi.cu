@@ -1203,3 +1203,10 @@ extern "C" wn_status wn_exp_set_schedule(wn_tree t, const int32_t* qorder, void*
   return WN_OK;
 }
 #endif
+
+namespace wn {
+wn_status eval_field(wn_tree_s* t, const float* mu, const float* q, int64_t m, float width, float theta, float* F,
+                     cudaStream_t s) {
+  return eval_common(t, OP_A, mu, nullptr, q, m, width, theta, F, (void*)s);
+}
+}  // namespace wn

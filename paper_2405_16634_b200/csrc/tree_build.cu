@@ -573,6 +573,9 @@ static wn_status sort_pairs(uint64_t* ka, int32_t* va, int64_t n, int bits, int3
 wn_status fmm_scan(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* total, cudaStream_t s) {
   return scan_excl(in, out, m, total, s);
 }
+wn_status scan_u32(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* total, cudaStream_t s) {
+  return scan_excl(in, out, m, total, s);
+}
 
 // ascending sort of n 64-bit keys on their low `bits` bits (stable LSD radix), out = the sorted keys
 __global__ void k_iota(int64_t n, int32_t* __restrict__ v) {

@@ -31,7 +31,8 @@ EXPORTED = ("wn_last_error", "wn_version", "wn_launch_count", "wn_prof_enable", 
             "wn_eval_adjoint", "wnnc_iterate", "wnnc_solve_host", "wn_comm_unique_id", "wn_comm_init",
             "wn_comm_destroy", "wn_shard_range", "wn_work_count_enable", "wn_work_count_read", "wn_query_work",
             "wn_tree_set_far_order", "wnnc_iterate_emulated", "wn_shard_plan", "wn_tree_schedule",
-            "wn_tree_schedule_stats", "wn_comm_init_local", "wn_comm_arena_export", "wn_comm_arena_import", "wn_eval_fmm", "wn_tree_set_fmm")
+            "wn_tree_schedule_stats", "wn_comm_init_local", "wn_comm_arena_export", "wn_comm_arena_import", "wn_eval_fmm", "wn_tree_set_fmm",
+            "wn_iso_cells")
 
 
 class wnnc_params(C.Structure):
@@ -70,6 +71,7 @@ _sig = {
     "wn_comm_arena_import": ([P, P], I32),
     "wn_eval_fmm": ([P, I32, P, F32, I32, F32, I32, P, P, P], I32),
     "wn_tree_set_fmm": ([P, I32, F32, I32], I32),
+    "wn_iso_cells": ([P, P, F32, F32, P, I32, I32, F32, F32, I64, P, P, P, P, P], I32),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_L, _name)
@@ -155,6 +157,28 @@ def wn_eval_fmm(tree: Tree, attr: torch.Tensor, width: float, op: int = 0, p: in
 def wn_tree_set_fmm(tree: Tree, p: int, theta_f: float = 0.5, leaf: int = 32):
     """wnnc_iterate's operators: p = 0 the paper's treecode (default), 1..6 the FMM."""
     _check(_L.wn_tree_set_fmm(tree.handle, int(p), float(theta_f), int(leaf)))
+
+
+def wn_iso_cells(tree: Tree, mu: torch.Tensor, width: float, theta: float = 2.0, box=None, base_level: int = 4,
+                 max_level: int = 8, iso: float = 0.5, band: float = 0.1, capacity: int = 1 << 20):
+    """Adaptive octree sampling of F around its iso level (the WNF hand-off): the max_level
+    cells the level set crosses as (cells int32 [k, 3], corner values [k, 8], F evaluations).  box defaults to
+    the tree's normalization cube (input frame)."""
+    _dev_f32(mu, 3)
+    if box is None:
+        c0, c1, c2, sc = tree.xform
+        box = (c0 - 1.0 / sc, c1 - 1.0 / sc, c2 - 1.0 / sc, c0 + 1.0 / sc, c1 + 1.0 / sc, c2 + 1.0 / sc)
+    bx = (C.c_float * 6)(*[float(v) for v in box])
+    cnt, ev = C.c_int64(0), C.c_int64(0)
+    while True:
+        cells = torch.empty(max(capacity, 1), 3, dtype=torch.int32, device=mu.device)
+        vals = torch.empty(max(capacity, 1), 8, dtype=torch.float32, device=mu.device)
+        _check(_L.wn_iso_cells(tree.handle, _ptr(mu), float(width), float(theta), bx, int(base_level), int(max_level),
+                               float(iso), float(band), int(capacity), _ptr(cells), _ptr(vals), C.byref(cnt),
+                               C.byref(ev), _stream()))
+        if cnt.value <= capacity:
+            return cells[:cnt.value], vals[:cnt.value], int(ev.value)
+        capacity = int(cnt.value)
 
 
 def wn_query_work(tree, mu, width, theta=2.0, op=0, q=None):
