@@ -194,15 +194,19 @@ constexpr int fmm_mi_of(int j, int comp) {
       }
   return -1;
 }
-template <int P>
+// CHP_ = 0: a full chunk (128 pairs for p ≤ 4, 64 above); else the small-chunk configuration (≤ 32 pairs)
+template <int P, int CHP_ = 0>
 struct M2lCfg {
   static constexpr int NP = fmm_np(P), E = 2 * P + 1, NT3 = E * E * E;
+  static constexpr int PPT = 2;                  // pairs per thread: one tensor read feeds PPT FMAs (4: slower)
   static constexpr int NSPLIT = (NP + 19) / 20;  // γ parts (≤ 20 accumulators per pair each)
   static constexpr int GCH = (NP + NSPLIT - 1) / NSPLIT;
-  static constexpr int CHP = NP <= 35 ? 128 : 64;  // pairs per block, two per thread (one T load, two FMAs)
-  static constexpr int HALF = CHP / 2;
+  static constexpr int CHP = CHP_ ? CHP_ : (NP <= 35 ? 128 : 64);  // pairs per block
+  static constexpr int HALF = CHP / PPT;         // threads per γ part
   static constexpr int THREADS = HALF * NSPLIT;
 };
+constexpr int kM2lSmall = 32;  // chunks of at most this many pairs (group remainders, small groups) go to
+                               // one-warp blocks instead of occupying a full block's slot
 inline int m2l_chunk(int p) { return fmm_np(p) <= 35 ? 128 : 64; }
 
 __global__ void k_fmm_m2l_gkey(int64_t m, const uint64_t* __restrict__ m2l, FmmGeom g, uint64_t* __restrict__ key) {
@@ -221,70 +225,84 @@ __global__ void k_fmm_m2l_gkey(int64_t m, const uint64_t* __restrict__ m2l, FmmG
   key[i] = ok ? k : ((1ull << 62) | (uint64_t)i);
 }
 
-// chunk starts (group boundaries and every kChunk-th position) and the inverse permutation
+// group starts (flags) and the inverse permutation
 __global__ void k_fmm_m2l_ginfo(int64_t m, const uint64_t* __restrict__ skey, const int32_t* __restrict__ gidx,
-                                int chunk, uint32_t* __restrict__ flag, uint32_t* __restrict__ gflag,
-                                int32_t* __restrict__ ginv) {
+                                uint32_t* __restrict__ gflag, int32_t* __restrict__ ginv) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= m) return;
   const bool gs = i == 0 || skey[i] != skey[i - 1];
-  flag[i] = (gs || i % chunk == 0) ? 1u : 0u;
   gflag[i] = gs ? 1u : 0u;
   ginv[gidx[i]] = (int32_t)i;
 }
-__global__ void k_fmm_chunks(int64_t m, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
-                             const uint32_t* __restrict__ gflag, const uint32_t* __restrict__ gpos,
-                             int32_t* __restrict__ chunks, int32_t* __restrict__ cgroup, int32_t* __restrict__ gstart) {
+__global__ void k_fmm_gstart(int64_t m, const uint32_t* __restrict__ gflag, const uint32_t* __restrict__ gpos,
+                             int64_t ngroups, int32_t* __restrict__ gstart) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < m && flag[i]) {
-    chunks[pos[i]] = (int32_t)i;
-    cgroup[pos[i]] = (int32_t)(gpos[i] + gflag[i]) - 1;  // the group of pair i
-  }
   if (i < m && gflag[i]) gstart[gpos[i]] = (int32_t)i;
-  if (i == m) chunks[pos[m]] = (int32_t)m;
+  if (i == m) gstart[ngroups] = (int32_t)m;
+}
+// chunks start at every chunk-th pair of a group; a chunk of ≤ kM2lSmall pairs is a small one
+__global__ void k_fmm_chunk_flags(int64_t m, const uint32_t* __restrict__ gflag, const uint32_t* __restrict__ gpos,
+                                  const int32_t* __restrict__ gstart, int chunk, uint32_t* __restrict__ big,
+                                  uint32_t* __restrict__ small) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t g = (int64_t)gpos[i] + gflag[i] - 1;  // the group of pair i
+  const int64_t rel = i - gstart[g], len = min((int64_t)chunk, (int64_t)gstart[g + 1] - i);
+  const bool start = rel % chunk == 0;
+  big[i] = start && len > kM2lSmall;
+  small[i] = start && len <= kM2lSmall;
+}
+__global__ void k_fmm_chunk_put(int64_t m, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                                const uint32_t* __restrict__ gflag, const uint32_t* __restrict__ gpos,
+                                const int32_t* __restrict__ gstart, int chunk, int4* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m || !flag[i]) return;
+  const int64_t g = (int64_t)gpos[i] + gflag[i] - 1;
+  const int64_t len = min((int64_t)chunk, (int64_t)gstart[g + 1] - i);
+  out[pos[i]] = make_int4((int)i, (int)len, (int)g, 0);
 }
 
 template <int P, int G0, int... J>
-__device__ __forceinline__ void m2l_row(double ma, double mb, const double* __restrict__ tb, double* acc_a,
-                                        double* acc_b, std::integer_sequence<int, J...>) {
-  using C = M2lCfg<P>;
+__device__ __forceinline__ void m2l_row(const double (&m)[M2lCfg<P>::PPT], const double* __restrict__ tb,
+                                        double (&acc)[M2lCfg<P>::PPT][M2lCfg<P>::GCH],
+                                        std::integer_sequence<int, J...>) {
+  using C = M2lCfg<P, 0>;
   (
       [&] {
         if constexpr (G0 + J < C::NP) {
           const double tv = tb[std::integral_constant<int, fmm_box_of(G0 + J, C::E)>::value];
-          acc_a[J] = fma(ma, tv, acc_a[J]);
-          acc_b[J] = fma(mb, tv, acc_b[J]);
+#pragma unroll
+          for (int q = 0; q < C::PPT; ++q) acc[q][J] = fma(m[q], tv, acc[q][J]);
         }
       }(),
       ...);
 }
-// two pairs (sources Ma, Mb) of one group, the γ of part PART: out_x[γ] = Σ_β M_x,β T_(β+γ)
-template <int P, int PART>
-__device__ __forceinline__ void m2l_contract(const double* Ma, const double* Mb, const double* T3, double* oa,
-                                             double* ob) {
-  using C = M2lCfg<P>;
+// PPT pairs (staged coefficients at Ms + q·HALF, stride CHP per β) of one group, the γ of part PART:
+// out[q][j] = Σ_β M_q,β T_(β+γ), γ = PART·GCH + j
+template <int P, int CHP, int PART>
+__device__ __forceinline__ void m2l_contract(const double* Ms, const double* T3,
+                                             double (&out)[M2lCfg<P>::PPT][M2lCfg<P>::GCH]) {
+  using C = M2lCfg<P, CHP>;
   constexpr int G0 = PART * C::GCH;
-  double acc_a[C::GCH], acc_b[C::GCH];
 #pragma unroll
-  for (int j = 0; j < C::GCH; ++j) acc_a[j] = acc_b[j] = 0.0;
+  for (int q = 0; q < C::PPT; ++q)
+#pragma unroll
+    for (int j = 0; j < C::GCH; ++j) out[q][j] = 0.0;
 #pragma unroll 1
   for (int be = 0; be < C::NP; ++be) {
     const int base = (c_mi[be][0] * C::E + c_mi[be][1]) * C::E + c_mi[be][2];  // warp-uniform
-    m2l_row<P, G0>(Ma[be * C::CHP], Mb[be * C::CHP], T3 + base, acc_a, acc_b,
-                   std::make_integer_sequence<int, C::GCH>{});
-  }
+    double m[C::PPT];
 #pragma unroll
-  for (int j = 0; j < C::GCH; ++j) {
-    oa[j] = acc_a[j];
-    ob[j] = acc_b[j];
+    for (int q = 0; q < C::PPT; ++q) m[q] = Ms[be * C::CHP + q * C::HALF];
+    m2l_row<P, G0>(m, T3 + base, out, std::make_integer_sequence<int, C::GCH>{});
   }
 }
-template <int P, int PART>
-__device__ __forceinline__ void m2l_part(int part, const double* Ma, const double* Mb, const double* T3, double* oa,
-                                         double* ob) {
-  if constexpr (PART < M2lCfg<P>::NSPLIT) {
-    if (part == PART) m2l_contract<P, PART>(Ma, Mb, T3, oa, ob);
-    else m2l_part<P, PART + 1>(part, Ma, Mb, T3, oa, ob);
+template <int P, int CHP, int PART>
+__device__ __forceinline__ void m2l_part(int part, const double* Ms, const double* T3,
+                                         double (&out)[M2lCfg<P>::PPT][M2lCfg<P>::GCH]) {
+  if constexpr (PART < M2lCfg<P, CHP>::NSPLIT) {
+    if (part == PART) m2l_contract<P, CHP, PART>(Ms, T3, out);
+    else m2l_part<P, CHP, PART + 1>(part, Ms, T3, out);
   }
 }
 
@@ -349,29 +367,31 @@ __global__ void __launch_bounds__(128) k_fmm_m2l_tensor(const int32_t* __restric
   }
 }
 
-template <int P>
+template <int P, int CHP = 0>
 constexpr size_t m2l_smem() {
-  return (size_t)(M2lCfg<P>::NT3 + M2lCfg<P>::CHP * M2lCfg<P>::NP) * sizeof(double) + M2lCfg<P>::CHP * sizeof(int);
+  using C = M2lCfg<P, CHP>;
+  return (size_t)(C::NT3 + C::CHP * C::NP) * sizeof(double) + C::CHP * sizeof(int);
 }
-// one chunk of ≤ CHP pairs of one group: the group's tensor into a (2P+1)³ box in shared memory, the
-// sources' coefficients staged [β][pair], two pairs per thread, the outputs written back as one run
-template <int P>
-__global__ void __launch_bounds__(M2lCfg<P>::THREADS) k_fmm_m2l_grp(const int32_t* __restrict__ chunks,
-                                                                     const int32_t* __restrict__ cgroup,
-                                                                     const int32_t* __restrict__ gidx,
-                                                                     const uint64_t* __restrict__ m2l,
-                                                                     const double* __restrict__ Tg,
-                                                                     const double* __restrict__ M,
-                                                                     double* __restrict__ Lp) {
-  using C = M2lCfg<P>;
+// one chunk {first pair, pairs, group} of ≤ CHP pairs of one group: the group's tensor into a (2P+1)³ box in
+// shared memory, the sources' coefficients staged [β][pair], two pairs per thread, the outputs written
+// back as one run
+template <int P, int CHP>
+__global__ void __launch_bounds__(M2lCfg<P, CHP>::THREADS) k_fmm_m2l_grp(const int4* __restrict__ chunks,
+                                                                          const int32_t* __restrict__ gidx,
+                                                                          const uint64_t* __restrict__ m2l,
+                                                                          const double* __restrict__ Tg,
+                                                                          const double* __restrict__ M,
+                                                                          double* __restrict__ Lp) {
+  using C = M2lCfg<P, CHP>;
   constexpr int E = C::E, NPT = fmm_np(2 * P);
   extern __shared__ double smem[];
   double* T3 = smem;                      // the group's derivative tensor, box layout
   double* sMO = smem + C::NT3;            // the chunk's multipole coefficients [β][pair], then outputs [pair][γ]
   int* sS = reinterpret_cast<int*>(sMO + C::CHP * C::NP);
   const int tid = threadIdx.x;
-  const int i0 = chunks[blockIdx.x], i1 = chunks[blockIdx.x + 1], npair = i1 - i0;
-  const double* Tgr = Tg + (int64_t)cgroup[blockIdx.x] * NPT;
+  const int4 ch = chunks[blockIdx.x];
+  const int i0 = ch.x, npair = ch.y;
+  const double* Tgr = Tg + (int64_t)ch.z * NPT;
   for (int j = tid; j < NPT; j += C::THREADS) {
     int a, b, c;
     fmm_mi_dev(j, a, b, c);
@@ -385,18 +405,20 @@ __global__ void __launch_bounds__(M2lCfg<P>::THREADS) k_fmm_m2l_grp(const int32_
     sMO[be * C::CHP + pr] = __ldg(M + (int64_t)sS[pr] * C::NP + be);
   }
   __syncthreads();
-  const int part = tid / C::HALF, pa = tid % C::HALF, pb = pa + C::HALF;
-  double outa[C::GCH], outb[C::GCH];
-  const bool va = pa < npair, vb = pb < npair;
-  if (va) m2l_part<P, 0>(part, sMO + pa, sMO + (vb ? pb : pa), T3, outa, outb);
+  // thread (part, pa): pairs pa + q·HALF (q < PPT; a slot past the chunk is read but its result dropped)
+  const int part = tid / C::HALF, pa = tid % C::HALF;
+  double out[C::PPT][C::GCH];
+  const bool va = pa < npair;
+  if (va) m2l_part<P, CHP, 0>(part, sMO + pa, T3, out);
   __syncthreads();  // every thread has read the staged coefficients
   if (va) {
 #pragma unroll
-    for (int j = 0; j < C::GCH; ++j) {
-      const int gi = part * C::GCH + j;
-      if (gi < C::NP) {
-        sMO[pa * C::NP + gi] = outa[j];
-        if (vb) sMO[pb * C::NP + gi] = outb[j];
+    for (int q = 0; q < C::PPT; ++q) {
+      const int pr = pa + q * C::HALF;
+#pragma unroll
+      for (int j = 0; j < C::GCH; ++j) {
+        const int gi = part * C::GCH + j;
+        if (gi < C::NP && pr < npair) sMO[pr * C::NP + gi] = out[q][j];
       }
     }
   }
@@ -981,20 +1003,32 @@ wn_status fmm_plan(wn_tree_s* t, int p, double theta, int leafsz, float wsep, cu
     k_fmm_m2l_gkey<<<g256(m), 256, 0, s>>>(m, F.m2l, g, gk);
     count_launches(1);
     WN_TRY(sort_keys_u64_perm(gk, m, 63, sk, F.gidx, s));
-    k_fmm_m2l_ginfo<<<g256(m), 256, 0, s>>>(m, sk, F.gidx, m2l_chunk(p), cflag, gflag, F.ginv);
-    uint32_t tot[2] = {0, 0};
-    WN_TRY(fmm_scan(cflag, cpos, m, cpos + m, s));
+    k_fmm_m2l_ginfo<<<g256(m), 256, 0, s>>>(m, sk, F.gidx, gflag, F.ginv);
     WN_TRY(fmm_scan(gflag, gpos, m, gpos + m, s));
+    uint32_t ng = 0;
+    WN_CUDA(cudaMemcpyAsync(&ng, gpos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaStreamSynchronize(s));
+    F.ngroups = ng;
+    int32_t* gstart = nullptr;
+    WN_TRY(alloc(&gstart, (F.ngroups + 1) * sizeof(int32_t), false));
+    k_fmm_gstart<<<g256(m + 1), 256, 0, s>>>(m, gflag, gpos, F.ngroups, gstart);
+    uint32_t *sflag = nullptr, *spos = nullptr;
+    WN_TRY(alloc(&sflag, (m + 1) * sizeof(uint32_t), false));
+    WN_TRY(alloc(&spos, (m + 1) * sizeof(uint32_t), false));
+    k_fmm_chunk_flags<<<g256(m), 256, 0, s>>>(m, gflag, gpos, gstart, m2l_chunk(p), cflag, sflag);
+    WN_TRY(fmm_scan(cflag, cpos, m, cpos + m, s));
+    WN_TRY(fmm_scan(sflag, spos, m, spos + m, s));
+    uint32_t tot[2] = {0, 0};
     WN_CUDA(cudaMemcpyAsync(&tot[0], cpos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    WN_CUDA(cudaMemcpyAsync(&tot[1], gpos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    WN_CUDA(cudaMemcpyAsync(&tot[1], spos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     WN_CUDA(cudaStreamSynchronize(s));
     F.nchunk = tot[0];
-    F.ngroups = tot[1];
-    WN_TRY(alloc(&F.chunks, (F.nchunk + 1) * sizeof(int32_t), true));
-    WN_TRY(alloc(&F.cgroup, std::max<int64_t>(F.nchunk, 1) * sizeof(int32_t), true));
-    int32_t* gstart = nullptr;
-    WN_TRY(alloc(&gstart, std::max<int64_t>(F.ngroups, 1) * sizeof(int32_t), false));
-    k_fmm_chunks<<<g256(m + 1), 256, 0, s>>>(m, cflag, cpos, gflag, gpos, F.chunks, F.cgroup, gstart);
+    F.nchunk_small = tot[1];
+    WN_TRY(alloc(&F.chunks, std::max<int64_t>(F.nchunk, 1) * sizeof(int4), true));
+    WN_TRY(alloc(&F.chunks_small, std::max<int64_t>(F.nchunk_small, 1) * sizeof(int4), true));
+    k_fmm_chunk_put<<<g256(m), 256, 0, s>>>(m, cflag, cpos, gflag, gpos, gstart, m2l_chunk(p), F.chunks);
+    k_fmm_chunk_put<<<g256(m), 256, 0, s>>>(m, sflag, spos, gflag, gpos, gstart, m2l_chunk(p), F.chunks_small);
+    count_launches(4);
     WN_TRY(alloc(&F.Tg, (size_t)std::max<int64_t>(F.ngroups, 1) * fmm_np(2 * p) * sizeof(double), true));
     switch (p) {
       case 1: k_fmm_m2l_tensor<1><<<(unsigned)F.ngroups, 128, 0, s>>>(gstart, F.gidx, F.m2l, g, F.Tg); break;
@@ -1074,14 +1108,20 @@ static int fmm_expansions(wn_tree_s* t, const FmmGeom& g, const float4* vec, con
       k_fmm_m2m<P><<<g256(F.ninner[l]), 256, 0, s>>>(F.ninner[l], F.inner[l], g, F.M);
       ++launches;
     }
-  if (F.nchunk > 0) {
+  if (F.nchunk + F.nchunk_small > 0) {
     static bool attr_set = false;
     if (!attr_set) {
-      cudaFuncSetAttribute(k_fmm_m2l_grp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m2l_smem<P>());
+      cudaFuncSetAttribute(k_fmm_m2l_grp<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m2l_smem<P, 0>());
+      cudaFuncSetAttribute(k_fmm_m2l_grp<P, kM2lSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)m2l_smem<P, kM2lSmall>());
       attr_set = true;
     }
-    k_fmm_m2l_grp<P><<<(unsigned)F.nchunk, M2lCfg<P>::THREADS, m2l_smem<P>(), s>>>(F.chunks, F.cgroup, F.gidx, F.m2l,
-                                                                                  F.Tg, F.M, F.Lp);
+    if (F.nchunk)
+      k_fmm_m2l_grp<P, 0><<<(unsigned)F.nchunk, M2lCfg<P, 0>::THREADS, m2l_smem<P, 0>(), s>>>(F.chunks, F.gidx, F.m2l,
+                                                                                          F.Tg, F.M, F.Lp);
+    if (F.nchunk_small)
+      k_fmm_m2l_grp<P, kM2lSmall><<<(unsigned)F.nchunk_small, M2lCfg<P, kM2lSmall>::THREADS, m2l_smem<P, kM2lSmall>(),
+                                    s>>>(F.chunks_small, F.gidx, F.m2l, F.Tg, F.M, F.Lp);
     k_fmm_m2l_reduce<<<g256(F.nm2lt * np), 256, 0, s>>>(F.nm2lt, F.m2lt, F.om, F.ginv, np, F.Lp, F.L);
     launches += 2;
   }

@@ -110,9 +110,11 @@ struct FmmPlan {
   int64_t nm2l = 0, np2p = 0;
   int32_t *om = nullptr, *op2 = nullptr;    // CSR offsets per target node
   // M2L pairs grouped by their translation vector c_t − c_s (equal vectors ⇒ one derivative tensor):
-  // gidx = the m2l positions in group order, ginv its inverse, chunks = [start) of ≤ kChunk pairs of one
-  // group (nchunk + 1 entries), Lp = the per-pair local expansions in group order (nm2l × np)
-  int32_t *gidx = nullptr, *ginv = nullptr, *chunks = nullptr, *cgroup = nullptr;
+  // gidx = the m2l positions in group order, ginv its inverse, chunks of ≤ 128 (p ≥ 5: 64) pairs of one
+  // group, Lp = the per-pair local expansions in group order (nm2l × np)
+  int32_t *gidx = nullptr, *ginv = nullptr;
+  int4 *chunks = nullptr, *chunks_small = nullptr;  // {first pair, pairs, group}: full and small chunks
+  int64_t nchunk_small = 0;
   double* Tg = nullptr;  // per group: the derivative tensor T_δ, |δ| ≤ 2p (graded order)
   int64_t nchunk = 0, ngroups = 0;
   double* Lp = nullptr;
