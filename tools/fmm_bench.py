@@ -18,7 +18,8 @@ s = torch.from_numpy(np.random.default_rng(3).uniform(-0.5, 0.5, n).astype(np.fl
 w = 0.002
 
 
-def timed(f, reps=3):
+def timed(f, reps=5):
+    f()  # (builds the FMM plan for new parameters)
     f()
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -35,8 +36,7 @@ for op, name in ((0, "F (A)"), (1, "A^T"), (2, "gradF (G)")):
     ref, tms = timed(tree_ops[op])
     for pdeg, th, leaf in ((2, 0.5, 32), (4, 0.5, 32), (4, 0.7, 32), (2, 0.7, 16), (3, 0.8, 16), (2, 0.9, 8)):
         attr = s if op == 1 else mu
-        (out, cnt), fms = timed(lambda: wn.wn_eval_fmm(t, attr, w, op=op, p=pdeg, theta_f=th, leaf=leaf, counts=True),
-                                reps=2)
+        (out, cnt), fms = timed(lambda: wn.wn_eval_fmm(t, attr, w, op=op, p=pdeg, theta_f=th, leaf=leaf, counts=True))
         d = (torch.linalg.norm(out - ref) / torch.linalg.norm(ref)).item()
         print(f"{cfg} {name:10s} treecode {tms:7.2f} ms | FMM p={pdeg} theta={th} leaf={leaf}: {fms:7.2f} ms, M2L {cnt[0]}, "
               f"P2P leaf pairs {cnt[1]}, rel. L2 difference to the treecode {d:.2e}")
