@@ -120,7 +120,8 @@ static wn_status ensure_scratch(wn_tree_s* t, cudaStream_t s) {
   WN_CUDA(cudaMallocAsync((void**)&it.s, n * sizeof(float), s));
   WN_CUDA(cudaMallocAsync((void**)&it.tmp, n * sizeof(float4), s));
   WN_CUDA(cudaMallocAsync((void**)&it.part, 3 * (size_t)it.nblk * sizeof(double), s));
-  WN_CUDA(cudaMallocAsync((void**)&it.alpha, sizeof(double), s));
+  WN_CUDA(cudaMallocAsync((void**)&it.alpha, alpha_words() * sizeof(double), s));
+  WN_CUDA(cudaMemsetAsync(it.alpha, 0, alpha_words() * sizeof(double), s));  // (the reduction's ticket = 0)
   return WN_OK;
 }
 

@@ -62,13 +62,17 @@ __global__ void k_normalize_queries(int64_t m, const float* __restrict__ q, doub
                        (float)(__dsub_rn((double)q[3 * i + 2], c2) * sc), 0.f);
 }
 
-// α = Σr² / Σ(Ar)² from fixed-order block partials (0 if the denominator is 0)
-constexpr int kAlphaThreads = 1024;
+// α = Σr² / Σ(Ar)² from fixed-order block partials (0 if the denominator is 0).
+// kAlphaBlocks blocks each sum a fixed stride of the partial slots (thread order, then a tree), publish
+// their three sums, and the last block to finish (a ticket) adds the block sums in block order: the same
+// order on every run and every rank.  alpha[0] = α, alpha[1 .. 3K] the block sums, alpha[3K + 1] the ticket.
+constexpr int kAlphaThreads = 256;
 __global__ void __launch_bounds__(kAlphaThreads) k_alpha(const double* __restrict__ part, int nblk, int64_t stride,
                                                          double w, double* alpha, double* stats) {
   __shared__ double sh[3][kAlphaThreads];
+  __shared__ bool last;
   double acc[3] = {0.0, 0.0, 0.0};
-  for (int b = threadIdx.x; b < nblk; b += kAlphaThreads)
+  for (int b = blockIdx.x * kAlphaThreads + threadIdx.x; b < nblk; b += kAlphaBlocks * kAlphaThreads)
     for (int c = 0; c < 3; ++c) acc[c] += part[c * stride + b];
   for (int c = 0; c < 3; ++c) sh[c][threadIdx.x] = acc[c];
   __syncthreads();
@@ -77,12 +81,26 @@ __global__ void __launch_bounds__(kAlphaThreads) k_alpha(const double* __restric
       for (int c = 0; c < 3; ++c) sh[c][threadIdx.x] += sh[c][threadIdx.x + o];
     __syncthreads();
   }
+  double* blk = alpha + 1;
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(alpha + 1 + 3 * kAlphaBlocks);
   if (threadIdx.x == 0) {
-    const double E = sh[0][0], rr = sh[1][0], qq = sh[2][0];
-    const double al = qq > 0.0 ? rr / qq : 0.0;
-    *alpha = al;
-    stats[0] = E; stats[1] = al; stats[2] = rr; stats[3] = qq; stats[4] = w;
+    for (int c = 0; c < 3; ++c) blk[c * kAlphaBlocks + blockIdx.x] = sh[c][0];
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == kAlphaBlocks - 1;
   }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double E = 0.0, rr = 0.0, qq = 0.0;
+  for (int k = 0; k < kAlphaBlocks; ++k) {
+    E += __ldcg(blk + k);
+    rr += __ldcg(blk + kAlphaBlocks + k);
+    qq += __ldcg(blk + 2 * kAlphaBlocks + k);
+  }
+  const double al = qq > 0.0 ? rr / qq : 0.0;
+  *alpha = al;
+  stats[0] = E; stats[1] = al; stats[2] = rr; stats[3] = qq; stats[4] = w;
+  *ticket = 0u;  // ready for the next α (stream-ordered)
 }
 
 // s = ½ − A(0) = ½ for every query and the group partials Σ s² = 0.25 · (queries in the group) — exactly the
@@ -135,7 +153,8 @@ void normalize_queries(int64_t m, const float* q, const double xf[4], float4* ou
 }
 void alpha_step(const double* part, int nblk, int64_t stride, double w, double* alpha, double* stats, cudaStream_t s) {
   ProfScope ps(WN_PROF_OTHER, s);
-  k_alpha<<<1, kAlphaThreads, 0, s>>>(part, nblk, stride, w, alpha, stats);
+  k_alpha<<<kAlphaBlocks, kAlphaThreads, 0, s>>>(part, nblk, stride, w, alpha, stats);
+  count_launches(1);
 }
 void s_half(int64_t n, float* s_out, double* part, cudaStream_t s) {
   k_s_half<<<g256(n), 256, 0, s>>>(n, s_out, part, kPartQ);

@@ -60,7 +60,7 @@ struct IterScratch {
   int64_t* dcounts = nullptr;  // (iters + 1) × 12 snapshots of the work counters (counting runs only)
   int64_t stats_cap = 0;
   unsigned long long* dstamp = nullptr;  // iters + 1 device timestamps (ns): iteration i runs between [i] and [i + 1]
-  double* alpha = nullptr;   // current α (device)
+  double* alpha = nullptr;   // current α (device) + the α reduction's block sums and ticket (alpha_words())
   float* tmp = nullptr;      // generic N×4 scratch
   int nblk = 0;
 };
@@ -379,6 +379,8 @@ inline int trav_blocks(int64_t nq) { return (int)((nq + kTravBlock - 1) / kTravB
 // Σ partials (s², |r|², (Ar)²) are kept per 32-query warp group of the query schedule: each warp writes its
 // own slot (no block barrier in the epilogues), and α sums the slots in one fixed order
 constexpr int kPartQ = 32;
+constexpr int kAlphaBlocks = 32;  // blocks of the α reduction (ops.cu:k_alpha)
+constexpr size_t alpha_words() { return 1 + 3 * kAlphaBlocks + 1; }
 static_assert(WN_SHARD_ALIGN % kPartQ == 0, "rank shards must hold whole partial groups");
 __host__ __device__ inline int64_t part_slots(int64_t nq) { return (nq + kPartQ - 1) / kPartQ; }
 
