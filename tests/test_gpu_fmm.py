@@ -63,6 +63,14 @@ def test_fmm_matches_oracle(wn, name, op, p, leaf):
     assert np.all(err <= lim), (np.max(err / lim), int(np.sum(err > lim)))
 
 
+@pytest.mark.parametrize("op", ["F", "AT", "gradF"])
+@pytest.mark.parametrize("p,leaf", [(1, 32), (3, 16), (5, 16), (6, 32)])
+def test_fmm_other_degrees(wn, op, p, leaf):
+    # every degree's kernels (P2M / M2M / M2L chunks of both sizes / L2L / L2P are templated on p; p ≥ 5 splits
+    # the coefficients into parts and uses 64-pair chunks) against the oracle's FMM of the same degree
+    test_fmm_matches_oracle(wn, "sphere3k", op, p, leaf)
+
+
 def test_fmm_all_direct_is_dense(wn):
     pts = CLOUDS["torus20k"]()
     n = len(pts)
