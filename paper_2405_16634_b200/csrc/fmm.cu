@@ -15,11 +15,13 @@
 // otherwise interact directly (P2P, cutoff r < w decided in fp32 as everywhere, R-prec); else the larger
 // cell (the target on ties) is split.  All expansion arithmetic is fp64.
 //
-// B200 mapping: the interaction lists come from a breadth-first dual traversal on the GPU (one thread per
-// cell pair per level, appends by atomics), sorted by (target, source) so that every sum runs in a fixed
-// order; P2M / M2M / M2L / L2L run one warp per cell with lanes over the expansion coefficients (the
-// derivative tensor of a pair is built degree by degree in shared memory); L2P + P2P one warp per leaf with
-// one lane per target point.  The test oracle implements the same algorithm independently in plain fp64 C.
+// B200 mapping (DESIGN.md §6 "FMM"): the interaction lists come from a breadth-first dual traversal on the
+// GPU (one thread per cell pair per level, appends by atomics), sorted by (target, source) so that every
+// sum runs in a fixed order.  Expansion kernels are templated on the degree p: P2M / M2M / L2L one thread
+// per cell with the coefficients in registers; M2L grouped by translation vector (one derivative tensor per
+// group, computed at plan time; chunks of pairs contracted against it from shared memory, per-pair results
+// summed per target in list order); L2P one warp per leaf; P2P in balanced work items of a leaf's direct
+// list.  The test oracle implements the same algorithm independently in plain fp64 C.
 #include <cuda_runtime.h>
 
 #include <algorithm>
