@@ -49,8 +49,10 @@ __constant__ double c_fact[kFmmMaxDeg + 2];
 static int fmm_count(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
 
 static wn_status fmm_tables() {
-  static bool done = false;
-  if (done) return WN_OK;
+  static uint64_t done = 0;  // per device: __constant__ symbols live on each device separately
+  int dev = 0;
+  WN_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && ((done >> dev) & 1)) return WN_OK;
   signed char mi[kFmmMaxT][3];
   static short lut[kFmmLut][kFmmLut][kFmmLut];
   double fact[kFmmMaxDeg + 2];
@@ -72,7 +74,7 @@ static wn_status fmm_tables() {
   WN_CUDA(cudaMemcpyToSymbol(c_mi, mi, sizeof(mi)));
   WN_CUDA(cudaMemcpyToSymbol(c_lut, lut, sizeof(lut)));
   WN_CUDA(cudaMemcpyToSymbol(c_fact, fact, sizeof(fact)));
-  done = true;
+  if (dev < 64) done |= 1ull << dev;
   return WN_OK;
 }
 
@@ -863,6 +865,16 @@ void fmm_plan_free(FmmPlan& F) {
   F = FmmPlan();
 }
 
+// dynamic shared memory of the M2L kernels of degree P (above 48 KB for p = 6); set on the current device
+// whenever a plan is built (not a stream operation: never inside a graph capture)
+template <int P>
+static wn_status m2l_attributes() {
+  WN_CUDA(cudaFuncSetAttribute(k_fmm_m2l_grp<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m2l_smem<P, 0>()));
+  WN_CUDA(cudaFuncSetAttribute(k_fmm_m2l_grp<P, kM2lSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)m2l_smem<P, kM2lSmall>()));
+  return WN_OK;
+}
+
 // The per-tree FMM plan (geometry, node lists, sorted interaction lists, expansion scratch) for
 // (p, θ_f, leaf, separation width wsep): built once — host-synchronizing, never inside a graph capture —
 // and reused by every fmm_run with a cutoff w ≤ wsep (every expanded pair stays beyond the cutoff).
@@ -876,6 +888,14 @@ wn_status fmm_plan(wn_tree_s* t, int p, double theta, int leafsz, float wsep, cu
   WN_CUDA(cudaStreamSynchronize(s));
   fmm_plan_free(F);
   WN_TRY(fmm_tables());
+  switch (p) {
+    case 1: WN_TRY(m2l_attributes<1>()); break;
+    case 2: WN_TRY(m2l_attributes<2>()); break;
+    case 3: WN_TRY(m2l_attributes<3>()); break;
+    case 4: WN_TRY(m2l_attributes<4>()); break;
+    case 5: WN_TRY(m2l_attributes<5>()); break;
+    default: WN_TRY(m2l_attributes<6>()); break;
+  }
   const int64_t nn = t->nn;
   const int np = fmm_count(p);
   std::vector<void*> tmpv;
@@ -1111,13 +1131,6 @@ static int fmm_expansions(wn_tree_s* t, const FmmGeom& g, const float4* vec, con
       ++launches;
     }
   if (F.nchunk + F.nchunk_small > 0) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_fmm_m2l_grp<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m2l_smem<P, 0>());
-      cudaFuncSetAttribute(k_fmm_m2l_grp<P, kM2lSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)m2l_smem<P, kM2lSmall>());
-      attr_set = true;
-    }
     if (F.nchunk)
       k_fmm_m2l_grp<P, 0><<<(unsigned)F.nchunk, M2lCfg<P, 0>::THREADS, m2l_smem<P, 0>(), s>>>(F.chunks, F.gidx, F.m2l,
                                                                                           F.Tg, F.M, F.Lp);

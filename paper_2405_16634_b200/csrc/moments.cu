@@ -464,10 +464,12 @@ void launch_tiles(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
   TilePlanView P{Pl.small, Pl.large, Pl.tile_soff, Pl.tile_loff, Pl.cross, Pl.ep_slot, Pl.tile_eoff, Pl.onept,
                  Pl.ep_key, Pl.epval, t->mom_ttot, Pl.ncross};
   constexpr size_t smem = (size_t)NC * kMomTile * sizeof(double);
-  static bool smem_set = false;  // per instantiation: beyond the 48 KB default
-  if (!smem_set) {
+  static uint64_t smem_set = 0;  // per instantiation and device: beyond the 48 KB default
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64 || !((smem_set >> dev) & 1)) {
     cudaFuncSetAttribute(mom_tiles<KIND, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_set = true;
+    if (dev < 64) smem_set |= 1ull << dev;
   }
   mom_tiles<KIND, ORD><<<(unsigned)t->mom_ntiles, kTileThreads, smem, s>>>(tv, m, t->n, P);
   if (Pl.ncross > 0) mom_cross<KIND, ORD><<<(unsigned)((Pl.ncross * 32 + 255) / 256), 256, 0, s>>>(tv, m, P);
