@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(kMomThreads, WN_EXP_MOM_LB) moments_range(Tree
 
 // ---------------- tile builds (per-iteration attributes: ATTR_VEC, ATTR_SCALAR) ----------------
 // Every octree node B covers a contiguous range [pb, pe) of the Morton-sorted points.  The sorted points
-// are cut into tiles of kMomTile (tree_build.cu:plan_moment_tiles lists, per tile, the nodes whose points
-// lie in it):
+// are cut into tiles of wn_tree_s::mom_tile points (choose_mom_tile; tree_build.cu:plan_moment_tiles
+// lists, per tile, the nodes whose points lie in it):
 //   mom_tiles  (one block per tile) computes every point's terms (|ν|, |ν|x, ν, …) once into shared memory
 //              (coalesced loads; μ' = μ + α r written here; a one-point node's V = ν_j written here), then
 //              sums each node's range directly — one thread per node below kMomWarpNode points, one warp
@@ -317,18 +317,20 @@ struct TilePlanView {
   double* epval;  // 2·ncross × kMomNC
   double* ttot;   // ntiles × kMomNC
   int64_t ncross;
+  int tile;       // points per tile (wn_tree_s::mom_tile)
 };
 
 constexpr int kTileThreads = 256, kTileWarps = kTileThreads / 32;
 
 // warp sum of NC planes over [l0, l1): lanes stride, then a fixed xor butterfly (every lane gets the same bits)
 template <int NC>
-__device__ __forceinline__ void warp_range_sum(const double* __restrict__ sm, int l0, int l1, int lane, double* d) {
+__device__ __forceinline__ void warp_range_sum(const double* __restrict__ sm, int T, int l0, int l1, int lane,
+                                               double* d) {
 #pragma unroll
   for (int c = 0; c < NC; ++c) d[c] = 0.0;
   for (int l = l0 + lane; l < l1; l += 32)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) d[c] += sm[c * kMomTile + l];
+    for (int c = 0; c < NC; ++c) d[c] += sm[c * T + l];
 #pragma unroll
   for (int o = 16; o; o >>= 1)
 #pragma unroll
@@ -348,13 +350,14 @@ __device__ __forceinline__ double pick(const double* d, int k) {
 template <int KIND, int ORD>
 __global__ void __launch_bounds__(kTileThreads) mom_tiles(TreeView tv, MomentArgs m, int64_t n, TilePlanView P) {
   constexpr int NC = Lay<KIND, ORD>::NC;
-  extern __shared__ double sm[];  // NC planes of kMomTile per-point terms
+  extern __shared__ double sm[];  // NC planes of P.tile per-point terms
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float alpha = (KIND == ATTR_VEC && m.axpy_r) ? (float)(*m.alpha) : 0.f;
   const bool axpy = KIND == ATTR_VEC && m.axpy_r;
   const bool scaled = m.a_sorted != nullptr;
-  const int64_t tile = blockIdx.x, base = tile * (int64_t)kMomTile;
-  const int nv = (int)(n - base < kMomTile ? n - base : kMomTile);
+  const int T = P.tile;
+  const int64_t tile = blockIdx.x, base = tile * (int64_t)T;
+  const int nv = (int)(n - base < T ? n - base : T);
   for (int jl = threadIdx.x; jl < nv; jl += kTileThreads) {  // coalesced
     const int64_t j = base + jl;
     float4 v = KIND == ATTR_VEC ? m.vec[j] : make_float4(m.scal[j], 0.f, 0.f, 0.f);
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kTileThreads) mom_tiles(TreeView tv, MomentArg
     double o[NC];
     point_terms<KIND, ORD>(tv.pts[j], v, f, scaled, o);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) sm[c * kMomTile + jl] = o[c];
+    for (int c = 0; c < NC; ++c) sm[c * T + jl] = o[c];
     const int2 op = P.onept[j];
     if (op.x >= 0) {  // one-point node: R = (x_j, −1), L, ext (= 0) fixed per tree; V = ν_j, the leaf term's ν
       if (m.write_W) tv.sums[8 * (int64_t)op.x] = o[0];
@@ -384,10 +387,10 @@ __global__ void __launch_bounds__(kTileThreads) mom_tiles(TreeView tv, MomentArg
     WN_DCHECK(l0 + 1 < l1 && l1 <= nv, "moment node range");
     double d[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) d[c] = sm[c * kMomTile + l0];
+    for (int c = 0; c < NC; ++c) d[c] = sm[c * T + l0];
     for (int l = l0 + 1; l < l1; ++l)
 #pragma unroll
-      for (int c = 0; c < NC; ++c) d[c] += sm[c * kMomTile + l];
+      for (int c = 0; c < NC; ++c) d[c] += sm[c * T + l];
     sums_record<KIND, ORD>(d4.x, l1 - l0, d, tv, m, d4.w >> 16, d4.z, d4.w & 0xffff);
   }
   // warp items: the large nodes, the endpoint sums, the tile total
@@ -399,18 +402,18 @@ __global__ void __launch_bounds__(kTileThreads) mom_tiles(TreeView tv, MomentArg
       const int4 d4 = P.large[L0 + w];
       const int l0 = d4.y & 0xffff, l1 = d4.y >> 16;
       WN_DCHECK(l0 < l1 && l1 <= nv, "moment node range");
-      warp_range_sum<NC>(sm, l0, l1, lane, d);
+      warp_range_sum<NC>(sm, T, l0, l1, lane, d);
       if (lane == 0) sums_record<KIND, ORD>(d4.x, l1 - l0, d, tv, m, d4.w >> 16, d4.z, d4.w & 0xffff);
     } else if (w < nl + ne) {
       const int e = E0 + w - nl, slot = P.ep_slot[e];
-      const int j = (int)(P.ep_key[e] - (uint64_t)tile * (kMomTile + 1));
+      const int j = (int)(P.ep_key[e] - (uint64_t)tile * (T + 1));
       WN_DCHECK(j >= 0 && j <= nv, "moment endpoint");
       // slot 2c: the node starts here — its points from j to the tile's end; 2c + 1: it ends here — [0, j)
-      if (slot & 1) warp_range_sum<NC>(sm, 0, j, lane, d);
-      else warp_range_sum<NC>(sm, j, nv, lane, d);
+      if (slot & 1) warp_range_sum<NC>(sm, T, 0, j, lane, d);
+      else warp_range_sum<NC>(sm, T, j, nv, lane, d);
       if (lane < NC) P.epval[(size_t)kMomNC * slot + lane] = pick<NC>(d, lane);
     } else {
-      warp_range_sum<NC>(sm, 0, nv, lane, d);
+      warp_range_sum<NC>(sm, T, 0, nv, lane, d);
       if (lane < NC) P.ttot[(size_t)kMomNC * tile + lane] = pick<NC>(d, lane);
     }
   }
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(256) mom_cross(TreeView tv, MomentArgs m, Tile
   if (c >= P.ncross) return;
   const int64_t i = P.cross[c];
   const int j0 = tv.pb[i], j1 = tv.pe[i];
-  const int64_t ta = j0 / kMomTile, tb = (j1 - 1) / kMomTile;
+  const int64_t ta = j0 / P.tile, tb = (j1 - 1) / P.tile;
   double d[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) d[k] = 0.0;
@@ -462,13 +465,14 @@ void launch_tiles(wn_tree_s* t, const MomentArgs& m, cudaStream_t s) {
   TreeView tv{t->pts, t->pb, t->pe, t->cb, t->cc, t->tdepth, t->topo, t->smask, t->sums, t->centroid};
   const MomPlan& Pl = t->mplan[(m.all_nodes || m.write_W || !t->mom_live) ? 1 : 0];
   TilePlanView P{Pl.small, Pl.large, Pl.tile_soff, Pl.tile_loff, Pl.cross, Pl.ep_slot, Pl.tile_eoff, Pl.onept,
-                 Pl.ep_key, Pl.epval, t->mom_ttot, Pl.ncross};
-  constexpr size_t smem = (size_t)NC * kMomTile * sizeof(double);
+                 Pl.ep_key, Pl.epval, t->mom_ttot, Pl.ncross, t->mom_tile};
+  const size_t smem = (size_t)NC * t->mom_tile * sizeof(double);
   static uint64_t smem_set = 0;  // per instantiation and device: beyond the 48 KB default
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 64 || !((smem_set >> dev) & 1)) {
-    cudaFuncSetAttribute(mom_tiles<KIND, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(mom_tiles<KIND, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)NC * kMomTileMax * sizeof(double)));
     if (dev < 64) smem_set |= 1ull << dev;
   }
   mom_tiles<KIND, ORD><<<(unsigned)t->mom_ntiles, kTileThreads, smem, s>>>(tv, m, t->n, P);
@@ -497,6 +501,27 @@ void launch_all(wn_tree_s* t, const MomentArgs& m, cudaStream_t s, const int64_t
 
 }  // namespace
 
+// Points per tile.  A tile block holds its points' terms in shared memory (7 fp64 planes for a vector
+// attribute: 57 KB at 1024 points, so 3 blocks per SM).  1024 by default; a cloud whose 1024-point tiles
+// would spill just over one wave of resident tiles (3 per SM) takes the multiple of 128 up to kMomTileMax
+// that fits one wave (C3 500k: 1152, 435 tiles: moments 7.3 → 6.6 ms per step); a cloud of fewer than two
+// 1024-point tiles per SM is cut into about two tiles per SM (multiples of 128, ≥ 256) — more blocks in
+// flight (40-iteration solve: C1 2k 256 points, 8.5 → 8.0 ms; C2 50k 256, 39.5 → 38.8; C4 200k 768,
+// 67.0 → 66.1); large clouds (many waves) keep 1024 (C5: 1152 would cost 34 → 36 ms of moments).
+int choose_mom_tile(int64_t n, int sms) {
+  if (WN_EXP_MOMTILE != 1024) return WN_EXP_MOMTILE;  // (experiment builds pin the tile)
+  const int64_t t1024 = (n + 1023) / 1024, wave = 3ll * sms;
+  if (t1024 < 2ll * sms) {  // few tiles: about two per SM, multiples of 128 points, at least 256
+    const int64_t want = ((n + 2ll * sms - 1) / (2ll * sms) + 127) / 128 * 128;
+    return (int)std::min<int64_t>(1024, std::max<int64_t>(256, want));
+  }
+  if (t1024 > wave) {
+    const int64_t need = ((n + wave - 1) / wave + 127) / 128 * 128;
+    if (need <= kMomTileMax) return (int)need;
+  }
+  return 1024;
+}
+
 wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
   // cut at the first level with ≥ 1024 nodes: the levels above it run in one block
   const int deepest = t->depth_used;
@@ -510,7 +535,11 @@ wn_status plan_moments(wn_tree_s* t, cudaStream_t s) {
   WN_CUDA(cudaMallocAsync((void**)&t->mom_loff, t->level_off.size() * sizeof(int64_t), s));
   WN_CUDA(cudaMemcpyAsync(t->mom_loff, t->level_off.data(), t->level_off.size() * sizeof(int64_t),
                           cudaMemcpyHostToDevice, s));
-  t->mom_ntiles = (t->n + kMomTile - 1) / kMomTile;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  t->mom_tile = choose_mom_tile(t->n, sms);
+  t->mom_ntiles = (t->n + t->mom_tile - 1) / t->mom_tile;
   WN_TRY(plan_moment_tiles(t, 0, s));
   return WN_OK;
 }

@@ -951,18 +951,18 @@ __global__ void k_node_keys(int64_t m, const int32_t* __restrict__ list, const i
 }
 
 // class of a listed node: 0 one point, 1 small (one tile), 2 large (one tile), 3 across tiles
-__device__ __forceinline__ int node_class(int32_t b, int32_t e) {
+__device__ __forceinline__ int node_class(int32_t b, int32_t e, int T) {
   if (e - b == 1) return 0;
-  if (b / kMomTile != (e - 1) / kMomTile) return 3;
+  if (b / T != (e - 1) / T) return 3;
   return e - b < kMomWarpNode ? 1 : 2;
 }
 
 __global__ void k_class_flag(int64_t m, const int32_t* __restrict__ list, const int32_t* __restrict__ pb,
-                             const int32_t* __restrict__ pe, int cls, uint32_t* __restrict__ flag) {
+                             const int32_t* __restrict__ pe, int cls, int T, uint32_t* __restrict__ flag) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= m) return;
   const int32_t i = list[k];
-  flag[k] = node_class(pb[i], pe[i]) == cls;
+  flag[k] = node_class(pb[i], pe[i], T) == cls;
 }
 
 // compaction of one class in list order; one-tile classes as descriptors (local point range, code, one-point
@@ -970,7 +970,7 @@ __global__ void k_class_flag(int64_t m, const int32_t* __restrict__ list, const 
 __global__ void k_class_put(int64_t m, const int32_t* __restrict__ list, const uint32_t* __restrict__ flag,
                             const uint32_t* __restrict__ pos, const int32_t* __restrict__ pb,
                             const int32_t* __restrict__ pe, const int32_t* __restrict__ topo,
-                            const int32_t* __restrict__ smask, const int32_t* __restrict__ tdepth,
+                            const int32_t* __restrict__ smask, const int32_t* __restrict__ tdepth, int T,
                             int4* __restrict__ desc, int32_t* __restrict__ ids) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= m || !flag[k]) return;
@@ -978,7 +978,7 @@ __global__ void k_class_put(int64_t m, const int32_t* __restrict__ list, const u
   if (ids) {
     ids[pos[k]] = i;
   } else {
-    const int32_t b0 = (pb[i] / kMomTile) * kMomTile;
+    const int32_t b0 = (pb[i] / T) * T;
     desc[pos[k]] = make_int4(i, (pb[i] - b0) | ((pe[i] - b0) << 16), topo[i], smask[i] | (tdepth[i] << 16));
   }
 }
@@ -991,12 +991,12 @@ __global__ void k_onept(int64_t m, const int32_t* __restrict__ list, const int32
   if (pe[i] - pb[i] == 1) onept[pb[i]] = make_int2(i, topo[i]);  // (a point's one-point node is its leaf: unique)
 }
 
-// tile k's descriptors start at the first whose first point is ≥ k·kMomTile (lists sorted by first point)
+// tile k's descriptors start at the first whose first point is ≥ k·T (lists sorted by first point)
 __global__ void k_tile_off(int64_t ntiles, const int4* __restrict__ desc, int64_t nd, const int32_t* __restrict__ pb,
-                           int32_t* __restrict__ off) {
+                           int T, int32_t* __restrict__ off) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k > ntiles) return;
-  const int64_t target = k * (int64_t)kMomTile;
+  const int64_t target = k * (int64_t)T;
   int64_t lo = 0, hi = nd;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
@@ -1008,21 +1008,23 @@ __global__ void k_tile_off(int64_t ntiles, const int4* __restrict__ desc, int64_
 
 // endpoints of the cross-tile nodes: Σ from pb to the end of pb's tile, Σ from the start of (pe − 1)'s tile to pe
 __global__ void k_ep_keys(int64_t nc, const int32_t* __restrict__ cross, const int32_t* __restrict__ pb,
-                          const int32_t* __restrict__ pe, uint64_t* __restrict__ key, int32_t* __restrict__ slot) {
+                          const int32_t* __restrict__ pe, int T, uint64_t* __restrict__ key,
+                          int32_t* __restrict__ slot) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nc) return;
   const int64_t b = pb[cross[c]], e = pe[cross[c]];
-  const int64_t ta = b / kMomTile, tb = (e - 1) / kMomTile;
-  key[2 * c] = (uint64_t)(ta * (kMomTile + 1) + (b - ta * kMomTile));
-  key[2 * c + 1] = (uint64_t)(tb * (kMomTile + 1) + (e - tb * kMomTile));
+  const int64_t ta = b / T, tb = (e - 1) / T;
+  key[2 * c] = (uint64_t)(ta * (T + 1) + (b - ta * T));
+  key[2 * c + 1] = (uint64_t)(tb * (T + 1) + (e - tb * T));
   slot[2 * c] = (int32_t)(2 * c);
   slot[2 * c + 1] = (int32_t)(2 * c + 1);
 }
 
-__global__ void k_tile_eoff(int64_t ntiles, const uint64_t* __restrict__ key, int64_t ne, int32_t* __restrict__ off) {
+__global__ void k_tile_eoff(int64_t ntiles, const uint64_t* __restrict__ key, int64_t ne, int T,
+                            int32_t* __restrict__ off) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k > ntiles) return;
-  const uint64_t target = (uint64_t)k * (kMomTile + 1);
+  const uint64_t target = (uint64_t)k * (T + 1);
   int64_t lo = 0, hi = ne;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
@@ -1042,7 +1044,9 @@ wn_status plan_moment_tiles(wn_tree_s* t, int which, cudaStream_t s) {
   MomPlan& P = t->mplan[which];
   if (P.ready) return WN_OK;
   TempSet tmp(s);
-  const int64_t n = t->n, ntiles = (n + kMomTile - 1) / kMomTile;
+  if (t->mom_tile <= 0) return set_error(WN_ERR_ARG, "internal: moment tile size not chosen");
+  const int T = t->mom_tile;
+  const int64_t n = t->n, ntiles = (n + T - 1) / T;
   // the node list in ascending first point: the visitable nodes (already sorted) or all nodes (sorted here)
   const int32_t* list = t->mom_live;
   int64_t m = t->mom_nlive;
@@ -1064,7 +1068,7 @@ wn_status plan_moment_tiles(wn_tree_s* t, int which, cudaStream_t s) {
   const unsigned g = (unsigned)((m + 255) / 256);
   int64_t cnt[4] = {0, 0, 0, 0};
   for (int cls = 1; cls <= 3; ++cls) {
-    k_class_flag<<<g, 256, 0, s>>>(m, list, t->pb, t->pe, cls, flag);
+    k_class_flag<<<g, 256, 0, s>>>(m, list, t->pb, t->pe, cls, T, flag);
     WN_TRY(scan_excl(flag, pos, m, pos + m, s));
     uint32_t c = 0;
     WN_CUDA(cudaMemcpyAsync(&c, pos + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -1082,7 +1086,7 @@ wn_status plan_moment_tiles(wn_tree_s* t, int which, cudaStream_t s) {
       WN_TRY(dalloc(&P.cross, std::max<int64_t>(c, 1), s));
       ids = P.cross;
     }
-    k_class_put<<<g, 256, 0, s>>>(m, list, flag, pos, t->pb, t->pe, t->topo, t->smask, t->tdepth, desc, ids);
+    k_class_put<<<g, 256, 0, s>>>(m, list, flag, pos, t->pb, t->pe, t->topo, t->smask, t->tdepth, T, desc, ids);
     count_launches(5);
   }
   P.nsmall = cnt[1];
@@ -1095,8 +1099,8 @@ wn_status plan_moment_tiles(wn_tree_s* t, int which, cudaStream_t s) {
   WN_TRY(dalloc(&P.tile_loff, ntiles + 1, s));
   WN_TRY(dalloc(&P.tile_eoff, ntiles + 1, s));
   const unsigned gt = (unsigned)((ntiles + 256) / 256);
-  k_tile_off<<<gt, 256, 0, s>>>(ntiles, P.small, P.nsmall, t->pb, P.tile_soff);
-  k_tile_off<<<gt, 256, 0, s>>>(ntiles, P.large, P.nlarge, t->pb, P.tile_loff);
+  k_tile_off<<<gt, 256, 0, s>>>(ntiles, P.small, P.nsmall, t->pb, T, P.tile_soff);
+  k_tile_off<<<gt, 256, 0, s>>>(ntiles, P.large, P.nlarge, t->pb, T, P.tile_loff);
   count_launches(3);
   const int64_t ne = 2 * P.ncross;
   WN_TRY(dalloc(&P.ep_key, std::max<int64_t>(ne, 1), s));
@@ -1107,11 +1111,11 @@ wn_status plan_moment_tiles(wn_tree_s* t, int which, cudaStream_t s) {
     int32_t* v = nullptr;
     WN_TRY(tmp.alloc(&k, ne));
     WN_TRY(tmp.alloc(&v, ne));
-    k_ep_keys<<<(unsigned)((P.ncross + 255) / 256), 256, 0, s>>>(P.ncross, P.cross, t->pb, t->pe, k, v);
+    k_ep_keys<<<(unsigned)((P.ncross + 255) / 256), 256, 0, s>>>(P.ncross, P.cross, t->pb, t->pe, T, k, v);
     count_launches(1);
-    WN_TRY(sort_pairs(k, v, ne, key_bits(ntiles * (int64_t)(kMomTile + 1)), P.ep_slot, s, P.ep_key));
+    WN_TRY(sort_pairs(k, v, ne, key_bits(ntiles * (int64_t)(T + 1)), P.ep_slot, s, P.ep_key));
   }
-  k_tile_eoff<<<gt, 256, 0, s>>>(ntiles, P.ep_key, ne, P.tile_eoff);
+  k_tile_eoff<<<gt, 256, 0, s>>>(ntiles, P.ep_key, ne, T, P.tile_eoff);
   count_launches(1);
   if (!t->mom_ttot) WN_TRY(dalloc(&t->mom_ttot, (size_t)kMomNC * ntiles, s));
   WN_CUDA(cudaGetLastError());

@@ -71,7 +71,10 @@ struct IterScratch {
 #ifndef WN_EXP_MOMTILE
 #define WN_EXP_MOMTILE 1024
 #endif
-constexpr int kMomTile = WN_EXP_MOMTILE;
+constexpr int kMomTile = WN_EXP_MOMTILE;  // the default tile; choose_mom_tile adapts it per cloud size
+constexpr int kMomTileMax = 1280;
+// points per moment-build tile for n points on `sms` SMs (moments.cu:choose_mom_tile)
+int choose_mom_tile(int64_t n, int sms);
 #ifndef WN_EXP_MOMWARP
 #define WN_EXP_MOMWARP 32
 #endif
@@ -170,6 +173,7 @@ struct wn_tree_s {
   double* mom_ttot = nullptr;    // per-tile totals of the running build (ntiles × kMomNC)
   wn::ShardPlan shard;           // work-weighted query shards for the last world size used
   int64_t mom_ntiles = 0;
+  int mom_tile = 0;              // points per tile of the moment builds (choose_mom_tile, per tree)
   bool mom_order1_ready = false;  // prefix scratch + set[0].ext sized for the first-order far field
   int far_order = 0;              // wn_tree_set_far_order: 0 (the paper's Alg. 4) or 1 (row f2)
   int fmm_p = 0, fmm_leaf = 32;   // wn_tree_set_fmm: wnnc_iterate's operators by FMM of degree fmm_p (0: treecode)

@@ -11,6 +11,11 @@ VARIANTS = {
     "lb5": ["WN_EXP_LBMIN=5"],  # resident 256-thread-equivalents per SM of the one-warp traversal
     "mt512": ["WN_EXP_MOMTILE=512"],  # moment-build tiles of 512 / 2048 points (default 1024)
     "mt2048": ["WN_EXP_MOMTILE=2048"],
+    "mt1152": ["WN_EXP_MOMTILE=1152"],  # C3: 435 tiles ≤ 148 SMs × 3 resident tiles (one wave)
+    "mt1280": ["WN_EXP_MOMTILE=1280"],
+    "mt256": ["WN_EXP_MOMTILE=256"],
+    "mt384": ["WN_EXP_MOMTILE=384"],
+    "mt768": ["WN_EXP_MOMTILE=768"],
     "mw64": ["WN_EXP_MOMWARP=64"],  # moment build: nodes of >= 64 / 128 points summed by a warp (default 32)
     "mw128": ["WN_EXP_MOMWARP=128"],
 }
