@@ -210,8 +210,8 @@ extern "C" wn_status wn_iso_cells(wn_tree t, const float* mu, float width, float
     const int64_t nn = 8 * (int64_t)nk;
     if (nn > kIsoMaxCells) return set_error(WN_ERR_ARG, "wn_iso_cells: more than 2^26 active cells (lower max_level)");
     uint64_t* next = nullptr;
-    std::vector<void*> prev;
-    prev.swap(keep_);  // the current cells: freed with this level's buffers
+    for (void* p : keep_) lvl.push_back(p);  // the current cells: freed with this level's buffers
+    keep_.clear();
     tgt = &keep_;
     WN_TRY(alloc(&next, nn * sizeof(uint64_t)));
     tgt = &lvl;
@@ -219,7 +219,6 @@ extern "C" wn_status wn_iso_cells(wn_tree t, const float* mu, float width, float
       k_iso_children<<<g256(nc), 256, 0, s>>>(nc, cur, keep, kpos, next);
       count_launches(1);
     }
-    for (void* p : prev) lvl.push_back(p);
     for (void* p : lvl) cudaFreeAsync(p, s);  // stream-ordered: after this level's kernels
     lvl.clear();
     cur = next;
