@@ -88,7 +88,9 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
     --sp;
     const int2 e = stk[sp];
     __syncwarp();
-    const int cb = e.x >> 4, ncc = (e.x & 7) + 1;
+    // lane 0's copies of words every lane read alike: warp-uniform loop control and branches (traverse.cu)
+    const int code = __shfl_sync(FULL, e.x, 0);
+    const int cb = code >> 4, ncc = (code & 7) + 1;
     const bool mine = ((uint32_t)e.y >> lane) & 1u;
     for (int k0 = 0; k0 < ncc; k0 += 4) {
       // up to four children: each lane's contributions v[4·kk + (x, y, z, ·)], then one reduce-scatter
@@ -117,14 +119,14 @@ __global__ void __launch_bounds__(kTravBlock) scatter_kernel(
           anylive |= live;
           const uint32_t open = __ballot_sync(FULL, mine && !far);
           if (open) {
-            const int topo = __float_as_int(__ldg(G + kRec * (int64_t)node + 1).w);
+            const int topo = __shfl_sync(FULL, __float_as_int(__ldg(G + kRec * (int64_t)node + 1).w), 0);
             if (topo != 0) {
               if (lane == 0) stk[sp] = make_int2(topo, (int)open);
               ++sp;
             } else {  // leaf-coded node: its points, one butterfly per point into U (grouping: no gain)
               const bool lm = (open >> lane) & 1u;
-              const int j1 = npe[node];
-              for (int j = npb[node]; j < j1; ++j) {
+              const int j0 = __shfl_sync(FULL, npb[node], 0), j1 = __shfl_sync(FULL, npe[node], 0);
+              for (int j = j0; j < j1; ++j) {
                 const float4 P = __ldg(pts + j);
                 const float px = __fsub_rn(P.x, xq.x), py = __fsub_rn(P.y, xq.y), pz = __fsub_rn(P.z, xq.z);
                 const float e2 = dist2(px, py, pz);

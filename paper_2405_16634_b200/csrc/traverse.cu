@@ -617,7 +617,8 @@ __global__ void __launch_bounds__(kTravBlock) trav_visits_kernel(const TravArgs 
     --sp;
     const int2 e = stk[sp];
     __syncwarp();
-    const int cb = e.x >> 4, ncc = (e.x & 7) + 1;
+    const int code = __shfl_sync(FULL, e.x, 0);  // (uniform trip count, as in trav_group)
+    const int cb = code >> 4, ncc = (code & 7) + 1;
     const bool mine = ((uint32_t)e.y >> lane) & 1u;
     wv += ncc;
     for (int k = 0; k < ncc; ++k) {
@@ -628,7 +629,7 @@ __global__ void __launch_bounds__(kTravBlock) trav_visits_kernel(const TravArgs 
                   ez = __fadd_rn(__fsub_rn(R.z, xq.z), L.z);
       const uint32_t open = __ballot_sync(FULL, mine && !(dist2(ex, ey, ez) > R.w));
       if (open) {
-        const int topo = __float_as_int(__ldg(rp + 1).w);
+        const int topo = __shfl_sync(FULL, __float_as_int(__ldg(rp + 1).w), 0);
         if (topo != 0) {
           WN_DCHECK(sp < a.stack_depth, "visit-count stack");
           stk[sp] = make_int2(topo, (int)open);
