@@ -326,7 +326,7 @@ def run_ours(args):
                 "bound_note": "the traversals are instruction-issue bound, not FP32-throughput bound: "
                               "ncu shows 72-81 % issue-slot utilization with ~37 instructions per "
                               "warp-level node visit, of which 13 flops are the algorithmic node test "
-                              "(profiles/r02_ncu_trav_v3.txt: 72.8 % issue active, FMA pipe 30 %, ALU 42 %; "
+                              "(profiles/r02_ncu_trav_v4.txt: 76.0 % issue active, FMA pipe 29 %, ALU 35 %; "
                               "DESIGN.md §6)",
                 "work": work}
     if args.fmm:  # FMM operators: the M2L contraction (fp64) of every application over the FMM runs' time
