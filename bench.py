@@ -317,8 +317,17 @@ def run_ours(args):
     except (OSError, ValueError, KeyError):
         pass
     interactions = sum(work[c]["live"] for c in ("A", "AT", "G"))
+    # the same traversals on SURVEY §8(d) d.4's FP32 lane-instruction basis (7 per node test; 7 / 7 / 15 per far
+    # term of A / Aᵀ / G; a near term 6 more) against the FP32 issue rate of 128 lanes per SM per cycle
+    per_term = {"A": 7, "AT": 7, "G": 15}
+    lane_instr = sum(7 * work[c]["tests"] + per_term[c] * work[c]["far"] + (per_term[c] + 6) * work[c]["near"]
+                     for c in ("A", "AT", "G"))
+    issue_peak = sm_count * 128 * fmax * 1e6
+    issue_basis = {"achieved": lane_instr / (trav_ms / 1e3), "peak": issue_peak, "unit": "FP32 lane-instructions/s",
+                   "frac": lane_instr / (trav_ms / 1e3) / issue_peak,
+                   "per_unit": "SURVEY 8(d) d.4: 7 per node test, 7/7/15 per far term (A/AT/G), +6 per near term"}
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic,
+                "frac": achieved / peak, "traffic": traffic, "issue_basis": issue_basis,
                 "kernel": "treecode traversals (trav_kernel A/AT/G), %.0f launches/step, %.3f ms/step"
                           % (trav_launches, trav_ms),
                 "peak_note": f"FP32 FMA pipe: {sm_count} SMs x 128 lanes x 2 flop x {fmax:.0f} MHz "
