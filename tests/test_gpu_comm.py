@@ -64,11 +64,12 @@ def test_world1_comm_transpose(wn):
     comm.close()
 
 
-@pytest.mark.parametrize("world,n", [(2, 30011), (3, 70001), (8, 30011)])
+@pytest.mark.parametrize("world,n", [(2, 30011), (3, 70001), (8, 30011), (8, 1000)])
 def test_emulated_ranks_transpose(wn, world, n):
     # W emulated ranks, transpose-mode adjoint (SURVEY §8(e) + row a7): each rank scatters its shard into its
     # own accumulators, every rank adds all ranks' in rank order and pushes down for all points — every
     # replica is the same bit for bit, and the trajectory is the single-GPU transpose one up to rounding
+    # (1000 points over 8 ranks: shards of 256 queries, so some ranks have none and only signal)
     p = torch.from_numpy(synth.config("C2" if n <= 50000 else "C3")["points"][:n]).cuda()
     t = wn.wn_build_tree(p)
     T = wn.WN_ADJ_TRANSPOSE

@@ -101,3 +101,15 @@ def test_iso_cells_errors(setup):
         args.update(kw)
         with pytest.raises(wn.WnError, match="ARG"):
             wn.wn_iso_cells(t, mu, w, **args)
+
+
+def test_iso_cells_single_level(setup):
+    # base_level = max_level: no refinement, the crossing cells of the 2^l lattice itself
+    wn, t, mu, box, w, lmax, Fd = setup
+    cells, vals, evals = wn.wn_iso_cells(t, mu, w, box=box, base_level=4, max_level=4, band=0.1)
+    f = 1 << (lmax - 4)
+    Fl = Fd[::f, ::f, ::f]  # the level-4 lattice is every 4th point of the level-6 one
+    got = _set(cells.cpu().numpy())
+    strict, loose = _set(_replay(Fl, 4, 4, 0.5, 0.1, -TOL)), _set(_replay(Fl, 4, 4, 0.5, 0.1, TOL))
+    assert strict <= got <= loose and len(got) > 0
+    assert evals == 17 ** 3
