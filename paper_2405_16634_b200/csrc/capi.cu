@@ -795,8 +795,11 @@ wn_status wn_moments(wn_tree t, const float* nu, int32_t dim, const float* a, fl
   return WN_OK;
 }
 
+// presorted: the queries are already spatially coherent (wn_iso_cells: corners in Morton order), so the
+// per-call Hilbert schedule is skipped and warps take consecutive queries
 static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a, const float* q, int64_t m,
-                             float width, float theta, float* out, void* stream, int32_t* qcounts = nullptr) {
+                             float width, float theta, float* out, void* stream, int32_t* qcounts = nullptr,
+                             bool presorted = false) {
   TreeUse use_(t, stream);
   if (!t || !mu || (!out && !qcounts)) return set_error(WN_ERR_ARG, "tree, mu or output is NULL");
   if (bad_width(width)) return set_error(WN_ERR_ARG, "width must be > 0");
@@ -837,12 +840,12 @@ static wn_status eval_common(wn_tree t, int op, const float* mu, const float* a,
       t->qcap = m;
     }
     normalize_queries(m, q, t->xf, t->qbuf, s);
-    WN_TRY(hilbert_schedule(t->qbuf, m, t->qbuf_order, s));  // coherent warps for arbitrary queries (f1)
+    if (!presorted) WN_TRY(hilbert_schedule(t->qbuf, m, t->qbuf_order, s));  // coherent warps for arbitrary queries (f1)
     ta.queries = t->qbuf;
     ta.q_end = m;
     ta.split = m <= split_max() ? split_factor(m) : 0;
     ta.out_map = nullptr;
-    ta.qorder = t->qbuf_order;
+    ta.qorder = presorted ? nullptr : t->qbuf_order;
   } else {
     ta.out_map = t->perm;
   }
@@ -1208,6 +1211,6 @@ extern "C" wn_status wn_exp_set_schedule(wn_tree t, const int32_t* qorder, void*
 namespace wn {
 wn_status eval_field(wn_tree_s* t, const float* mu, const float* q, int64_t m, float width, float theta, float* F,
                      cudaStream_t s) {
-  return eval_common(t, OP_A, mu, nullptr, q, m, width, theta, F, (void*)s);
+  return eval_common(t, OP_A, mu, nullptr, q, m, width, theta, F, (void*)s, nullptr, true);
 }
 }  // namespace wn

@@ -8,11 +8,15 @@
 // cells, a cell stays active if its corner values come within `band` of the iso value (min ≤ iso + band and
 // max ≥ iso − band), and every active cell is split in eight.  At the finest level the cells the level set
 // crosses (min < iso ≤ max) are returned with their eight corner values: the input of a marching-cubes
-// mesher.  Corners are keyed on the level's lattice (21 bits per axis), sorted and deduplicated, so a
-// corner shared by up to eight cells is evaluated once.
+// mesher.  Corners are keyed on the level's lattice (Morton codes, 21 bits per axis), sorted and
+// deduplicated, so a corner shared by up to eight cells is evaluated once, and evaluated in Z order — coherent
+// warps without the per-call Hilbert schedule of wn_eval.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "wn_internal.cuh"
@@ -21,27 +25,62 @@ namespace wn {
 namespace {
 
 constexpr int kIsoBits = 21;
-constexpr uint64_t kIsoMask = (1ull << kIsoBits) - 1;
 constexpr int64_t kIsoMaxCells = 1ll << 26;  // active cells per level (8 corner keys each, 32-bit scans)
 
+// lattice points and cells are keyed by their Morton code (21 bits per axis, interleaved): sorted keys are a
+// Z-order walk of the box, so the distinct corners come out spatially coherent for the traversal's warps,
+// and a cell's children are its key × 8 + (0..7)
+__host__ __device__ inline uint64_t spread3(uint64_t v) {  // 21 bits → every third bit
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+__host__ __device__ inline uint64_t compact3(uint64_t v) {  // inverse of spread3
+  v &= 0x1249249249249249ull;
+  v = (v ^ (v >> 2)) & 0x10c30c30c30c30c3ull;
+  v = (v ^ (v >> 4)) & 0x100f00f00f00f00full;
+  v = (v ^ (v >> 8)) & 0x1f0000ff0000ffull;
+  v = (v ^ (v >> 16)) & 0x1f00000000ffffull;
+  v = (v ^ (v >> 32)) & 0x1fffff;
+  return v;
+}
 __host__ __device__ inline uint64_t iso_key(uint64_t i, uint64_t j, uint64_t k) {
-  return i | (j << kIsoBits) | (k << (2 * kIsoBits));
+  return spread3(i) | (spread3(j) << 1) | (spread3(k) << 2);
+}
+__host__ __device__ inline void iso_ijk(uint64_t key, uint64_t& i, uint64_t& j, uint64_t& k) {
+  i = compact3(key);
+  j = compact3(key >> 1);
+  k = compact3(key >> 2);
 }
 
 __global__ void k_iso_base(int level, uint64_t* __restrict__ cells) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t side = 1ll << level;
   if (c >= side * side * side) return;
-  cells[c] = iso_key(c % side, (c / side) % side, c / (side * side));
+  cells[c] = iso_key(c % side, (c / side) % side, c / (side * side));  // (any order: corners are sorted)
 }
 
 __global__ void k_iso_corner_keys(int64_t nc, const uint64_t* __restrict__ cells, uint64_t* __restrict__ ck) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= 8 * nc) return;
-  const uint64_t c = cells[t >> 3];
+  uint64_t i, j, k;
+  iso_ijk(cells[t >> 3], i, j, k);
   const int b = (int)(t & 7);
-  ck[t] = iso_key((c & kIsoMask) + (b & 1), ((c >> kIsoBits) & kIsoMask) + ((b >> 1) & 1),
-                  (c >> (2 * kIsoBits)) + ((b >> 2) & 1));
+  ck[t] = iso_key(i + (b & 1), j + ((b >> 1) & 1), k + ((b >> 2) & 1));
+}
+// below the base level the active cells are the eight children of each kept parent, whose corners are the
+// parent's 3 × 3 × 3 lattice points on the finer level: 27 keys per parent instead of 64
+__global__ void k_iso_corner_keys27(int64_t np, const uint64_t* __restrict__ parents, uint64_t* __restrict__ ck) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= 27 * np) return;
+  uint64_t i, j, k;
+  iso_ijk(parents[t / 27], i, j, k);
+  const int b = (int)(t % 27);
+  ck[t] = iso_key(2 * i + b % 3, 2 * j + (b / 3) % 3, 2 * k + b / 9);
 }
 
 __global__ void k_iso_uniq_flag(int64_t m, const uint64_t* __restrict__ sk, uint32_t* __restrict__ flag) {
@@ -55,13 +94,15 @@ __global__ void k_iso_uniq(int64_t m, const uint64_t* __restrict__ sk, const uin
                            double ey, double ez, uint64_t* __restrict__ uk, float* __restrict__ q) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= m || !flag[i]) return;
-  const uint64_t k = sk[i];
+  const uint64_t key = sk[i];
   const int64_t u = pos[i];
-  uk[u] = k;
+  uk[u] = key;
+  uint64_t a, b, c;
+  iso_ijk(key, a, b, c);
   const double inv = ldexp(1.0, -level);
-  q[3 * u + 0] = (float)(lx + ex * ((double)(k & kIsoMask) * inv));
-  q[3 * u + 1] = (float)(ly + ey * ((double)((k >> kIsoBits) & kIsoMask) * inv));
-  q[3 * u + 2] = (float)(lz + ez * ((double)(k >> (2 * kIsoBits)) * inv));
+  q[3 * u + 0] = (float)(lx + ex * ((double)a * inv));
+  q[3 * u + 1] = (float)(ly + ey * ((double)b * inv));
+  q[3 * u + 2] = (float)(lz + ez * ((double)c * inv));
 }
 
 __device__ __forceinline__ int64_t iso_find(const uint64_t* __restrict__ uk, int64_t m, uint64_t key) {
@@ -80,11 +121,11 @@ __global__ void k_iso_decide(int64_t nc, const uint64_t* __restrict__ cells, con
                              float* __restrict__ cv, uint32_t* __restrict__ keep) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nc) return;
-  const uint64_t k = cells[c];
+  uint64_t ci, cj, ck3;
+  iso_ijk(cells[c], ci, cj, ck3);
   float lo = 3.4e38f, hi = -3.4e38f;
   for (int b = 0; b < 8; ++b) {
-    const uint64_t key = iso_key((k & kIsoMask) + (b & 1), ((k >> kIsoBits) & kIsoMask) + ((b >> 1) & 1),
-                                 (k >> (2 * kIsoBits)) + ((b >> 2) & 1));
+    const uint64_t key = iso_key(ci + (b & 1), cj + ((b >> 1) & 1), ck3 + ((b >> 2) & 1));
     const float v = F[iso_find(uk, m, key)];
     cv[8 * c + b] = v;
     lo = fminf(lo, v);
@@ -94,12 +135,12 @@ __global__ void k_iso_decide(int64_t nc, const uint64_t* __restrict__ cells, con
 }
 
 __global__ void k_iso_children(int64_t nc, const uint64_t* __restrict__ cells, const uint32_t* __restrict__ keep,
-                               const uint32_t* __restrict__ pos, uint64_t* __restrict__ next) {
+                               const uint32_t* __restrict__ pos, uint64_t* __restrict__ next,
+                               uint64_t* __restrict__ parents) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nc || !keep[c]) return;
-  const uint64_t k = cells[c];
-  const uint64_t i = 2 * (k & kIsoMask), j = 2 * ((k >> kIsoBits) & kIsoMask), l = 2 * (k >> (2 * kIsoBits));
-  for (int b = 0; b < 8; ++b) next[8 * (int64_t)pos[c] + b] = iso_key(i + (b & 1), j + ((b >> 1) & 1), l + ((b >> 2) & 1));
+  parents[pos[c]] = cells[c];
+  for (int b = 0; b < 8; ++b) next[8 * (int64_t)pos[c] + b] = cells[c] * 8 + (uint64_t)b;  // (Morton: children)
 }
 
 __global__ void k_iso_out(int64_t nc, const uint64_t* __restrict__ cells, const uint32_t* __restrict__ keep,
@@ -109,10 +150,11 @@ __global__ void k_iso_out(int64_t nc, const uint64_t* __restrict__ cells, const 
   if (c >= nc || !keep[c]) return;
   const int64_t o = pos[c];
   if (o >= cap) return;
-  const uint64_t k = cells[c];
-  out_cells[3 * o + 0] = (int32_t)(k & kIsoMask);
-  out_cells[3 * o + 1] = (int32_t)((k >> kIsoBits) & kIsoMask);
-  out_cells[3 * o + 2] = (int32_t)(k >> (2 * kIsoBits));
+  uint64_t i, j, k;
+  iso_ijk(cells[c], i, j, k);
+  out_cells[3 * o + 0] = (int32_t)i;
+  out_cells[3 * o + 1] = (int32_t)j;
+  out_cells[3 * o + 2] = (int32_t)k;
   for (int b = 0; b < 8; ++b) out_vals[8 * o + b] = cv[8 * c + b];
 }
 
@@ -154,26 +196,30 @@ extern "C" wn_status wn_iso_cells(wn_tree t, const float* mu, float width, float
   const double lx = box[0], ly = box[1], lz = box[2];
   const double ex = (double)box[3] - box[0], ey = (double)box[4] - box[1], ez = (double)box[5] - box[2];
   int64_t nc = 1ll << (3 * base_level);  // ≤ 2^21
-  uint64_t* cur = nullptr;
+  uint64_t *cur = nullptr, *par = nullptr;  // the level's cells; the previous level's kept cells (parents)
   tgt = &keep_;
   WN_TRY(alloc(&cur, nc * sizeof(uint64_t)));
   tgt = &lvl;
   k_iso_base<<<g256(nc), 256, 0, s>>>(base_level, cur);
   count_launches(1);
   int64_t total_evals = 0;
+  const bool verbose = getenv("WN_ISO_VERBOSE") != nullptr;  // (diagnostic: per-level wall times on stderr)
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
   for (int level = base_level;; ++level) {
+    const auto t_lvl = tnow();
     const bool fin = level == max_level;
     *count = 0;
     if (nc == 0) break;
-    // the level's distinct corners
-    const int64_t m8 = 8 * nc;
+    // the level's distinct corners: 8 per cell on the base level, 27 per kept parent below it
+    const int64_t m8 = level == base_level ? 8 * nc : 27 * (nc / 8);
     uint64_t *ck = nullptr, *sk = nullptr, *uk = nullptr;
     uint32_t *flag = nullptr, *pos = nullptr;
     WN_TRY(alloc(&ck, m8 * sizeof(uint64_t)));
     WN_TRY(alloc(&sk, m8 * sizeof(uint64_t)));
     WN_TRY(alloc(&flag, (m8 + 1) * sizeof(uint32_t)));
     WN_TRY(alloc(&pos, (m8 + 1) * sizeof(uint32_t)));
-    k_iso_corner_keys<<<g256(m8), 256, 0, s>>>(nc, cur, ck);
+    if (level == base_level) k_iso_corner_keys<<<g256(m8), 256, 0, s>>>(nc, cur, ck);
+    else k_iso_corner_keys27<<<g256(m8), 256, 0, s>>>(nc / 8, par, ck);
     WN_TRY(sort_keys_u64(ck, m8, 3 * kIsoBits, sk, s));
     k_iso_uniq_flag<<<g256(m8), 256, 0, s>>>(m8, sk, flag);
     WN_TRY(scan_u32(flag, pos, m8, pos + m8, s));
@@ -186,7 +232,14 @@ extern "C" wn_status wn_iso_cells(wn_tree t, const float* mu, float width, float
     WN_TRY(alloc(&F, (size_t)m * sizeof(float)));
     k_iso_uniq<<<g256(m8), 256, 0, s>>>(m8, sk, flag, pos, level, lx, ly, lz, ex, ey, ez, uk, q);
     count_launches(3);
+    const auto t_sort = tnow();
     WN_TRY(eval_field(t, mu, q, m, width, theta, F, s));  // the Alg. 4 traversal of wn_eval
+    if (verbose) {
+      cudaStreamSynchronize(s);
+      fprintf(stderr, "wn_iso_cells level %d: %lld cells, %u corners, keys %.2f ms, F %.2f ms\n", level, (long long)nc, m,
+              std::chrono::duration<double, std::milli>(t_sort - t_lvl).count(),
+              std::chrono::duration<double, std::milli>(tnow() - t_sort).count());
+    }
     total_evals += m;
     // decisions
     uint32_t *keep = nullptr, *kpos = nullptr;
@@ -210,13 +263,14 @@ extern "C" wn_status wn_iso_cells(wn_tree t, const float* mu, float width, float
     const int64_t nn = 8 * (int64_t)nk;
     if (nn > kIsoMaxCells) return set_error(WN_ERR_ARG, "wn_iso_cells: more than 2^26 active cells (lower max_level)");
     uint64_t* next = nullptr;
-    for (void* p : keep_) lvl.push_back(p);  // the current cells: freed with this level's buffers
+    for (void* p : keep_) lvl.push_back(p);  // the current cells and parents: freed with this level's buffers
     keep_.clear();
     tgt = &keep_;
     WN_TRY(alloc(&next, nn * sizeof(uint64_t)));
+    WN_TRY(alloc(&par, std::max<int64_t>(nk, 1) * sizeof(uint64_t)));
     tgt = &lvl;
     if (nk > 0) {
-      k_iso_children<<<g256(nc), 256, 0, s>>>(nc, cur, keep, kpos, next);
+      k_iso_children<<<g256(nc), 256, 0, s>>>(nc, cur, keep, kpos, next, par);
       count_launches(1);
     }
     for (void* p : lvl) cudaFreeAsync(p, s);  // stream-ordered: after this level's kernels

@@ -238,7 +238,8 @@ wn_status kd_schedule(const float4* pts, int64_t n, int32_t* order, cudaStream_t
 wn_status sort_keys_u64(const uint64_t* keys, int64_t n, int bits, uint64_t* out, cudaStream_t s);
 // exclusive scan of m uint32 flags (tree_build.cu), *total = the sum (device)
 wn_status scan_u32(const uint32_t* in, uint32_t* out, int64_t m, uint32_t* total, cudaStream_t s);
-// F at m input-frame queries q[m×3] (wn_eval's path: moments of mu, Hilbert-scheduled traversal), F[m]
+// F at m input-frame queries q[m×3] given in a spatially coherent order (wn_eval's path — moments of mu,
+// traversal — without the per-call Hilbert schedule), F[m]
 wn_status eval_field(wn_tree_s* t, const float* mu, const float* q, int64_t m, float width, float theta, float* F,
                      cudaStream_t s);
 wn_status sort_keys_u64_perm(const uint64_t* keys, int64_t n, int bits, uint64_t* out, int32_t* perm,
