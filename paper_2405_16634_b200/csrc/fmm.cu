@@ -403,10 +403,28 @@ __global__ void __launch_bounds__(M2lCfg<P, CHP>::THREADS) k_fmm_m2l_grp(const i
   }
   for (int e = tid; e < npair; e += C::THREADS) sS[e] = (int)(uint32_t)m2l[gidx[i0 + e]];
   __syncthreads();
-  // the sources' coefficients, staged (each pair's np values contiguous in M: coalesced runs)
-  for (int e = tid; e < npair * C::NP; e += C::THREADS) {
-    const int pr = e / C::NP, be = e - pr * C::NP;
-    sMO[be * C::CHP + pr] = __ldg(M + (int64_t)sS[pr] * C::NP + be);
+  // the sources' coefficients, staged (each pair's np values contiguous in M: coalesced runs); four loads
+  // in flight per thread
+  {
+    const int tot = npair * C::NP;
+    int e = tid;
+    for (; e + 3 * C::THREADS < tot; e += 4 * C::THREADS) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = e + u * C::THREADS, pr = x / C::NP, be = x - pr * C::NP;
+        v[u] = __ldg(M + (int64_t)sS[pr] * C::NP + be);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = e + u * C::THREADS, pr = x / C::NP, be = x - pr * C::NP;
+        sMO[be * C::CHP + pr] = v[u];
+      }
+    }
+    for (; e < tot; e += C::THREADS) {
+      const int pr = e / C::NP, be = e - pr * C::NP;
+      sMO[be * C::CHP + pr] = __ldg(M + (int64_t)sS[pr] * C::NP + be);
+    }
   }
   __syncthreads();
   // thread (part, pa): pairs pa + q·HALF (q < PPT; a slot past the chunk is read but its result dropped)
